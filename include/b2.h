@@ -1,0 +1,197 @@
+/*
+ * b2.h -- C ABI of the B200-native dense core (libb2.so).
+ *
+ * Plain pointers and sizes only; no torch or Python types. Every entry point
+ * returns 0 on success and a nonzero status otherwise; b2_last_error()
+ * returns the message of the most recent failure on the calling thread.
+ * Device pointers are float32 (or int64 labels / double slots where named)
+ * allocated with b2_alloc. Strides are in ELEMENTS; a stride of 0 marks a
+ * broadcast axis (the reference's stride-0 expand view, core.py:381-392).
+ * `stream` may be NULL for the engine's default compute stream.
+ *
+ * Each group below names the reference seam it replaces (paths relative to
+ * /root/reference/pkg/src/tensorlite/). The reference is pure Python; these
+ * are the pure-compute calls inside each op (SURVEY 8b "Kernel seams").
+ */
+#ifndef B2_H
+#define B2_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B2_MAX_DIMS 8
+
+/* ---------------------------------------------------------------- runtime */
+const char* b2_last_error(void);
+int b2_version(int* major, int* minor);
+int b2_init(int device);                 /* select device, create streams */
+int b2_device_count(int* n);
+int b2_device_info(int* sm_count, int* cc_major, int* cc_minor, size_t* total_mem);
+int b2_default_stream(void** stream);
+int b2_stream_create(void** stream);
+int b2_stream_destroy(void* stream);
+int b2_stream_sync(void* stream);
+int b2_device_sync(void);
+int b2_event_create(void** ev);
+int b2_event_destroy(void* ev);
+int b2_event_record(void* ev, void* stream);
+int b2_event_elapsed_ms(void* start, void* end, float* ms);
+int b2_stream_wait_event(void* stream, void* ev);
+/* kernels launched by this library since process start (launch counter) */
+int b2_launch_count(uint64_t* n);
+
+/* ---------------------------------------------------------------- storage
+ * Replaces Buffer(array('f')) per op output (core.py:68-75, 315-330): a
+ * caching device allocator with size-class bins and stream-ordered frees.
+ */
+int b2_alloc(size_t bytes, void* stream, void** out);
+int b2_free(void* ptr, void* stream);
+int b2_alloc_stats(size_t* in_use, size_t* cached, size_t* peak, uint64_t* n_cuda_malloc);
+int b2_empty_cache(void);
+int b2_host_alloc(size_t bytes, void** out);   /* pinned host staging */
+int b2_host_free(void* ptr);
+int b2_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+int b2_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
+int b2_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
+int b2_fill_f32(float* dst, float value, int64_t n, void* stream);
+
+/* ---------------------------------------------------------------- elementwise
+ * Replaces _elementwise/_binary/_unary (core.py:430-546) and the fused
+ * pointwise activations (nn.py:95-111). out is contiguous with `shape`.
+ */
+enum b2_binary_op { B2_ADD = 0, B2_SUB = 1, B2_MUL = 2, B2_DIV = 3,
+                    B2_RELU_BWD = 4 /* a * (b > 0 ? 1 : 0), nn.py:101-103 */,
+                    B2_SIGN_MUL = 5 /* a * sign(b), core.py:533-546 */ };
+enum b2_unary_op { B2_NEG = 0, B2_EXP = 1, B2_LOG = 2, B2_SQRT = 3, B2_ABS = 4,
+                   B2_RELU = 5, B2_RELU_MASK = 6, B2_COPY = 7, B2_CLAMP = 8,
+                   B2_SCALE = 9 /* x * alpha */, B2_DIV_SCALAR = 10 /* x / f32(alpha) */,
+                   B2_CLAMP_MASK = 11 /* alpha <= x <= beta ? 1 : 0 */ };
+int b2_binary(int op, float* out, int ndim, const int64_t* shape,
+              const float* a, const int64_t* a_strides,
+              const float* b, const int64_t* b_strides, void* stream);
+/* binary op with one operand a Python scalar promoted to f32 (core.py:352-357) */
+int b2_binary_scalar(int op, float* out, int ndim, const int64_t* shape,
+                     const float* x, const int64_t* x_strides, float scalar,
+                     int scalar_left, void* stream);
+int b2_unary(int op, float* out, int ndim, const int64_t* shape,
+             const float* x, const int64_t* x_strides,
+             double alpha, double beta, void* stream);
+/* strided (or stride-0 broadcast) gather into a contiguous tensor */
+int b2_copy_strided(float* out, int ndim, const int64_t* shape,
+                    const float* x, const int64_t* x_strides, void* stream);
+/* strided scatter-write of a contiguous source into a (possibly strided) view */
+int b2_write_strided(float* dst, int ndim, const int64_t* shape,
+                     const int64_t* dst_strides, const float* src, void* stream);
+
+/* Fused op+grad for y = relu(a*b + c) with a:[R,C], b,c broadcast rows [C]
+ * (BASELINE config 2; core.py:453-483 + nn.py:108-111 in one pass).
+ * fwd writes y (and optionally the pre-activation q). bwd of sum(y) w.r.t.
+ * a and b in GradStore order: ga = mask*b, gb = f32(count) + f32(sum mask*a)
+ * (autograd.py:140-145). */
+int b2_fused_muladd_relu_fwd(float* y, const float* a, const float* b,
+                             const float* c, int64_t rows, int64_t cols, void* stream);
+int b2_fused_muladd_relu_bwd(float* ga, float* gb, const float* a,
+                             const float* b, int64_t rows, int64_t cols, void* stream);
+
+/* ---------------------------------------------------------------- reductions
+ * Replaces _sum_all / _axis_scan + sum/mean/max (core.py:581-728).
+ * reduce_mask: bit d set => axis d is reduced. out is contiguous over the
+ * kept axes (row-major). For B2_RED_MAX, argr (int64, may be NULL) receives
+ * the index of the first maximum within the reduced subspace (row-major over
+ * the reduced axes), the position the gradient is routed to.
+ * Sums accumulate in fp64 with a fixed-order two-stage combine.
+ */
+enum b2_reduce_op { B2_RED_SUM = 0, B2_RED_MEAN = 1, B2_RED_MAX = 2 };
+int b2_reduce(int op, float* out, int64_t* argr, int ndim, const int64_t* shape,
+              const float* x, const int64_t* x_strides, uint32_t reduce_mask,
+              void* stream);
+/* max pullback (core.py:721-726): gx = zeros(shape); gx[pos(o, argr[o])] = g[o] */
+int b2_max_scatter(float* gx, int ndim, const int64_t* shape, uint32_t reduce_mask,
+                   const float* g, const int64_t* argr, void* stream);
+
+/* ---------------------------------------------------------------- matmul
+ * Replaces matmul.block (core.py:802-807) and its pullbacks (:815-817).
+ * C[M,N] = opA(A) . opB(B) (+ bias[N]) (relu). Row-major with leading
+ * dimensions lda/ldb/ldc in elements. trans_a: A stored [K,M]; trans_b: B
+ * stored [N,K] (the reference's x.w^T is trans_b=1).
+ * algo: 0 auto, 1 FP32 SIMT (FFMA), 2 3xTF32 on tcgen05 (fp32 accuracy),
+ *       3 1xTF32 on tcgen05 (fast, ~1e-3 rel; never chosen by auto).
+ */
+enum b2_gemm_algo { B2_GEMM_AUTO = 0, B2_GEMM_SIMT = 1, B2_GEMM_3XTF32 = 2,
+                    B2_GEMM_1XTF32 = 3 };
+enum b2_epilogue { B2_EPI_NONE = 0, B2_EPI_BIAS = 1, B2_EPI_BIAS_RELU = 2, B2_EPI_RELU = 3 };
+int b2_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
+            const float* A, int64_t lda, const float* B, int64_t ldb,
+            float* C, int64_t ldc, const float* bias, int epilogue, int algo,
+            void* stream);
+/* which algorithm b2_gemm(algo=0) picks for a shape (for tests/bench) */
+int b2_gemm_select(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
+                   int64_t lda, int64_t ldb, int* algo);
+/* split a [rows, cols] (leading dim ld) matrix into contiguous hi = tf32(x)
+ * (round to nearest) and lo = x - hi, both exact fp32 (3xTF32 operands) */
+int b2_tf32_split(float* hi, float* lo, const float* x, int64_t rows, int64_t cols,
+                  int64_t ld, void* stream);
+/* 3xTF32 GEMM on caller-provided contiguous splits (A: [M,K] or [K,M] if
+ * trans_a; B: [N,K] if trans_b else [K,N]); lets the host reuse a split. */
+int b2_gemm_presplit(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
+                     const float* A_hi, const float* A_lo, const float* B_hi,
+                     const float* B_lo, float* C, int64_t ldc, const float* bias,
+                     int epilogue, void* stream);
+
+/* ---------------------------------------------------------------- losses
+ * cross_entropy (nn.py:453-503): fwd writes the mean loss (f32 scalar) and
+ * per-row stats (max, sum exp) in double; bwd writes
+ * dlogits = (exp(z-m)/se - onehot) * (g[0] * inv_b).
+ * labels are int64, validated on the host (nn.py:465-472).
+ */
+int b2_xent_fwd(float* loss, double* row_stats, const float* logits,
+                const int64_t* labels, int64_t rows, int64_t cols, double inv_b,
+                void* stream);
+int b2_xent_bwd(float* dlogits, const float* g, const double* row_stats,
+                const float* logits, const int64_t* labels, int64_t rows,
+                int64_t cols, double inv_b, void* stream);
+/* row softmax over the last axis, composed-semantics:
+ * m = rowmax (detached), e = f32(exp(f32(z-m))), s = f32(sum64 e), y = f32(e/s).
+ * bwd mirrors the GradStore order of the composition:
+ * gz = f32(f32(f32(gy/s) + f32(sum64 f32(-f32(f32(gy*e)/f32(s*s))))) * e). */
+int b2_softmax_fwd(float* y, float* row_s, float* row_m, const float* z,
+                   int64_t rows, int64_t cols, void* stream);
+int b2_softmax_bwd(float* gz, const float* gy, const float* z, const float* row_s,
+                   const float* row_m, int64_t rows, int64_t cols, void* stream);
+
+/* ---------------------------------------------------------------- optimizers
+ * Optimizer.step/_update + step_all (optim.py:39-136) as ONE multi-tensor
+ * launch. Slots are double, like the reference. Per-tensor bias corrections
+ * (Adam's t is per parameter, optim.py:84-91) come from the host.
+ */
+typedef struct b2_opt_tensor {
+  float* param;
+  const float* grad;
+  double* slot0;      /* SGD v / Adam m */
+  double* slot1;      /* Adam v (unused by SGD) */
+  int64_t n;
+  double bc1, bc2;    /* Adam: 1-b1^t, 1-b2^t */
+} b2_opt_tensor;
+int b2_sgd_multi(const b2_opt_tensor* tensors, int count, double lr, double momentum,
+                 double weight_decay, void* stream);
+int b2_adam_multi(const b2_opt_tensor* tensors, int count, double lr, double beta1,
+                  double beta2, double eps, double weight_decay, void* stream);
+
+/* ---------------------------------------------------------------- collectives
+ * Data-parallel gradient exchange (new; the reference is single-process).
+ * NCCL over NVLink/NVSwitch; one communicator per process (one GPU each).
+ */
+int b2_comm_unique_id(unsigned char* out128);
+int b2_comm_init(int rank, int nranks, const unsigned char* uid128);
+int b2_comm_destroy(void);
+/* in-place sum (op=0) / average (op=1) / max (op=2) over all ranks, fp32 */
+int b2_allreduce_f32(float* buf, int64_t n, int op, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B2_H */

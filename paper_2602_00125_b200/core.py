@@ -1,0 +1,929 @@
+"""Device tensors with strided views, broadcasting and recorded ops.
+
+Drop-in for the reference engine module (tensorlite/core.py:1-820): same
+function names, argument meanings, shapes, exception classes and messages;
+the storage lives in B200 HBM and every op is one (or a few) sm_100a kernel
+launches on the engine's CUDA stream through the C ABI (include/b2.h).
+
+Storage and views (core.py:68-191): a ``Buffer`` owns one block from the
+caching device allocator (freed in stream order when the last view dies)
+and a mutation ``version``. A ``Tensor`` is (buffer, shape, strides,
+offset); reshape of contiguous data, transpose2d and stride-0 broadcasts
+are views, exactly as in the reference, and kernels read the views in
+place (strided / broadcast operands, transposed GEMM operands).
+
+Numerics: + - * / are IEEE fp32 (== the reference's
+f32(double op)); exp/log are f32(double libm); sums accumulate in fp64;
+max keeps the first maximum; matmul is fp32-accurate (3xTF32 on tcgen05
+or FFMA) and lands within the 1e-4 tolerance of the reference's double
+dot products.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import random
+import weakref
+
+import numpy as np
+
+from . import _lib as L
+from .autograd import record
+from .errors import BroadcastError, ShapeError
+
+_py_sum = sum
+_py_max = max
+
+
+# ---------------------------------------------------------------------------
+# storage
+
+
+class Buffer:
+    """One device allocation plus a version counter (core.py:68-75)."""
+
+    __slots__ = ("ptr", "nbytes", "version", "_splits", "__weakref__")
+
+    def __init__(self, nbytes: int):
+        L.ensure_device()
+        p = ctypes.c_void_p()
+        L.check(L.lib().b2_alloc(_py_max(int(nbytes), 4), None, ctypes.byref(p)))
+        self.ptr = p.value
+        self.nbytes = int(nbytes)
+        self.version = 0
+        self._splits = None  # {(offset, rows, cols, ld): (version, hi, lo)} 3xTF32 operand cache
+
+    def __del__(self):
+        try:
+            if self.ptr and L._lib is not None:
+                L._lib.b2_free(self.ptr, None)
+        except Exception:
+            pass
+        self.ptr = 0
+
+
+def _contig_strides(shape):
+    st = [0] * len(shape)
+    acc = 1
+    for d in range(len(shape) - 1, -1, -1):
+        st[d] = acc
+        acc *= shape[d]
+    return tuple(st)
+
+
+def _numel(shape):
+    n = 1
+    for s in shape:
+        n *= s
+    return n
+
+
+def _check_shape(shape):
+    if isinstance(shape, int):
+        shape = (shape,)
+    shape = tuple(shape)
+    for s in shape:
+        if not isinstance(s, (int, np.integer)) or s < 0:
+            raise ShapeError(f"invalid shape {shape}")
+    return tuple(int(s) for s in shape)
+
+
+class Tensor:
+    __slots__ = ("buffer", "shape", "strides", "offset", "requires_grad", "node", "__weakref__")
+
+    def __init__(self, buffer, shape, strides=None, offset=0, requires_grad=False):
+        self.buffer = buffer
+        self.shape = tuple(shape)
+        self.strides = _contig_strides(self.shape) if strides is None else tuple(strides)
+        self.offset = offset
+        self.requires_grad = requires_grad
+        self.node = None
+
+    @property
+    def size(self) -> int:
+        return _numel(self.shape)
+
+    @property
+    def ndim(self) -> int:
+        return len(self.shape)
+
+    @property
+    def is_contiguous(self) -> bool:
+        return self.strides == _contig_strides(self.shape)
+
+    @property
+    def data_ptr(self) -> int:
+        return self.buffer.ptr + 4 * self.offset
+
+    def __repr__(self):
+        vals = self.flat()
+        head = ", ".join(f"{v:g}" for v in vals[:6])
+        if self.size > 6:
+            head += ", ..."
+        grad = ", requires_grad=True" if self.requires_grad else ""
+        return f"Tensor(shape={self.shape}, [{head}]{grad}, device=b200)"
+
+    # -- reading values out (device -> host copies)
+
+    def numpy(self) -> np.ndarray:
+        """A host float32 copy in row-major logical order."""
+        out = np.empty(self.shape, dtype=np.float32)
+        if self.size == 0:
+            return out
+        src = self if (self.ndim == 0 or self.is_contiguous) else _copy_contig(self)
+        L.call("b2_memcpy_d2h", out.ctypes.data, src.data_ptr, self.size * 4, None)
+        return out
+
+    def flat(self) -> list:
+        return self.numpy().ravel().astype(np.float64).tolist()
+
+    def item(self) -> float:
+        if self.size != 1:
+            raise ShapeError(f"item() needs a single-element tensor, got shape {self.shape}")
+        v = np.empty(1, np.float32)
+        L.call("b2_memcpy_d2h", v.ctypes.data, self.data_ptr, 4, None)
+        return float(v[0])
+
+    def tolist(self):
+        if self.ndim == 0:
+            return self.item()
+        return self.numpy().astype(np.float64).tolist()
+
+    # -- mutation (bumps the buffer version so stale pullbacks are caught)
+
+    def fill_(self, value: float):
+        if self.is_contiguous:
+            L.call("b2_fill_f32", self.data_ptr, float(value), self.size, None)
+            self.buffer.version += 1
+            return self
+        return self.write_flat([value] * self.size)
+
+    def set_flat(self, index: int, value: float):
+        if not 0 <= index < self.size:
+            raise IndexError(f"flat index {index} out of range for shape {self.shape}")
+        off = self.offset
+        rem = index
+        for d in range(self.ndim - 1, -1, -1):
+            off += (rem % self.shape[d]) * self.strides[d]
+            rem //= self.shape[d]
+        v = np.array([value], np.float32)
+        L.call("b2_memcpy_h2d", self.buffer.ptr + 4 * off, v.ctypes.data, 4, None)
+        self.buffer.version += 1
+        return self
+
+    def write_flat(self, values):
+        arr = np.asarray(values if isinstance(values, np.ndarray) else list(values),
+                         dtype=np.float32).ravel()
+        if arr.size != self.size:
+            raise ShapeError(f"expected {self.size} values, got {arr.size}")
+        arr = np.ascontiguousarray(arr)
+        if self.size:
+            if self.is_contiguous:
+                L.call("b2_memcpy_h2d", self.data_ptr, arr.ctypes.data, arr.nbytes, None)
+                L.synchronize()  # arr is pageable and may be freed by the caller
+            else:
+                src = from_numpy(arr.reshape(self.shape))
+                L.call("b2_write_strided", self.data_ptr, self.ndim, L.i64s(self.shape),
+                       L.i64s(self.strides), src.data_ptr, None)
+        self.buffer.version += 1
+        return self
+
+    def detach(self) -> "Tensor":
+        return Tensor(self.buffer, self.shape, self.strides, self.offset)
+
+    def copy(self) -> "Tensor":
+        return _copy_contig(self)
+
+
+def _empty(shape) -> Tensor:
+    shape = tuple(shape)
+    return Tensor(Buffer(4 * _numel(shape)), shape)
+
+
+def _copy_contig(t: Tensor) -> Tensor:
+    out = _empty(t.shape)
+    if t.size:
+        L.call("b2_copy_strided", out.data_ptr, t.ndim, L.i64s(t.shape), t.data_ptr,
+               L.i64s(t.strides), None)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# constructors (core.py:254-357)
+
+
+def from_numpy(arr, requires_grad=False) -> Tensor:
+    """Upload a host array (any float dtype is rounded to f32 once)."""
+    a = np.ascontiguousarray(arr, dtype=np.float32)
+    t = _empty(a.shape)
+    if a.size:
+        L.call("b2_memcpy_h2d", t.data_ptr, a.ctypes.data, a.nbytes, None)
+        L.synchronize()
+    t.requires_grad = requires_grad
+    return t
+
+
+def _infer_nested(data):
+    if isinstance(data, (int, float)) and not isinstance(data, bool) or isinstance(data, bool):
+        return (), [float(data)]
+    if not isinstance(data, (list, tuple)):
+        raise TypeError(f"cannot build a tensor from {type(data).__name__}")
+    if not data:
+        return (0,), []
+    parts = [_infer_nested(d) for d in data]
+    child = parts[0][0]
+    if any(s != child for s, _ in parts[1:]):
+        raise ShapeError("ragged nested data")
+    flat = []
+    for _, f in parts:
+        flat.extend(f)
+    return (len(data),) + child, flat
+
+
+def tensor(data, requires_grad=False) -> Tensor:
+    """A tensor from a number or nested lists of numbers (core.py:254-259)."""
+    shape, flat = _infer_nested(data)
+    t = from_numpy(np.array(flat, dtype=np.float32).reshape(shape))
+    t.requires_grad = requires_grad
+    return t
+
+
+def from_flat(values, shape, requires_grad=False) -> Tensor:
+    shape = _check_shape(shape)
+    arr = np.asarray(values if isinstance(values, np.ndarray) else list(values), dtype=np.float32)
+    if arr.size != _numel(shape):
+        raise ShapeError(f"{arr.size} values cannot fill shape {shape}")
+    t = from_numpy(arr.reshape(shape))
+    t.requires_grad = requires_grad
+    return t
+
+
+def from_buffer(obj, shape, requires_grad=False) -> Tensor:
+    """Upload external float32 storage (core.py:290-312 validation rules).
+
+    The reference aliases host memory; HBM cannot alias a host buffer, so
+    this copies once (documented divergence)."""
+    mv = memoryview(obj)
+    if mv.format != "f":
+        raise TypeError(f"expected float32 storage (format 'f'), got {mv.format!r}")
+    if mv.readonly:
+        raise ValueError("buffer must be writable")
+    if not mv.c_contiguous:
+        raise ValueError("buffer must be C-contiguous")
+    shape = _check_shape(shape)
+    arr = np.frombuffer(mv.cast("B"), dtype=np.float32)
+    if arr.size != _numel(shape):
+        raise ShapeError(f"{arr.size} buffered values cannot fill shape {shape}")
+    return from_numpy(arr.reshape(shape), requires_grad=requires_grad)
+
+
+def full(shape, value, requires_grad=False) -> Tensor:
+    shape = _check_shape(shape)
+    t = _empty(shape)
+    if t.size:
+        L.call("b2_fill_f32", t.data_ptr, float(value), t.size, None)
+    t.requires_grad = requires_grad
+    return t
+
+
+def zeros(shape, requires_grad=False) -> Tensor:
+    return full(shape, 0.0, requires_grad)
+
+
+def ones(shape, requires_grad=False) -> Tensor:
+    return full(shape, 1.0, requires_grad)
+
+
+def zeros_like(t, requires_grad=False) -> Tensor:
+    return zeros(t.shape, requires_grad=requires_grad)
+
+
+def ones_like(t, requires_grad=False) -> Tensor:
+    return ones(t.shape, requires_grad=requires_grad)
+
+
+def uniform(shape, low=-1.0, high=1.0, rng=None, requires_grad=False) -> Tensor:
+    """Same Python MT19937 stream as the reference (core.py:333-341), so a
+    seeded Dense gets bit-identical initial weights."""
+    if rng is None:
+        rng = random.Random()
+    elif isinstance(rng, int):
+        rng = random.Random(rng)
+    shape = _check_shape(shape)
+    vals = [rng.uniform(low, high) for _ in range(_numel(shape))]
+    return from_flat(vals, shape, requires_grad=requires_grad)
+
+
+class _Scalar:
+    """A Python number operand: f32-rounded like tensor(float(x))
+    (core.py:352-357), passed to kernels by value instead of being uploaded."""
+
+    __slots__ = ("value",)
+    shape = ()
+    requires_grad = False
+
+    def __init__(self, v):
+        self.value = float(np.float32(v))
+
+
+def _as_operand(x):
+    if isinstance(x, (Tensor, _Scalar)):
+        return x
+    if isinstance(x, (int, float)) and not isinstance(x, bool) or isinstance(x, (bool, np.floating)):
+        return _Scalar(x)
+    raise TypeError(f"expected a Tensor or number, got {type(x).__name__}")
+
+
+def _as_tensor(x) -> Tensor:
+    if isinstance(x, Tensor):
+        return x
+    if isinstance(x, _Scalar):
+        return full((), x.value)
+    if isinstance(x, (int, float)):
+        return full((), float(x))
+    raise TypeError(f"expected a Tensor or number, got {type(x).__name__}")
+
+
+# ---------------------------------------------------------------------------
+# broadcasting (core.py:364-423)
+
+
+def broadcast_shapes(s1, s2):
+    n1, n2 = len(s1), len(s2)
+    n = _py_max(n1, n2)
+    out = []
+    for i in range(n):
+        a = s1[n1 - n + i] if n1 - n + i >= 0 else 1
+        b = s2[n2 - n + i] if n2 - n + i >= 0 else 1
+        if a == b or b == 1:
+            out.append(a)
+        elif a == 1:
+            out.append(b)
+        else:
+            raise BroadcastError(f"cannot broadcast {tuple(s1)} with {tuple(s2)}")
+    return tuple(out)
+
+
+def _expand_strides(t, shape):
+    pad = len(shape) - t.ndim
+    st = [0] * len(shape)
+    for i in range(t.ndim):
+        if t.shape[i] == shape[pad + i]:
+            st[pad + i] = t.strides[i]
+        elif t.shape[i] == 1:
+            st[pad + i] = 0
+        else:
+            raise BroadcastError(f"cannot expand {t.shape} to {tuple(shape)}")
+    return tuple(st)
+
+
+def _expand_view(t: Tensor, shape) -> Tensor:
+    return Tensor(t.buffer, shape, _expand_strides(t, shape), t.offset,
+                  requires_grad=t.requires_grad)
+
+
+def broadcast_to(x: Tensor, shape) -> Tensor:
+    shape = _check_shape(shape)
+    if len(shape) < x.ndim:
+        raise BroadcastError(f"cannot broadcast {x.shape} to smaller rank {shape}")
+    v = _expand_view(x, shape)
+    out = Tensor(v.buffer, v.shape, v.strides, v.offset)
+    return record("broadcast_to", (x,), out, (lambda g: reduce_to_shape(g, x.shape),))
+
+
+def reduce_to_shape(t: Tensor, shape) -> Tensor:
+    """Sum t down to `shape` (adjoint of broadcasting; core.py:405-423)."""
+    shape = _check_shape(shape)
+    if t.shape == shape:
+        return t
+    pad = t.ndim - len(shape)
+    if pad < 0:
+        raise ShapeError(f"cannot reduce {t.shape} to larger rank {shape}")
+    padded = (1,) * pad + shape
+    axes = []
+    for i, (have, want) in enumerate(zip(t.shape, padded)):
+        if want == have:
+            continue
+        if want == 1:
+            axes.append(i)
+        else:
+            raise ShapeError(f"{shape} is not a broadcast source of {t.shape}")
+    out = sum(t, axis=tuple(axes), keepdims=True) if axes else t
+    return reshape(out, shape)
+
+
+# ---------------------------------------------------------------------------
+# elementwise (core.py:430-546)
+
+
+def _launch_binary(op, a, b, shape) -> Tensor:
+    out = _empty(shape)
+    if out.size == 0:
+        return out
+    nd = len(shape)
+    if isinstance(a, _Scalar) or isinstance(b, _Scalar):
+        if isinstance(a, _Scalar) and isinstance(b, _Scalar):
+            a = full((), a.value)
+        if isinstance(b, _Scalar):
+            L.call("b2_binary_scalar", op, out.data_ptr, nd, L.i64s(shape), a.data_ptr,
+                   L.i64s(_expand_strides(a, shape)), b.value, 0, None)
+        else:
+            L.call("b2_binary_scalar", op, out.data_ptr, nd, L.i64s(shape), b.data_ptr,
+                   L.i64s(_expand_strides(b, shape)), a.value, 1, None)
+        return out
+    L.call("b2_binary", op, out.data_ptr, nd, L.i64s(shape), a.data_ptr,
+           L.i64s(_expand_strides(a, shape)), b.data_ptr, L.i64s(_expand_strides(b, shape)), None)
+    return out
+
+
+def _binary(kind, op, a, b, pullbacks, save):
+    a = _as_operand(a)
+    b = _as_operand(b)
+    shape = broadcast_shapes(a.shape, b.shape)
+    out = _launch_binary(op, a, b, shape)
+    pa, pb = pullbacks(a, b, out)
+    saved = tuple(t for t in save(a, b) if isinstance(t, Tensor))
+    return record(kind, (a, b), out, (pa, pb), saved=saved)
+
+
+def add(a, b) -> Tensor:
+    return _binary("add", L.ADD, a, b,
+                   lambda a, b, out: (lambda g: reduce_to_shape(g, a.shape),
+                                      lambda g: reduce_to_shape(g, b.shape)),
+                   lambda a, b: ())
+
+
+def sub(a, b) -> Tensor:
+    return _binary("sub", L.SUB, a, b,
+                   lambda a, b, out: (lambda g: reduce_to_shape(g, a.shape),
+                                      lambda g: reduce_to_shape(neg(g), b.shape)),
+                   lambda a, b: ())
+
+
+def mul(a, b) -> Tensor:
+    return _binary("mul", L.MUL, a, b,
+                   lambda a, b, out: (lambda g: reduce_to_shape(mul(g, b), a.shape),
+                                      lambda g: reduce_to_shape(mul(g, a), b.shape)),
+                   lambda a, b: (a, b))
+
+
+def div(a, b) -> Tensor:
+    return _binary("div", L.DIV, a, b,
+                   lambda a, b, out: (
+                       lambda g: reduce_to_shape(div(g, b), a.shape),
+                       # d(a/b)/db = -a/b^2, composed exactly like core.py:492
+                       lambda g: reduce_to_shape(neg(div(mul(g, a), mul(b, b))), b.shape)),
+                   lambda a, b: (a, b))
+
+
+def _launch_unary(op, x, alpha=0.0, beta=0.0) -> Tensor:
+    out = _empty(x.shape)
+    if out.size:
+        L.call("b2_unary", op, out.data_ptr, x.ndim, L.i64s(x.shape), x.data_ptr,
+               L.i64s(x.strides), float(alpha), float(beta), None)
+    return out
+
+
+def _unary(kind, op, x, pullback, save):
+    x = _as_tensor(_as_operand(x))
+    out = _launch_unary(op, x)
+    return record(kind, (x,), out, (pullback(x, out),), saved=save(x, out))
+
+
+def neg(x) -> Tensor:
+    return _unary("neg", L.NEG, x, lambda x, out: lambda g: neg(g), lambda x, out: ())
+
+
+def exp(x) -> Tensor:
+    return _unary("exp", L.EXP, x, lambda x, out: lambda g: mul(g, out), lambda x, out: (out,))
+
+
+def log(x) -> Tensor:
+    return _unary("log", L.LOG, x, lambda x, out: lambda g: div(g, x), lambda x, out: (x,))
+
+
+def sqrt(x) -> Tensor:
+    return _unary("sqrt", L.SQRT, x, lambda x, out: lambda g: div(g, mul(out, 2.0)),
+                  lambda x, out: (out,))
+
+
+def _sign_mul(g, x):
+    shape = broadcast_shapes(g.shape, x.shape)
+    return _launch_binary(L.SIGN_MUL, g, x, shape)
+
+
+def absolute(x) -> Tensor:
+    return _unary("abs", L.ABS, x, lambda x, out: lambda g: _sign_mul(g, x), lambda x, out: (x,))
+
+
+abs_ = absolute
+
+
+def relu(x) -> Tensor:
+    """nn.relu (nn.py:108-111): v if v > 0 else 0.0; grad mask v > 0."""
+    x = _as_tensor(_as_operand(x))
+    out = _launch_unary(L.RELU, x)
+
+    def pull(g):
+        return _launch_binary(L.RELU_BWD, g, x, broadcast_shapes(g.shape, x.shape))
+
+    return record("relu", (x,), out, (pull,), saved=(x,))
+
+
+def clamp(x, low, high) -> Tensor:
+    """min(max(x, low), high). Not a reference op (the BASELINE config-2 clamp
+    happens on the host there); gradient passes where low<=x<=high."""
+    x = _as_tensor(_as_operand(x))
+    out = _launch_unary(L.CLAMP, x, low, high)
+
+    def pull(g):
+        inside = _launch_unary(L.CLAMP_MASK, x, low, high)
+        return _launch_binary(L.RELU_BWD, g, inside, broadcast_shapes(g.shape, x.shape))
+
+    return record("clamp", (x,), out, (pull,), saved=(x,))
+
+
+# ---------------------------------------------------------------------------
+# reductions (core.py:556-728)
+
+
+def _normalize_axes(axis, ndim):
+    if axis is None:
+        return tuple(range(ndim))
+    if isinstance(axis, (int, np.integer)):
+        axis = (int(axis),)
+    axes = []
+    for a in axis:
+        if not isinstance(a, (int, np.integer)):
+            raise ShapeError(f"axis must be an int, got {a!r}")
+        a = int(a)
+        if a < 0:
+            a += ndim
+        if not 0 <= a < ndim:
+            raise ShapeError(f"axis {a} out of range for {ndim}-d tensor")
+        axes.append(a)
+    if len(set(axes)) != len(axes):
+        raise ShapeError(f"duplicate axes in {axis}")
+    return tuple(sorted(axes))
+
+
+def _reduced_shapes(shape, axes, keepdims):
+    kshape = tuple(1 if i in axes else s for i, s in enumerate(shape))
+    oshape = kshape if keepdims else tuple(s for i, s in enumerate(shape) if i not in axes)
+    return kshape, oshape
+
+
+def _mask(axes):
+    m = 0
+    for a in axes:
+        m |= 1 << a
+    return m
+
+
+def _reduce(op, x, axes, oshape, want_arg=False):
+    out = _empty(oshape)
+    arg = None
+    if want_arg:
+        arg = Buffer(8 * _py_max(out.size, 1))
+    if x.ndim == 0:
+        L.call("b2_copy_strided", out.data_ptr, 0, L.i64s(()), x.data_ptr, L.i64s(()), None)
+        if arg is not None:
+            L.call("b2_fill_f32", arg.ptr, 0.0, 2, None)  # int64 zero
+        return out, arg
+    L.call("b2_reduce", op, out.data_ptr, arg.ptr if arg else None, x.ndim, L.i64s(x.shape),
+           x.data_ptr, L.i64s(x.strides), _mask(axes), None)
+    return out, arg
+
+
+def _sum_pullback(x, axes, kshape):
+    def pull(g):
+        g = reshape(g, kshape)
+        return _copy_contig(_expand_view(g, x.shape))
+
+    return pull
+
+
+def sum(x, axis=None, keepdims=False) -> Tensor:
+    x = _as_tensor(_as_operand(x))
+    axes = _normalize_axes(axis, x.ndim)
+    kshape, oshape = _reduced_shapes(x.shape, axes, keepdims)
+    out, _ = _reduce(L.RED_SUM, x, axes, oshape)
+    return record("sum", (x,), out, (_sum_pullback(x, axes, kshape),))
+
+
+def mean(x, axis=None, keepdims=False) -> Tensor:
+    x = _as_tensor(_as_operand(x))
+    axes = _normalize_axes(axis, x.ndim)
+    kshape, oshape = _reduced_shapes(x.shape, axes, keepdims)
+    count = 1
+    for a in axes:
+        count *= x.shape[a]
+    if len(axes) == x.ndim and x.ndim > 0:
+        oshape = kshape if keepdims else ()
+    out, _ = _reduce(L.RED_MEAN, x, axes, oshape)
+    fcount = _Scalar(float(count))
+
+    def pull(g):
+        # div(expand(g), float(count)) in one pass (the expand copy is exact)
+        gk = reshape(g, kshape)
+        res = _empty(x.shape)
+        if res.size:
+            L.call("b2_binary_scalar", L.DIV, res.data_ptr, x.ndim, L.i64s(x.shape), gk.data_ptr,
+                   L.i64s(_expand_strides(gk, x.shape)), fcount.value, 0, None)
+        return res
+
+    return record("mean", (x,), out, (pull,))
+
+
+def max(x, axis=None, keepdims=False) -> Tensor:
+    """Maximum over axes; ties resolve to the first element in row-major
+    order, which is also where the gradient goes (core.py:692-728)."""
+    x = _as_tensor(_as_operand(x))
+    axes = _normalize_axes(axis, x.ndim)
+    kshape, oshape = _reduced_shapes(x.shape, axes, keepdims)
+    for a in axes:
+        if x.shape[a] == 0:
+            raise ShapeError("max over a zero-extent axis is undefined")
+    out, arg = _reduce(L.RED_MAX, x, axes, oshape, want_arg=True)
+    in_shape = x.shape
+    mask = _mask(axes)
+
+    def pull(g):
+        gc = g if g.is_contiguous else _copy_contig(g)
+        gx = _empty(in_shape)
+        if gx.size:
+            L.call("b2_max_scatter", gx.data_ptr, len(in_shape), L.i64s(in_shape), mask,
+                   gc.data_ptr, arg.ptr, None)
+        return gx
+
+    return record("max", (x,), out, (pull,), saved=(x,))
+
+
+# ---------------------------------------------------------------------------
+# shape ops (core.py:735-761)
+
+
+def reshape(x, shape) -> Tensor:
+    x = _as_tensor(_as_operand(x))
+    shape = list(shape) if not isinstance(shape, int) else [shape]
+    if shape.count(-1) > 1:
+        raise ShapeError("at most one -1 allowed in reshape")
+    if -1 in shape:
+        rest = _numel([s for s in shape if s != -1])
+        if rest == 0 or x.size % rest:
+            raise ShapeError(f"cannot infer -1 reshaping {x.shape} to {tuple(shape)}")
+        shape[shape.index(-1)] = x.size // rest
+    shape = _check_shape(shape)
+    if _numel(shape) != x.size:
+        raise ShapeError(f"cannot reshape {x.shape} ({x.size} elements) to {shape}")
+    if x.ndim == 0 or x.is_contiguous:
+        out = Tensor(x.buffer, shape, offset=x.offset)
+    else:
+        c = _copy_contig(x)
+        out = Tensor(c.buffer, shape)
+    old = x.shape
+    return record("reshape", (x,), out, (lambda g: reshape(g, old),))
+
+
+def transpose2d(x) -> Tensor:
+    x = _as_tensor(_as_operand(x))
+    if x.ndim != 2:
+        raise ShapeError(f"transpose2d needs a 2-d tensor, got shape {x.shape}")
+    out = Tensor(x.buffer, (x.shape[1], x.shape[0]), (x.strides[1], x.strides[0]), x.offset)
+    return record("transpose2d", (x,), out, (lambda g: transpose2d(g),))
+
+
+# ---------------------------------------------------------------------------
+# matrix product (core.py:768-820)
+
+
+def _as_A(t):
+    """Operand with logical shape (M, K) -> (trans, ld, tensor)."""
+    M, K = t.shape
+    s0, s1 = t.strides
+    if (s1 == 1 or K <= 1) and (M <= 1 or s0 >= K):
+        return 0, (s0 if M > 1 else K), t
+    if (s0 == 1 or M <= 1) and (K <= 1 or s1 >= M):
+        return 1, (s1 if K > 1 else M), t
+    c = _copy_contig(t)
+    return 0, K, c
+
+
+def _as_B(t):
+    """Operand with logical shape (N, K) (the reference's w) -> (trans_b, ld, tensor).
+    trans_b=1: stored [N, K] row-major; trans_b=0: stored [K, N]."""
+    N, K = t.shape
+    s0, s1 = t.strides
+    if (s1 == 1 or K <= 1) and (N <= 1 or s0 >= K):
+        return 1, (s0 if N > 1 else K), t
+    if (s0 == 1 or N <= 1) and (K <= 1 or s1 >= N):
+        return 0, (s1 if K > 1 else N), t
+    c = _copy_contig(t)
+    return 1, K, c
+
+
+def _split(t, rows, cols, ld):
+    """Cached (hi, lo) 3xTF32 split of the stored matrix region of t."""
+    buf = t.buffer
+    key = (t.offset, rows, cols, ld)
+    if buf._splits is None:
+        buf._splits = {}
+    ent = buf._splits.get(key)
+    if ent is not None and ent[0] == buf.version:
+        return ent[1], ent[2]
+    n = rows * cols
+    hi, lo = Buffer(4 * n), Buffer(4 * n)
+    L.call("b2_tf32_split", hi.ptr, lo.ptr, t.data_ptr, rows, cols, ld, None)
+    buf._splits[key] = (buf.version, hi, lo)
+    return hi, lo
+
+
+_ALGO_OVERRIDE = None
+
+
+def set_gemm_algo(name):
+    """Force 'simt' | '3xtf32' | '1xtf32' | None (auto) for subsequent matmuls."""
+    global _ALGO_OVERRIDE
+    _ALGO_OVERRIDE = {None: None, "auto": None, "simt": L.GEMM_SIMT, "3xtf32": L.GEMM_3XTF32,
+                      "1xtf32": L.GEMM_1XTF32}[name]
+
+
+def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE):
+    """out[M,N] = x[M,K] . w[N,K]^T (+bias)(relu); x, w arbitrary 2-D views."""
+    M, K = x.shape
+    N = w.shape[0]
+    ta, lda, xa = _as_A(x)
+    tb, ldb, wb = _as_B(w)
+    algo = _ALGO_OVERRIDE
+    if algo is None:
+        sel = ctypes.c_int()
+        L.check(L.lib().b2_gemm_select(ta, tb, M, N, K, lda, ldb, ctypes.byref(sel)))
+        algo = sel.value
+    bptr = bias.data_ptr if bias is not None else None
+    if algo == L.GEMM_3XTF32 and K > 0 and (M if ta else K) % 4 == 0 and (K if tb else N) % 4 == 0 \
+            and lda % 4 == 0 and ldb % 4 == 0:
+        ar, ac = (K, M) if ta else (M, K)
+        br, bc = (N, K) if tb else (K, N)
+        ahi, alo = _split(xa, ar, ac, lda)
+        bhi, blo = _split(wb, br, bc, ldb)
+        L.call("b2_gemm_presplit", ta, tb, M, N, K, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr,
+               out.data_ptr, N, bptr, epi, None)
+    else:
+        if algo == L.GEMM_3XTF32:
+            algo = L.GEMM_SIMT
+        L.call("b2_gemm", ta, tb, M, N, K, xa.data_ptr, lda, wb.data_ptr, ldb, out.data_ptr, N,
+               bptr, epi, algo, None)
+    return out
+
+
+def matmul(x, w) -> Tensor:
+    """y = x @ w^T: (m, k) with (d, k) gives (m, d) (core.py:784-820)."""
+    x = _as_tensor(_as_operand(x))
+    w = _as_tensor(_as_operand(w))
+    if x.ndim != 2 or w.ndim != 2:
+        raise ShapeError(f"matmul needs 2-d tensors, got {x.shape} and {w.shape}")
+    m, k = x.shape
+    d, k2 = w.shape
+    if k != k2:
+        raise ShapeError(f"inner dimensions differ: {x.shape} vs {w.shape}")
+    out = _empty((m, d))
+    if out.size:
+        _gemm_into(out, x, w)
+    return record("matmul", (x, w), out,
+                  (lambda g: matmul(g, transpose2d(w)),               # x_bar = g w
+                   lambda g: matmul(transpose2d(g), transpose2d(x))),  # w_bar = g^T x
+                  saved=(x, w))
+
+
+def mm(a, b) -> Tensor:
+    """PyTorch-convention product a @ b for a (..., k) and b (k, n): the
+    reference's matmul(a, transpose2d(b)) with leading dims flattened
+    (rank-3 matmul via reshape)."""
+    a = _as_tensor(_as_operand(a))
+    b = _as_tensor(_as_operand(b))
+    if b.ndim != 2 or a.ndim < 2:
+        raise ShapeError(f"mm needs (..., k) @ (k, n), got {a.shape} and {b.shape}")
+    lead = a.shape[:-1]
+    a2 = reshape(a, (-1, a.shape[-1])) if a.ndim > 2 else a
+    y = matmul(a2, transpose2d(b))
+    return reshape(y, lead + (b.shape[1],)) if a.ndim > 2 else y
+
+
+def linear(x, weight, bias=None, relu_out=False) -> Tensor:
+    """Fused Dense forward: relu?(x @ W^T + b) in ONE tcgen05 GEMM whose
+    epilogue adds the bias and applies the ReLU. Values are bit-identical to
+    the reference's add(matmul(x, W), b) then relu (nn.py:78-82, 108-111):
+    f32(f32(acc) + b) then v > 0 ? v : 0. One tape node; its pullback applies
+    the ReLU mask once and feeds the NN (x_bar), TN (W_bar) GEMMs and the
+    bias column sum, exactly the cotangents of the composed ops."""
+    x = _as_tensor(_as_operand(x))
+    if x.ndim != 2 or weight.ndim != 2:
+        raise ShapeError(f"matmul needs 2-d tensors, got {x.shape} and {weight.shape}")
+    m, k = x.shape
+    d, k2 = weight.shape
+    if k != k2:
+        raise ShapeError(f"inner dimensions differ: {x.shape} vs {weight.shape}")
+    if bias is not None and bias.shape != (d,):
+        raise BroadcastError(f"cannot broadcast {(m, d)} with {bias.shape}")
+    out = _empty((m, d))
+    if out.size:
+        epi = (L.EPI_BIAS_RELU if relu_out else L.EPI_BIAS) if bias is not None else \
+            (L.EPI_RELU if relu_out else L.EPI_NONE)
+        bc = bias if (bias is None or bias.is_contiguous) else _copy_contig(bias)
+        _gemm_into(out, x, weight, bc, epi)
+    memo = [None, None]
+
+    def pre(g):  # cotangent at the pre-activation (relu pullback, nn.py:101-103)
+        if not relu_out:
+            return g
+        if memo[0] is not g:
+            memo[0] = g
+            memo[1] = _launch_binary(L.RELU_BWD, g, out, out.shape)
+        return memo[1]
+
+    pulls = [lambda g: matmul(pre(g), transpose2d(weight)),
+             lambda g: matmul(transpose2d(pre(g)), transpose2d(x))]
+    inputs = [x, weight]
+    if bias is not None:
+        inputs.append(bias)
+        pulls.append(lambda g: reduce_to_shape(pre(g), bias.shape))
+    return record("linear_relu" if relu_out else "linear", tuple(inputs), out, tuple(pulls),
+                  saved=(x, weight, out) if relu_out else (x, weight))
+
+
+# ---------------------------------------------------------------------------
+# fused / row-wise ops
+
+
+def softmax(x, axis=-1) -> Tensor:
+    """Row softmax over the last axis, bit-identical to the reference
+    composition with the max detached; one kernel each way."""
+    x = _as_tensor(_as_operand(x))
+    if x.ndim == 0:
+        raise ShapeError("softmax needs at least one axis")
+    ax = _normalize_axes(axis, x.ndim)
+    if ax != (x.ndim - 1,):
+        raise ShapeError("softmax is implemented over the last axis")
+    xc = x if x.is_contiguous else _copy_contig(x)
+    C = x.shape[-1]
+    R = x.size // C if C else 0
+    y = _empty(x.shape)
+    rs, rm = Buffer(4 * _py_max(R, 1)), Buffer(4 * _py_max(R, 1))
+    if y.size:
+        L.call("b2_softmax_fwd", y.data_ptr, rs.ptr, rm.ptr, xc.data_ptr, R, C, None)
+
+    def pull(g):
+        gc = g if g.is_contiguous else _copy_contig(g)
+        gz = _empty(x.shape)
+        if gz.size:
+            L.call("b2_softmax_bwd", gz.data_ptr, gc.data_ptr, xc.data_ptr, rs.ptr, rm.ptr, R, C,
+                   None)
+        return gz
+
+    return record("softmax", (x,), y, (pull,), saved=(xc,))
+
+
+def fused_muladd_relu(a, b, c=None) -> Tensor:
+    """relu(a*b + c) for a (R, C) and row vectors b, c of length C in one pass
+    (the BASELINE config-2 chain, core.py:453-483 + nn.py:108-111); c defaults
+    to b. One tape node whose pullback is the composed reference pullback in
+    GradStore order (autograd.py:140-145), so gradients are bit-identical."""
+    if c is None:
+        c = b
+    if a.ndim != 2 or b.size != a.shape[1] or c.size != a.shape[1]:
+        raise ShapeError("fused_muladd_relu expects a (R, C) with row vectors of length C")
+    R, C = a.shape
+    if not (a.is_contiguous and b.is_contiguous and c.is_contiguous) or C % 4:
+        return relu(add(mul(a, b), c))
+    y = _empty(a.shape)
+    L.call("b2_fused_muladd_relu_fwd", y.data_ptr, a.data_ptr, b.data_ptr, c.data_ptr, R, C, None)
+    memo = [None, None]
+
+    def pre(g):
+        if memo[0] is not g:
+            memo[0], memo[1] = g, _launch_binary(L.RELU_BWD, g, y, y.shape)
+        return memo[1]
+
+    if c is b:
+        return record("muladd_relu", (a, b), y,
+                      (lambda g: mul(pre(g), b),
+                       lambda g: add(reduce_to_shape(pre(g), b.shape),
+                                     reduce_to_shape(mul(pre(g), a), b.shape))),
+                      saved=(a, b))
+    return record("muladd_relu", (a, b, c), y,
+                  (lambda g: mul(pre(g), b),
+                   lambda g: reduce_to_shape(mul(pre(g), a), b.shape),
+                   lambda g: reduce_to_shape(pre(g), c.shape)), saved=(a, b, c))
+
+
+def muladd_relu_sum_grads(a, b):
+    """Gradients of sum(relu(a*b + b)) w.r.t. a (R, C) and b (C,) / (1, C) in
+    ONE pass over a (fused op+grad kernel): ga = f32(mask*b) and
+    gb = f32(count) + f32(sum64(mask*a)) in GradStore order. Bit-identical to
+    backward(sum(relu(add(mul(a, b), b)))) on the reference."""
+    R, C = a.shape
+    ga = _empty(a.shape)
+    gb = _empty(b.shape)
+    L.call("b2_fused_muladd_relu_bwd", ga.data_ptr, gb.data_ptr, a.data_ptr, b.data_ptr, R, C, None)
+    return ga, gb

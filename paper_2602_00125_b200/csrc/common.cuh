@@ -1,0 +1,58 @@
+// Shared plumbing for libb2: error capture, streams, launch accounting.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <atomic>
+#include <string>
+
+#include "../../include/b2.h"
+
+namespace b2 {
+
+void set_error(const std::string& msg);
+int fail(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+cudaStream_t resolve(void* stream);
+int sm_count();
+int ensure_init();
+extern std::atomic<uint64_t> g_launches;
+
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// check a launch, count it, map errors to a status
+inline int launched(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  count_launch();
+  return 0;
+}
+
+// grid sizing: a multiple of the SM count (148 on B200) x resident CTAs
+inline int grid_for(int64_t work_items, int per_cta, int ctas_per_sm = 4) {
+  int64_t need = (work_items + per_cta - 1) / per_cta;
+  int64_t cap = (int64_t)sm_count() * ctas_per_sm;
+  if (need < 1) need = 1;
+  return (int)(need < cap ? need : cap);
+}
+
+}  // namespace b2
+
+#define B2_TRY(expr)                      \
+  do {                                    \
+    int _rc = (expr);                     \
+    if (_rc != 0) return _rc;             \
+  } while (0)
+
+#define B2_CUDA(expr)                                  \
+  do {                                                 \
+    cudaError_t _e = (expr);                           \
+    if (_e != cudaSuccess) return b2::cuda_fail(_e, #expr); \
+  } while (0)
+
+// Collapsed N-d iteration descriptor (dims merged where strides allow).
+struct B2Shape {
+  int ndim;
+  int64_t shape[B2_MAX_DIMS];
+  int64_t st[3][B2_MAX_DIMS];  // up to 3 operands (out + 2 inputs)
+};

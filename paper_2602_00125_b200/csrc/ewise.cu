@@ -1,0 +1,608 @@
+// Broadcasting / strided elementwise engine.
+//
+// Replaces tensorlite/core.py:430-546 (_elementwise/_binary/_unary) and the
+// pointwise activations of nn.py:95-111. Semantics: every result is the
+// IEEE fp32 op, which equals the reference's f32(double op) for + - * /
+// (double rounding is innocuous since 53 >= 2*24+2); exp/log are computed as
+// f32(double libm) exactly like the reference. No FMA contraction anywhere in
+// this file (explicit __f*_rn intrinsics, and the TU is built -fmad=false).
+//
+// Layout strategy (HBM-bound; index math hoisted per row, never per element):
+//  * shapes/strides are collapsed on the host (adjacent dims merged when every
+//    operand is contiguous across them, size-1 dims dropped);
+//  * 1-D result  -> flat grid-stride kernel, 128-bit loads/stores;
+//  * N-D result  -> "rows" kernel: rows = product of outer dims, the row base
+//    offset of each operand is computed once per row, the innermost dim is
+//    walked with float4 when its stride is 1 and rows are 16-B aligned, a
+//    stride-0 operand is a register broadcast.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+struct Nd {
+  int ndim;  // collapsed rank (>= 1)
+  int64_t shape[B2_MAX_DIMS];
+  int64_t st[3][B2_MAX_DIMS];  // [0]=out (contiguous), [1]=a, [2]=b
+};
+
+// merge dims and drop size-1 axes; nops operands (out first)
+Nd collapse(int ndim, const int64_t* shape, int nops, const int64_t* const* strides) {
+  Nd r;
+  r.ndim = 0;
+  for (int d = 0; d < ndim; ++d) {
+    if (shape[d] == 1) continue;
+    int k = r.ndim;
+    if (k > 0) {
+      bool merge = true;
+      for (int o = 0; o < nops; ++o)
+        if (r.st[o][k - 1] != strides[o][d] * shape[d]) merge = false;
+      if (merge) {
+        r.shape[k - 1] *= shape[d];
+        for (int o = 0; o < nops; ++o) r.st[o][k - 1] = strides[o][d];
+        continue;
+      }
+    }
+    r.shape[k] = shape[d];
+    for (int o = 0; o < nops; ++o) r.st[o][k] = strides[o][d];
+    r.ndim++;
+  }
+  if (r.ndim == 0) {
+    r.ndim = 1;
+    r.shape[0] = 1;
+    for (int o = 0; o < nops; ++o) r.st[o][0] = 1;
+  }
+  return r;
+}
+
+void contig_strides(int ndim, const int64_t* shape, int64_t* st) {
+  int64_t acc = 1;
+  for (int d = ndim - 1; d >= 0; --d) {
+    st[d] = acc;
+    acc *= shape[d];
+  }
+}
+
+int64_t numel(int ndim, const int64_t* shape) {
+  int64_t n = 1;
+  for (int d = 0; d < ndim; ++d) n *= shape[d];
+  return n;
+}
+
+// ------------------------------------------------------------------ ops
+
+__device__ __forceinline__ float sign_of(float v) {
+  return v > 0.0f ? 1.0f : (v < 0.0f ? -1.0f : 0.0f);  // core.py:533-538
+}
+
+template <int OP>
+struct Bin {
+  __device__ __forceinline__ float operator()(float a, float b) const {
+    if constexpr (OP == B2_ADD) return __fadd_rn(a, b);
+    if constexpr (OP == B2_SUB) return __fsub_rn(a, b);
+    if constexpr (OP == B2_MUL) return __fmul_rn(a, b);
+    if constexpr (OP == B2_DIV) return __fdiv_rn(a, b);
+    if constexpr (OP == B2_RELU_BWD) return __fmul_rn(a, b > 0.0f ? 1.0f : 0.0f);
+    if constexpr (OP == B2_SIGN_MUL) return __fmul_rn(a, sign_of(b));
+    return 0.0f;
+  }
+};
+
+template <int OP>
+struct Un {
+  double alpha, beta;
+  __device__ __forceinline__ float operator()(float x) const {
+    if constexpr (OP == B2_NEG) return -x;
+    if constexpr (OP == B2_EXP) return __double2float_rn(exp((double)x));
+    if constexpr (OP == B2_LOG) return __double2float_rn(log((double)x));
+    if constexpr (OP == B2_SQRT) return __fsqrt_rn(x);
+    if constexpr (OP == B2_ABS) return fabsf(x);
+    if constexpr (OP == B2_RELU) return x > 0.0f ? x : 0.0f;  // nn.py:110
+    if constexpr (OP == B2_RELU_MASK) return x > 0.0f ? 1.0f : 0.0f;
+    if constexpr (OP == B2_COPY) return x;
+    if constexpr (OP == B2_CLAMP) return fminf(fmaxf(x, (float)alpha), (float)beta);
+    if constexpr (OP == B2_SCALE) return __fmul_rn(x, (float)alpha);
+    if constexpr (OP == B2_DIV_SCALAR) return __fdiv_rn(x, (float)alpha);
+    if constexpr (OP == B2_CLAMP_MASK) return (x >= (float)alpha && x <= (float)beta) ? 1.0f : 0.0f;
+    return x;
+  }
+};
+
+struct Fill {
+  float v;
+  __device__ __forceinline__ float operator()(float) const { return v; }
+};
+
+// binary with one operand replaced by an fp32 scalar
+template <int OP, bool LEFT>
+struct BinScalar {
+  float s;
+  __device__ __forceinline__ float operator()(float x) const {
+    Bin<OP> f;
+    return LEFT ? f(s, x) : f(x, s);
+  }
+};
+
+// ------------------------------------------------------------------ kernels
+
+// flat: out[i] = f(a[i*sa], b[i*sb]); sa, sb in {0, 1}
+template <class F, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_bin_flat(float* __restrict__ out,
+                                                       const float* __restrict__ a,
+                                                       const float* __restrict__ b, int64_t n,
+                                                       int sa, int sb, F f) {
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  if (VEC) {
+    int64_t n4 = n >> 2;
+    float as = a[0], bs = b[0];
+    for (int64_t i = tid; i < n4; i += nth) {
+      float4 va = sa ? reinterpret_cast<const float4*>(a)[i] : make_float4(as, as, as, as);
+      float4 vb = sb ? reinterpret_cast<const float4*>(b)[i] : make_float4(bs, bs, bs, bs);
+      float4 r;
+      r.x = f(va.x, vb.x);
+      r.y = f(va.y, vb.y);
+      r.z = f(va.z, vb.z);
+      r.w = f(va.w, vb.w);
+      reinterpret_cast<float4*>(out)[i] = r;
+    }
+    for (int64_t i = (n4 << 2) + tid; i < n; i += nth) out[i] = f(a[i * sa], b[i * sb]);
+  } else {
+    for (int64_t i = tid; i < n; i += nth) out[i] = f(a[i * sa], b[i * sb]);
+  }
+}
+
+template <class F, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_un_flat(float* __restrict__ out,
+                                                      const float* __restrict__ x, int64_t n,
+                                                      int64_t sx, F f) {
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  if (VEC) {
+    int64_t n4 = n >> 2;
+    for (int64_t i = tid; i < n4; i += nth) {
+      float4 v = reinterpret_cast<const float4*>(x)[i];
+      float4 r;
+      r.x = f(v.x);
+      r.y = f(v.y);
+      r.z = f(v.z);
+      r.w = f(v.w);
+      reinterpret_cast<float4*>(out)[i] = r;
+    }
+    for (int64_t i = (n4 << 2) + tid; i < n; i += nth) out[i] = f(x[i]);
+  } else {
+    for (int64_t i = tid; i < n; i += nth) out[i] = f(x[i * sx]);
+  }
+}
+
+struct RowGeom {
+  int nd;                         // number of OUTER dims (collapsed ndim - 1)
+  int64_t oshape[B2_MAX_DIMS];    // outer dims
+  int64_t ost[3][B2_MAX_DIMS];    // outer strides per operand
+  int64_t inner;                  // innermost extent
+  int64_t ist[3];                 // innermost stride per operand
+  int64_t rows;
+};
+
+__device__ __forceinline__ void row_base(const RowGeom& g, int64_t r, int64_t* base, int nops) {
+  for (int o = 0; o < nops; ++o) base[o] = 0;
+  for (int d = g.nd - 1; d >= 0; --d) {
+    int64_t ext = g.oshape[d];
+    int64_t q = r / ext;
+    int64_t i = r - q * ext;
+    r = q;
+    for (int o = 0; o < nops; ++o) base[o] += i * g.ost[o][d];
+  }
+}
+
+// N-d binary: grid.x strides rows, grid.y splits the inner extent
+template <class F, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_bin_rows(float* __restrict__ out,
+                                                       const float* __restrict__ a,
+                                                       const float* __restrict__ b, RowGeom g,
+                                                       int64_t chunk, F f) {
+  int64_t c0 = blockIdx.y * chunk;
+  int64_t c1 = min(g.inner, c0 + chunk);
+  for (int64_t r = blockIdx.x; r < g.rows; r += gridDim.x) {
+    int64_t base[3];
+    row_base(g, r, base, 3);
+    float* o = out + base[0];
+    const float* pa = a + base[1];
+    const float* pb = b + base[2];
+    if (VEC) {  // ist[0]==1, ist[1],ist[2] in {0,1}, rows 16B aligned, chunk%4==0
+      float as = pa[0], bs = pb[0];
+      for (int64_t c = c0 + 4 * threadIdx.x; c < c1; c += 4 * blockDim.x) {
+        if (c + 3 < c1) {
+          float4 va = g.ist[1] ? *reinterpret_cast<const float4*>(pa + c) : make_float4(as, as, as, as);
+          float4 vb = g.ist[2] ? *reinterpret_cast<const float4*>(pb + c) : make_float4(bs, bs, bs, bs);
+          float4 rr;
+          rr.x = f(va.x, vb.x);
+          rr.y = f(va.y, vb.y);
+          rr.z = f(va.z, vb.z);
+          rr.w = f(va.w, vb.w);
+          *reinterpret_cast<float4*>(o + c) = rr;
+        } else {
+          for (int64_t k = c; k < c1; ++k) o[k] = f(pa[k * g.ist[1]], pb[k * g.ist[2]]);
+        }
+      }
+    } else {
+      for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x)
+        o[c * g.ist[0]] = f(pa[c * g.ist[1]], pb[c * g.ist[2]]);
+    }
+  }
+}
+
+template <class F, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_un_rows(float* __restrict__ out,
+                                                      const float* __restrict__ x, RowGeom g,
+                                                      int64_t chunk, F f) {
+  int64_t c0 = blockIdx.y * chunk;
+  int64_t c1 = min(g.inner, c0 + chunk);
+  for (int64_t r = blockIdx.x; r < g.rows; r += gridDim.x) {
+    int64_t base[3];
+    row_base(g, r, base, 2);
+    float* o = out + base[0];
+    const float* px = x + base[1];
+    if (VEC) {
+      float xs = px[0];
+      for (int64_t c = c0 + 4 * threadIdx.x; c < c1; c += 4 * blockDim.x) {
+        if (c + 3 < c1) {
+          float4 v = g.ist[1] ? *reinterpret_cast<const float4*>(px + c) : make_float4(xs, xs, xs, xs);
+          float4 rr;
+          rr.x = f(v.x);
+          rr.y = f(v.y);
+          rr.z = f(v.z);
+          rr.w = f(v.w);
+          *reinterpret_cast<float4*>(o + c * g.ist[0]) = rr;
+        } else {
+          for (int64_t k = c; k < c1; ++k) o[k * g.ist[0]] = f(px[k * g.ist[1]]);
+        }
+      }
+    } else {
+      for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x)
+        o[c * g.ist[0]] = f(px[c * g.ist[1]]);
+    }
+  }
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+RowGeom make_rows(const Nd& nd, int nops) {
+  RowGeom g;
+  g.nd = nd.ndim - 1;
+  g.rows = 1;
+  for (int d = 0; d < g.nd; ++d) {
+    g.oshape[d] = nd.shape[d];
+    g.rows *= nd.shape[d];
+    for (int o = 0; o < nops; ++o) g.ost[o][d] = nd.st[o][d];
+  }
+  for (int o = nops; o < 3; ++o)
+    for (int d = 0; d < g.nd; ++d) g.ost[o][d] = 0;
+  g.inner = nd.shape[nd.ndim - 1];
+  for (int o = 0; o < 3; ++o) g.ist[o] = o < nops ? nd.st[o][nd.ndim - 1] : 0;
+  return g;
+}
+
+// rows 16B-aligned for every vector operand
+bool rows_vec_ok(const RowGeom& g, const float* const* ptrs, int nops) {
+  for (int o = 0; o < nops; ++o) {
+    if (g.ist[o] != 1 && !(o > 0 && g.ist[o] == 0)) return false;
+    if (g.ist[o] == 1) {
+      if (!aligned16(ptrs[o])) return false;
+      for (int d = 0; d < g.nd; ++d)
+        if (g.ost[o][d] % 4) return false;
+    }
+  }
+  return true;
+}
+
+void rows_grid(const RowGeom& g, dim3* grid, int64_t* chunk) {
+  int target = b2::sm_count() * 8;
+  int64_t gx = std::min<int64_t>(g.rows, target);
+  int64_t gy = 1;
+  if (g.rows < target) {
+    gy = std::max<int64_t>(1, target / std::max<int64_t>(g.rows, 1));
+    gy = std::min<int64_t>(gy, std::max<int64_t>(1, g.inner / (4 * kThreads)));
+  }
+  int64_t ch = (g.inner + gy - 1) / gy;
+  ch = (ch + 3) & ~int64_t(3);
+  gy = (g.inner + ch - 1) / ch;
+  if (gy < 1) gy = 1;
+  *grid = dim3((unsigned)std::max<int64_t>(gx, 1), (unsigned)gy);
+  *chunk = ch;
+}
+
+template <class F>
+int launch_binary(float* out, const Nd& nd, const float* a, const float* b, F f, cudaStream_t st) {
+  int64_t n = 1;
+  for (int d = 0; d < nd.ndim; ++d) n *= nd.shape[d];
+  if (n == 0) return 0;
+  if (nd.ndim == 1 && (nd.st[1][0] == 0 || nd.st[1][0] == 1) && (nd.st[2][0] == 0 || nd.st[2][0] == 1)) {
+    bool vec = aligned16(out) && (nd.st[1][0] == 0 || aligned16(a)) && (nd.st[2][0] == 0 || aligned16(b));
+    int grid = b2::grid_for(n, kThreads * 4 * 4, 8);
+    if (vec)
+      k_bin_flat<F, true><<<grid, kThreads, 0, st>>>(out, a, b, n, (int)nd.st[1][0], (int)nd.st[2][0], f);
+    else
+      k_bin_flat<F, false><<<grid, kThreads, 0, st>>>(out, a, b, n, (int)nd.st[1][0], (int)nd.st[2][0], f);
+    return b2::launched("b2_binary(flat)");
+  }
+  RowGeom g = make_rows(nd, 3);
+  dim3 grid;
+  int64_t chunk;
+  rows_grid(g, &grid, &chunk);
+  const float* ptrs[3] = {out, a, b};
+  if (rows_vec_ok(g, ptrs, 3))
+    k_bin_rows<F, true><<<grid, kThreads, 0, st>>>(out, a, b, g, chunk, f);
+  else
+    k_bin_rows<F, false><<<grid, kThreads, 0, st>>>(out, a, b, g, chunk, f);
+  return b2::launched("b2_binary(rows)");
+}
+
+template <class F>
+int launch_unary(float* out, const Nd& nd, const float* x, F f, cudaStream_t st) {
+  int64_t n = 1;
+  for (int d = 0; d < nd.ndim; ++d) n *= nd.shape[d];
+  if (n == 0) return 0;
+  if (nd.ndim == 1 && nd.st[0][0] == 1) {
+    bool vec = nd.st[1][0] == 1 && aligned16(out) && aligned16(x);
+    int grid = b2::grid_for(n, kThreads * 4 * 4, 8);
+    if (vec)
+      k_un_flat<F, true><<<grid, kThreads, 0, st>>>(out, x, n, 1, f);
+    else
+      k_un_flat<F, false><<<grid, kThreads, 0, st>>>(out, x, n, nd.st[1][0], f);
+    return b2::launched("b2_unary(flat)");
+  }
+  RowGeom g = make_rows(nd, 2);
+  dim3 grid;
+  int64_t chunk;
+  rows_grid(g, &grid, &chunk);
+  const float* ptrs[2] = {out, x};
+  if (rows_vec_ok(g, ptrs, 2))
+    k_un_rows<F, true><<<grid, kThreads, 0, st>>>(out, x, g, chunk, f);
+  else
+    k_un_rows<F, false><<<grid, kThreads, 0, st>>>(out, x, g, chunk, f);
+  return b2::launched("b2_unary(rows)");
+}
+
+int check_nd(int ndim, const int64_t* shape) {
+  if (ndim < 0 || ndim > B2_MAX_DIMS) return b2::fail("rank exceeds B2_MAX_DIMS (8)");
+  for (int d = 0; d < ndim; ++d)
+    if (shape[d] < 0) return b2::fail("negative extent");
+  return 0;
+}
+
+// ------------------------------------------------------------------ fused config-2 chain
+
+// y = relu(f32(f32(a*b) + c)); a:[R,C] contiguous, b,c: [C]
+__global__ void __launch_bounds__(kThreads) k_muladd_relu_fwd(float* __restrict__ y,
+                                                              const float* __restrict__ a,
+                                                              const float* __restrict__ b,
+                                                              const float* __restrict__ c,
+                                                              int64_t rows, int64_t cols) {
+  int64_t c4 = cols >> 2;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float4* pa = reinterpret_cast<const float4*>(a + r * cols);
+    float4* py = reinterpret_cast<float4*>(y + r * cols);
+    for (int64_t j = threadIdx.x; j < c4; j += blockDim.x) {
+      float4 va = pa[j];
+      float4 vb = reinterpret_cast<const float4*>(b)[j];
+      float4 vc = reinterpret_cast<const float4*>(c)[j];
+      float4 o;
+      float q;
+      q = __fadd_rn(__fmul_rn(va.x, vb.x), vc.x); o.x = q > 0.f ? q : 0.f;
+      q = __fadd_rn(__fmul_rn(va.y, vb.y), vc.y); o.y = q > 0.f ? q : 0.f;
+      q = __fadd_rn(__fmul_rn(va.z, vb.z), vc.z); o.z = q > 0.f ? q : 0.f;
+      q = __fadd_rn(__fmul_rn(va.w, vb.w), vc.w); o.w = q > 0.f ? q : 0.f;
+      py[j] = o;
+    }
+  }
+}
+
+// backward of sum(relu(a*b + b)): ga = f32(mask*b); partial column sums of
+// mask*a (fp64) and mask counts per row-split.
+__global__ void __launch_bounds__(kThreads) k_muladd_relu_bwd(float* __restrict__ ga,
+                                                              double* __restrict__ psum,
+                                                              int* __restrict__ pcnt,
+                                                              const float* __restrict__ a,
+                                                              const float* __restrict__ b,
+                                                              int64_t rows, int64_t cols,
+                                                              int64_t rows_per_split) {
+  // grid: x = column block of 4*kThreads columns, y = row split
+  int64_t col = (blockIdx.x * (int64_t)kThreads + threadIdx.x) * 4;
+  int64_t r0 = blockIdx.y * rows_per_split;
+  int64_t r1 = min(rows, r0 + rows_per_split);
+  if (col >= cols) return;
+  float4 vb = *reinterpret_cast<const float4*>(b + col);
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  int n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    float4 va = *reinterpret_cast<const float4*>(a + r * cols + col);
+    float m0 = __fadd_rn(__fmul_rn(va.x, vb.x), vb.x) > 0.f ? 1.f : 0.f;
+    float m1 = __fadd_rn(__fmul_rn(va.y, vb.y), vb.y) > 0.f ? 1.f : 0.f;
+    float m2 = __fadd_rn(__fmul_rn(va.z, vb.z), vb.z) > 0.f ? 1.f : 0.f;
+    float m3 = __fadd_rn(__fmul_rn(va.w, vb.w), vb.w) > 0.f ? 1.f : 0.f;
+    float4 g;
+    g.x = __fmul_rn(m0, vb.x);
+    g.y = __fmul_rn(m1, vb.y);
+    g.z = __fmul_rn(m2, vb.z);
+    g.w = __fmul_rn(m3, vb.w);
+    *reinterpret_cast<float4*>(ga + r * cols + col) = g;
+    s0 += (double)__fmul_rn(m0, va.x);
+    s1 += (double)__fmul_rn(m1, va.y);
+    s2 += (double)__fmul_rn(m2, va.z);
+    s3 += (double)__fmul_rn(m3, va.w);
+    n0 += m0 > 0.f;
+    n1 += m1 > 0.f;
+    n2 += m2 > 0.f;
+    n3 += m3 > 0.f;
+  }
+  int64_t o = blockIdx.y * cols + col;
+  psum[o] = s0; psum[o + 1] = s1; psum[o + 2] = s2; psum[o + 3] = s3;
+  pcnt[o] = n0; pcnt[o + 1] = n1; pcnt[o + 2] = n2; pcnt[o + 3] = n3;
+}
+
+__global__ void k_muladd_relu_bwd_final(float* __restrict__ gb, const double* __restrict__ psum,
+                                        const int* __restrict__ pcnt, int64_t cols, int splits) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  double s = 0;
+  int64_t n = 0;
+  for (int k = 0; k < splits; ++k) {  // fixed order -> deterministic
+    s += psum[k * cols + c];
+    n += pcnt[k * cols + c];
+  }
+  // GradStore: count (add pullback) first, then f32(sum mask*a) (mul pullback)
+  gb[c] = __fadd_rn((float)n, __double2float_rn(s));
+}
+
+}  // namespace
+
+extern "C" {
+
+int b2_fill_f32(float* dst, float v, int64_t n, void* stream) {
+  if (n <= 0) return 0;
+  Nd nd;
+  nd.ndim = 1;
+  nd.shape[0] = n;
+  nd.st[0][0] = 1;
+  nd.st[1][0] = 1;
+  return launch_unary(dst, nd, dst, Fill{v}, b2::resolve(stream));
+}
+
+int b2_binary(int op, float* out, int ndim, const int64_t* shape, const float* a,
+              const int64_t* as, const float* b, const int64_t* bs, void* stream) {
+  B2_TRY(check_nd(ndim, shape));
+  int64_t os[B2_MAX_DIMS];
+  contig_strides(ndim, shape, os);
+  const int64_t* sts[3] = {os, as, bs};
+  Nd nd = collapse(ndim, shape, 3, sts);
+  cudaStream_t st = b2::resolve(stream);
+  switch (op) {
+    case B2_ADD: return launch_binary(out, nd, a, b, Bin<B2_ADD>{}, st);
+    case B2_SUB: return launch_binary(out, nd, a, b, Bin<B2_SUB>{}, st);
+    case B2_MUL: return launch_binary(out, nd, a, b, Bin<B2_MUL>{}, st);
+    case B2_DIV: return launch_binary(out, nd, a, b, Bin<B2_DIV>{}, st);
+    case B2_RELU_BWD: return launch_binary(out, nd, a, b, Bin<B2_RELU_BWD>{}, st);
+    case B2_SIGN_MUL: return launch_binary(out, nd, a, b, Bin<B2_SIGN_MUL>{}, st);
+  }
+  return b2::fail("b2_binary: unknown op");
+}
+
+int b2_binary_scalar(int op, float* out, int ndim, const int64_t* shape, const float* x,
+                     const int64_t* xs, float s, int scalar_left, void* stream) {
+  B2_TRY(check_nd(ndim, shape));
+  int64_t os[B2_MAX_DIMS];
+  contig_strides(ndim, shape, os);
+  const int64_t* sts[2] = {os, xs};
+  Nd nd = collapse(ndim, shape, 2, sts);
+  cudaStream_t st = b2::resolve(stream);
+#define B2_BS(OPC)                                                                     \
+  case OPC:                                                                            \
+    return scalar_left ? launch_unary(out, nd, x, BinScalar<OPC, true>{s}, st)        \
+                       : launch_unary(out, nd, x, BinScalar<OPC, false>{s}, st);
+  switch (op) {
+    B2_BS(B2_ADD)
+    B2_BS(B2_SUB)
+    B2_BS(B2_MUL)
+    B2_BS(B2_DIV)
+    B2_BS(B2_RELU_BWD)
+  }
+#undef B2_BS
+  return b2::fail("b2_binary_scalar: unknown op");
+}
+
+int b2_unary(int op, float* out, int ndim, const int64_t* shape, const float* x,
+             const int64_t* xs, double alpha, double beta, void* stream) {
+  B2_TRY(check_nd(ndim, shape));
+  int64_t os[B2_MAX_DIMS];
+  contig_strides(ndim, shape, os);
+  const int64_t* sts[2] = {os, xs};
+  Nd nd = collapse(ndim, shape, 2, sts);
+  cudaStream_t st = b2::resolve(stream);
+  switch (op) {
+    case B2_NEG: return launch_unary(out, nd, x, Un<B2_NEG>{alpha, beta}, st);
+    case B2_EXP: return launch_unary(out, nd, x, Un<B2_EXP>{alpha, beta}, st);
+    case B2_LOG: return launch_unary(out, nd, x, Un<B2_LOG>{alpha, beta}, st);
+    case B2_SQRT: return launch_unary(out, nd, x, Un<B2_SQRT>{alpha, beta}, st);
+    case B2_ABS: return launch_unary(out, nd, x, Un<B2_ABS>{alpha, beta}, st);
+    case B2_RELU: return launch_unary(out, nd, x, Un<B2_RELU>{alpha, beta}, st);
+    case B2_RELU_MASK: return launch_unary(out, nd, x, Un<B2_RELU_MASK>{alpha, beta}, st);
+    case B2_COPY: return launch_unary(out, nd, x, Un<B2_COPY>{alpha, beta}, st);
+    case B2_CLAMP: return launch_unary(out, nd, x, Un<B2_CLAMP>{alpha, beta}, st);
+    case B2_SCALE: return launch_unary(out, nd, x, Un<B2_SCALE>{alpha, beta}, st);
+    case B2_DIV_SCALAR: return launch_unary(out, nd, x, Un<B2_DIV_SCALAR>{alpha, beta}, st);
+    case B2_CLAMP_MASK: return launch_unary(out, nd, x, Un<B2_CLAMP_MASK>{alpha, beta}, st);
+  }
+  return b2::fail("b2_unary: unknown op");
+}
+
+int b2_copy_strided(float* out, int ndim, const int64_t* shape, const float* x,
+                    const int64_t* xs, void* stream) {
+  return b2_unary(B2_COPY, out, ndim, shape, x, xs, 0.0, 0.0, stream);
+}
+
+int b2_write_strided(float* dst, int ndim, const int64_t* shape, const int64_t* ds,
+                     const float* src, void* stream) {
+  B2_TRY(check_nd(ndim, shape));
+  int64_t ss[B2_MAX_DIMS];
+  contig_strides(ndim, shape, ss);
+  const int64_t* sts[2] = {ds, ss};
+  Nd nd = collapse(ndim, shape, 2, sts);
+  int64_t n = numel(ndim, shape);
+  if (n == 0) return 0;
+  RowGeom g = make_rows(nd, 2);
+  dim3 grid;
+  int64_t chunk;
+  rows_grid(g, &grid, &chunk);
+  k_un_rows<Un<B2_COPY>, false><<<grid, kThreads, 0, b2::resolve(stream)>>>(dst, src, g, chunk,
+                                                                              Un<B2_COPY>{0, 0});
+  return b2::launched("b2_write_strided");
+}
+
+int b2_fused_muladd_relu_fwd(float* y, const float* a, const float* b, const float* c,
+                             int64_t rows, int64_t cols, void* stream) {
+  if (rows * cols == 0) return 0;
+  if (cols % 4 || !aligned16(a) || !aligned16(b) || !aligned16(c) || !aligned16(y))
+    return b2::fail("b2_fused_muladd_relu_fwd: needs cols%4==0 and 16-B aligned rows");
+  int grid = (int)std::min<int64_t>(rows, b2::sm_count() * 8);
+  k_muladd_relu_fwd<<<grid, kThreads, 0, b2::resolve(stream)>>>(y, a, b, c, rows, cols);
+  return b2::launched("b2_fused_muladd_relu_fwd");
+}
+
+int b2_fused_muladd_relu_bwd(float* ga, float* gb, const float* a, const float* b,
+                             int64_t rows, int64_t cols, void* stream) {
+  if (cols == 0) return 0;
+  if (cols % 4 || !aligned16(a) || !aligned16(b) || !aligned16(ga))
+    return b2::fail("b2_fused_muladd_relu_bwd: needs cols%4==0 and 16-B aligned rows");
+  cudaStream_t st = b2::resolve(stream);
+  int64_t colblocks = (cols + 4 * kThreads - 1) / (4 * kThreads);
+  int64_t splits = std::max<int64_t>(1, (b2::sm_count() * 4) / colblocks);
+  splits = std::min<int64_t>(splits, std::max<int64_t>(rows, 1));
+  int64_t rps = (rows + splits - 1) / splits;
+  if (rps == 0) rps = 1;
+  splits = std::max<int64_t>(1, (rows + rps - 1) / rps);
+  void* ws = nullptr;
+  size_t bytes = (size_t)splits * cols * (sizeof(double) + sizeof(int));
+  B2_TRY(b2_alloc(bytes, stream, &ws));
+  double* psum = (double*)ws;
+  int* pcnt = (int*)(psum + splits * cols);
+  dim3 grid((unsigned)colblocks, (unsigned)splits);
+  k_muladd_relu_bwd<<<grid, kThreads, 0, st>>>(ga, psum, pcnt, a, b, rows, cols, rps);
+  int rc = b2::launched("b2_fused_muladd_relu_bwd");
+  if (!rc) {
+    k_muladd_relu_bwd_final<<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(gb, psum, pcnt, cols,
+                                                                           (int)splits);
+    rc = b2::launched("b2_fused_muladd_relu_bwd_final");
+  }
+  b2_free(ws, stream);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,334 @@
+// Runtime plumbing + the caching device allocator.
+//
+// Replaces the reference's per-op `Buffer(array('f'))` storage
+// (tensorlite/core.py:68-75, 315-330): device blocks come from size-class
+// free lists and are returned on free in STREAM ORDER -- a block freed on its
+// owning stream is reusable immediately by later work on that stream (the
+// stream serialises the old and new users); a block freed from another
+// stream is parked behind a CUDA event until that stream passes the free.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace b2 {
+
+static thread_local std::string t_err;
+std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { t_err = msg; }
+int fail(const std::string& msg) {
+  set_error(msg);
+  return 1;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+  return 2;
+}
+
+static std::mutex g_init_mu;
+static int g_device = -1;
+static int g_sms = 0;
+static cudaStream_t g_stream = nullptr;
+
+int ensure_init() {
+  if (g_stream) return 0;
+  return b2_init(-1);
+}
+
+cudaStream_t resolve(void* stream) {
+  if (stream) return (cudaStream_t)stream;
+  if (!g_stream) ensure_init();
+  return g_stream;
+}
+
+int sm_count() {
+  if (!g_sms) ensure_init();
+  return g_sms ? g_sms : 148;
+}
+
+// ------------------------------------------------------------ allocator
+
+struct Block {
+  void* ptr;
+  size_t size;
+  cudaStream_t stream;  // owning stream
+};
+
+struct Pending {
+  Block* blk;
+  cudaEvent_t ev;
+};
+
+static std::mutex g_mu;
+static std::unordered_map<void*, Block*> g_live;
+// free lists keyed by (stream) -> size -> blocks
+static std::map<cudaStream_t, std::multimap<size_t, Block*>> g_free;
+static std::vector<Pending> g_pending;
+static size_t g_in_use = 0, g_cached = 0, g_peak = 0;
+static uint64_t g_nmalloc = 0;
+
+static size_t round_size(size_t n) {
+  if (n == 0) n = 1;
+  if (n < (1u << 20)) return (n + 511) & ~size_t(511);        // 512 B classes
+  return (n + (2u << 20) - 1) & ~size_t((2u << 20) - 1);       // 2 MiB classes
+}
+
+static void drain_pending_locked() {
+  size_t w = 0;
+  for (size_t i = 0; i < g_pending.size(); ++i) {
+    Pending p = g_pending[i];
+    if (cudaEventQuery(p.ev) == cudaSuccess) {
+      cudaEventDestroy(p.ev);
+      g_free[p.blk->stream].emplace(p.blk->size, p.blk);
+    } else {
+      g_pending[w++] = p;
+    }
+  }
+  g_pending.resize(w);
+  cudaGetLastError();  // clear cudaErrorNotReady
+}
+
+static int release_cached_locked() {
+  drain_pending_locked();
+  for (auto& kv : g_free) {
+    for (auto& sb : kv.second) {
+      cudaFree(sb.second->ptr);
+      g_cached -= sb.second->size;
+      delete sb.second;
+    }
+    kv.second.clear();
+  }
+  return 0;
+}
+
+}  // namespace b2
+
+using namespace b2;
+
+extern "C" {
+
+const char* b2_last_error(void) { return t_err.c_str(); }
+
+int b2_version(int* major, int* minor) {
+  if (major) *major = 0;
+  if (minor) *minor = 1;
+  return 0;
+}
+
+int b2_init(int device) {
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  if (g_stream && (device < 0 || device == g_device)) return 0;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail("b2_init: no CUDA device visible (libb2 has no CPU fallback)");
+  if (device < 0) {
+    B2_CUDA(cudaGetDevice(&device));
+  }
+  B2_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  B2_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail("b2_init: libb2 is built for sm_100a (B200); found sm_" +
+                std::to_string(prop.major) + std::to_string(prop.minor));
+  g_sms = prop.multiProcessorCount;
+  B2_CUDA(cudaStreamCreateWithFlags(&g_stream, cudaStreamNonBlocking));
+  g_device = device;
+  return 0;
+}
+
+int b2_device_count(int* n) {
+  cudaError_t e = cudaGetDeviceCount(n);
+  if (e != cudaSuccess) {
+    *n = 0;
+    cudaGetLastError();
+  }
+  return 0;
+}
+
+int b2_device_info(int* sm, int* maj, int* min, size_t* total) {
+  B2_TRY(ensure_init());
+  cudaDeviceProp prop;
+  B2_CUDA(cudaGetDeviceProperties(&prop, g_device));
+  if (sm) *sm = prop.multiProcessorCount;
+  if (maj) *maj = prop.major;
+  if (min) *min = prop.minor;
+  if (total) *total = prop.totalGlobalMem;
+  return 0;
+}
+
+int b2_default_stream(void** s) {
+  B2_TRY(ensure_init());
+  *s = (void*)g_stream;
+  return 0;
+}
+int b2_stream_create(void** s) {
+  B2_TRY(ensure_init());
+  cudaStream_t st;
+  B2_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  *s = (void*)st;
+  return 0;
+}
+int b2_stream_destroy(void* s) {
+  B2_CUDA(cudaStreamDestroy((cudaStream_t)s));
+  return 0;
+}
+int b2_stream_sync(void* s) {
+  B2_CUDA(cudaStreamSynchronize(resolve(s)));
+  return 0;
+}
+int b2_device_sync(void) {
+  B2_CUDA(cudaDeviceSynchronize());
+  return 0;
+}
+int b2_event_create(void** ev) {
+  B2_TRY(ensure_init());
+  cudaEvent_t e;
+  B2_CUDA(cudaEventCreate(&e));
+  *ev = (void*)e;
+  return 0;
+}
+int b2_event_destroy(void* ev) {
+  B2_CUDA(cudaEventDestroy((cudaEvent_t)ev));
+  return 0;
+}
+int b2_event_record(void* ev, void* s) {
+  B2_CUDA(cudaEventRecord((cudaEvent_t)ev, resolve(s)));
+  return 0;
+}
+int b2_event_elapsed_ms(void* a, void* b, float* ms) {
+  B2_CUDA(cudaEventSynchronize((cudaEvent_t)b));
+  B2_CUDA(cudaEventElapsedTime(ms, (cudaEvent_t)a, (cudaEvent_t)b));
+  return 0;
+}
+int b2_stream_wait_event(void* s, void* ev) {
+  B2_CUDA(cudaStreamWaitEvent(resolve(s), (cudaEvent_t)ev, 0));
+  return 0;
+}
+int b2_launch_count(uint64_t* n) {
+  *n = g_launches.load();
+  return 0;
+}
+
+// ------------------------------------------------------------ allocator API
+
+int b2_alloc(size_t bytes, void* stream, void** out) {
+  B2_TRY(ensure_init());
+  cudaStream_t st = resolve(stream);
+  size_t sz = round_size(bytes);
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_pending.empty()) drain_pending_locked();
+  auto& fl = g_free[st];
+  // best fit, but never hand out a block more than 2x (large) the request
+  auto it = fl.lower_bound(sz);
+  if (it != fl.end() && (it->first <= 2 * sz || it->first - sz < (1u << 20))) {
+    Block* b = it->second;
+    fl.erase(it);
+    g_live[b->ptr] = b;
+    g_in_use += b->size;
+    if (g_in_use > g_peak) g_peak = g_in_use;
+    *out = b->ptr;
+    return 0;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, sz);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    release_cached_locked();
+    e = cudaMalloc(&p, sz);
+    if (e != cudaSuccess) {
+      char buf[160];
+      snprintf(buf, sizeof buf, "b2_alloc: out of device memory allocating %zu bytes (in use %zu)",
+               sz, g_in_use);
+      cudaGetLastError();
+      return fail(buf);
+    }
+  }
+  ++g_nmalloc;
+  Block* b = new Block{p, sz, st};
+  g_live[p] = b;
+  g_in_use += sz;
+  g_cached += sz;
+  if (g_in_use > g_peak) g_peak = g_in_use;
+  *out = p;
+  return 0;
+}
+
+int b2_free(void* ptr, void* stream) {
+  if (!ptr) return 0;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_live.find(ptr);
+  if (it == g_live.end()) return fail("b2_free: pointer not owned by the allocator");
+  Block* b = it->second;
+  g_live.erase(it);
+  g_in_use -= b->size;
+  cudaStream_t fs = stream ? (cudaStream_t)stream : b->stream;
+  if (fs == b->stream) {
+    g_free[b->stream].emplace(b->size, b);
+  } else {
+    // last use was on another stream: reusable once that stream passes here
+    cudaEvent_t ev;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev, fs) != cudaSuccess) {
+      cudaStreamSynchronize(fs);
+      g_free[b->stream].emplace(b->size, b);
+      cudaGetLastError();
+    } else {
+      g_pending.push_back({b, ev});
+    }
+  }
+  return 0;
+}
+
+int b2_alloc_stats(size_t* in_use, size_t* cached, size_t* peak, uint64_t* nm) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (in_use) *in_use = g_in_use;
+  if (cached) *cached = g_cached;
+  if (peak) *peak = g_peak;
+  if (nm) *nm = g_nmalloc;
+  return 0;
+}
+
+int b2_empty_cache(void) {
+  B2_CUDA(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> lk(g_mu);
+  return release_cached_locked();
+}
+
+int b2_host_alloc(size_t bytes, void** out) {
+  B2_TRY(ensure_init());
+  B2_CUDA(cudaMallocHost(out, bytes ? bytes : 1));
+  return 0;
+}
+int b2_host_free(void* p) {
+  B2_CUDA(cudaFreeHost(p));
+  return 0;
+}
+
+int b2_memcpy_h2d(void* dst, const void* src, size_t bytes, void* s) {
+  if (!bytes) return 0;
+  B2_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, resolve(s)));
+  return 0;
+}
+// synchronous w.r.t. the host: the data is valid when this returns
+int b2_memcpy_d2h(void* dst, const void* src, size_t bytes, void* s) {
+  if (!bytes) return 0;
+  cudaStream_t st = resolve(s);
+  B2_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+  B2_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+int b2_memcpy_d2d(void* dst, const void* src, size_t bytes, void* s) {
+  if (!bytes) return 0;
+  B2_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, resolve(s)));
+  return 0;
+}
+
+}  // extern "C"

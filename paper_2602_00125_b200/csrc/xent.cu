@@ -1,0 +1,243 @@
+// Row-wise losses: fused cross-entropy (fwd + pullback) and row softmax.
+//
+// cross_entropy mirrors tensorlite/nn.py:453-503 in double precision:
+//   m = row max, se = sum exp(v - m), row loss = m + log(se) - z[y],
+//   loss = f32((sum of row losses) / b);   pullback:
+//   dz = f32((exp(v - m) / se - onehot) * (g / b)).
+// The reference takes se from math.fsum in the pullback; here se is a
+// compensated (Neumaier) sum in the forward, kept per row in `row_stats`, so
+// the pullback does not redo the reductions.
+//
+// softmax mirrors the reference COMPOSITION (max detached, then
+// sub/exp/sum/div as separate engine ops, each rounded to f32) and its
+// GradStore-ordered pullback, so results are bit-identical to composing the
+// ops on the reference engine.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "common.cuh"
+
+extern "C" int b2_alloc(size_t, void*, void**);
+extern "C" int b2_free(void*, void*);
+
+namespace {
+
+__device__ __forceinline__ float warp_max_first(float m) {
+  // row max VALUE (ties are irrelevant for the value); NaN handled by caller
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    float o = __shfl_xor_sync(0xffffffffu, m, off);
+    m = o > m ? o : m;
+  }
+  return m;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// two-sum combine of Neumaier accumulators (s, c)
+__device__ __forceinline__ void neu_add(double& s, double& c, double x) {
+  double t = s + x;
+  if (fabs(s) >= fabs(x))
+    c += (s - t) + x;
+  else
+    c += (x - t) + s;
+  s = t;
+}
+
+// Reference row max semantics for the value: strict '>' scan from v[0]
+// (nn.py:478-481) -- a NaN at v[0] sticks, later NaNs are skipped.
+__device__ __forceinline__ float row_max(const float* row, int64_t C, int lane) {
+  float m = -INFINITY;
+  bool any = false;
+  for (int64_t j = lane; j < C; j += 32) {
+    float v = row[j];
+    if (!isnan(v)) {
+      m = any ? (v > m ? v : m) : v;
+      any = true;
+    }
+  }
+  m = warp_max_first(any ? m : -INFINITY);
+  float v0 = row[0];
+  return isnan(v0) ? v0 : m;
+}
+
+// ---------------------------------------------------------------- cross-entropy
+// one warp per row; grid-stride over rows
+__global__ void __launch_bounds__(256) k_xent_rows(double* __restrict__ row_loss,
+                                                   double* __restrict__ row_stats,
+                                                   const float* __restrict__ z,
+                                                   const int64_t* __restrict__ labels,
+                                                   int64_t B, int64_t C) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < B; r += nw) {
+    const float* row = z + r * C;
+    double m = (double)row_max(row, C, lane);
+    double s = 0, c = 0;
+    for (int64_t j = lane; j < C; j += 32) neu_add(s, c, exp((double)row[j] - m));
+    // per-lane compensated partials, then a fixed butterfly over 32 lanes
+    double tot = warp_sum(s + c);
+    if (lane == 0) {
+      double se = tot;
+      row_stats[2 * r] = m;
+      row_stats[2 * r + 1] = se;
+      row_loss[r] = m + log(se) - (double)row[labels[r]];
+    }
+  }
+}
+
+// fixed-order sum of row losses by one CTA, loss = f32(total / denom)
+__global__ void __launch_bounds__(1024) k_xent_final(float* __restrict__ loss,
+                                                     const double* __restrict__ row_loss,
+                                                     int64_t B, double denom) {
+  __shared__ double sh[32];
+  double acc = 0;
+  for (int64_t r = threadIdx.x; r < B; r += blockDim.x) acc += row_loss[r];
+  acc = warp_sum(acc);
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh[w] = acc;
+  __syncthreads();
+  if (w == 0) {
+    double t = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) *loss = __double2float_rn(t / denom);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_xent_bwd(float* __restrict__ dz, const float* __restrict__ g,
+                                                  const double* __restrict__ row_stats,
+                                                  const float* __restrict__ z,
+                                                  const int64_t* __restrict__ labels, int64_t B,
+                                                  int64_t C, double denom) {
+  double gv = (double)g[0] / denom;  // nn.py:489
+  int64_t total = B * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / C;
+    int64_t j = i - r * C;
+    double m = row_stats[2 * r], se = row_stats[2 * r + 1];
+    double p = exp((double)z[i] - m) / se - (j == labels[r] ? 1.0 : 0.0);
+    dz[i] = __double2float_rn(p * gv);  // nn.py:500
+  }
+}
+
+// ---------------------------------------------------------------- softmax (composed)
+__global__ void __launch_bounds__(256) k_softmax_fwd(float* __restrict__ y, float* __restrict__ rs,
+                                                     float* __restrict__ rm,
+                                                     const float* __restrict__ z, int64_t B,
+                                                     int64_t C) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < B; r += nw) {
+    const float* row = z + r * C;
+    float m = row_max(row, C, lane);
+    double acc = 0;
+    for (int64_t j = lane; j < C; j += 32) {
+      float e = __double2float_rn(exp((double)__fsub_rn(row[j], m)));  // exp(sub(z, m))
+      acc += (double)e;
+    }
+    acc = warp_sum(acc);
+    float s = __double2float_rn(acc);  // sum(e, -1, keepdims)
+    float* yr = y + r * C;
+    for (int64_t j = lane; j < C; j += 32) {
+      float e = __double2float_rn(exp((double)__fsub_rn(row[j], m)));
+      yr[j] = __fdiv_rn(e, s);  // div(e, s)
+    }
+    if (lane == 0) {
+      rs[r] = s;
+      rm[r] = m;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_softmax_bwd(float* __restrict__ gz,
+                                                     const float* __restrict__ gy,
+                                                     const float* __restrict__ z,
+                                                     const float* __restrict__ rs,
+                                                     const float* __restrict__ rm, int64_t B,
+                                                     int64_t C) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < B; r += nw) {
+    const float* row = z + r * C;
+    const float* grow = gy + r * C;
+    float s = rs[r], m = rm[r];
+    float ss = __fmul_rn(s, s);
+    double acc = 0;
+    for (int64_t j = lane; j < C; j += 32) {
+      float e = __double2float_rn(exp((double)__fsub_rn(row[j], m)));
+      float t = __fdiv_rn(__fmul_rn(grow[j], e), ss);  // div(mul(g, e), mul(s, s))
+      acc += (double)(-t);                              // neg, then sum(axis=-1)
+    }
+    acc = warp_sum(acc);
+    float gs = __double2float_rn(acc);
+    float* out = gz + r * C;
+    for (int64_t j = lane; j < C; j += 32) {
+      float e = __double2float_rn(exp((double)__fsub_rn(row[j], m)));
+      float ge = __fdiv_rn(grow[j], s);            // div(g, s) -- stored first
+      float tot = __fadd_rn(ge, gs);               // GradStore add(cur, g)
+      out[j] = __fmul_rn(tot, e);                  // exp pullback mul(g, out)
+    }
+  }
+}
+
+int rows_grid(int64_t B) {
+  int64_t warps = B;
+  int64_t ctas = (warps + 7) / 8;
+  int64_t cap = (int64_t)b2::sm_count() * 16;
+  return (int)(ctas < cap ? (ctas > 0 ? ctas : 1) : cap);
+}
+
+}  // namespace
+
+extern "C" {
+
+int b2_xent_fwd(float* loss, double* row_stats, const float* logits, const int64_t* labels,
+                int64_t rows, int64_t cols, double denom, void* stream) {
+  if (rows <= 0 || cols <= 0) return b2::fail("b2_xent_fwd: empty logits");
+  cudaStream_t st = b2::resolve(stream);
+  void* ws = nullptr;
+  B2_TRY(b2_alloc((size_t)rows * sizeof(double), st, &ws));
+  k_xent_rows<<<rows_grid(rows), 256, 0, st>>>((double*)ws, row_stats, logits, labels, rows, cols);
+  int rc = b2::launched("b2_xent_fwd(rows)");
+  if (!rc) {
+    k_xent_final<<<1, 1024, 0, st>>>(loss, (const double*)ws, rows, denom);
+    rc = b2::launched("b2_xent_fwd(final)");
+  }
+  b2_free(ws, st);
+  return rc;
+}
+
+int b2_xent_bwd(float* dlogits, const float* g, const double* row_stats, const float* logits,
+                const int64_t* labels, int64_t rows, int64_t cols, double denom, void* stream) {
+  if (rows <= 0 || cols <= 0) return 0;
+  cudaStream_t st = b2::resolve(stream);
+  int grid = b2::grid_for(rows * cols, 256 * 8, 8);
+  k_xent_bwd<<<grid, 256, 0, st>>>(dlogits, g, row_stats, logits, labels, rows, cols, denom);
+  return b2::launched("b2_xent_bwd");
+}
+
+int b2_softmax_fwd(float* y, float* row_s, float* row_m, const float* z, int64_t rows,
+                   int64_t cols, void* stream) {
+  if (rows <= 0 || cols <= 0) return 0;
+  cudaStream_t st = b2::resolve(stream);
+  k_softmax_fwd<<<rows_grid(rows), 256, 0, st>>>(y, row_s, row_m, z, rows, cols);
+  return b2::launched("b2_softmax_fwd");
+}
+
+int b2_softmax_bwd(float* gz, const float* gy, const float* z, const float* row_s,
+                   const float* row_m, int64_t rows, int64_t cols, void* stream) {
+  if (rows <= 0 || cols <= 0) return 0;
+  cudaStream_t st = b2::resolve(stream);
+  k_softmax_bwd<<<rows_grid(rows), 256, 0, st>>>(gz, gy, z, row_s, row_m, rows, cols);
+  return b2::launched("b2_softmax_bwd");
+}
+
+}  // extern "C"

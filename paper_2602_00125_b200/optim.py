@@ -1,0 +1,125 @@
+"""SGD / Adam as single multi-tensor kernel launches (tensorlite/optim.py).
+
+Semantics follow optim.py:16-136: per-parameter slots keyed by identity,
+coupled weight decay, SGD momentum ``v = mu*v + g``, Adam debiased with eps
+outside the sqrt, slot arithmetic in DOUBLE (the slots live in HBM as fp64)
+and one f32 rounding of theta per step. ``step_all`` skips parameters
+without a gradient and returns how many it updated. The difference is the
+launch shape: every parameter of a step is updated by ONE kernel over a
+tensor table (b2_sgd_multi / b2_adam_multi), not a Python loop per element.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib as L
+from . import core as T
+from .errors import ShapeError
+
+
+class Optimizer:
+    def __init__(self, lr: float, weight_decay: float = 0.0):
+        self.lr = lr
+        self.weight_decay = weight_decay
+        self._state = {}
+
+    _nslots = 1
+
+    def state_for(self, param) -> dict:
+        st = self._state.get(id(param))
+        if st is None:
+            slots = []
+            for _ in range(self._nslots):
+                b = T.Buffer(8 * max(param.size, 1))
+                if param.size:
+                    # zero the double slots (two f32 zeros == one double zero)
+                    L.call("b2_fill_f32", b.ptr, 0.0, 2 * param.size, None)
+                slots.append(b)
+            st = {"param": param, "slots": slots, "t": 0}
+            self._state[id(param)] = st
+        return st
+
+    def _entry(self, param, grad):
+        if grad.shape != param.shape:
+            raise ShapeError(f"gradient shape {grad.shape} does not match parameter {param.shape}")
+        if not param.is_contiguous:
+            raise ShapeError("optimizer parameters must be contiguous leaves")
+        g = grad if grad.is_contiguous else T._copy_contig(grad)
+        st = self.state_for(param)
+        st["t"] += 1
+        e = L.OptTensor()
+        e.param = param.data_ptr
+        e.grad = g.data_ptr
+        e.slot0 = st["slots"][0].ptr
+        e.slot1 = st["slots"][1].ptr if len(st["slots"]) > 1 else None
+        e.n = param.size
+        e.bc1, e.bc2 = self._bias_corrections(st["t"])
+        return e, g
+
+    def _bias_corrections(self, t):
+        return 1.0, 1.0
+
+    def _launch(self, table, count):
+        raise NotImplementedError
+
+    def step_many(self, pairs):
+        """Update every (param, grad) pair with one kernel launch."""
+        pairs = list(pairs)
+        if not pairs:
+            return 0
+        entries, keep = [], []
+        for p, g in pairs:
+            e, gg = self._entry(p, g)
+            entries.append(e)
+            keep.append(gg)
+        table = (L.OptTensor * len(entries))(*entries)
+        self._launch(table, len(entries))
+        for p, _ in pairs:
+            p.buffer.version += 1  # in-place write, like param.write_flat
+        return len(pairs)
+
+    def step(self, param, grad):
+        self.step_many([(param, grad)])
+        return param
+
+
+class SGD(Optimizer):
+    """v = mu*v + g + lambda*theta; theta -= lr*v (optim.py:54-72)."""
+
+    def __init__(self, lr=0.01, momentum=0.0, weight_decay=0.0):
+        super().__init__(lr, weight_decay)
+        self.momentum = momentum
+
+    def _launch(self, table, count):
+        L.call("b2_sgd_multi", table, count, float(self.lr), float(self.momentum),
+               float(self.weight_decay), None)
+
+
+class Adam(Optimizer):
+    """Debiased moments, eps outside the square root (optim.py:75-100)."""
+
+    _nslots = 2
+
+    def __init__(self, lr=0.001, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.0):
+        super().__init__(lr, weight_decay)
+        self.beta1, self.beta2 = betas
+        self.eps = eps
+
+    def _bias_corrections(self, t):
+        return 1.0 - self.beta1 ** t, 1.0 - self.beta2 ** t  # optim.py:90-91
+
+    def _launch(self, table, count):
+        L.call("b2_adam_multi", table, count, float(self.lr), float(self.beta1),
+               float(self.beta2), float(self.eps), float(self.weight_decay), None)
+
+
+def step_all(optimizer: Optimizer, parameters, grad_store):
+    """Update every parameter that has a gradient entry; skip the rest
+    (optim.py:125-136). Returns the number updated. One kernel launch."""
+    pairs = []
+    for p in parameters:
+        g = grad_store.get(p)
+        if g is not None:
+            pairs.append((p, g))
+    return optimizer.step_many(pairs)

@@ -1,0 +1,37 @@
+import sys, time, numpy as np
+sys.path.insert(0, '.')
+import paper_2602_00125_b200 as P
+from paper_2602_00125_b200 import _lib as L
+def timeit(fn, iters=10):
+    fn(); L.synchronize()
+    e0, e1 = L.Event(), L.Event()
+    e0.record(); 
+    for _ in range(iters): fn()
+    e1.record(); return e0.elapsed_ms(e1) / iters
+for n in (1024, 4096, 8192):
+    rng = np.random.default_rng(0)
+    A = rng.uniform(-1,1,(n,n)).astype(np.float32); B = rng.uniform(-1,1,(n,n)).astype(np.float32)
+    At, Bt = P.from_numpy(A), P.from_numpy(B)
+    C = P.zeros((n,n))
+    ref = None
+    if n <= 4096:
+        ref = A.astype(np.float64) @ B.astype(np.float64).T
+    for name, algo in (("1xtf32", L.GEMM_1XTF32), ("3xtf32", L.GEMM_3XTF32), ("simt", L.GEMM_SIMT)):
+        if name == "simt" and n > 4096: continue
+        f = lambda: L.call("b2_gemm", 0, 1, n, n, n, At.data_ptr, n, Bt.data_ptr, n, C.data_ptr, n, None, 0, algo, None)
+        ms = timeit(f, 5 if n == 8192 else 10)
+        err = ""
+        if ref is not None:
+            c = C.numpy(); err = f"err={np.abs(c-ref).max()/np.abs(ref).max():.2e}"
+        print(f"n={n} {name}: {ms:.3f} ms  {2*n**3/ms/1e9:.1f} TFLOP/s {err}", flush=True)
+    # presplit kernel alone
+    if True:
+        hi, lo, hib, lob = P.zeros((n,n)), P.zeros((n,n)), P.zeros((n,n)), P.zeros((n,n))
+        L.call("b2_tf32_split", hi.data_ptr, lo.data_ptr, At.data_ptr, n, n, n, None)
+        L.call("b2_tf32_split", hib.data_ptr, lob.data_ptr, Bt.data_ptr, n, n, n, None)
+        f = lambda: L.call("b2_gemm_presplit", 0, 1, n, n, n, hi.data_ptr, lo.data_ptr, hib.data_ptr, lob.data_ptr, C.data_ptr, n, None, 0, None)
+        ms = timeit(f, 5)
+        print(f"n={n} 3xtf32-presplit kernel: {ms:.3f} ms  {2*n**3/ms/1e9:.1f} TFLOP/s", flush=True)
+        f = lambda: L.call("b2_tf32_split", hi.data_ptr, lo.data_ptr, At.data_ptr, n, n, n, None)
+        ms = timeit(f, 10)
+        print(f"n={n} split: {ms:.3f} ms  {3*4*n*n/ms/1e6:.0f} GB/s", flush=True)

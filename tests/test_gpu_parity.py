@@ -1,0 +1,462 @@
+"""Device parity: libb2 (through the package API and the C ABI) vs the
+reference-pinned goldens and the NumPy oracle.
+
+Bit-exact where SURVEY 8a says the reference is bit-exact-achievable
+(elementwise, relu masks, sums/means via fp64, max/argmax routing, CE in
+double, SGD/Adam in double, composed softmax); fp32 tolerance
+``max|dev-ref| <= 1e-4 * max|ref|`` (normwise) wherever a GEMM
+sits on the path.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2602_00125_b200 as P
+from paper_2602_00125_b200 import nn, optim
+from oracle import tensorlite_np as O
+from tests.golden import inputs as I
+from tests.golden.load import bits_equal, load, normwise
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def dev(a, grad=False):
+    return P.from_numpy(np.asarray(a, np.float32), requires_grad=grad)
+
+
+def host(t):
+    return t.numpy()
+
+
+# ---------------------------------------------------------------- elementwise
+
+
+def test_broadcast_binary_bit_exact():
+    g = load("elementwise.npz")
+    ops = {"add": P.add, "sub": P.sub, "mul": P.mul, "div": P.div}
+    for i, (kind, va, vb) in enumerate(I.broadcast_cases()):
+        got = ops[kind](dev(va), dev(vb))
+        want = g[f"bc{i}_{kind}_out"]
+        assert got.shape == want.shape, (i, kind)
+        assert bits_equal(host(got), want), (i, kind)
+
+
+@pytest.mark.parametrize("name", ["neg", "exp", "log", "sqrt", "absolute", "relu"])
+def test_unary_bit_exact(name):
+    g = load("elementwise.npz")
+    got = getattr(P, name)(dev(g["unary_x"]))
+    assert bits_equal(host(got), g[f"unary_{name}"]), name
+
+
+def test_relu_grad_bit_exact():
+    g = load("elementwise.npz")
+    x = dev(g["unary_x"], grad=True)
+    store = P.backward(P.sum(P.relu(x)))
+    assert bits_equal(host(store[x]), g["unary_relu_grad"])
+
+
+def test_div_ieee_specials():
+    g = load("elementwise.npz")
+    got = P.div(dev(g["div_special_num"]), dev(g["div_special_den"]))
+    assert bits_equal(host(got), g["div_special_out"])
+
+
+def test_scalar_promotion_and_strided_views():
+    x = np.arange(12, dtype=np.float32).reshape(3, 4) - 5.5
+    t = dev(x)
+    assert bits_equal(host(P.add(t, 1)), O.add(x, np.float32(1)))
+    assert bits_equal(host(P.mul(3, t)), O.mul(np.float32(3), x))
+    assert bits_equal(host(P.div(2.0, t)), O.div(np.float32(2), x))
+    tt = P.transpose2d(t)
+    assert bits_equal(host(P.exp(tt)), O.exp(x.T))
+    assert bits_equal(host(P.sub(tt, P.transpose2d(t))), np.zeros((4, 3), np.float32))
+    bt = P.broadcast_to(dev(x[:1]), (5, 3, 4))
+    assert bits_equal(host(P.mul(bt, t)), O.mul(np.broadcast_to(x[:1], (5, 3, 4)), x))
+
+
+def test_large_elementwise_vectorized_paths():
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((1023, 4097)).astype(np.float32)
+    b = rng.standard_normal((1, 4097)).astype(np.float32)
+    assert bits_equal(host(P.mul(dev(a), dev(b))), O.mul(a, b))
+    a4 = rng.standard_normal((512, 4096)).astype(np.float32)
+    b4 = rng.standard_normal((4096,)).astype(np.float32)
+    assert bits_equal(host(P.add(dev(a4), dev(b4))), O.add(a4, b4))
+    col = rng.standard_normal((512, 1)).astype(np.float32)
+    assert bits_equal(host(P.sub(dev(a4), dev(col))), O.sub(a4, col))
+
+
+# ---------------------------------------------------------------- reductions
+
+
+def test_reductions_bit_exact():
+    g = load("reductions.npz")
+    for i, (x, axes, keep) in enumerate(I.reduction_cases()):
+        for kind in ("sum", "mean", "max"):
+            P.reset_tape()
+            xt = dev(x, grad=True)
+            r = getattr(P, kind)(xt, axis=axes, keepdims=keep)
+            want = g[f"r{i}_{kind}"]
+            assert r.shape == want.shape, (i, kind)
+            assert bits_equal(host(r), want), (i, kind, x.shape, axes, keep)
+            if kind == "max":
+                store = P.backward(P.sum(r))
+                assert bits_equal(host(store[xt]), g[f"r{i}_maxgrad"]), (i, "maxgrad")
+
+
+def test_chunked_full_sum_bit_exact():
+    g = load("reductions.npz")
+    assert bits_equal(host(P.sum(dev(g["chunked_x"]))), g["chunked_sum"])
+
+
+def test_large_reductions_vs_oracle():
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((2048, 3000)).astype(np.float32)
+    t = dev(x)
+    for ax in (0, 1, None):
+        assert bits_equal(host(P.sum(t, axis=ax)), O.axis_sum(x, ax)), ax
+        assert bits_equal(host(P.mean(t, axis=ax)), O.axis_mean(x, ax)), ax
+        assert bits_equal(host(P.max(t, axis=ax)), O.axis_max(x, ax)[0]), ax
+    x3 = rng.standard_normal((6, 70, 9, 5)).astype(np.float32)
+    t3 = dev(x3)
+    for ax in ((1,), (0, 2), (1, 3), (0, 1, 2)):
+        assert bits_equal(host(P.sum(t3, axis=ax)), O.axis_sum(x3, ax)), ax
+        v, _ = O.axis_max(x3, ax)
+        assert bits_equal(host(P.max(t3, axis=ax)), v), ax
+
+
+def test_max_nan_and_ties_semantics():
+    x = np.array([[np.nan, 1.0, 2.0], [1.0, np.nan, 0.5], [3.0, 3.0, 1.0], [-0.0, 0.0, -1.0]],
+                 np.float32)
+    xt = dev(x, grad=True)
+    r = P.max(xt, axis=1)
+    v, pos = O.axis_max(x, 1)
+    assert bits_equal(host(r), v)
+    store = P.backward(P.sum(r))
+    assert bits_equal(host(store[xt]), O.max_pullback(np.ones(4, np.float32), pos, x.shape))
+
+
+def test_zero_extent_reductions():
+    e = P.zeros((0, 3))
+    assert P.sum(e).item() == 0.0
+    assert np.isnan(P.mean(e).item())
+    with pytest.raises(P.ShapeError):
+        P.max(e)
+    assert P.sum(e, axis=1).shape == (0,)
+
+
+# ---------------------------------------------------------------- matmul
+
+
+@pytest.mark.parametrize("algo", ["simt", "3xtf32"])
+def test_matmul_goldens(algo):
+    g = load("matmul.npz")
+    P.set_gemm_algo(algo)
+    try:
+        for i, (x, w, gr) in enumerate(I.matmul_cases()):
+            P.reset_tape()
+            xt, wt = dev(x, True), dev(w, True)
+            y = P.matmul(xt, wt)
+            store = P.backward(y, seed=dev(gr))
+            for got, key in ((y, "y"), (store[xt], "dx"), (store[wt], "dw")):
+                want = g[f"m{i}_{key}"]
+                assert got.shape == want.shape
+                assert normwise(host(got), want) <= 2e-6, (algo, i, key)
+    finally:
+        P.set_gemm_algo(None)
+
+
+def _ref_gemm(A, B, ta, tb):
+    a = A.astype(np.float64).T if ta else A.astype(np.float64)
+    b = B.astype(np.float64) if tb else B.astype(np.float64).T
+    return a @ b.T  # a [M,K] . b[N,K]^T
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 1), (0, 0), (1, 0), (1, 1)])
+@pytest.mark.parametrize("shape", [(128, 256, 32), (300, 520, 200), (1000, 260, 1028), (64, 8, 4)])
+def test_gemm_layouts_tc(ta, tb, shape):
+    """tcgen05 3xTF32 and 1xTF32 against fp64, every operand layout, ragged tiles."""
+    import ctypes
+    from paper_2602_00125_b200 import _lib as L
+
+    M, N, K = shape
+    rng = np.random.default_rng(M + N + K + 2 * ta + tb)
+    A = rng.uniform(-1, 1, (K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.uniform(-1, 1, (N, K) if tb else (K, N)).astype(np.float32)
+    bias = rng.uniform(-1, 1, N).astype(np.float32)
+    ref = _ref_gemm(A, B, ta, tb)
+    At, Bt, bt = dev(A), dev(B), dev(bias)
+    # 3xTF32 with K-chunk promotion is sgemm-grade (~1e-6); 1xTF32 is TF32-grade
+    for algo, tol in ((L.GEMM_3XTF32, 5e-6), (L.GEMM_1XTF32, 3e-3), (L.GEMM_SIMT, 5e-6)):
+        C = P.zeros((M, N))
+        L.call("b2_gemm", ta, tb, M, N, K, At.data_ptr, A.shape[1], Bt.data_ptr, B.shape[1],
+               C.data_ptr, N, bt.data_ptr, L.EPI_BIAS_RELU, algo, None)
+        want = np.maximum(ref + bias.astype(np.float64), 0)
+        err = normwise(host(C), want)
+        assert err <= tol, (algo, ta, tb, shape, err)
+
+
+def test_gemm_accuracy_long_k():
+    """K-chunk promotion keeps 3xTF32 at sgemm accuracy for the config-3 K."""
+    from paper_2602_00125_b200 import _lib as L
+
+    M, N, K = 256, 256, 8192
+    rng = np.random.default_rng(8)
+    A = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    B = rng.uniform(-1, 1, (N, K)).astype(np.float32)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    C = P.zeros((M, N))
+    At, Bt = dev(A), dev(B)
+    L.call("b2_gemm", 0, 1, M, N, K, At.data_ptr, K, Bt.data_ptr, K, C.data_ptr, N, None,
+           L.EPI_NONE, L.GEMM_3XTF32, None)
+    assert normwise(host(C), ref) <= 3e-6
+
+
+def test_tf32_hardware_rounding_probe(capsys):
+    """Records how kind::tf32 consumes raw fp32 bits (informational)."""
+    from paper_2602_00125_b200 import _lib as L
+
+    M, N, K = 128, 256, 32
+    a = np.full((M, K), 1.0 + 2.0 ** -11 + 2.0 ** -20, np.float32)
+    b = np.zeros((N, K), np.float32)
+    b[:, 0] = 1.0
+    At, Bt = dev(a), dev(b)
+    C = P.zeros((M, N))
+    L.call("b2_gemm", 0, 1, M, N, K, At.data_ptr, K, Bt.data_ptr, K, C.data_ptr, N, None,
+           L.EPI_NONE, L.GEMM_1XTF32, None)
+    v = float(host(C)[0, 0])
+    mode = {1.0: "truncate", 1.0 + 2.0 ** -10: "round"}.get(v, f"other({v!r})")
+    with capsys.disabled():
+        print(f"\n[tf32 probe] raw fp32 1+2^-11+2^-20 consumed as {v!r} -> {mode}")
+
+
+# ---------------------------------------------------------------- losses
+
+
+def test_cross_entropy_goldens_bit_exact():
+    g = load("ce_optim.npz")
+    for i, (z, labels) in enumerate(I.ce_cases()):
+        P.reset_tape()
+        zt = dev(z, True)
+        loss = nn.cross_entropy(zt, labels)
+        store = P.backward(loss)
+        assert bits_equal(host(loss), g[f"ce{i}_loss"]), i
+        assert bits_equal(host(store[zt]), g[f"ce{i}_grad"]), i
+
+
+def test_cross_entropy_label_validation():
+    z = P.zeros((2, 3))
+    with pytest.raises(ValueError):
+        nn.cross_entropy(z, [0, 3])
+    with pytest.raises(P.ShapeError):
+        nn.cross_entropy(z, [0])
+
+
+def test_softmax_matches_composed_reference_bit_exact():
+    rng = np.random.default_rng(4)
+    z = (rng.standard_normal((33, 1024)) * 3).astype(np.float32)
+    gy = rng.standard_normal((33, 1024)).astype(np.float32)
+    zt = dev(z, True)
+    y = P.softmax(zt)
+    yo, e, s = O.softmax_rows_composed(z)
+    assert bits_equal(host(y), yo)
+    store = P.backward(y, seed=dev(gy))
+    assert bits_equal(host(store[zt]), O.softmax_backward_composed(gy, e, s))
+
+
+# ---------------------------------------------------------------- optimizers
+
+
+@pytest.mark.parametrize("name,ctor", [
+    ("sgd", lambda: optim.SGD(lr=0.01)),
+    ("sgd_mom_wd", lambda: optim.SGD(lr=0.05, momentum=0.9, weight_decay=0.01)),
+    ("adam", lambda: optim.Adam(lr=1e-3)),
+    ("adam_wd", lambda: optim.Adam(lr=3e-3, betas=(0.8, 0.99), eps=1e-6, weight_decay=0.1)),
+])
+def test_optimizer_sequences_bit_exact(name, ctor):
+    g = load("ce_optim.npz")
+    opt = ctor()
+    p = dev(g["opt_theta0"])
+    for k in range(4):
+        opt.step(p, dev(g["opt_grads"][k]))
+        assert bits_equal(host(p), g[f"opt_{name}"][k]), (name, k)
+
+
+def test_multi_tensor_step_matches_single_steps():
+    rng = np.random.default_rng(9)
+    shapes = [(300, 7), (1,), (8193,), (64, 65)]
+    ps = [rng.standard_normal(s).astype(np.float32) for s in shapes]
+    gs = [rng.standard_normal(s).astype(np.float32) for s in shapes]
+    a, b = optim.Adam(lr=1e-2), optim.Adam(lr=1e-2)
+    pa = [dev(p) for p in ps]
+    pb = [dev(p) for p in ps]
+    for _ in range(3):
+        a.step_many([(p, dev(gg)) for p, gg in zip(pa, gs)])
+        for p, gg in zip(pb, gs):
+            b.step(p, dev(gg))
+    for x, y in zip(pa, pb):
+        assert bits_equal(host(x), host(y))
+
+
+# ---------------------------------------------------------------- BASELINE configs (small)
+
+
+def _mlp_device(params, relu_between=True):
+    layers = []
+    for i, (w, b) in enumerate(params):
+        d = nn.Dense(w.shape[1], w.shape[0], rng=0)
+        d.weight.write_flat(w.ravel())
+        d.bias.write_flat(b.ravel())
+        layers.append(d)
+        if relu_between and i < len(params) - 1:
+            layers.append(nn.ReLU())
+    return nn.Sequential(*layers), [l for l in layers if isinstance(l, nn.Dense)]
+
+
+def _run_mlp_device(params, x, labels, opt, steps):
+    model, dense = _mlp_device(params)
+    xt = dev(x)
+    losses = []
+    for _ in range(steps):
+        P.reset_tape()
+        loss = nn.cross_entropy(model(xt), labels)
+        losses.append(loss.item())
+        store = P.backward(loss)
+        grads = [(host(store[d.weight]), host(store[d.bias])) for d in dense]
+        optim.step_all(opt, model.parameters(), store)
+    return np.array(losses, np.float32), grads, [(host(d.weight), host(d.bias)) for d in dense]
+
+
+@pytest.mark.parametrize("algo", ["simt", "3xtf32"])
+def test_config1_train_step(algo):
+    golden = load("config1.npz")
+    params, x, labels = I.config1_inputs()
+    P.set_gemm_algo(algo)
+    try:
+        losses, grads, newp = _run_mlp_device(params, x, labels, optim.SGD(lr=0.01), 1)
+    finally:
+        P.set_gemm_algo(None)
+    assert normwise(losses, golden["loss"]) <= TOL
+    for i, ((gw, gb), (w, b)) in enumerate(zip(grads, newp)):
+        assert normwise(gw, golden[f"gw{i}"]) <= TOL, i
+        assert normwise(gb, golden[f"gb{i}"]) <= TOL, i
+        assert normwise(w, golden[f"w{i}"]) <= TOL, i
+        assert normwise(b, golden[f"b{i}"]) <= TOL, i
+
+
+def test_config5_small_adam_3_steps():
+    golden = load("config5_small.npz")
+    params, x, labels = I.config5_inputs(width=64, classes=10, batch=32, depth=4)
+    losses, grads, newp = _run_mlp_device(params, x, labels, optim.Adam(lr=1e-3), 3)
+    assert normwise(losses, golden["loss"]) <= TOL
+    for i, ((gw, gb), (w, b)) in enumerate(zip(grads, newp)):
+        assert normwise(gw, golden[f"gw{i}"]) <= TOL, i
+        assert normwise(w, golden[f"w{i}"]) <= TOL, i
+
+
+def test_config2_small_bit_exact_composed_and_fused():
+    g = load("config2_small.npz")
+    a, b = I.config2_inputs(rows=256, cols=512)
+    # composed reference ops
+    P.reset_tape()
+    at, bt = dev(a, True), dev(b, True)
+    y = P.relu(P.add(P.mul(at, bt), bt))
+    assert bits_equal(host(y), g["y"])
+    assert bits_equal(host(P.exp(P.clamp(dev(a), -10, 10))), g["e"])
+    with P.no_grad():
+        for d in (0, 1):
+            assert bits_equal(host(P.sum(y, axis=d)), g[f"sum{d}"]), d
+            assert bits_equal(host(P.mean(y, axis=d)), g[f"mean{d}"]), d
+            assert bits_equal(host(P.max(y, axis=d)), g[f"max{d}"]), d
+        assert bits_equal(host(P.sum(y)), g["sum_all"])
+    store = P.backward(P.sum(y))
+    assert bits_equal(host(store[at]), g["grad_a"])
+    assert bits_equal(host(store[bt]), g["grad_b"])
+    # fused kernels
+    P.reset_tape()
+    at, bt = dev(a, True), dev(b, True)
+    yf = P.fused_muladd_relu(at, bt)
+    assert bits_equal(host(yf), g["y"])
+    store = P.backward(P.sum(yf))
+    assert bits_equal(host(store[at]), g["grad_a"])
+    assert bits_equal(host(store[bt]), g["grad_b"])
+    ga, gb = P.muladd_relu_sum_grads(dev(a), dev(b))
+    assert bits_equal(host(ga), g["grad_a"]) and bits_equal(host(gb), g["grad_b"])
+
+
+def test_config3_small_matmul_fwd_bwd():
+    g = load("config3_small.npz")
+    A, B, dC = I.config3_inputs(n=96)
+    P.set_gemm_algo("3xtf32")
+    try:
+        at, bt = dev(A, True), dev(B, True)
+        C = P.mm(at, bt)
+        store = P.backward(C, seed=dev(dC))
+    finally:
+        P.set_gemm_algo(None)
+    assert normwise(host(C), g["C"]) <= TOL
+    assert normwise(host(store[at]), g["dA"]) <= TOL
+    assert normwise(host(store[bt]), g["dB"]) <= TOL
+
+
+def test_config4_small_softmax_linear():
+    g = load("config4_small.npz")
+    X, W, bias, Tt = I.config4_inputs(b=2, s=16, k=64)
+    xt, wt, bt = dev(X, True), dev(W, True), dev(bias, True)
+    z = P.add(P.mm(xt, wt), bt)
+    Y = P.softmax(z)
+    loss = P.mean(P.mul(Y, dev(Tt)))
+    store = P.backward(loss)
+    assert normwise(host(loss), g["loss"]) <= TOL
+    assert normwise(host(Y).reshape(-1, 64), g["Y"]) <= TOL
+    assert normwise(host(store[xt]).reshape(-1, 64), g["dX"]) <= TOL
+    assert normwise(host(store[wt]), g["dW"]) <= TOL
+    assert normwise(host(store[bt]), g["dbias"]) <= TOL
+
+
+# ---------------------------------------------------------------- autograd contract
+
+
+def test_autograd_contract_on_device():
+    x = dev([3.0], True)
+    assert host(P.backward(P.sum(P.add(x, x)))[x]).tolist() == [2.0]
+    P.reset_tape()
+    x = dev([1.0, 2.0, 3.0], True)
+    y = dev([[1.0], [2.0]], True)
+    s = P.backward(P.sum(P.mul(x, y)))
+    assert s[x].shape == (3,) and host(s[x]).tolist() == [3.0, 3.0, 3.0]
+    assert s[y].shape == (2, 1) and host(s[y]).tolist() == [[6.0], [6.0]]
+    P.reset_tape()
+    x = dev([[1.0, 7.0, 7.0]], True)
+    assert host(P.backward(P.sum(P.max(x, axis=1)))[x]).tolist() == [[0.0, 1.0, 0.0]]
+    P.reset_tape()
+    x = dev([[1.0, 2.0], [3.0, 4.0]], True)
+    yv = P.reshape(P.transpose2d(x), (4,))
+    assert host(P.backward(P.sum(P.mul(yv, yv)))[x]).tolist() == [[2.0, 4.0], [6.0, 8.0]]
+    P.reset_tape()
+    x = dev([1.0, 2.0, 3.0, 4.0], True)
+    assert host(P.backward(P.mean(x))[x]).tolist() == [0.25] * 4
+
+
+def test_mutation_guard():
+    x = dev([1.0, 2.0], True)
+    y = P.mul(x, x)
+    x.write_flat([5.0, 6.0])
+    with pytest.raises(P.GradError):
+        P.backward(P.sum(y))
+
+
+def test_allocator_reuses_blocks_and_counts_launches():
+    from paper_2602_00125_b200 import _lib as L
+
+    t = P.add(P.ones((1024, 1024)), 1.0)
+    del t
+    n0 = L.launch_count()
+    m0 = L.alloc_stats()["cuda_mallocs"]
+    for _ in range(20):
+        t = P.add(P.ones((1024, 1024)), 1.0)
+        del t
+    assert L.launch_count() - n0 >= 40
+    assert L.alloc_stats()["cuda_mallocs"] - m0 == 0  # every block came from the cache
