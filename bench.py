@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark: BASELINE config 5 -- data-parallel MLP training step, samples/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+One step = forward of 4 x Linear(4096,4096)+ReLU + Linear(4096,1000) over the
+rank's shard of the 65536-sample global batch, mean cross-entropy, backward,
+gradient all-reduce over NCCL (N > 1), one fused Adam(lr=1e-3) update. fp32
+everywhere (3xTF32 tcgen05 GEMMs = fp32 accuracy). Global batch fixed ->
+strong scaling. Timing: W warm-up steps, barrier + device sync, CUDA events on
+the engine stream around exactly K steps, max over ranks. Inputs (1 GiB per
+rank at N=1) are larger than L2, so no explicit flush.
+
+Keys beyond the base contract:
+  e2e         same metric through the public API with the batch copied
+              host(pinned)->device every step and the loss read back
+  roofline    dominant kernel (tcgen05 3xTF32 GEMM): algorithmic FLOPs per
+              launch / its CUDA-event duration inside a real step
+  cpu_baseline  the NumPy oracle port of the reference on this host's cores
+  ops         the per-op benchmarks of configs 2-4 (1 GPU, rank 0)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GLOBAL_BATCH = 65536
+WIDTH, CLASSES, DEPTH = 4096, 1000, 4
+METRIC = "MLP train samples/s (BASELINE config 5: 4x4096 + 4096->1000, global batch 65536, Adam)"
+
+
+def flops_per_step(batch):
+    """fwd 2*B*(4*4096^2 + 4096*1000); dW same; dX for layers 2..5 (x needs no grad)."""
+    fw = 2 * batch * (DEPTH * WIDTH * WIDTH + WIDTH * CLASSES)
+    dx = 2 * batch * ((DEPTH - 1) * WIDTH * WIDTH + WIDTH * CLASSES)
+    return fw + fw + dx
+
+
+# --------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the GEMM kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("flops_per_launch")
+    except Exception:
+        return None, None
+
+
+# --------------------------------------------------------------------- reference arm
+
+
+def cpu_oracle_step_rate(sample_rows=512, width=WIDTH, seed=0, budget_s=25.0):
+    """The NumPy f64 restatement of the reference (oracle/tensorlite_np.py) on
+    this host: fwd+bwd over `sample_rows` rows of the config-5 workload and one
+    Adam step over all 71.2M parameters; extrapolated to the 65536 batch as
+    65536 / (t_fwdbwd * 65536/rows + t_adam) (the optimizer is
+    charged once per step)."""
+    from oracle import tensorlite_np as O
+    from paper_2602_00125_b200.data import mlp_config5
+
+    params = mlp_config5(seed, WIDTH, CLASSES, DEPTH)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((sample_rows, width), dtype=np.float32)
+    labels = rng.integers(0, CLASSES, sample_rows)
+
+    class _NoOpt:
+        def step(self, key, th, g):
+            return th
+
+    t0 = time.perf_counter()
+    r = O.mlp_train_step(params, x, labels, _NoOpt())
+    t_fb = time.perf_counter() - t0
+    adam = O.Adam(lr=1e-3)
+    t0 = time.perf_counter()
+    for i, ((w, b), (gw, gb)) in enumerate(zip(params, r["grads"])):
+        adam.step(("w", i), w, gw)
+        adam.step(("b", i), b, gb)
+    t_adam = time.perf_counter() - t0
+    step_s = t_fb * (GLOBAL_BATCH / sample_rows) + t_adam
+    return GLOBAL_BATCH / step_s, {"t_fwdbwd_s": t_fb, "t_adam_s": t_adam, "rows": sample_rows}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    vals = []
+    info = None
+    for _ in range(max(args.warmup, 0)):
+        cpu_oracle_step_rate(sample_rows=256)
+    for _ in range(args.steps):
+        v, info = cpu_oracle_step_rate()
+        vals.append(v)
+    v = statistics.median(vals)
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": GLOBAL_BATCH / v * 1000.0, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64 (fp32 stores)", "data": "synthetic",
+        "config": {"workload": "config5_mlp_4x4096_1000_b65536_adam", "global_batch": GLOBAL_BATCH,
+                   "parallelism": "cpu"},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
+                         "sample": f"{info['rows']} rows fwd+bwd + full Adam per step, "
+                                   f"extrapolated to 65536 (oracle/tensorlite_np.py, numpy BLAS "
+                                   f"threads={cores})"},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- op benchmarks (configs 2-4)
+
+
+def op_benchmarks():
+    import paper_2602_00125_b200 as P
+    from paper_2602_00125_b200 import _lib as L
+
+    out = {}
+
+    def timed(fn, iters):
+        fn()
+        L.synchronize()
+        e0, e1 = L.Event(), L.Event()
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        return e0.elapsed_ms(e1) / iters
+
+    # config 2: fused relu(a*b+b) fwd + fused bwd, and the 6 axis reductions
+    rng = np.random.default_rng(0)
+    a = P.from_numpy(rng.standard_normal((4096, 4096), dtype=np.float32))
+    b = P.from_numpy(rng.uniform(-1, 1, (1, 4096)).astype(np.float32))
+    n = 4096 * 4096
+    with P.no_grad():
+        ms = timed(lambda: P.fused_muladd_relu(a, b), 20)
+        out["config2_fused_fwd_gbs"] = 2 * 4 * n / ms / 1e6
+        ms = timed(lambda: P.muladd_relu_sum_grads(a, b), 20)
+        out["config2_fused_bwd_gbs"] = 2 * 4 * n / ms / 1e6
+        ms = timed(lambda: P.exp(a), 20)
+        out["config2_exp_gbs"] = 2 * 4 * n / ms / 1e6
+        ms = timed(lambda: P.mul(a, b), 20)
+        out["config2_mul_bcast_gbs"] = 2 * 4 * n / ms / 1e6
+        for ax in (0, 1):
+            ms = timed(lambda: P.sum(a, axis=ax), 20)
+            out[f"config2_sum_dim{ax}_gbs"] = 4 * n / ms / 1e6
+            ms = timed(lambda: P.max(a, axis=ax), 20)
+            out[f"config2_max_dim{ax}_gbs"] = 4 * n / ms / 1e6
+        ms = timed(lambda: P.sum(a), 20)
+        out["config2_sum_all_gbs"] = 4 * n / ms / 1e6
+    del a, b
+    # config 3: square matmul fwd+bwd (3 GEMMs, 6 n^3 flops)
+    for size in (1024, 4096, 8192):
+        A = P.from_numpy(rng.uniform(-1, 1, (size, size)).astype(np.float32), requires_grad=True)
+        B = P.from_numpy(rng.uniform(-1, 1, (size, size)).astype(np.float32), requires_grad=True)
+        dC = P.from_numpy(rng.standard_normal((size, size), dtype=np.float32))
+
+        def fb():
+            P.reset_tape()
+            A.buffer.version += 1  # fresh operands every iteration: no split reuse
+            B.buffer.version += 1
+            C = P.mm(A, B)
+            P.backward(C, seed=dC)
+
+        ms = timed(fb, 3 if size == 8192 else 5)
+        out[f"config3_n{size}_fwdbwd_tflops"] = 6 * size ** 3 / ms / 1e9
+        del A, B, dC
+    P.reset_tape()
+    # config 4: softmax(X@W + b), loss = mean(Y*T), full backward
+    X = P.from_numpy(rng.standard_normal((64, 512, 1024), dtype=np.float32), requires_grad=True)
+    W = P.from_numpy(rng.normal(0, 0.03, (1024, 1024)).astype(np.float32), requires_grad=True)
+    bias = P.zeros((1024,), requires_grad=True)
+    Tt = P.from_numpy(rng.uniform(0, 1, (64, 512, 1024)).astype(np.float32))
+
+    def c4():
+        P.reset_tape()
+        X.buffer.version += 1
+        W.buffer.version += 1
+        Y = P.softmax(P.add(P.mm(X, W), bias))
+        P.backward(P.mean(P.mul(Y, Tt)))
+
+    ms = timed(c4, 5)
+    out["config4_ms_per_step"] = ms
+    out["config4_gemm_tflops_effective"] = 3 * 2 * 32768 * 1024 * 1024 / ms / 1e9
+    P.reset_tape()
+    return out
+
+
+# --------------------------------------------------------------------- main arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-ops", action="store_true", help="skip the config 2-4 op benchmarks")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import paper_2602_00125_b200 as P
+    from paper_2602_00125_b200 import _lib as L, dist, nn, optim
+    from paper_2602_00125_b200 import core as C
+    from paper_2602_00125_b200.data import PinnedFeeder, batch_shard, build_mlp, mlp_config5
+
+    env = dist.env_from_os()
+    comm = dist.Communicator(env)
+    world, rank = env.world, env.rank
+    lo, hi = dist.shard_rows(GLOBAL_BATCH, rank, world)
+    rows = hi - lo
+
+    model = build_mlp(mlp_config5(0, WIDTH, CLASSES, DEPTH))
+    params = model.parameters()
+    opt = optim.Adam(lr=1e-3, betas=(0.9, 0.999), eps=1e-8)
+    x_np, y_np = batch_shard(1234, rank, rows, WIDTH, CLASSES)
+    feeder = PinnedFeeder(x_np, y_np)
+    x_dev = P.from_numpy(x_np)
+    y_dev = nn.labels_buffer(y_np)
+    del x_np
+
+    gemm_log = []
+
+    def step(x, labels, read_loss=False):
+        P.reset_tape()
+        x.buffer.version += 1  # a new batch each step: its 3xTF32 split is redone
+        logits = model(x)
+        loss = nn.cross_entropy(logits, labels, denom=rows)
+        red = dist.GradReducer(comm, params)
+        store = P.backward(loss, on_leaf_ready=red.hook)
+        red.finish()
+        optim.step_all(opt, params, store)
+        return loss.item() if read_loss else loss
+
+    for _ in range(max(args.warmup, 0)):
+        step(x_dev, y_dev)
+    comm.barrier()
+
+    sampler = ClockSampler(env.local_rank)
+    sampler.start()
+    n0 = L.launch_count()
+    e0, e1 = L.Event(), L.Event()
+    e0.record()
+    for _ in range(args.steps):
+        last = step(x_dev, y_dev)
+    e1.record()
+    L.synchronize()
+    launches = L.launch_count() - n0
+    comm.barrier()
+    ms_local = e0.elapsed_ms(e1) / args.steps
+    clocks = sampler.stop()
+    ms = comm.max_scalar(ms_local)
+    value = GLOBAL_BATCH / (ms / 1000.0)
+    loss_val = last.item()
+
+    # e2e: same step through the public API, batch H2D from pinned host memory
+    # every step and the loss read back to the host every step
+    for _ in range(2):
+        xb, yb = feeder.next()
+        step(xb, yb, read_loss=True)
+    comm.barrier()
+    e2, e3 = L.Event(), L.Event()
+    e2.record()
+    for _ in range(args.steps):
+        xb, yb = feeder.next()
+        step(xb, yb, read_loss=True)
+    e3.record()
+    L.synchronize()
+    comm.barrier()
+    ms_e2e = comm.max_scalar(e2.elapsed_ms(e3) / args.steps)
+
+    # roofline of the dominant kernel: time every GEMM launch of one step
+    C.GEMM_TIMER = gemm_log
+    step(x_dev, y_dev)
+    L.synchronize()
+    C.GEMM_TIMER = None
+    g_flops = sum(f for f, _, _ in gemm_log)
+    g_ms = sum(s.elapsed_ms(e) for _, s, e in gemm_log)
+    n_gemm = len(gemm_log)
+    achieved = g_flops / (g_ms / 1000.0) / 1e12
+    peaks, src = measured_peaks()
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    traffic, tr_flops = ncu_traffic()
+    roof = {
+        "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved / peak, "traffic": traffic,
+        "kernel": "k_gemm_tc<3xTF32> (tcgen05.mma kind::tf32, 3 MMAs per fp32 MAC)",
+        "algorithmic_flops_per_step": g_flops, "gemm_launches_per_step": n_gemm,
+        "gemm_ms_per_step": g_ms, "gemm_share_of_step": g_ms / ms,
+        "peak_source": f"{src} bf16 dense sustained (MEASURED_PEAKS.json)",
+        "frac_of_3xtf32_ceiling": achieved / (peak / 6.0),
+        "note": "3xTF32 issues 3 tf32 MMAs per fp32 MAC at half the bf16 rate: ceiling = bf16/6",
+    }
+
+    ops = None
+    cpu = None
+    if rank == 0 and world == 1:
+        if not args.no_ops:
+            ops = op_benchmarks()
+        if not args.no_cpu:
+            v_cpu, info = cpu_oracle_step_rate()
+            cpu = {"value": v_cpu, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"{info['rows']} rows fwd+bwd ({info['t_fwdbwd_s']:.2f}s) + full Adam "
+                             f"({info['t_adam_s']:.2f}s), extrapolated to 65536 rows"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic (seeded N(0,1) inputs, uniform labels; reference Dense init)",
+            "config": {"workload": "config5_mlp_4x4096_1000_b65536_adam",
+                       "global_batch": GLOBAL_BATCH, "per_gpu_batch": rows,
+                       "layers": "4xLinear(4096,4096)+ReLU, Linear(4096,1000)",
+                       "optimizer": "Adam lr=1e-3 betas=(0.9,0.999) eps=1e-8",
+                       "gemm": "3xTF32 tcgen05 (fp32 accuracy)",
+                       "parallelism": f"dp{world}", "l2": "inputs > L2 (1 GiB/rank at N=1)"},
+            "e2e": {"value": GLOBAL_BATCH / (ms_e2e / 1000.0), "unit": "samples/s",
+                    "h2d_bytes_per_step": feeder.h2d_bytes, "d2h_bytes_per_step": 4},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "launches_per_step": launches / args.steps,
+            "tflops_per_gpu": flops_per_step(rows) / (ms / 1000.0) / 1e12,
+            "final_loss": loss_val,
+            "ops": ops,
+        }
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -488,7 +488,10 @@ def _launch_unary(op, x, alpha=0.0, beta=0.0) -> Tensor:
 def _unary(kind, op, x, pullback, save):
     x = _as_tensor(_as_operand(x))
     out = _launch_unary(op, x)
-    return record(kind, (x,), out, (pullback(x, out),), saved=save(x, out))
+    # pullbacks see a node-less alias of `out`: output -> node -> closure -> output
+    # would be a reference cycle that keeps HBM alive until the cyclic GC runs
+    keep = out.detach()
+    return record(kind, (x,), out, (pullback(x, keep),), saved=save(x, keep))
 
 
 def neg(x) -> Tensor:
@@ -740,6 +743,7 @@ def _split(t, rows, cols, ld):
 
 
 _ALGO_OVERRIDE = None
+GEMM_TIMER = None  # bench/profiling: a list receiving (flops, start_event, end_event) per GEMM kernel
 
 
 def set_gemm_algo(name):
@@ -767,14 +771,28 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE):
         br, bc = (N, K) if tb else (K, N)
         ahi, alo = _split(xa, ar, ac, lda)
         bhi, blo = _split(wb, br, bc, ldb)
+        ev = _timer_start()
         L.call("b2_gemm_presplit", ta, tb, M, N, K, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr,
                out.data_ptr, N, bptr, epi, None)
     else:
         if algo == L.GEMM_3XTF32:
             algo = L.GEMM_SIMT
+        ev = _timer_start()
         L.call("b2_gemm", ta, tb, M, N, K, xa.data_ptr, lda, wb.data_ptr, ldb, out.data_ptr, N,
                bptr, epi, algo, None)
+    if ev is not None:
+        end = L.Event()
+        end.record()
+        GEMM_TIMER.append((2.0 * M * N * K, ev, end))
     return out
+
+
+def _timer_start():
+    if GEMM_TIMER is None:
+        return None
+    ev = L.Event()
+    ev.record()
+    return ev
 
 
 def matmul(x, w) -> Tensor:
@@ -833,13 +851,14 @@ def linear(x, weight, bias=None, relu_out=False) -> Tensor:
         bc = bias if (bias is None or bias.is_contiguous) else _copy_contig(bias)
         _gemm_into(out, x, weight, bc, epi)
     memo = [None, None]
+    y = out.detach()  # no output->node->closure->output cycle (see _unary)
 
     def pre(g):  # cotangent at the pre-activation (relu pullback, nn.py:101-103)
         if not relu_out:
             return g
         if memo[0] is not g:
             memo[0] = g
-            memo[1] = _launch_binary(L.RELU_BWD, g, out, out.shape)
+            memo[1] = _launch_binary(L.RELU_BWD, g, y, y.shape)
         return memo[1]
 
     pulls = [lambda g: matmul(pre(g), transpose2d(weight)),
@@ -849,7 +868,7 @@ def linear(x, weight, bias=None, relu_out=False) -> Tensor:
         inputs.append(bias)
         pulls.append(lambda g: reduce_to_shape(pre(g), bias.shape))
     return record("linear_relu" if relu_out else "linear", tuple(inputs), out, tuple(pulls),
-                  saved=(x, weight, out) if relu_out else (x, weight))
+                  saved=(x, weight, y) if relu_out else (x, weight))
 
 
 # ---------------------------------------------------------------------------
@@ -899,10 +918,11 @@ def fused_muladd_relu(a, b, c=None) -> Tensor:
     y = _empty(a.shape)
     L.call("b2_fused_muladd_relu_fwd", y.data_ptr, a.data_ptr, b.data_ptr, c.data_ptr, R, C, None)
     memo = [None, None]
+    yk = y.detach()
 
     def pre(g):
         if memo[0] is not g:
-            memo[0], memo[1] = g, _launch_binary(L.RELU_BWD, g, y, y.shape)
+            memo[0], memo[1] = g, _launch_binary(L.RELU_BWD, g, yk, yk.shape)
         return memo[1]
 
     if c is b:

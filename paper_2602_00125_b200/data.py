@@ -1,0 +1,108 @@
+"""Synthetic inputs for the BASELINE configs and a pinned-memory batch feeder.
+
+No dataset is involved anywhere (the reference's demos are
+synthetic, BASELINE.json names none); batches come from seeded
+numpy.random.default_rng streams with the shapes and distributions of
+BASELINE.json's configs.
+
+``PinnedFeeder`` is the host->device path of a training loop: batches live in
+page-locked host memory and are copied into device buffers with
+cudaMemcpyAsync on the engine stream, so a step's H2D is part of its stream
+(this is what bench.py's ``e2e`` number times).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _lib as L
+from . import core as T
+
+
+def linear_params(rng, fan_in, fan_out):
+    """Kaiming-uniform (PyTorch Linear default) == the reference Dense bound
+    U(+-1/sqrt(in)) for W and b (nn.py:64-76)."""
+    bound = 1.0 / math.sqrt(fan_in)
+    w = rng.uniform(-bound, bound, size=(fan_out, fan_in)).astype(np.float32)
+    b = rng.uniform(-bound, bound, size=fan_out).astype(np.float32)
+    return w, b
+
+
+def mlp_config5(seed=0, width=4096, classes=1000, depth=4):
+    """BASELINE config 5 parameters: depth x Linear(width,width)+ReLU, then
+    Linear(width, classes)."""
+    rng = np.random.default_rng(seed)
+    params = [linear_params(rng, width, width) for _ in range(depth)]
+    params.append(linear_params(rng, width, classes))
+    return params
+
+
+def batch_shard(seed, rank, rows, width, classes):
+    """This rank's rows of the global batch: x ~ N(0,1) f32, labels ~ U{0..C-1}."""
+    rng = np.random.default_rng([seed, rank])
+    x = rng.standard_normal((rows, width), dtype=np.float32)
+    labels = rng.integers(0, classes, size=rows, dtype=np.int64)
+    return x, labels
+
+
+def build_mlp(params):
+    """nn.Sequential of Dense(+ReLU) layers with the given (W, b) values."""
+    from . import nn
+
+    layers = []
+    for i, (w, b) in enumerate(params):
+        d = nn.Dense.__new__(nn.Dense)
+        nn.Layer.__init__(d)
+        d.in_features, d.out_features = w.shape[1], w.shape[0]
+        d.weight = T.from_numpy(w, requires_grad=True)
+        d.bias = T.from_numpy(b, requires_grad=True)
+        layers.append(d)
+        if i < len(params) - 1:
+            layers.append(nn.ReLU())
+    return nn.Sequential(*layers)
+
+
+class PinnedHost:
+    """A page-locked host array (cudaMallocHost) viewed as a numpy array."""
+
+    def __init__(self, shape, dtype):
+        L.ensure_device()
+        self.nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = ctypes.c_void_p()
+        L.check(L.lib().b2_host_alloc(max(self.nbytes, 1), ctypes.byref(p)))
+        self.ptr = p.value
+        buf = (ctypes.c_char * max(self.nbytes, 1)).from_address(self.ptr)
+        self.array = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def __del__(self):
+        try:
+            if self.ptr and L._lib is not None:
+                L._lib.b2_host_free(self.ptr)
+        except Exception:
+            pass
+
+
+class PinnedFeeder:
+    """Host batch (pinned) -> device tensor + int64 label buffer, per step."""
+
+    def __init__(self, x, labels):
+        self.hx = PinnedHost(x.shape, np.float32)
+        self.hx.array[...] = x
+        self.hl = PinnedHost(labels.shape, np.int64)
+        self.hl.array[...] = labels
+        self.dx = T._empty(x.shape)
+        self.dl = T.Buffer(8 * max(labels.size, 1))
+
+    @property
+    def h2d_bytes(self):
+        return self.hx.nbytes + self.hl.nbytes
+
+    def next(self):
+        """Queue this step's H2D copies on the engine stream; returns (x, labels)."""
+        L.call("b2_memcpy_h2d", self.dx.data_ptr, self.hx.ptr, self.hx.nbytes, None)
+        L.call("b2_memcpy_h2d", self.dl.ptr, self.hl.ptr, self.hl.nbytes, None)
+        self.dx.buffer.version += 1
+        return self.dx, self.dl

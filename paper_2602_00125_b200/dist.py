@@ -1,0 +1,152 @@
+"""Data-parallel training over NCCL (new: the reference is single-process,
+SURVEY 2.1 / 8e).
+
+One process per GPU (torchrun / torch.distributed.run env). The NCCL unique
+id travels over torch.distributed's TCPStore -- torch is plumbing here; the
+communicator itself lives in libb2 (b2_comm_init / b2_allreduce_f32) and the
+all-reduce runs on a libb2 stream next to the backward kernels.
+
+Config 5 is the only partitioned path: every rank holds a full replica,
+takes a contiguous 1/N slice of the global batch, computes the mean loss of
+its slice, and gradients are averaged (ncclAvg) -- the mean of equal-shard
+means is the global mean. Gradient all-reduces are issued as soon as a
+parameter's last gradient contribution has been queued by ``backward``
+(reverse layer order), on a dedicated communication stream, so they overlap
+the remaining backward GEMMs; the optimizer's stream waits for them.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+from . import _lib as L
+
+AVG, SUM, MAX = 1, 0, 2
+
+
+@dataclass
+class Env:
+    rank: int = 0
+    world: int = 1
+    local_rank: int = 0
+    master_addr: str = "127.0.0.1"
+    master_port: int = 29500
+
+
+def env_from_os() -> Env:
+    return Env(rank=int(os.environ.get("RANK", 0)), world=int(os.environ.get("WORLD_SIZE", 1)),
+               local_rank=int(os.environ.get("LOCAL_RANK", 0)),
+               master_addr=os.environ.get("MASTER_ADDR", "127.0.0.1"),
+               master_port=int(os.environ.get("MASTER_PORT", 29500)))
+
+
+def shard_rows(global_rows: int, rank: int, world: int):
+    """Contiguous [start, stop) rows of rank's shard; equal shards required so
+    that the average of shard means is the global mean."""
+    if global_rows % world:
+        raise ValueError(f"global batch {global_rows} is not divisible by {world} ranks")
+    per = global_rows // world
+    return rank * per, (rank + 1) * per
+
+
+def exchange_unique_id(store, rank: int, make_uid, key="b2_nccl_uid") -> bytes:
+    """Rank 0 publishes `make_uid()` under `key`; everyone returns it.
+    `store` is any torch.distributed Store (TCPStore / FileStore / HashStore)."""
+    if rank == 0:
+        uid = bytes(make_uid())
+        store.set(key, uid)
+        return uid
+    store.wait([key])
+    return bytes(store.get(key))
+
+
+def make_store(env: Env, port_offset=1):
+    import datetime
+
+    from torch.distributed import TCPStore
+
+    return TCPStore(env.master_addr, env.master_port + port_offset, env.world, env.rank == 0,
+                    timeout=datetime.timedelta(seconds=300))
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    L.check(L.lib().b2_comm_unique_id(buf))
+    return buf.raw
+
+
+class Communicator:
+    """libb2's NCCL communicator for this process's GPU."""
+
+    def __init__(self, env: Env, store=None):
+        self.env = env
+        L.ensure_device(env.local_rank)
+        self.comm_stream = None
+        if env.world > 1:
+            store = store or make_store(env)
+            self._store = store
+            uid = exchange_unique_id(store, env.rank, nccl_unique_id)
+            L.check(L.lib().b2_comm_init(env.rank, env.world, uid))
+            s = ctypes.c_void_p()
+            L.check(L.lib().b2_stream_create(ctypes.byref(s)))
+            self.comm_stream = s.value
+
+    @property
+    def world(self):
+        return self.env.world
+
+    def allreduce_(self, t, op=AVG, stream=None):
+        if self.env.world > 1 and t.size:
+            L.call("b2_allreduce_f32", t.data_ptr, t.size, op, stream)
+        return t
+
+    def barrier(self):
+        if self.env.world > 1:
+            from . import core as T
+
+            t = T.ones((1,))
+            self.allreduce_(t, SUM)
+        L.call("b2_device_sync")
+
+    def max_scalar(self, v: float) -> float:
+        """Max of a host float over ranks (device NCCL allreduce)."""
+        if self.env.world == 1:
+            return v
+        from . import core as T
+
+        t = T.full((1,), v)
+        self.allreduce_(t, MAX)
+        return t.item()
+
+
+class GradReducer:
+    """Overlapped gradient averaging for one backward pass.
+
+    Pass ``hook`` as ``backward(loss, on_leaf_ready=reducer.hook)``; call
+    ``finish()`` before the optimizer step."""
+
+    def __init__(self, comm: Communicator, params):
+        self.comm = comm
+        self._ids = {}
+        self._params = list(params)
+        self._pending = []
+
+    def hook(self, node_id, grad):
+        if self.comm.world == 1:
+            return
+        s = self.comm.comm_stream
+        ev = L.Event()
+        ev.record(None)  # grad produced on the compute stream
+        L.call("b2_stream_wait_event", s, ev.h)
+        self.comm.allreduce_(grad, AVG, s)
+        self._pending.append(ev)
+
+    def finish(self):
+        if self.comm.world == 1:
+            return
+        done = L.Event()
+        done.record(self.comm.comm_stream)
+        L.call("b2_stream_wait_event", None, done.h)  # optimizer waits for the reduces
+        self._pending.clear()
