@@ -460,3 +460,27 @@ def test_allocator_reuses_blocks_and_counts_launches():
         del t
     assert L.launch_count() - n0 >= 40
     assert L.alloc_stats()["cuda_mallocs"] - m0 == 0  # every block came from the cache
+
+
+def test_train_steps_do_not_leak_device_memory():
+    from paper_2602_00125_b200 import _lib as L
+    from paper_2602_00125_b200.data import build_mlp, mlp_config5
+
+    model = build_mlp(mlp_config5(0, width=256, classes=10, depth=2))
+    opt = optim.Adam(lr=1e-3)
+    x = dev(np.random.default_rng(0).standard_normal((512, 256)))
+    labels = np.arange(512) % 10
+    use = []
+    for _ in range(6):
+        P.reset_tape()
+        loss = nn.cross_entropy(model(x), labels)
+        optim.step_all(opt, model.parameters(), P.backward(loss))
+        L.synchronize()
+        use.append(L.alloc_stats()["in_use"])
+    assert use[-1] == use[-3] and use[-2] == use[-4], use  # steady state, no growth
+
+
+def test_smoke_entry_point():
+    import __graft_entry__
+
+    __graft_entry__.smoke()
