@@ -119,10 +119,12 @@ int b2_max_scatter(float* gx, int ndim, const int64_t* shape, uint32_t reduce_ma
  * dimensions lda/ldb/ldc in elements. trans_a: A stored [K,M]; trans_b: B
  * stored [N,K] (the reference's x.w^T is trans_b=1).
  * algo: 0 auto, 1 FP32 SIMT (FFMA), 2 3xTF32 on tcgen05 (fp32 accuracy),
- *       3 1xTF32 on tcgen05 (fast, ~1e-3 rel; never chosen by auto).
+ *       3 1xTF32 on tcgen05 (fast, ~1e-3 rel; never chosen by auto),
+ *       4 TF32X: tf32 main product + the two cross terms as bf16 MMAs
+ *         (2 tf32-equivalent MMAs per fp32 MAC, fp32-grade accuracy).
  */
 enum b2_gemm_algo { B2_GEMM_AUTO = 0, B2_GEMM_SIMT = 1, B2_GEMM_3XTF32 = 2,
-                    B2_GEMM_1XTF32 = 3 };
+                    B2_GEMM_1XTF32 = 3, B2_GEMM_TF32X = 4 /* tf32 hi*hi + bf16 hi*lo + lo*hi */ };
 enum b2_epilogue { B2_EPI_NONE = 0, B2_EPI_BIAS = 1, B2_EPI_BIAS_RELU = 2, B2_EPI_RELU = 3 };
 int b2_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
             const float* A, int64_t lda, const float* B, int64_t ldb,
@@ -141,6 +143,15 @@ int b2_gemm_presplit(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
                      const float* A_hi, const float* A_lo, const float* B_hi,
                      const float* B_lo, float* C, int64_t ldc, const float* bias,
                      int epilogue, void* stream);
+
+/* split into contiguous bf16(trunc_tf32(x)) and bf16(x - trunc_tf32(x)); cols % 8 == 0 */
+int b2_bf16x2_split(void* hi16, void* lo16, const float* x, int64_t rows, int64_t cols,
+                    int64_t ld, void* stream);
+/* TF32X GEMM: A/B raw fp32 (lda/ldb) + their contiguous b2_bf16x2_split halves */
+int b2_gemm_tf32x(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
+                  const float* A, int64_t lda, const void* A_hi16, const void* A_lo16,
+                  const float* B, int64_t ldb, const void* B_hi16, const void* B_lo16,
+                  float* C, int64_t ldc, const float* bias, int epilogue, void* stream);
 
 /* ---------------------------------------------------------------- losses
  * cross_entropy (nn.py:453-503): fwd writes the mean loss (f32 scalar) and

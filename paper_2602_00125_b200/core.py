@@ -726,18 +726,22 @@ def _as_B(t):
     return 1, K, c
 
 
-def _split(t, rows, cols, ld):
-    """Cached (hi, lo) 3xTF32 split of the stored matrix region of t."""
+def _split(t, rows, cols, ld, kind):
+    """Cached split of the stored matrix region of t for a tensor-core GEMM:
+    kind "tf32x" -> (bf16 hi, bf16 lo) of trunc_tf32(x) / x - trunc (2 B each),
+    kind "3xtf32" -> (fp32 hi, fp32 lo). Invalidated by the buffer version."""
     buf = t.buffer
-    key = (t.offset, rows, cols, ld)
+    key = (kind, t.offset, rows, cols, ld)
     if buf._splits is None:
         buf._splits = {}
     ent = buf._splits.get(key)
     if ent is not None and ent[0] == buf.version:
         return ent[1], ent[2]
     n = rows * cols
-    hi, lo = Buffer(4 * n), Buffer(4 * n)
-    L.call("b2_tf32_split", hi.ptr, lo.ptr, t.data_ptr, rows, cols, ld, None)
+    esz = 2 if kind == "tf32x" else 4
+    hi, lo = Buffer(esz * n), Buffer(esz * n)
+    fn = "b2_bf16x2_split" if kind == "tf32x" else "b2_tf32_split"
+    L.call(fn, hi.ptr, lo.ptr, t.data_ptr, rows, cols, ld, None)
     buf._splits[key] = (buf.version, hi, lo)
     return hi, lo
 
@@ -750,7 +754,7 @@ def set_gemm_algo(name):
     """Force 'simt' | '3xtf32' | '1xtf32' | None (auto) for subsequent matmuls."""
     global _ALGO_OVERRIDE
     _ALGO_OVERRIDE = {None: None, "auto": None, "simt": L.GEMM_SIMT, "3xtf32": L.GEMM_3XTF32,
-                      "1xtf32": L.GEMM_1XTF32}[name]
+                      "1xtf32": L.GEMM_1XTF32, "tf32x": L.GEMM_TF32X}[name]
 
 
 def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE):
@@ -765,17 +769,24 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE):
         L.check(L.lib().b2_gemm_select(ta, tb, M, N, K, lda, ldb, ctypes.byref(sel)))
         algo = sel.value
     bptr = bias.data_ptr if bias is not None else None
-    if algo == L.GEMM_3XTF32 and K > 0 and (M if ta else K) % 4 == 0 and (K if tb else N) % 4 == 0 \
-            and lda % 4 == 0 and ldb % 4 == 0:
-        ar, ac = (K, M) if ta else (M, K)
-        br, bc = (N, K) if tb else (K, N)
-        ahi, alo = _split(xa, ar, ac, lda)
-        bhi, blo = _split(wb, br, bc, ldb)
+    tc_ok = (K > 0 and (M if ta else K) % 8 == 0 and (K if tb else N) % 8 == 0
+             and lda % 4 == 0 and ldb % 4 == 0 and xa.data_ptr % 16 == 0 and wb.data_ptr % 16 == 0)
+    ar, ac = (K, M) if ta else (M, K)
+    br, bc = (N, K) if tb else (K, N)
+    if algo == L.GEMM_TF32X and tc_ok:
+        ahi, alo = _split(xa, ar, ac, lda, "tf32x")
+        bhi, blo = _split(wb, br, bc, ldb, "tf32x")
+        ev = _timer_start()
+        L.call("b2_gemm_tf32x", ta, tb, M, N, K, xa.data_ptr, lda, ahi.ptr, alo.ptr, wb.data_ptr,
+               ldb, bhi.ptr, blo.ptr, out.data_ptr, N, bptr, epi, None)
+    elif algo == L.GEMM_3XTF32 and tc_ok:
+        ahi, alo = _split(xa, ar, ac, lda, "3xtf32")
+        bhi, blo = _split(wb, br, bc, ldb, "3xtf32")
         ev = _timer_start()
         L.call("b2_gemm_presplit", ta, tb, M, N, K, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr,
                out.data_ptr, N, bptr, epi, None)
     else:
-        if algo == L.GEMM_3XTF32:
+        if algo in (L.GEMM_3XTF32, L.GEMM_TF32X):
             algo = L.GEMM_SIMT
         ev = _timer_start()
         L.call("b2_gemm", ta, tb, M, N, K, xa.data_ptr, lda, wb.data_ptr, ldb, out.data_ptr, N,

@@ -11,11 +11,14 @@ namespace b2 {
 int gemm_simt(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
               const float* B, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
               cudaStream_t st);
-int gemm_tc(int ta, int tb, int nprod, int64_t M, int64_t N, int64_t K, const float* Ahi,
-            const float* Alo, int64_t lda, const float* Bhi, const float* Blo, int64_t ldb,
-            float* C, int64_t ldc, const float* bias, int epi, cudaStream_t st);
+int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const void* a0,
+            const void* a1, const void* a2, int64_t lda, const void* b0, const void* b1,
+            const void* b2_, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
+            cudaStream_t st);
 int tf32_split(float* hi, float* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
                cudaStream_t st);
+int bf16x2_split(void* hi, void* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
+                 cudaStream_t st);
 bool tc_supported(int ta, int tb, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb);
 }  // namespace b2
 
@@ -30,6 +33,7 @@ int forced_algo() {
       if (!strcmp(e, "simt")) v = B2_GEMM_SIMT;
       else if (!strcmp(e, "3xtf32")) v = B2_GEMM_3XTF32;
       else if (!strcmp(e, "1xtf32")) v = B2_GEMM_1XTF32;
+      else if (!strcmp(e, "tf32x")) v = B2_GEMM_TF32X;
     }
   }
   return v;
@@ -42,7 +46,7 @@ int select(int ta, int tb, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t
   if (f) return f;
   // the tensor-core path pays a split pass + TMEM setup; small problems stay on FFMA
   double work = (double)M * (double)N * (double)K;
-  return work >= (double)(1 << 26) ? B2_GEMM_3XTF32 : B2_GEMM_SIMT;
+  return work >= (double)(1 << 26) ? B2_GEMM_TF32X : B2_GEMM_SIMT;
 }
 
 }  // namespace
@@ -78,7 +82,27 @@ int b2_gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, int
     case B2_GEMM_1XTF32:
       if (((uintptr_t)A & 15) || ((uintptr_t)B & 15))
         return b2::fail("b2_gemm(1xtf32): operands must be 16-byte aligned for TMA");
-      return b2::gemm_tc(ta, tb, 1, M, N, K, A, nullptr, lda, B, nullptr, ldb, C, ldc, bias, epi, st);
+      return b2::gemm_tc(ta, tb, 1, M, N, K, A, nullptr, nullptr, lda, B, nullptr, nullptr, ldb, C,
+                         ldc, bias, epi, st);
+    case B2_GEMM_TF32X: {
+      if (((uintptr_t)A & 15) || ((uintptr_t)B & 15))
+        return b2::fail("b2_gemm(tf32x): operands must be 16-byte aligned for TMA");
+      int64_t ar = ta ? K : M, ac = ta ? M : K;
+      int64_t br = tb ? N : K, bc = tb ? K : N;
+      size_t abytes = (size_t)ar * ac * 2, bbytes = (size_t)br * bc * 2;
+      abytes = (abytes + 255) & ~(size_t)255;
+      bbytes = (bbytes + 255) & ~(size_t)255;
+      void* ws = nullptr;
+      B2_TRY(b2_alloc(2 * (abytes + bbytes), st, &ws));
+      char* w = (char*)ws;
+      int rc = b2::bf16x2_split(w, w + abytes, A, ar, ac, lda, st);
+      if (!rc) rc = b2::bf16x2_split(w + 2 * abytes, w + 2 * abytes + bbytes, B, br, bc, ldb, st);
+      if (!rc)
+        rc = b2::gemm_tc(ta, tb, 2, M, N, K, A, w, w + abytes, lda, B, w + 2 * abytes,
+                         w + 2 * abytes + bbytes, ldb, C, ldc, bias, epi, st);
+      b2_free(ws, st);
+      return rc;
+    }
     case B2_GEMM_3XTF32: {
       // A: [M,K] (K-major) or stored [K,M]; B: [N,K] (trans_b) or stored [K,N]
       int64_t ar = ta ? K : M, ac = ta ? M : K;
@@ -92,7 +116,9 @@ int b2_gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, int
       float* blo = (float*)((char*)ws + 2 * abytes + bbytes);
       int rc = b2::tf32_split(ahi, alo, A, ar, ac, lda, st);
       if (!rc) rc = b2::tf32_split(bhi, blo, B, br, bc, ldb, st);
-      if (!rc) rc = b2::gemm_tc(ta, tb, 3, M, N, K, ahi, alo, ac, bhi, blo, bc, C, ldc, bias, epi, st);
+      if (!rc)
+        rc = b2::gemm_tc(ta, tb, 3, M, N, K, ahi, alo, nullptr, ac, bhi, blo, nullptr, bc, C, ldc,
+                         bias, epi, st);
       b2_free(ws, st);
       return rc;
     }
@@ -109,8 +135,26 @@ int b2_gemm_presplit(int ta, int tb, int64_t M, int64_t N, int64_t K, const floa
   int64_t ac = ta ? M : K, bc = tb ? K : N;
   if (!b2::tc_supported(ta, tb, M, N, K, ac, bc))
     return b2::fail("b2_gemm_presplit: operands not TMA-compatible");
-  return b2::gemm_tc(ta, tb, 3, M, N, K, Ahi, Alo, ac, Bhi, Blo, bc, C, ldc, bias, epi,
-                     b2::resolve(stream));
+  return b2::gemm_tc(ta, tb, 3, M, N, K, Ahi, Alo, nullptr, ac, Bhi, Blo, nullptr, bc, C, ldc, bias,
+                     epi, b2::resolve(stream));
+}
+
+int b2_bf16x2_split(void* hi16, void* lo16, const float* x, int64_t rows, int64_t cols, int64_t ld,
+                    void* stream) {
+  return b2::bf16x2_split(hi16, lo16, x, rows, cols, ld, b2::resolve(stream));
+}
+
+// TF32 main product on the raw fp32 operands + the two cross terms as bf16
+// MMAs on caller-provided contiguous splits (b2_bf16x2_split of A and B).
+int b2_gemm_tf32x(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                  const void* A_hi16, const void* A_lo16, const float* B, int64_t ldb,
+                  const void* B_hi16, const void* B_lo16, float* C, int64_t ldc, const float* bias,
+                  int epi, void* stream) {
+  if (M == 0 || N == 0) return 0;
+  if (!b2::tc_supported(ta, tb, M, N, K, lda, ldb) || ((uintptr_t)A & 15) || ((uintptr_t)B & 15))
+    return b2::fail("b2_gemm_tf32x: operands not TMA-compatible");
+  return b2::gemm_tc(ta, tb, 2, M, N, K, A, A_hi16, A_lo16, lda, B, B_hi16, B_lo16, ldb, C, ldc,
+                     bias, epi, b2::resolve(stream));
 }
 
 }  // extern "C"

@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <cuda_bf16.h>
 
 #include <cstdlib>
 #include <cstring>
@@ -146,6 +147,24 @@ __host__ __device__ constexpr uint32_t idesc_tf32(bool a_mn, bool b_mn) {
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])              \
       : "r"(taddr))
 
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+// instruction descriptor, kind::f16 with BF16 inputs and an F32 accumulator
+__host__ __device__ constexpr uint32_t idesc_bf16(bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
 struct TcParams {
   float* C;
   const float* bias;
@@ -155,21 +174,80 @@ struct TcParams {
   int tiles_n, num_tiles;
 };
 
-template <bool A_MN, bool B_MN, int NPROD, int STAGES>
+// MODE 1: 1xTF32            tiles A32 | B32
+// MODE 3: 3xTF32            tiles Ahi | Alo | Bhi | Blo (fp32 arrays, hi = tf32(x))
+// MODE 2: TF32 + 2xBF16     tiles A32 | B32 | Ah16 | Al16 | Bh16 | Bl16: the main
+//         product runs on the raw fp32 operands (the tensor core truncates them
+//         to tf32: hi = trunc(x), probed on B200) and the two cross terms
+//         hi*lo + lo*hi run as kind::f16 MMAs on bf16(hi), bf16(lo) at twice the
+//         tf32 rate -- 2 tf32-equivalents per fp32 MAC instead of 3.
+template <int MODE>
 struct Cfg {
-  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
-  static constexpr int B_BYTES = BN * BK * 4;  // 32 KB
-  static constexpr int NA = NPROD == 3 ? 2 : 1;
-  static constexpr int STAGE_BYTES = NA * (A_BYTES + B_BYTES);
+  static constexpr int A32 = BM * BK * 4;  // 16 KB
+  static constexpr int B32 = BN * BK * 4;  // 32 KB
+  static constexpr int A16 = BM * BK * 2;  // 8 KB
+  static constexpr int B16 = BN * BK * 2;  // 16 KB
+  static constexpr int STAGE_BYTES = MODE == 1 ? A32 + B32 : (MODE == 3 ? 2 * (A32 + B32)
+                                                                       : A32 + B32 + 2 * (A16 + B16));
+  static constexpr int STAGES = MODE == 1 ? 4 : 2;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // byte offsets inside a stage
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_ALO = A32;                                 // MODE 3
+  static constexpr int OFF_B = MODE == 3 ? 2 * A32 : A32;
+  static constexpr int OFF_BLO = 2 * A32 + B32;                       // MODE 3
+  static constexpr int OFF_AH16 = A32 + B32;                          // MODE 2
+  static constexpr int OFF_AL16 = A32 + B32 + A16;
+  static constexpr int OFF_BH16 = A32 + B32 + 2 * A16;
+  static constexpr int OFF_BL16 = A32 + B32 + 2 * A16 + B16;
 };
 
-template <bool A_MN, bool B_MN, int NPROD, int STAGES>
+// fp32 tile (tf32 consumption): K-major = one box {32 K, rows}; MN-major = 32x32 boxes
+template <bool MN, int ROWS>
+__device__ __forceinline__ void load32(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, int mn0,
+                                       int k0) {
+  if (MN) {
+#pragma unroll
+    for (int j = 0; j < ROWS / 32; ++j) tma_load_2d(dst + j * 4096, tm, bar, mn0 + 32 * j, k0);
+  } else {
+    tma_load_2d(dst, tm, bar, k0, mn0);
+  }
+}
+
+// bf16 tile: K-major = one box {32 K (64 B), rows}; MN-major = boxes {64 MN (128 B), 32 K}
+template <bool MN, int ROWS>
+__device__ __forceinline__ void load16(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, int mn0,
+                                       int k0) {
+  if (MN) {
+#pragma unroll
+    for (int j = 0; j < ROWS / 64; ++j) tma_load_2d(dst + j * 4096, tm, bar, mn0 + 64 * j, k0);
+  } else {
+    tma_load_2d(dst, tm, bar, k0, mn0);
+  }
+}
+
+// UMMA descriptors for one k-step
+__device__ __forceinline__ uint64_t desc32(uint32_t base, bool mn, int ks) {
+  // tf32, K=8 per MMA. K-major: 128-B swizzle, +32 B per k-step, SBO 8 rows x 128 B.
+  // MN-major: 128-B/32-B-atom swizzle, +8 rows x 128 B per k-step, LBO = next
+  // 32-element box (4 KB), SBO = next 4-row atom (512 B).
+  return mn ? umma_desc(base + ks * 1024, 4096, 512, 1) : umma_desc(base + ks * 32, 16, 1024, 2);
+}
+__device__ __forceinline__ uint64_t desc16(uint32_t base, bool mn, int ks) {
+  // bf16, K=16 per MMA. K-major: 64-B swizzle (rows of 32 bf16), +32 B per
+  // k-step, SBO 8 rows x 64 B. MN-major: 128-B swizzle, +16 rows x 128 B per
+  // k-step, LBO = next 64-element box (4 KB), SBO 8 rows x 128 B.
+  return mn ? umma_desc(base + ks * 2048, 4096, 1024, 2) : umma_desc(base + ks * 32, 16, 512, 4);
+}
+
+template <bool A_MN, bool B_MN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
-              const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBlo,
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
+              const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB3,
               const TcParams p) {
-  using CF = Cfg<A_MN, B_MN, NPROD, STAGES>;
+  using CF = Cfg<MODE>;
+  constexpr int STAGES = CF::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + STAGES * CF::STAGE_BYTES);
@@ -215,28 +293,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = (tile / p.tiles_n) * BM, n0 = (tile % p.tiles_n) * BN;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * CF::STAGE_BYTES;
-          uint8_t* sb = sa + CF::NA * CF::A_BYTES;
-          mbar_expect_tx(&full[stage], CF::STAGE_BYTES);
+          uint8_t* st = smem + stage * CF::STAGE_BYTES;
+          uint64_t* fb = &full[stage];
+          mbar_expect_tx(fb, CF::STAGE_BYTES);
           const int k0 = kb * BK;
-#pragma unroll
-          for (int h = 0; h < CF::NA; ++h) {
-            const CUtensorMap* ta = h ? &tmAlo : &tmA;
-            const CUtensorMap* tb = h ? &tmBlo : &tmB;
-            uint8_t* da = sa + h * CF::A_BYTES;
-            uint8_t* db = sb + h * CF::B_BYTES;
-            if (A_MN) {
-#pragma unroll
-              for (int j = 0; j < BM / 32; ++j) tma_load_2d(da + j * 4096, ta, &full[stage], m0 + 32 * j, k0);
-            } else {
-              tma_load_2d(da, ta, &full[stage], k0, m0);
-            }
-            if (B_MN) {
-#pragma unroll
-              for (int j = 0; j < BN / 32; ++j) tma_load_2d(db + j * 4096, tb, &full[stage], n0 + 32 * j, k0);
-            } else {
-              tma_load_2d(db, tb, &full[stage], k0, n0);
-            }
+          load32<A_MN, BM>(st + CF::OFF_A, &tmA, fb, m0, k0);
+          load32<B_MN, BN>(st + CF::OFF_B, &tmB, fb, n0, k0);
+          if (MODE == 3) {
+            load32<A_MN, BM>(st + CF::OFF_ALO, &tmA2, fb, m0, k0);
+            load32<B_MN, BN>(st + CF::OFF_BLO, &tmB2, fb, n0, k0);
+          } else if (MODE == 2) {
+            load16<A_MN, BM>(st + CF::OFF_AH16, &tmA2, fb, m0, k0);
+            load16<A_MN, BM>(st + CF::OFF_AL16, &tmA3, fb, m0, k0);
+            load16<B_MN, BN>(st + CF::OFF_BH16, &tmB2, fb, n0, k0);
+            load16<B_MN, BN>(st + CF::OFF_BL16, &tmB3, fb, n0, k0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -247,11 +317,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    // The accumulator is restarted every KC k-blocks (K = 256): the tensor
-    // core's fp32 accumulation loses ~1 ulp per MMA step, so long K runs drift
-    // (measured 2e-5 normwise at K=8192); the epilogue promotes each K-chunk
-    // into an RN fp32 running sum held in registers (sgemm-grade accuracy).
-    constexpr uint32_t idesc = idesc_tf32(A_MN, B_MN);
+    // The accumulator restarts every KC k-blocks (K = 256): the tensor core's
+    // fp32 accumulation loses ~1 ulp per MMA step (2e-5 normwise at K=8192 with
+    // exact inputs), so the epilogue promotes each chunk into RN fp32 sums.
+    constexpr uint32_t id32 = idesc_tf32(A_MN, B_MN);
+    constexpr uint32_t id16 = idesc_bf16(A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int chunk = 0;
@@ -268,27 +338,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t sa = smem_u32(smem + stage * CF::STAGE_BYTES);
-          const uint32_t sb = sa + CF::NA * CF::A_BYTES;
+          const uint32_t s0 = smem_u32(smem + stage * CF::STAGE_BYTES);
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {
-            // K-major: +32 B per k-step inside the swizzled 128-B row;
-            // MN-major: +8 rows x 128 B per k-step
-            const uint32_t aoff = A_MN ? ks * 1024 : ks * 32;
-            const uint32_t boff = B_MN ? ks * 1024 : ks * 32;
-            // MN-major: LBO = next 32-element MN box (4 KB), SBO = next 4-row K atom
-            const uint32_t alb = A_MN ? 4096 : 16, blb = B_MN ? 4096 : 16;
-            const uint32_t asb = A_MN ? 512 : 1024, bsb = B_MN ? 512 : 1024;
-            const uint32_t alt = A_MN ? 1 : 2, blt = B_MN ? 1 : 2;
-            const uint64_t a_hi = umma_desc(sa + aoff, alb, asb, alt);
-            const uint64_t b_hi = umma_desc(sb + boff, blb, bsb, blt);
-            const uint32_t acc0 = (kc | ks) ? 1u : 0u;
-            tc_mma_tf32(d_tmem, a_hi, b_hi, idesc, acc0);
-            if (NPROD == 3) {
-              const uint64_t a_lo = umma_desc(sa + CF::A_BYTES + aoff, alb, asb, alt);
-              const uint64_t b_lo = umma_desc(sb + CF::B_BYTES + boff, blb, bsb, blt);
-              tc_mma_tf32(d_tmem, a_hi, b_lo, idesc, 1u);
-              tc_mma_tf32(d_tmem, a_lo, b_hi, idesc, 1u);
+            const uint64_t a = desc32(s0 + CF::OFF_A, A_MN, ks);
+            const uint64_t b = desc32(s0 + CF::OFF_B, B_MN, ks);
+            tc_mma_tf32(d_tmem, a, b, id32, (kc | ks) ? 1u : 0u);
+            if (MODE == 3) {
+              tc_mma_tf32(d_tmem, a, desc32(s0 + CF::OFF_BLO, B_MN, ks), id32, 1u);
+              tc_mma_tf32(d_tmem, desc32(s0 + CF::OFF_ALO, A_MN, ks), b, id32, 1u);
+            }
+          }
+          if (MODE == 2) {
+#pragma unroll
+            for (int ks = 0; ks < BK / 16; ++ks) {
+              tc_mma_f16(d_tmem, desc16(s0 + CF::OFF_AH16, A_MN, ks),
+                         desc16(s0 + CF::OFF_BL16, B_MN, ks), id16, 1u);
+              tc_mma_f16(d_tmem, desc16(s0 + CF::OFF_AL16, A_MN, ks),
+                         desc16(s0 + CF::OFF_BH16, B_MN, ks), id16, 1u);
             }
           }
           tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
@@ -369,8 +436,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// ---------------------------------------------------------------- split kernel
-// hi = tf32 round-to-nearest(x), lo = x - hi (exact). rows x cols with ld.
+// ---------------------------------------------------------------- split kernels
+// 3xTF32: hi = tf32 round-to-nearest(x), lo = x - hi (exact).
 __global__ void k_tf32_split(float* __restrict__ hi, float* __restrict__ lo,
                              const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ld) {
   int64_t n = rows * cols;
@@ -404,6 +471,38 @@ __global__ void k_tf32_split_vec(float* __restrict__ hi, float* __restrict__ lo,
   }
 }
 
+// TF32 + 2xBF16: t = trunc_tf32(x) (what the tensor core uses), hi16 = bf16(t),
+// lo16 = bf16(x - t). 8 elements per thread-iteration (32 B in, 2 x 16 B out).
+__device__ __forceinline__ void bf16x2_pair(float v, __nv_bfloat16& h, __nv_bfloat16& l) {
+  const float t = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+  h = __float2bfloat16_rn(t);
+  l = __float2bfloat16_rn(__fsub_rn(v, t));
+}
+
+__global__ void k_bf16x2_split(__nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
+                               const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ld) {
+  const int64_t c8 = cols >> 3;  // cols % 8 == 0 (checked on the host)
+  const int64_t n8 = rows * c8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / c8, c = (i - r * c8) * 8;
+    const float* src = x + r * ld + c;
+    float v[8];
+    if (((uintptr_t)src & 15) == 0) {
+      float4 a = reinterpret_cast<const float4*>(src)[0], b = reinterpret_cast<const float4*>(src)[1];
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = src[j];
+    }
+    __align__(16) __nv_bfloat16 h[8], l[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bf16x2_pair(v[j], h[j], l[j]);
+    *reinterpret_cast<uint4*>(hi + r * cols + c) = *reinterpret_cast<const uint4*>(h);
+    *reinterpret_cast<uint4*>(lo + r * cols + c) = *reinterpret_cast<const uint4*>(l);
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -421,52 +520,62 @@ int get_encode() {
   return g_encode ? 0 : b2::fail("cuTensorMapEncodeTiled unavailable from the driver");
 }
 
-// 2-D fp32 tensor map over a row-major [rows, cols] matrix with leading dim ld
-// (elements); box = {32 (inner, 128 B), box_rows}. K-major tiles use the
-// 128-B swizzle; MN-major tiles the 128-B swizzle with 32-B atoms (matching
-// UMMA's SWIZZLE_128B_BASE32B).
-int make_map(CUtensorMap* tm, const float* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
-             bool mn_major) {
+// 2-D tensor map over a row-major [rows, cols] matrix with leading dim ld (elements).
+//   fp32 operand (tf32): box {32, box_rows}; K-major 128-B swizzle, MN-major
+//     128-B swizzle with 32-B atoms (UMMA SWIZZLE_128B_BASE32B).
+//   bf16 operand: K-major box {32 (64 B), box_rows} with 64-B swizzle; MN-major
+//     box {64 (128 B), 32} with 128-B swizzle.
+int make_map(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+             bool mn_major, bool bf16) {
+  const int esz = bf16 ? 2 : 4;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * esz};
+  cuuint32_t box[2] = {(cuuint32_t)(bf16 && mn_major ? 64 : 32), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+  CUtensorMapSwizzle sw = bf16 ? (mn_major ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)
+                               : (mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B);
+  CUresult r = g_encode(tm, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                        (void*)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return b2::fail("cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
   return 0;
 }
 
-template <bool A_MN, bool B_MN, int NPROD, int STAGES>
-int launch_tc(const float* Ahi, const float* Alo, int64_t lda, const float* Bhi, const float* Blo,
-              int64_t ldb, const TcParams& p, cudaStream_t st) {
-  using CF = Cfg<A_MN, B_MN, NPROD, STAGES>;
-  CUtensorMap ta, talo, tb, tblo;
+struct Operands {
+  const void* a[3];   // MODE 1: {A}; MODE 3: {Ahi, Alo}; MODE 2: {A, Ah16, Al16}
+  const void* b[3];
+  int64_t lda, ldb;   // leading dims of a[0], b[0]; the other arrays are contiguous
+};
+
+template <bool A_MN, bool B_MN, int MODE>
+int launch_tc(const Operands& o, const TcParams& p, cudaStream_t st) {
+  using CF = Cfg<MODE>;
+  CUtensorMap m[6];
   // A is [M,K] (K-major) or stored [K,M] (MN-major); B is [N,K] or stored [K,N]
-  if (A_MN) {
-    B2_TRY(make_map(&ta, Ahi, p.K, p.M, lda, 32, true));
-    B2_TRY(make_map(&talo, NPROD == 3 ? Alo : Ahi, p.K, p.M, NPROD == 3 ? p.M : lda, 32, true));
-  } else {
-    B2_TRY(make_map(&ta, Ahi, p.M, p.K, lda, BM, false));
-    B2_TRY(make_map(&talo, NPROD == 3 ? Alo : Ahi, p.M, p.K, NPROD == 3 ? p.K : lda, BM, false));
+  const int64_t ar = A_MN ? p.K : p.M, ac = A_MN ? p.M : p.K;
+  const int64_t br = B_MN ? p.K : p.N, bc = B_MN ? p.N : p.K;
+  const int abox = A_MN ? 32 : BM, bbox = B_MN ? 32 : BN;
+  B2_TRY(make_map(&m[0], o.a[0], ar, ac, o.lda, abox, A_MN, false));
+  B2_TRY(make_map(&m[1], o.b[0], br, bc, o.ldb, bbox, B_MN, false));
+  m[2] = m[0]; m[3] = m[1]; m[4] = m[0]; m[5] = m[1];
+  if (MODE == 3) {
+    B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, false));
+    B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, false));
+  } else if (MODE == 2) {
+    B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, true));
+    B2_TRY(make_map(&m[4], o.a[2], ar, ac, ac, abox, A_MN, true));
+    B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, true));
+    B2_TRY(make_map(&m[5], o.b[2], br, bc, bc, bbox, B_MN, true));
   }
-  if (B_MN) {
-    B2_TRY(make_map(&tb, Bhi, p.K, p.N, ldb, 32, true));
-    B2_TRY(make_map(&tblo, NPROD == 3 ? Blo : Bhi, p.K, p.N, NPROD == 3 ? p.N : ldb, 32, true));
-  } else {
-    B2_TRY(make_map(&tb, Bhi, p.N, p.K, ldb, BN, false));
-    B2_TRY(make_map(&tblo, NPROD == 3 ? Blo : Bhi, p.N, p.K, NPROD == 3 ? p.K : ldb, BN, false));
-  }
-  auto kern = k_gemm_tc<A_MN, B_MN, NPROD, STAGES>;
+  auto kern = k_gemm_tc<A_MN, B_MN, MODE>;
   static bool attr_set = false;
   if (!attr_set) {
     B2_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
     attr_set = true;
   }
   int grid = p.num_tiles < b2::sm_count() ? p.num_tiles : b2::sm_count();
-  kern<<<grid, kThreads, CF::SMEM, st>>>(ta, talo, tb, tblo, p);
+  // tensor-map argument order: A, B, then the MODE-specific second/third arrays
+  kern<<<grid, kThreads, CF::SMEM, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
   return b2::launched("b2_gemm(tcgen05)");
 }
 
@@ -474,7 +583,7 @@ int launch_tc(const float* Ahi, const float* Alo, int64_t lda, const float* Bhi,
 
 namespace b2 {
 
-// split a [rows, cols] (ld) matrix into contiguous hi/lo arrays
+// split a [rows, cols] (ld) matrix into contiguous hi/lo fp32 arrays (3xTF32)
 int tf32_split(float* hi, float* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
                cudaStream_t st) {
   int64_t n = rows * cols;
@@ -488,20 +597,34 @@ int tf32_split(float* hi, float* lo, const float* x, int64_t rows, int64_t cols,
   return launched("b2_tf32_split");
 }
 
+// split a [rows, cols] (ld) matrix into contiguous bf16(trunc_tf32(x)), bf16(x - trunc)
+int bf16x2_split(void* hi, void* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
+                 cudaStream_t st) {
+  int64_t n = rows * cols;
+  if (n == 0) return 0;
+  if (cols % 8 || ((uintptr_t)hi & 15) || ((uintptr_t)lo & 15))
+    return fail("b2_bf16x2_split: cols must be a multiple of 8 and outputs 16-B aligned");
+  k_bf16x2_split<<<grid_for(n / 8, 256 * 4, 8), 256, 0, st>>>(
+      (__nv_bfloat16*)hi, (__nv_bfloat16*)lo, x, rows, cols, ld);
+  return launched("b2_bf16x2_split");
+}
+
 bool tc_supported(int ta, int tb, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb) {
   if (M > INT32_MAX / 2 || N > INT32_MAX / 2 || K > INT32_MAX / 2) return false;
   if (lda % 4 || ldb % 4) return false;  // TMA: row strides multiple of 16 bytes
   // the contiguous split copies use their column count as leading dimension
-  if ((ta ? M : K) % 4 || (tb ? K : N) % 4) return false;
+  // (bf16 rows need 16-byte strides: multiples of 8 elements)
+  if ((ta ? M : K) % 8 || (tb ? K : N) % 8) return false;
   if (M < 1 || N < 1 || K < 1) return false;
   return true;
 }
 
-// A_hi/B_hi may be the raw operands for NPROD==1; for NPROD==3 the *_lo are
-// contiguous split arrays and *_hi the contiguous tf32-rounded arrays.
-int gemm_tc(int ta, int tb, int nprod, int64_t M, int64_t N, int64_t K, const float* Ahi,
-            const float* Alo, int64_t lda, const float* Bhi, const float* Blo, int64_t ldb,
-            float* C, int64_t ldc, const float* bias, int epi, cudaStream_t st) {
+// mode 1: a0/b0 raw; mode 3: a0/b0 = hi arrays, a1/b1 = lo arrays (contiguous);
+// mode 2: a0/b0 raw fp32 (lda/ldb), a1/b1 = bf16 hi, a2/b2 = bf16 lo (contiguous)
+int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const void* a0,
+            const void* a1, const void* a2, int64_t lda, const void* b0, const void* b1,
+            const void* b2_, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
+            cudaStream_t st) {
   B2_TRY(get_encode());
   TcParams p;
   p.C = C;
@@ -513,11 +636,13 @@ int gemm_tc(int ta, int tb, int nprod, int64_t M, int64_t N, int64_t K, const fl
   p.epi = epi;
   p.tiles_n = (int)((N + BN - 1) / BN);
   p.num_tiles = (int)(((M + BM - 1) / BM) * p.tiles_n);
+  Operands o{{a0, a1, a2}, {b0, b1, b2_}, lda, ldb};
   const bool a_mn = ta != 0, b_mn = tb == 0;
-#define B2_TC(AMN, BMN)                                                                    \
-  if (a_mn == AMN && b_mn == BMN) {                                                        \
-    if (nprod == 3) return launch_tc<AMN, BMN, 3, 2>(Ahi, Alo, lda, Bhi, Blo, ldb, p, st); \
-    return launch_tc<AMN, BMN, 1, 4>(Ahi, Alo, lda, Bhi, Blo, ldb, p, st);                 \
+#define B2_TC(AMN, BMN)                                                  \
+  if (a_mn == AMN && b_mn == BMN) {                                      \
+    if (mode == 3) return launch_tc<AMN, BMN, 3>(o, p, st);              \
+    if (mode == 2) return launch_tc<AMN, BMN, 2>(o, p, st);              \
+    return launch_tc<AMN, BMN, 1>(o, p, st);                             \
   }
   B2_TC(false, false)
   B2_TC(false, true)

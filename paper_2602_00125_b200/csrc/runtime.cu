@@ -226,9 +226,11 @@ int b2_alloc(size_t bytes, void* stream, void** out) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_pending.empty()) drain_pending_locked();
   auto& fl = g_free[st];
-  // best fit, but never hand out a block more than 2x (large) the request
+  // best fit; small blocks may be up to 2x the request, large ones at most
+  // 1/8 (>= 2 MiB) bigger, so steady-state reuse never balloons the footprint
   auto it = fl.lower_bound(sz);
-  if (it != fl.end() && (it->first <= 2 * sz || it->first - sz < (1u << 20))) {
+  const size_t slack = sz < (1u << 20) ? sz : (sz / 8 > (2u << 20) ? sz / 8 : (2u << 20));
+  if (it != fl.end() && it->first - sz <= slack) {
     Block* b = it->second;
     fl.erase(it);
     g_live[b->ptr] = b;

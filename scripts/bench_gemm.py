@@ -16,7 +16,7 @@ for n in (1024, 4096, 8192):
     ref = None
     if n <= 4096:
         ref = A.astype(np.float64) @ B.astype(np.float64).T
-    for name, algo in (("1xtf32", L.GEMM_1XTF32), ("3xtf32", L.GEMM_3XTF32), ("simt", L.GEMM_SIMT)):
+    for name, algo in (("1xtf32", L.GEMM_1XTF32), ("3xtf32", L.GEMM_3XTF32), ("tf32x", L.GEMM_TF32X), ("simt", L.GEMM_SIMT)):
         if name == "simt" and n > 4096: continue
         f = lambda: L.call("b2_gemm", 0, 1, n, n, n, At.data_ptr, n, Bt.data_ptr, n, C.data_ptr, n, None, 0, algo, None)
         ms = timeit(f, 5 if n == 8192 else 10)
@@ -35,3 +35,13 @@ for n in (1024, 4096, 8192):
         f = lambda: L.call("b2_tf32_split", hi.data_ptr, lo.data_ptr, At.data_ptr, n, n, n, None)
         ms = timeit(f, 10)
         print(f"n={n} split: {ms:.3f} ms  {3*4*n*n/ms/1e6:.0f} GB/s", flush=True)
+        h16, l16, hb16, lb16 = [P.zeros((n, n // 2)) for _ in range(4)]
+        L.call("b2_bf16x2_split", h16.data_ptr, l16.data_ptr, At.data_ptr, n, n, n, None)
+        L.call("b2_bf16x2_split", hb16.data_ptr, lb16.data_ptr, Bt.data_ptr, n, n, n, None)
+        for ta, tb in ((0, 1), (0, 0), (1, 0)):
+            f = lambda: L.call("b2_gemm_tf32x", ta, tb, n, n, n, At.data_ptr, n, h16.data_ptr, l16.data_ptr, Bt.data_ptr, n, hb16.data_ptr, lb16.data_ptr, C.data_ptr, n, None, 0, None)
+            ms = timeit(f, 5)
+            print(f"n={n} tf32x-presplit kernel ta={ta} tb={tb}: {ms:.3f} ms  {2*n**3/ms/1e9:.1f} TFLOP/s", flush=True)
+        f = lambda: L.call("b2_bf16x2_split", h16.data_ptr, l16.data_ptr, At.data_ptr, n, n, n, None)
+        ms = timeit(f, 10)
+        print(f"n={n} bf16x2 split: {ms:.3f} ms  {2*4*n*n/ms/1e6:.0f} GB/s", flush=True)

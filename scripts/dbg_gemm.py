@@ -14,7 +14,7 @@ for (M,N,K) in [(128,256,32),(128,256,64),(256,512,32),(1000,260,1028)]:
     At,Bt=P.from_numpy(A),P.from_numpy(B)
     r=ref(A,B,ta,tb)
     out=[]
-    for algo in (L.GEMM_1XTF32, L.GEMM_3XTF32):
+    for algo in (L.GEMM_1XTF32, L.GEMM_3XTF32, L.GEMM_TF32X):
         C=P.zeros((M,N))
         L.call("b2_gemm",ta,tb,M,N,K,At.data_ptr,A.shape[1],Bt.data_ptr,B.shape[1],C.data_ptr,N,None,0,algo,None)
         c=C.numpy()

@@ -150,7 +150,7 @@ def test_zero_extent_reductions():
 # ---------------------------------------------------------------- matmul
 
 
-@pytest.mark.parametrize("algo", ["simt", "3xtf32"])
+@pytest.mark.parametrize("algo", ["simt", "3xtf32", "tf32x"])
 def test_matmul_goldens(algo):
     g = load("matmul.npz")
     P.set_gemm_algo(algo)
@@ -175,7 +175,7 @@ def _ref_gemm(A, B, ta, tb):
 
 
 @pytest.mark.parametrize("ta,tb", [(0, 1), (0, 0), (1, 0), (1, 1)])
-@pytest.mark.parametrize("shape", [(128, 256, 32), (300, 520, 200), (1000, 260, 1028), (64, 8, 4)])
+@pytest.mark.parametrize("shape", [(128, 256, 32), (304, 520, 200), (1000, 264, 1024), (64, 8, 16)])
 def test_gemm_layouts_tc(ta, tb, shape):
     """tcgen05 3xTF32 and 1xTF32 against fp64, every operand layout, ragged tiles."""
     import ctypes
@@ -189,7 +189,8 @@ def test_gemm_layouts_tc(ta, tb, shape):
     ref = _ref_gemm(A, B, ta, tb)
     At, Bt, bt = dev(A), dev(B), dev(bias)
     # 3xTF32 with K-chunk promotion is sgemm-grade (~1e-6); 1xTF32 is TF32-grade
-    for algo, tol in ((L.GEMM_3XTF32, 5e-6), (L.GEMM_1XTF32, 3e-3), (L.GEMM_SIMT, 5e-6)):
+    for algo, tol in ((L.GEMM_3XTF32, 5e-6), (L.GEMM_TF32X, 5e-6), (L.GEMM_1XTF32, 3e-3),
+                      (L.GEMM_SIMT, 5e-6)):
         C = P.zeros((M, N))
         L.call("b2_gemm", ta, tb, M, N, K, At.data_ptr, A.shape[1], Bt.data_ptr, B.shape[1],
                C.data_ptr, N, bt.data_ptr, L.EPI_BIAS_RELU, algo, None)
@@ -207,11 +208,12 @@ def test_gemm_accuracy_long_k():
     A = rng.uniform(-1, 1, (M, K)).astype(np.float32)
     B = rng.uniform(-1, 1, (N, K)).astype(np.float32)
     ref = A.astype(np.float64) @ B.astype(np.float64).T
-    C = P.zeros((M, N))
     At, Bt = dev(A), dev(B)
-    L.call("b2_gemm", 0, 1, M, N, K, At.data_ptr, K, Bt.data_ptr, K, C.data_ptr, N, None,
-           L.EPI_NONE, L.GEMM_3XTF32, None)
-    assert normwise(host(C), ref) <= 3e-6
+    for algo in (L.GEMM_3XTF32, L.GEMM_TF32X):
+        C = P.zeros((M, N))
+        L.call("b2_gemm", 0, 1, M, N, K, At.data_ptr, K, Bt.data_ptr, K, C.data_ptr, N, None,
+               L.EPI_NONE, algo, None)
+        assert normwise(host(C), ref) <= 3e-6, algo
 
 
 def test_tf32_hardware_rounding_probe(capsys):
@@ -329,7 +331,7 @@ def _run_mlp_device(params, x, labels, opt, steps):
     return np.array(losses, np.float32), grads, [(host(d.weight), host(d.bias)) for d in dense]
 
 
-@pytest.mark.parametrize("algo", ["simt", "3xtf32"])
+@pytest.mark.parametrize("algo", ["simt", "3xtf32", "tf32x"])
 def test_config1_train_step(algo):
     golden = load("config1.npz")
     params, x, labels = I.config1_inputs()
@@ -389,7 +391,7 @@ def test_config2_small_bit_exact_composed_and_fused():
 def test_config3_small_matmul_fwd_bwd():
     g = load("config3_small.npz")
     A, B, dC = I.config3_inputs(n=96)
-    P.set_gemm_algo("3xtf32")
+    P.set_gemm_algo("tf32x")
     try:
         at, bt = dev(A, True), dev(B, True)
         C = P.mm(at, bt)
