@@ -68,6 +68,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// ---- cluster (CTA pair) helpers for cta_group::2
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of `local`'s twin in CTA `rank` of this cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// 2-SM TMA: data lands in this CTA's smem, the transaction bytes are counted on
+// the mbarrier at `bar_cluster` (the leader CTA's barrier)
+__device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* tm, uint32_t bar_cluster,
+                                                int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)tm), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0,
                                             int c1) {
   asm volatile(
@@ -91,16 +122,45 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
       : "memory");
 }
 
-__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                            uint32_t idesc, uint32_t accum) {
+// commit this CTA pair's MMAs to the barrier at the same offset in both CTAs
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
   asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
       : "memory");
+}
+
+template <int CG>
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accum, bool f16) {
+  if (CG == 1) {
+    if (f16)
+      asm volatile(
+          "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+          "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+          "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+          : "memory");
+    else
+      asm volatile(
+          "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+          "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+          : "memory");
+  } else {
+    if (f16)
+      asm volatile(
+          "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+          "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+          "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+          : "memory");
+    else
+      asm volatile(
+          "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+          "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+          "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+          : "memory");
+  }
 }
 
 // UMMA shared-memory descriptor (sm_100): start>>4 [0,14), LBO>>4 [16,30),
@@ -119,13 +179,7 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
-// instruction descriptor, kind::tf32: D=F32 [4,6), A=B=TF32(2) [7,10)/[10,13),
-// a_major [15], b_major [16], N>>3 [17,23), M>>4 [24,29)
-__host__ __device__ constexpr uint32_t idesc_tf32(bool a_mn, bool b_mn) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-}
-
+// 32 lanes x 32 bit x 16 columns of TMEM -> 16 registers per thread
 #define TMEM_LD16(taddr, v)                                                                        \
   asm volatile(                                                                                    \
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "                                                   \
@@ -135,34 +189,11 @@ __host__ __device__ constexpr uint32_t idesc_tf32(bool a_mn, bool b_mn) {
         "=r"(v[14]), "=r"(v[15])                                                                   \
       : "r"(taddr))
 
-#define TMEM_LD32(taddr, v)                                                                        \
-  asm volatile(                                                                                    \
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "                                                   \
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"                                   \
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                  \
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),       \
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),   \
-        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),             \
-        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),             \
-        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])              \
-      : "r"(taddr))
-
-__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                           uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
-}
-
-// instruction descriptor, kind::f16 with BF16 inputs and an F32 accumulator
-__host__ __device__ constexpr uint32_t idesc_bf16(bool a_mn, bool b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// instruction descriptor: D=F32 [4,6), A/B format [7,10)/[10,13) (TF32=2, BF16=1),
+// a_major [15], b_major [16], N>>3 [17,23), M>>4 [24,29). M = 128 per CTA (256 per pair).
+__host__ __device__ constexpr uint32_t make_idesc(bool f16, bool a_mn, bool b_mn, int m) {
+  return (1u << 4) | ((f16 ? 1u : 2u) << 7) | ((f16 ? 1u : 2u) << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 struct TcParams {
@@ -171,7 +202,7 @@ struct TcParams {
   int64_t ldc;
   int M, N, K;
   int epi;
-  int tiles_n, num_tiles;
+  int tiles_n, num_tiles;  // tiles of BM*CG x BN
 };
 
 // MODE 1: 1xTF32            tiles A32 | B32
@@ -181,15 +212,20 @@ struct TcParams {
 //         to tf32: hi = trunc(x), probed on B200) and the two cross terms
 //         hi*lo + lo*hi run as kind::f16 MMAs on bf16(hi), bf16(lo) at twice the
 //         tf32 rate -- 2 tf32-equivalents per fp32 MAC instead of 3.
-template <int MODE>
+// CG 1: one CTA computes a 128x256 tile. CG 2: a CTA pair (cluster of 2)
+//         computes 256x256 with tcgen05 cta_group::2: each CTA holds its 128
+//         rows of A and HALF (128 rows) of B, the leader issues M=256 MMAs that
+//         read both CTAs' smem -- per-SM operand ingress drops by a third.
+template <int MODE, int CG>
 struct Cfg {
+  static constexpr int BNL = BN / CG;      // B rows loaded per CTA
   static constexpr int A32 = BM * BK * 4;  // 16 KB
-  static constexpr int B32 = BN * BK * 4;  // 32 KB
-  static constexpr int A16 = BM * BK * 2;  // 8 KB
-  static constexpr int B16 = BN * BK * 2;  // 16 KB
+  static constexpr int B32 = BNL * BK * 4;
+  static constexpr int A16 = BM * BK * 2;
+  static constexpr int B16 = BNL * BK * 2;
   static constexpr int STAGE_BYTES = MODE == 1 ? A32 + B32 : (MODE == 3 ? 2 * (A32 + B32)
                                                                        : A32 + B32 + 2 * (A16 + B16));
-  static constexpr int STAGES = MODE == 1 ? 4 : 2;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   // byte offsets inside a stage
   static constexpr int OFF_A = 0;
@@ -202,27 +238,38 @@ struct Cfg {
   static constexpr int OFF_BL16 = A32 + B32 + 2 * A16 + B16;
 };
 
+// Loads a tile into this CTA's smem, counting bytes on `bar` (a local
+// barrier for CG 1, the leader's barrier as a shared::cluster address for CG 2).
+template <int CG>
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t* bar, uint32_t bar_cl,
+                                      int c0, int c1) {
+  if (CG == 1)
+    tma_load_2d(dst, tm, bar, c0, c1);
+  else
+    tma_load_2d_cg2(dst, tm, bar_cl, c0, c1);
+}
+
 // fp32 tile (tf32 consumption): K-major = one box {32 K, rows}; MN-major = 32x32 boxes
-template <bool MN, int ROWS>
-__device__ __forceinline__ void load32(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, int mn0,
-                                       int k0) {
+template <bool MN, int ROWS, int CG>
+__device__ __forceinline__ void load32(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
+                                       uint32_t bar_cl, int mn0, int k0) {
   if (MN) {
 #pragma unroll
-    for (int j = 0; j < ROWS / 32; ++j) tma_load_2d(dst + j * 4096, tm, bar, mn0 + 32 * j, k0);
+    for (int j = 0; j < ROWS / 32; ++j) tma2d<CG>(dst + j * 4096, tm, bar, bar_cl, mn0 + 32 * j, k0);
   } else {
-    tma_load_2d(dst, tm, bar, k0, mn0);
+    tma2d<CG>(dst, tm, bar, bar_cl, k0, mn0);
   }
 }
 
 // bf16 tile: K-major = one box {32 K (64 B), rows}; MN-major = boxes {64 MN (128 B), 32 K}
-template <bool MN, int ROWS>
-__device__ __forceinline__ void load16(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, int mn0,
-                                       int k0) {
+template <bool MN, int ROWS, int CG>
+__device__ __forceinline__ void load16(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
+                                       uint32_t bar_cl, int mn0, int k0) {
   if (MN) {
 #pragma unroll
-    for (int j = 0; j < ROWS / 64; ++j) tma_load_2d(dst + j * 4096, tm, bar, mn0 + 64 * j, k0);
+    for (int j = 0; j < ROWS / 64; ++j) tma2d<CG>(dst + j * 4096, tm, bar, bar_cl, mn0 + 64 * j, k0);
   } else {
-    tma_load_2d(dst, tm, bar, k0, mn0);
+    tma2d<CG>(dst, tm, bar, bar_cl, k0, mn0);
   }
 }
 
@@ -240,13 +287,13 @@ __device__ __forceinline__ uint64_t desc16(uint32_t base, bool mn, int ks) {
   return mn ? umma_desc(base + ks * 2048, 4096, 1024, 2) : umma_desc(base + ks * 32, 16, 512, 4);
 }
 
-template <bool A_MN, bool B_MN, int MODE>
+template <bool A_MN, bool B_MN, int MODE, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
               const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB3,
               const TcParams p) {
-  using CF = Cfg<MODE>;
+  using CF = Cfg<MODE, CG>;
   constexpr int STAGES = CF::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -259,6 +306,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = (p.K + BK - 1) / BK;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int cl_id = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int cl_num = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -267,46 +318,56 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 16);
+      mbar_init(&tempty[b], 16 * CG);  // every epilogue warp of the pair drains before reuse
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------ TMA producer
+    // ------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int m0 = (tile / p.tiles_n) * BM, n0 = (tile % p.tiles_n) * BN;
+      for (int tile = cl_id; tile < p.num_tiles; tile += cl_num) {
+        const int m0 = (tile / p.tiles_n) * (BM * CG) + (int)rank * BM;
+        const int n0 = (tile % p.tiles_n) * BN + (int)rank * CF::BNL;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * CF::STAGE_BYTES;
           uint64_t* fb = &full[stage];
-          mbar_expect_tx(fb, CF::STAGE_BYTES);
+          const uint32_t fb_cl = CG == 2 ? mapa(smem_u32(fb), 0) : 0;
+          if (leader) mbar_expect_tx(fb, CF::STAGE_BYTES * CG);
           const int k0 = kb * BK;
-          load32<A_MN, BM>(st + CF::OFF_A, &tmA, fb, m0, k0);
-          load32<B_MN, BN>(st + CF::OFF_B, &tmB, fb, n0, k0);
+          load32<A_MN, BM, CG>(st + CF::OFF_A, &tmA, fb, fb_cl, m0, k0);
+          load32<B_MN, CF::BNL, CG>(st + CF::OFF_B, &tmB, fb, fb_cl, n0, k0);
           if (MODE == 3) {
-            load32<A_MN, BM>(st + CF::OFF_ALO, &tmA2, fb, m0, k0);
-            load32<B_MN, BN>(st + CF::OFF_BLO, &tmB2, fb, n0, k0);
+            load32<A_MN, BM, CG>(st + CF::OFF_ALO, &tmA2, fb, fb_cl, m0, k0);
+            load32<B_MN, CF::BNL, CG>(st + CF::OFF_BLO, &tmB2, fb, fb_cl, n0, k0);
           } else if (MODE == 2) {
-            load16<A_MN, BM>(st + CF::OFF_AH16, &tmA2, fb, m0, k0);
-            load16<A_MN, BM>(st + CF::OFF_AL16, &tmA3, fb, m0, k0);
-            load16<B_MN, BN>(st + CF::OFF_BH16, &tmB2, fb, n0, k0);
-            load16<B_MN, BN>(st + CF::OFF_BL16, &tmB3, fb, n0, k0);
+            load16<A_MN, BM, CG>(st + CF::OFF_AH16, &tmA2, fb, fb_cl, m0, k0);
+            load16<A_MN, BM, CG>(st + CF::OFF_AL16, &tmA3, fb, fb_cl, m0, k0);
+            load16<B_MN, CF::BNL, CG>(st + CF::OFF_BH16, &tmB2, fb, fb_cl, n0, k0);
+            load16<B_MN, CF::BNL, CG>(st + CF::OFF_BL16, &tmB3, fb, fb_cl, n0, k0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -316,61 +377,70 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
+    // ------------------------------------------------ MMA issuer (leader CTA only)
     // The accumulator restarts every KC k-blocks (K = 256): the tensor core's
     // fp32 accumulation loses ~1 ulp per MMA step (2e-5 normwise at K=8192 with
     // exact inputs), so the epilogue promotes each chunk into RN fp32 sums.
-    constexpr uint32_t id32 = idesc_tf32(A_MN, B_MN);
-    constexpr uint32_t id16 = idesc_bf16(A_MN, B_MN);
-    int stage = 0;
-    uint32_t phase = 0;
-    int chunk = 0;
-    uint32_t d_tmem = tmem_base;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int kc = kb % KC;
-        if (kc == 0) {  // claim the next chunk accumulator (ping-pong)
-          const int cb = chunk & 1;
-          mbar_wait(&tempty[cb], ((chunk >> 1) & 1) ^ 1);
+    if (leader) {
+      constexpr uint32_t id32 = make_idesc(false, A_MN, B_MN, BM * CG);
+      constexpr uint32_t id16 = make_idesc(true, A_MN, B_MN, BM * CG);
+      int stage = 0;
+      uint32_t phase = 0;
+      int chunk = 0;
+      uint32_t d_tmem = tmem_base;
+      for (int tile = cl_id; tile < p.num_tiles; tile += cl_num) {
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int kc = kb % KC;
+          if (kc == 0) {  // claim the next chunk accumulator (ping-pong)
+            const int cb = chunk & 1;
+            mbar_wait(&tempty[cb], ((chunk >> 1) & 1) ^ 1);
+            tc_fence_after();
+            d_tmem = tmem_base + cb * BN;
+          }
+          mbar_wait(&full[stage], phase);
           tc_fence_after();
-          d_tmem = tmem_base + cb * BN;
-        }
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t s0 = smem_u32(smem + stage * CF::STAGE_BYTES);
+          if (lane == 0) {
+            const uint32_t s0 = smem_u32(smem + stage * CF::STAGE_BYTES);
 #pragma unroll
-          for (int ks = 0; ks < BK / 8; ++ks) {
-            const uint64_t a = desc32(s0 + CF::OFF_A, A_MN, ks);
-            const uint64_t b = desc32(s0 + CF::OFF_B, B_MN, ks);
-            tc_mma_tf32(d_tmem, a, b, id32, (kc | ks) ? 1u : 0u);
-            if (MODE == 3) {
-              tc_mma_tf32(d_tmem, a, desc32(s0 + CF::OFF_BLO, B_MN, ks), id32, 1u);
-              tc_mma_tf32(d_tmem, desc32(s0 + CF::OFF_ALO, A_MN, ks), b, id32, 1u);
+            for (int ks = 0; ks < BK / 8; ++ks) {
+              const uint64_t a = desc32(s0 + CF::OFF_A, A_MN, ks);
+              const uint64_t b = desc32(s0 + CF::OFF_B, B_MN, ks);
+              tc_mma<CG>(d_tmem, a, b, id32, (kc | ks) ? 1u : 0u, false);
+              if (MODE == 3) {
+                tc_mma<CG>(d_tmem, a, desc32(s0 + CF::OFF_BLO, B_MN, ks), id32, 1u, false);
+                tc_mma<CG>(d_tmem, desc32(s0 + CF::OFF_ALO, A_MN, ks), b, id32, 1u, false);
+              }
+            }
+            if (MODE == 2) {
+#pragma unroll
+              for (int ks = 0; ks < BK / 16; ++ks) {
+                tc_mma<CG>(d_tmem, desc16(s0 + CF::OFF_AH16, A_MN, ks),
+                           desc16(s0 + CF::OFF_BL16, B_MN, ks), id16, 1u, true);
+                tc_mma<CG>(d_tmem, desc16(s0 + CF::OFF_AL16, A_MN, ks),
+                           desc16(s0 + CF::OFF_BH16, B_MN, ks), id16, 1u, true);
+              }
+            }
+            // smem slot free (in both CTAs) once these MMAs retire; chunk ready
+            const bool last = kc == KC - 1 || kb == nkb - 1;
+            if (CG == 1) {
+              tc_commit(&empty[stage]);
+              if (last) tc_commit(&tfull[chunk & 1]);
+            } else {
+              tc_commit_pair(&empty[stage]);
+              if (last) tc_commit_pair(&tfull[chunk & 1]);
             }
           }
-          if (MODE == 2) {
-#pragma unroll
-            for (int ks = 0; ks < BK / 16; ++ks) {
-              tc_mma_f16(d_tmem, desc16(s0 + CF::OFF_AH16, A_MN, ks),
-                         desc16(s0 + CF::OFF_BL16, B_MN, ks), id16, 1u);
-              tc_mma_f16(d_tmem, desc16(s0 + CF::OFF_AL16, A_MN, ks),
-                         desc16(s0 + CF::OFF_BH16, B_MN, ks), id16, 1u);
-            }
+          __syncwarp();
+          if (kc == KC - 1 || kb == nkb - 1) ++chunk;
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
           }
-          tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
-          if (kc == KC - 1 || kb == nkb - 1) tc_commit(&tfull[chunk & 1]);  // chunk ready
-        }
-        __syncwarp();
-        if (kc == KC - 1 || kb == nkb - 1) ++chunk;
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
         }
       }
     }
   } else if (warp >= 4) {
-    // ------------------------------------------------ epilogue (warps 4..19)
+    // ------------------------------------------------ epilogue (warps 4..19, both CTAs)
     // warp w drains TMEM lanes 32*(w%4).. (its lane quarter) for the 64-column
     // group (w-4)/4, keeps the tile's running sums for those 64 outputs of its
     // row in registers, and stores them (+bias, relu) after the last chunk.
@@ -380,8 +450,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nch = (nkb + KC - 1) / KC;
     const bool vec_ok = (p.ldc % 4) == 0 && (((uintptr_t)p.C) & 15) == 0;
     int chunk = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      const int m0 = (tile / p.tiles_n) * BM, n0 = (tile % p.tiles_n) * BN;
+    for (int tile = cl_id; tile < p.num_tiles; tile += cl_num) {
+      const int m0 = (tile / p.tiles_n) * (BM * CG) + (int)rank * BM;
+      const int n0 = (tile % p.tiles_n) * BN;
       float acc[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j) acc[j] = 0.0f;
@@ -400,7 +471,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[cb]);
+        if (lane == 0) {
+          if (CG == 1)
+            mbar_arrive(&tempty[cb]);
+          else
+            mbar_arrive_remote(mapa(smem_u32(&tempty[cb]), 0));  // the leader's barrier
+        }
       }
       const int64_t m = m0 + row;
       if (m < p.M) {
@@ -429,10 +505,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   __syncthreads();
+  if (CG == 2) cluster_sync();  // the peer may still be reading our smem / arriving on us
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols));
+    if (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(kTmemCols));
   }
 }
 
@@ -547,14 +628,14 @@ struct Operands {
   int64_t lda, ldb;   // leading dims of a[0], b[0]; the other arrays are contiguous
 };
 
-template <bool A_MN, bool B_MN, int MODE>
-int launch_tc(const Operands& o, const TcParams& p, cudaStream_t st) {
-  using CF = Cfg<MODE>;
+template <bool A_MN, bool B_MN, int MODE, int CG>
+int launch_tc(const Operands& o, TcParams p, cudaStream_t st) {
+  using CF = Cfg<MODE, CG>;
   CUtensorMap m[6];
   // A is [M,K] (K-major) or stored [K,M] (MN-major); B is [N,K] or stored [K,N]
   const int64_t ar = A_MN ? p.K : p.M, ac = A_MN ? p.M : p.K;
   const int64_t br = B_MN ? p.K : p.N, bc = B_MN ? p.N : p.K;
-  const int abox = A_MN ? 32 : BM, bbox = B_MN ? 32 : BN;
+  const int abox = A_MN ? 32 : BM, bbox = B_MN ? 32 : CF::BNL;
   B2_TRY(make_map(&m[0], o.a[0], ar, ac, o.lda, abox, A_MN, false));
   B2_TRY(make_map(&m[1], o.b[0], br, bc, o.ldb, bbox, B_MN, false));
   m[2] = m[0]; m[3] = m[1]; m[4] = m[0]; m[5] = m[1];
@@ -567,15 +648,30 @@ int launch_tc(const Operands& o, const TcParams& p, cudaStream_t st) {
     B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, true));
     B2_TRY(make_map(&m[5], o.b[2], br, bc, bc, bbox, B_MN, true));
   }
-  auto kern = k_gemm_tc<A_MN, B_MN, MODE>;
+  p.tiles_n = (p.N + BN - 1) / BN;
+  p.num_tiles = ((p.M + BM * CG - 1) / (BM * CG)) * p.tiles_n;
+  auto kern = k_gemm_tc<A_MN, B_MN, MODE, CG>;
   static bool attr_set = false;
   if (!attr_set) {
     B2_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+    if (CG == 2) B2_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     attr_set = true;
   }
-  int grid = p.num_tiles < b2::sm_count() ? p.num_tiles : b2::sm_count();
-  // tensor-map argument order: A, B, then the MODE-specific second/third arrays
-  kern<<<grid, kThreads, CF::SMEM, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
+  int sms = b2::sm_count();
+  int grid = (p.num_tiles * CG < sms) ? p.num_tiles * CG : (sms / CG) * CG;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = CF::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  B2_CUDA(cudaLaunchKernelEx(&cfg, kern, m[0], m[1], m[2], m[3], m[4], m[5], p));
   return b2::launched("b2_gemm(tcgen05)");
 }
 
@@ -619,6 +715,15 @@ bool tc_supported(int ta, int tb, int64_t M, int64_t N, int64_t K, int64_t lda, 
   return true;
 }
 
+static int cg_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("B2_GEMM_CG");
+    v = e ? atoi(e) : 0;  // 0 auto, 1 or 2 forced
+  }
+  return v;
+}
+
 // mode 1: a0/b0 raw; mode 3: a0/b0 = hi arrays, a1/b1 = lo arrays (contiguous);
 // mode 2: a0/b0 raw fp32 (lda/ldb), a1/b1 = bf16 hi, a2/b2 = bf16 lo (contiguous)
 int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const void* a0,
@@ -634,15 +739,25 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   p.N = (int)N;
   p.K = (int)K;
   p.epi = epi;
-  p.tiles_n = (int)((N + BN - 1) / BN);
-  p.num_tiles = (int)(((M + BM - 1) / BM) * p.tiles_n);
+  p.tiles_n = p.num_tiles = 0;
   Operands o{{a0, a1, a2}, {b0, b1, b2_}, lda, ldb};
   const bool a_mn = ta != 0, b_mn = tb == 0;
-#define B2_TC(AMN, BMN)                                                  \
-  if (a_mn == AMN && b_mn == BMN) {                                      \
-    if (mode == 3) return launch_tc<AMN, BMN, 3>(o, p, st);              \
-    if (mode == 2) return launch_tc<AMN, BMN, 2>(o, p, st);              \
-    return launch_tc<AMN, BMN, 1>(o, p, st);                             \
+  // CTA pairs once there are enough 256-row tiles to fill the chip
+  int cg = cg_mode();
+  if (cg != 1 && cg != 2) {
+    int64_t pair_tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+    cg = pair_tiles >= sm_count() / 2 ? 2 : 1;
+  }
+#define B2_TC(AMN, BMN)                                                             \
+  if (a_mn == AMN && b_mn == BMN) {                                                 \
+    if (cg == 2) {                                                                  \
+      if (mode == 3) return launch_tc<AMN, BMN, 3, 2>(o, p, st);                    \
+      if (mode == 2) return launch_tc<AMN, BMN, 2, 2>(o, p, st);                    \
+      return launch_tc<AMN, BMN, 1, 2>(o, p, st);                                   \
+    }                                                                               \
+    if (mode == 3) return launch_tc<AMN, BMN, 3, 1>(o, p, st);                      \
+    if (mode == 2) return launch_tc<AMN, BMN, 2, 1>(o, p, st);                      \
+    return launch_tc<AMN, BMN, 1, 1>(o, p, st);                                     \
   }
   B2_TC(false, false)
   B2_TC(false, true)
