@@ -1,19 +1,22 @@
-// tcgen05 / TMEM / TMA GEMM for sm_100a with fp32-accurate 3xTF32.
+// tcgen05 / TMEM / TMA GEMM for sm_100a with fp32 accuracy.
 //
 // Replaces matmul.block (tensorlite/core.py:802-807) + pullbacks (:815-817)
 // for every shape big enough to fill the chip. The reference computes each
 // output as one double dot rounded to f32; the fp32 tolerance (1e-4, SURVEY
-// 8a.3) rules out plain TF32 (~2.5e-4 normwise), so each operand is split
-// x = hi + lo (hi = tf32(x), lo = x - hi, both exact in fp32) and the kernel
-// accumulates hi*hi + hi*lo + lo*hi on the tensor cores into one fp32 TMEM
-// accumulator (~5e-7 normwise, indistinguishable from an FFMA GEMM).
+// 8a.3) rules out plain TF32 (~2.5e-4 normwise), so operands are split
+// x = hi + lo and the tensor cores accumulate hi*hi + hi*lo + lo*hi:
+//   3xTF32 (MODE 3): three kind::tf32 MMAs on fp32 hi/lo arrays;
+//   TF32X  (MODE 2, default): the tf32 MMA reads the raw fp32 operand (the
+//          hardware truncates to tf32, so hi = trunc(x)) and the two cross
+//          terms run as kind::f16 MMAs on bf16(hi), bf16(lo) at twice the tf32
+//          rate: 2 tf32-equivalents per fp32 MAC, ~2e-6 normwise error.
 //
-// Structure (one CTA per SM, persistent over output tiles):
-//   warp 0      TMA producer: per k-block loads A_hi, A_lo, B_hi, B_lo tiles
-//               (cp.async.bulk.tensor, 128-byte swizzle) into a STAGES ring
-//   warp 1      MMA issuer: one elected thread issues tcgen05.mma.kind::tf32
-//               (M=128, N=256, K=8) x 4 k-steps x 3 products per k-block,
-//               tcgen05.commit frees the smem slot / signals the epilogue
+// Structure (persistent; one CTA per SM, CTA pairs for big problems):
+//   warp 0      TMA producer: per k-block loads the mode's operand tiles
+//               (cp.async.bulk.tensor, 128/64-byte swizzles) into a ring
+//   warp 1      MMA issuer (leader CTA): one thread issues the tcgen05.mma's
+//               (M=128 per CTA or 256 per pair, N=256, K=8/16), tcgen05.commit
+//               frees smem slots and hands K-chunks to the epilogue
 //   warp 2      TMEM allocator (512 columns = two 128x256 fp32 accumulators,
 //               ping-ponged per K-chunk of 256)
 //   warps 4..19 epilogue: drain each K-chunk (tcgen05.ld) into RN fp32
@@ -21,8 +24,8 @@
 //               accumulator; after the last chunk +bias -> relu -> stores
 // Operand majorness comes from the reference's three layouts: NT (forward,
 // x.w^T), NN (x_bar = g.w), TN (w_bar = g^T.x): K-major tiles are one TMA box
-// of 32 K-elements (128 B) x rows; MN-major tiles are 32(MN) x 32(K) boxes
-// laid side by side (UMMA LBO = box bytes, SBO = 8 rows x 128 B).
+// per operand; MN-major tiles are 128-byte-wide boxes laid side by side
+// (UMMA LBO = box bytes).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -203,7 +206,21 @@ struct TcParams {
   int M, N, K;
   int epi;
   int tiles_n, num_tiles;  // tiles of BM*CG x BN
+  int tiles_m;
 };
+
+// Grouped raster: tiles walk M inside groups of kGroupN tile-columns, so the
+// ~74-148 tiles resident at once cover a ~9 x 8 block of the output and the
+// B panels of a group stay in L2 across waves (the plain row-major order
+// re-read all of B from DRAM every wave: 12.8 GB/launch for 3.4 GB of data).
+constexpr int kGroupN = 8;
+__device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& tm, int& tn) {
+  const int group = kGroupN * p.tiles_m;
+  const int g = t / group, r = t - g * group;
+  const int w = min(kGroupN, p.tiles_n - g * kGroupN);
+  tm = r / w;
+  tn = g * kGroupN + (r - tm * w);
+}
 
 // MODE 1: 1xTF32            tiles A32 | B32
 // MODE 3: 3xTF32            tiles Ahi | Alo | Bhi | Blo (fp32 arrays, hi = tf32(x))
@@ -349,8 +366,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cl_id; tile < p.num_tiles; tile += cl_num) {
-        const int m0 = (tile / p.tiles_n) * (BM * CG) + (int)rank * BM;
-        const int n0 = (tile % p.tiles_n) * BN + (int)rank * CF::BNL;
+        int tm, tn;
+        tile_coords(p, tile, tm, tn);
+        const int m0 = tm * (BM * CG) + (int)rank * BM;
+        const int n0 = tn * BN + (int)rank * CF::BNL;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * CF::STAGE_BYTES;
@@ -451,8 +470,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool vec_ok = (p.ldc % 4) == 0 && (((uintptr_t)p.C) & 15) == 0;
     int chunk = 0;
     for (int tile = cl_id; tile < p.num_tiles; tile += cl_num) {
-      const int m0 = (tile / p.tiles_n) * (BM * CG) + (int)rank * BM;
-      const int n0 = (tile % p.tiles_n) * BN;
+      int tm, tn;
+      tile_coords(p, tile, tm, tn);
+      const int m0 = tm * (BM * CG) + (int)rank * BM;
+      const int n0 = tn * BN;
       float acc[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j) acc[j] = 0.0f;
@@ -649,7 +670,8 @@ int launch_tc(const Operands& o, TcParams p, cudaStream_t st) {
     B2_TRY(make_map(&m[5], o.b[2], br, bc, bc, bbox, B_MN, true));
   }
   p.tiles_n = (p.N + BN - 1) / BN;
-  p.num_tiles = ((p.M + BM * CG - 1) / (BM * CG)) * p.tiles_n;
+  p.tiles_m = (p.M + BM * CG - 1) / (BM * CG);
+  p.num_tiles = p.tiles_m * p.tiles_n;
   auto kern = k_gemm_tc<A_MN, B_MN, MODE, CG>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -739,7 +761,7 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   p.N = (int)N;
   p.K = (int)K;
   p.epi = epi;
-  p.tiles_n = p.num_tiles = 0;
+  p.tiles_n = p.num_tiles = p.tiles_m = 0;
   Operands o{{a0, a1, a2}, {b0, b1, b2_}, lda, ldb};
   const bool a_mn = ta != 0, b_mn = tb == 0;
   // CTA pairs once there are enough 256-row tiles to fill the chip
