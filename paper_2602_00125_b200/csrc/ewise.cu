@@ -419,21 +419,16 @@ __global__ void __launch_bounds__(kThreads) k_muladd_relu_bwd(float* __restrict_
   int64_t r0 = blockIdx.y * rows_per_split;
   int64_t r1 = min(rows, r0 + rows_per_split);
   if (col >= cols) return;
-  float4 vb = *reinterpret_cast<const float4*>(b + col);
+  const float4 vb = *reinterpret_cast<const float4*>(b + col);
   double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
   int n0 = 0, n1 = 0, n2 = 0, n3 = 0;
-  for (int64_t r = r0; r < r1; ++r) {
-    float4 va = *reinterpret_cast<const float4*>(a + r * cols + col);
-    float m0 = __fadd_rn(__fmul_rn(va.x, vb.x), vb.x) > 0.f ? 1.f : 0.f;
-    float m1 = __fadd_rn(__fmul_rn(va.y, vb.y), vb.y) > 0.f ? 1.f : 0.f;
-    float m2 = __fadd_rn(__fmul_rn(va.z, vb.z), vb.z) > 0.f ? 1.f : 0.f;
-    float m3 = __fadd_rn(__fmul_rn(va.w, vb.w), vb.w) > 0.f ? 1.f : 0.f;
-    float4 g;
-    g.x = __fmul_rn(m0, vb.x);
-    g.y = __fmul_rn(m1, vb.y);
-    g.z = __fmul_rn(m2, vb.z);
-    g.w = __fmul_rn(m3, vb.w);
-    *reinterpret_cast<float4*>(ga + r * cols + col) = g;
+  auto one = [&](const float4& va, float4* dst) {
+    const float m0 = __fadd_rn(__fmul_rn(va.x, vb.x), vb.x) > 0.f ? 1.f : 0.f;
+    const float m1 = __fadd_rn(__fmul_rn(va.y, vb.y), vb.y) > 0.f ? 1.f : 0.f;
+    const float m2 = __fadd_rn(__fmul_rn(va.z, vb.z), vb.z) > 0.f ? 1.f : 0.f;
+    const float m3 = __fadd_rn(__fmul_rn(va.w, vb.w), vb.w) > 0.f ? 1.f : 0.f;
+    *dst = make_float4(__fmul_rn(m0, vb.x), __fmul_rn(m1, vb.y), __fmul_rn(m2, vb.z),
+                       __fmul_rn(m3, vb.w));
     s0 += (double)__fmul_rn(m0, va.x);
     s1 += (double)__fmul_rn(m1, va.y);
     s2 += (double)__fmul_rn(m2, va.z);
@@ -442,7 +437,21 @@ __global__ void __launch_bounds__(kThreads) k_muladd_relu_bwd(float* __restrict_
     n1 += m1 > 0.f;
     n2 += m2 > 0.f;
     n3 += m3 > 0.f;
+  };
+  int64_t r = r0;
+  for (; r + 3 < r1; r += 4) {  // 4 independent 128-bit loads in flight
+    const float4 v0 = *reinterpret_cast<const float4*>(a + r * cols + col);
+    const float4 v1 = *reinterpret_cast<const float4*>(a + (r + 1) * cols + col);
+    const float4 v2 = *reinterpret_cast<const float4*>(a + (r + 2) * cols + col);
+    const float4 v3 = *reinterpret_cast<const float4*>(a + (r + 3) * cols + col);
+    one(v0, reinterpret_cast<float4*>(ga + r * cols + col));
+    one(v1, reinterpret_cast<float4*>(ga + (r + 1) * cols + col));
+    one(v2, reinterpret_cast<float4*>(ga + (r + 2) * cols + col));
+    one(v3, reinterpret_cast<float4*>(ga + (r + 3) * cols + col));
   }
+  for (; r < r1; ++r)
+    one(*reinterpret_cast<const float4*>(a + r * cols + col),
+        reinterpret_cast<float4*>(ga + r * cols + col));
   int64_t o = blockIdx.y * cols + col;
   psum[o] = s0; psum[o + 1] = s1; psum[o + 2] = s2; psum[o + 3] = s3;
   pcnt[o] = n0; pcnt[o + 1] = n1; pcnt[o + 2] = n2; pcnt[o + 3] = n3;

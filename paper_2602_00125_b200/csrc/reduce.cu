@@ -5,11 +5,16 @@
 //   Python doubles); mean = f32(dsum / count) in double (core.py:671, 682);
 // * max keeps (value, first index): strict '>' scan semantics, ties go to the
 //   lower row-major index, a NaN in the first scanned slot sticks and later
-//   NaNs are skipped (core.py:709-713) -- the combine below is associative so
-//   the parallel order cannot change the winner;
+//   NaNs are skipped (core.py:709-713). Inside a thread a plain `v > best`
+//   scan skips NaNs for free; the first-slot NaN is checked once per output;
+//   the cross-thread combine is associative so the parallel order cannot
+//   change the winner;
 // * deterministic: work is partitioned by a fixed function of the shape and
 //   the SM count, partials combine in a fixed order (the reference's
 //   worker-count-independent chunk contract, parallel.py:1-8, 48-63).
+//
+// HBM-bound: every thread keeps 4 independent 128-bit loads in flight
+// (unrolled, independent accumulators).
 //
 // Canonical forms (after dropping size-1 axes):
 //   contiguous x with the reduced axes one contiguous block  -> [O1, R, I]
@@ -46,13 +51,11 @@ __device__ __forceinline__ MaxAcc max_combine(const MaxAcc& a, const MaxAcc& b) 
   return a.i < b.i ? a : b;
 }
 
-__device__ __forceinline__ void max_push(MaxAcc& a, float v, int64_t i) {
-  if (isnan(v)) {
-    if (i == 0) a = MaxAcc{v, 0};
-    return;
-  }
-  if (sticky(a)) return;
-  if (a.i == kNone || v > a.v || (v == a.v && i < a.i)) a = MaxAcc{v, i};
+// in-order scan step: NaN never compares greater, so it is skipped
+__device__ __forceinline__ void max_scan(float& best, int64_t& bi, float v, int64_t i) {
+  const bool gt = v > best;  // predicated selects, no branch
+  best = gt ? v : best;
+  bi = gt ? i : bi;
 }
 
 __device__ __forceinline__ MaxAcc shfl_max(MaxAcc a, int off) {
@@ -110,59 +113,100 @@ __global__ void __launch_bounds__(256) k_rows(const float* __restrict__ x, int64
   __shared__ double shd[8];
   __shared__ MaxAcc shm[8];
   constexpr int RPC = 256 / GROUP;
-  int g = threadIdx.x / GROUP, t = threadIdx.x % GROUP;
-  int64_t o = blockIdx.x * (int64_t)RPC + g;
-  int S = gridDim.y, s = blockIdx.y;
-  int64_t r0 = s * Rs, r1 = min(R, r0 + Rs);
-  bool live = o < O;
+  const int g = threadIdx.x / GROUP, t = threadIdx.x % GROUP;
+  const int64_t o = blockIdx.x * (int64_t)RPC + g;
+  const int S = gridDim.y, s = blockIdx.y;
+  const int64_t r0 = s * Rs, r1 = min(R, r0 + Rs);
+  const bool live = o < O;
   const float* row = x + (live ? o : 0) * R;
   if (OP != B2_RED_MAX) {
-    double acc = 0;
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
     if (live) {
       if (VEC) {
-        for (int64_t r = r0 + 4 * t; r < r1; r += 4 * GROUP) {
+        int64_t r = r0 + 4 * t;
+        for (; r + 12 * GROUP + 3 < r1; r += 16 * GROUP) {  // 4 x 128-bit loads in flight
+          const float4 v0 = *reinterpret_cast<const float4*>(row + r);
+          const float4 v1 = *reinterpret_cast<const float4*>(row + r + 4 * GROUP);
+          const float4 v2 = *reinterpret_cast<const float4*>(row + r + 8 * GROUP);
+          const float4 v3 = *reinterpret_cast<const float4*>(row + r + 12 * GROUP);
+          a0 += (double)v0.x + (double)v0.y + (double)v0.z + (double)v0.w;
+          a1 += (double)v1.x + (double)v1.y + (double)v1.z + (double)v1.w;
+          a2 += (double)v2.x + (double)v2.y + (double)v2.z + (double)v2.w;
+          a3 += (double)v3.x + (double)v3.y + (double)v3.z + (double)v3.w;
+        }
+        for (; r < r1; r += 4 * GROUP) {
           if (r + 3 < r1) {
-            float4 v = *reinterpret_cast<const float4*>(row + r);
-            acc += (double)v.x;
-            acc += (double)v.y;
-            acc += (double)v.z;
-            acc += (double)v.w;
+            const float4 v = *reinterpret_cast<const float4*>(row + r);
+            a0 += (double)v.x + (double)v.y + (double)v.z + (double)v.w;
           } else {
-            for (int64_t k = r; k < r1; ++k) acc += (double)row[k];
+            for (int64_t k = r; k < r1; ++k) a0 += (double)row[k];
           }
         }
       } else {
-        for (int64_t r = r0 + t; r < r1; r += GROUP) acc += (double)row[r];
+        int64_t r = r0 + t;
+        for (; r + 3 * GROUP < r1; r += 4 * GROUP) {
+          a0 += (double)row[r];
+          a1 += (double)row[r + GROUP];
+          a2 += (double)row[r + 2 * GROUP];
+          a3 += (double)row[r + 3 * GROUP];
+        }
+        for (; r < r1; r += GROUP) a0 += (double)row[r];
       }
     }
-    double tot = group_sum<GROUP>(acc, shd);
+    const double tot = group_sum<GROUP>((a0 + a1) + (a2 + a3), shd);
     if (live && t == 0) {
-      if (S > 1) {
+      if (S > 1)
         psum[(int64_t)s * O + o] = tot;
-      } else {
+      else
         out[o] = OP == B2_RED_MEAN ? __double2float_rn(tot / count) : __double2float_rn(tot);
-      }
     }
   } else {
-    MaxAcc acc{0.f, kNone};
+    // each of the 4 lanes of the unroll scans its own index sequence in order
+    float b0 = -INFINITY, b1 = -INFINITY, b2 = -INFINITY, b3 = -INFINITY;
+    int64_t i0 = kNone, i1 = kNone, i2 = kNone, i3 = kNone;
     if (live) {
       if (VEC) {
-        for (int64_t r = r0 + 4 * t; r < r1; r += 4 * GROUP) {
+        int64_t r = r0 + 4 * t;
+        for (; r + 12 * GROUP + 3 < r1; r += 16 * GROUP) {  // 4 x 128-bit loads in flight
+          const float4 v0 = *reinterpret_cast<const float4*>(row + r);
+          const float4 v1 = *reinterpret_cast<const float4*>(row + r + 4 * GROUP);
+          const float4 v2 = *reinterpret_cast<const float4*>(row + r + 8 * GROUP);
+          const float4 v3 = *reinterpret_cast<const float4*>(row + r + 12 * GROUP);
+          const int64_t q1 = r + 4 * GROUP, q2 = r + 8 * GROUP, q3 = r + 12 * GROUP;
+          max_scan(b0, i0, v0.x, r);  max_scan(b1, i1, v0.y, r + 1);
+          max_scan(b2, i2, v0.z, r + 2);  max_scan(b3, i3, v0.w, r + 3);
+          max_scan(b0, i0, v1.x, q1);  max_scan(b1, i1, v1.y, q1 + 1);
+          max_scan(b2, i2, v1.z, q1 + 2);  max_scan(b3, i3, v1.w, q1 + 3);
+          max_scan(b0, i0, v2.x, q2);  max_scan(b1, i1, v2.y, q2 + 1);
+          max_scan(b2, i2, v2.z, q2 + 2);  max_scan(b3, i3, v2.w, q2 + 3);
+          max_scan(b0, i0, v3.x, q3);  max_scan(b1, i1, v3.y, q3 + 1);
+          max_scan(b2, i2, v3.z, q3 + 2);  max_scan(b3, i3, v3.w, q3 + 3);
+        }
+        for (; r < r1; r += 4 * GROUP) {
           if (r + 3 < r1) {
-            float4 v = *reinterpret_cast<const float4*>(row + r);
-            max_push(acc, v.x, r);
-            max_push(acc, v.y, r + 1);
-            max_push(acc, v.z, r + 2);
-            max_push(acc, v.w, r + 3);
+            const float4 v = *reinterpret_cast<const float4*>(row + r);
+            max_scan(b0, i0, v.x, r);
+            max_scan(b1, i1, v.y, r + 1);
+            max_scan(b2, i2, v.z, r + 2);
+            max_scan(b3, i3, v.w, r + 3);
           } else {
-            for (int64_t k = r; k < r1; ++k) max_push(acc, row[k], k);
+            for (int64_t k = r; k < r1; ++k) max_scan(b0, i0, row[k], k);
           }
         }
       } else {
-        for (int64_t r = r0 + t; r < r1; r += GROUP) max_push(acc, row[r], r);
+        for (int64_t r = r0 + t; r < r1; r += GROUP) max_scan(b0, i0, row[r], r);
       }
     }
-    MaxAcc best = group_max<GROUP>(acc, shm);
+    MaxAcc acc = max_combine(max_combine(MaxAcc{b0, i0}, MaxAcc{b1, i1}),
+                             max_combine(MaxAcc{b2, i2}, MaxAcc{b3, i3}));
+    if (live && s == 0 && t == 0) {
+      const float v0 = row[0];
+      if (isnan(v0)) acc = MaxAcc{v0, 0};          // first-slot NaN sticks
+      else if (acc.i == kNone || !(acc.v > v0)) {  // all -inf/NaN: x0 at index 0
+        if (acc.i == kNone || acc.v == v0) acc = max_combine(acc, MaxAcc{v0, 0});
+      }
+    }
+    const MaxAcc best = group_max<GROUP>(acc, shm);
     if (live && t == 0) {
       if (S > 1) {
         pmax[(int64_t)s * O + o] = best;
@@ -175,63 +219,148 @@ __global__ void __launch_bounds__(256) k_rows(const float* __restrict__ x, int64
 }
 
 // ---------------------------------------------------------------- mid reduce
-// x: [O1, R, I] contiguous; output o = o1*I + i. grid = (cb * O1, S), cb = ceil(I/256)
-template <int OP>
-__global__ void __launch_bounds__(256) k_mid(const float* __restrict__ x, int64_t O1, int64_t R,
+// x: [O1, R, I] contiguous; output o = o1*I + i. Each thread owns 4
+// consecutive columns (float4; I % 4 == 0) or one column; rows unrolled x4.
+// grid = (cb * O1, S), cb = ceil(I / (256 * V)).
+template <int OP, int V>
+__global__ void __launch_bounds__(256, 4) k_mid(const float* __restrict__ x, int64_t O1, int64_t R,
                                              int64_t I, int64_t Rs, float* __restrict__ out,
                                              int64_t* __restrict__ argr, double* __restrict__ psum,
                                              MaxAcc* __restrict__ pmax, double count, int64_t cb) {
-  int64_t o1 = blockIdx.x / cb;
-  int64_t i = (blockIdx.x - o1 * cb) * (int64_t)blockDim.x + threadIdx.x;
-  int S = gridDim.y, s = blockIdx.y;
+  const int64_t o1 = blockIdx.x / cb;
+  const int64_t i = ((blockIdx.x - o1 * cb) * (int64_t)blockDim.x + threadIdx.x) * V;
+  const int S = gridDim.y, s = blockIdx.y;
   if (i >= I) return;
-  int64_t r0 = s * Rs, r1 = min(R, r0 + Rs);
+  const int64_t r0 = s * Rs, r1 = min(R, r0 + Rs);
   const float* base = x + o1 * R * I + i;
-  int64_t o = o1 * I + i;
-  int64_t O = O1 * I;
+  const int64_t o = o1 * I + i;
+  const int64_t O = O1 * I;
+  if (OP != B2_RED_MAX) {
+    double a[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) a[j] = 0.0;
+    int64_t r = r0;
+    if (V == 4) {
+      for (; r + 3 < r1; r += 4) {
+        const float4 v0 = *reinterpret_cast<const float4*>(base + r * I);
+        const float4 v1 = *reinterpret_cast<const float4*>(base + (r + 1) * I);
+        const float4 v2 = *reinterpret_cast<const float4*>(base + (r + 2) * I);
+        const float4 v3 = *reinterpret_cast<const float4*>(base + (r + 3) * I);
+        a[0] += (double)v0.x + (double)v1.x + (double)v2.x + (double)v3.x;
+        a[1] += (double)v0.y + (double)v1.y + (double)v2.y + (double)v3.y;
+        a[2] += (double)v0.z + (double)v1.z + (double)v2.z + (double)v3.z;
+        a[3] += (double)v0.w + (double)v1.w + (double)v2.w + (double)v3.w;
+      }
+      for (; r < r1; ++r) {
+        const float4 v = *reinterpret_cast<const float4*>(base + r * I);
+        a[0] += (double)v.x;
+        a[1] += (double)v.y;
+        a[2] += (double)v.z;
+        a[3] += (double)v.w;
+      }
+    } else {
+      for (; r + 3 < r1; r += 4)
+        a[0] += (double)base[r * I] + (double)base[(r + 1) * I] + (double)base[(r + 2) * I] +
+                (double)base[(r + 3) * I];
+      for (; r < r1; ++r) a[0] += (double)base[r * I];
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (S > 1)
+        psum[(int64_t)s * O + o + j] = a[j];
+      else
+        out[o + j] = OP == B2_RED_MEAN ? __double2float_rn(a[j] / count) : __double2float_rn(a[j]);
+    }
+  } else {
+    float b[V];
+    int64_t bi[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      b[j] = -INFINITY;
+      bi[j] = kNone;
+    }
+    for (int64_t r = r0; r < r1; ++r) {
+      if (V == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(base + r * I);
+        max_scan(b[0], bi[0], v.x, r);
+        max_scan(b[1], bi[1], v.y, r);
+        max_scan(b[2], bi[2], v.z, r);
+        max_scan(b[3], bi[3], v.w, r);
+      } else {
+        max_scan(b[0], bi[0], base[r * I], r);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      MaxAcc acc{b[j], bi[j]};
+      if (s == 0) {
+        const float v0 = base[j];
+        if (isnan(v0)) acc = MaxAcc{v0, 0};
+        else if (acc.i == kNone || acc.v == v0) acc = max_combine(acc, MaxAcc{v0, 0});
+      }
+      if (S > 1) {
+        pmax[(int64_t)s * O + o + j] = acc;
+      } else {
+        out[o + j] = acc.v;
+        if (argr) argr[o + j] = acc.i;
+      }
+    }
+  }
+}
+
+// Second stage over partials [S][O]. A CTA owns `cpt` consecutive outputs
+// (a power of two <= 32) with 256/cpt threads per output: thread (c, k) folds
+// partials s = k, k + lpc, ... (warps read consecutive outputs: coalesced) and
+// a fixed shared-memory tree combines the k's -- deterministic for a given S.
+template <int OP>
+__global__ void __launch_bounds__(256) k_final(int64_t O, int S, const double* __restrict__ psum,
+                                               const MaxAcc* __restrict__ pmax,
+                                               float* __restrict__ out, int64_t* __restrict__ argr,
+                                               double count, int cpt) {
+  __shared__ double shd[256];
+  __shared__ MaxAcc shm[256];
+  const int lpc = 256 / cpt;
+  const int c = threadIdx.x % cpt, k = threadIdx.x / cpt;
+  const int64_t o = blockIdx.x * (int64_t)cpt + c;
+  const bool live = o < O;
   if (OP != B2_RED_MAX) {
     double acc = 0;
-    int64_t r = r0;
-    for (; r + 3 < r1; r += 4) {  // 4 independent loads in flight
-      float a0 = base[r * I], a1 = base[(r + 1) * I], a2 = base[(r + 2) * I], a3 = base[(r + 3) * I];
-      acc += (double)a0;
-      acc += (double)a1;
-      acc += (double)a2;
-      acc += (double)a3;
+    if (live)
+      for (int s = k; s < S; s += lpc) acc += psum[(int64_t)s * O + o];
+    shd[threadIdx.x] = acc;
+    __syncthreads();
+    for (int h = lpc / 2; h > 0; h >>= 1) {
+      if (k < h) shd[threadIdx.x] += shd[threadIdx.x + h * cpt];
+      __syncthreads();
     }
-    for (; r < r1; ++r) acc += (double)base[r * I];
-    if (S > 1)
-      psum[(int64_t)s * O + o] = acc;
-    else
-      out[o] = OP == B2_RED_MEAN ? __double2float_rn(acc / count) : __double2float_rn(acc);
+    if (live && k == 0) {
+      const double tot = shd[c];
+      out[o] = OP == B2_RED_MEAN ? __double2float_rn(tot / count) : __double2float_rn(tot);
+    }
   } else {
-    MaxAcc acc{0.f, kNone};
-    for (int64_t r = r0; r < r1; ++r) max_push(acc, base[r * I], r);
-    if (S > 1) {
-      pmax[(int64_t)s * O + o] = acc;
-    } else {
-      out[o] = acc.v;
-      if (argr) argr[o] = acc.i;
+    MaxAcc a{0.f, kNone};
+    if (live)
+      for (int s = k; s < S; s += lpc) a = max_combine(a, pmax[(int64_t)s * O + o]);
+    shm[threadIdx.x] = a;
+    __syncthreads();
+    for (int h = lpc / 2; h > 0; h >>= 1) {
+      if (k < h) shm[threadIdx.x] = max_combine(shm[threadIdx.x], shm[threadIdx.x + h * cpt]);
+      __syncthreads();
+    }
+    if (live && k == 0) {
+      out[o] = shm[c].v;
+      if (argr) argr[o] = shm[c].i;
     }
   }
 }
 
 template <int OP>
-__global__ void k_final(int64_t O, int S, const double* __restrict__ psum,
-                        const MaxAcc* __restrict__ pmax, float* __restrict__ out,
-                        int64_t* __restrict__ argr, double count) {
-  int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (o >= O) return;
-  if (OP != B2_RED_MAX) {
-    double acc = 0;
-    for (int s = 0; s < S; ++s) acc += psum[(int64_t)s * O + o];
-    out[o] = OP == B2_RED_MEAN ? __double2float_rn(acc / count) : __double2float_rn(acc);
-  } else {
-    MaxAcc a{0.f, kNone};
-    for (int s = 0; s < S; ++s) a = max_combine(a, pmax[(int64_t)s * O + o]);
-    out[o] = a.v;
-    if (argr) argr[o] = a.i;
-  }
+void launch_final(int64_t O, int64_t S, const double* psum, const MaxAcc* pmax, float* out,
+                  int64_t* argr, double count, cudaStream_t st) {
+  int cpt = 32;
+  while (cpt > 1 && cpt / 2 >= O) cpt /= 2;
+  k_final<OP><<<(unsigned)((O + cpt - 1) / cpt), 256, 0, st>>>(O, (int)S, psum, pmax, out, argr,
+                                                                count, cpt);
 }
 
 __global__ void k_fill_out(float* out, int64_t* argr, int64_t n, float v) {
@@ -270,14 +399,16 @@ __global__ void k_max_scatter(float* __restrict__ gx, const float* __restrict__ 
 template <int OP>
 int run_rows(const float* x, int64_t O, int64_t R, float* out, int64_t* argr, double count,
              cudaStream_t st) {
-  bool vec = ((uintptr_t)x & 15) == 0 && R % 4 == 0;
-  int sms = b2::sm_count();
-  int group = R >= 2048 ? 256 : 32;
-  int rpc = 256 / group;
-  int64_t ctas = (O + rpc - 1) / rpc;
+  const bool vec = ((uintptr_t)x & 15) == 0 && R % 4 == 0;
+  const int sms = b2::sm_count();
+  // a warp per row up to 16K elements (8 rows per CTA: no block barrier, and
+  // enough bytes in flight per CTA); a whole CTA per row beyond that
+  const int group = R > 16384 ? 256 : 32;
+  const int rpc = 256 / group;
+  const int64_t ctas = (O + rpc - 1) / rpc;
   int64_t S = 1;
-  if (ctas < 2 * sms && R >= 8192) {  // few long rows: split R across CTAs
-    S = std::min<int64_t>((4 * sms + ctas - 1) / ctas, (R + 4095) / 4096);
+  if (ctas < 2 * sms && R >= 16384) {  // few long rows: split R so ~2 CTAs per SM
+    S = std::min<int64_t>((2 * sms + ctas - 1) / ctas, (R + 16383) / 16384);
     S = std::max<int64_t>(S, 1);
   }
   int64_t Rs = (R + S - 1) / S;
@@ -303,7 +434,7 @@ int run_rows(const float* x, int64_t O, int64_t R, float* out, int64_t* argr, do
 #undef B2_ROWS
   int rc = b2::launched("b2_reduce(rows)");
   if (!rc && S > 1) {
-    k_final<OP><<<(unsigned)((O + 255) / 256), 256, 0, st>>>(O, (int)S, psum, pmax, out, argr, count);
+    launch_final<OP>(O, S, psum, pmax, out, argr, count, st);
     rc = b2::launched("b2_reduce(final)");
   }
   if (ws) b2_free(ws, st);
@@ -313,9 +444,10 @@ int run_rows(const float* x, int64_t O, int64_t R, float* out, int64_t* argr, do
 template <int OP>
 int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_t* argr,
             double count, cudaStream_t st) {
-  int sms = b2::sm_count();
-  int64_t cb = (I + 255) / 256;
-  int64_t ctas = cb * O1;
+  const int sms = b2::sm_count();
+  const int V = (I % 4 == 0 && ((uintptr_t)x & 15) == 0) ? 4 : 1;
+  const int64_t cb = (I + 256 * V - 1) / (256 * V);
+  const int64_t ctas = cb * O1;
   int64_t S = 1;
   if (ctas < 4 * sms && R >= 64) {
     S = std::min<int64_t>((4 * sms + ctas - 1) / ctas, R / 16);
@@ -324,7 +456,7 @@ int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_
   int64_t Rs = (R + S - 1) / S;
   S = (R + Rs - 1) / Rs;
   if (S < 1) S = 1;
-  int64_t O = O1 * I;
+  const int64_t O = O1 * I;
   void* ws = nullptr;
   double* psum = nullptr;
   MaxAcc* pmax = nullptr;
@@ -335,10 +467,13 @@ int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_
     pmax = (MaxAcc*)ws;
   }
   dim3 grid((unsigned)(cb * O1), (unsigned)S);
-  k_mid<OP><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, cb);
+  if (V == 4)
+    k_mid<OP, 4><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, cb);
+  else
+    k_mid<OP, 1><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, cb);
   int rc = b2::launched("b2_reduce(mid)");
   if (!rc && S > 1) {
-    k_final<OP><<<(unsigned)((O + 255) / 256), 256, 0, st>>>(O, (int)S, psum, pmax, out, argr, count);
+    launch_final<OP>(O, S, psum, pmax, out, argr, count, st);
     rc = b2::launched("b2_reduce(final)");
   }
   if (ws) b2_free(ws, st);
