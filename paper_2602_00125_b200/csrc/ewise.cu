@@ -386,22 +386,31 @@ __global__ void __launch_bounds__(kThreads) k_muladd_relu_fwd(float* __restrict_
                                                               const float* __restrict__ b,
                                                               const float* __restrict__ c,
                                                               int64_t rows, int64_t cols) {
-  int64_t c4 = cols >> 2;
+  const int64_t c4 = cols >> 2;
+  auto one = [&](const float4& va, int64_t j) {
+    const float4 vb = reinterpret_cast<const float4*>(b)[j];
+    const float4 vc = reinterpret_cast<const float4*>(c)[j];
+    float4 o;
+    float q;
+    q = __fadd_rn(__fmul_rn(va.x, vb.x), vc.x); o.x = q > 0.f ? q : 0.f;
+    q = __fadd_rn(__fmul_rn(va.y, vb.y), vc.y); o.y = q > 0.f ? q : 0.f;
+    q = __fadd_rn(__fmul_rn(va.z, vb.z), vc.z); o.z = q > 0.f ? q : 0.f;
+    q = __fadd_rn(__fmul_rn(va.w, vb.w), vc.w); o.w = q > 0.f ? q : 0.f;
+    return o;
+  };
+  const int64_t B = blockDim.x;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     const float4* pa = reinterpret_cast<const float4*>(a + r * cols);
     float4* py = reinterpret_cast<float4*>(y + r * cols);
-    for (int64_t j = threadIdx.x; j < c4; j += blockDim.x) {
-      float4 va = pa[j];
-      float4 vb = reinterpret_cast<const float4*>(b)[j];
-      float4 vc = reinterpret_cast<const float4*>(c)[j];
-      float4 o;
-      float q;
-      q = __fadd_rn(__fmul_rn(va.x, vb.x), vc.x); o.x = q > 0.f ? q : 0.f;
-      q = __fadd_rn(__fmul_rn(va.y, vb.y), vc.y); o.y = q > 0.f ? q : 0.f;
-      q = __fadd_rn(__fmul_rn(va.z, vb.z), vc.z); o.z = q > 0.f ? q : 0.f;
-      q = __fadd_rn(__fmul_rn(va.w, vb.w), vc.w); o.w = q > 0.f ? q : 0.f;
-      py[j] = o;
+    int64_t j = threadIdx.x;
+    for (; j + 3 * B < c4; j += 4 * B) {  // 4 independent 128-bit loads in flight
+      const float4 v0 = pa[j], v1 = pa[j + B], v2 = pa[j + 2 * B], v3 = pa[j + 3 * B];
+      py[j] = one(v0, j);
+      py[j + B] = one(v1, j + B);
+      py[j + 2 * B] = one(v2, j + 2 * B);
+      py[j + 3 * B] = one(v3, j + 3 * B);
     }
+    for (; j < c4; j += B) py[j] = one(pa[j], j);
   }
 }
 
@@ -457,18 +466,35 @@ __global__ void __launch_bounds__(kThreads) k_muladd_relu_bwd(float* __restrict_
   pcnt[o] = n0; pcnt[o + 1] = n1; pcnt[o + 2] = n2; pcnt[o + 3] = n3;
 }
 
-__global__ void k_muladd_relu_bwd_final(float* __restrict__ gb, const double* __restrict__ psum,
-                                        const int* __restrict__ pcnt, int64_t cols, int splits) {
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= cols) return;
+// 32 columns per CTA x 8 split-lanes per column: lane k folds splits k, k+8,
+// ... (warps read 32 consecutive columns), then a fixed smem tree -> deterministic
+__global__ void __launch_bounds__(256) k_muladd_relu_bwd_final(float* __restrict__ gb,
+                                                               const double* __restrict__ psum,
+                                                               const int* __restrict__ pcnt,
+                                                               int64_t cols, int splits) {
+  __shared__ double ss[256];
+  __shared__ int64_t sn[256];
+  const int c = threadIdx.x & 31, k = threadIdx.x >> 5;
+  const int64_t col = blockIdx.x * 32ll + c;
   double s = 0;
   int64_t n = 0;
-  for (int k = 0; k < splits; ++k) {  // fixed order -> deterministic
-    s += psum[k * cols + c];
-    n += pcnt[k * cols + c];
+  if (col < cols)
+    for (int q = k; q < splits; q += 8) {
+      s += psum[q * cols + col];
+      n += pcnt[q * cols + col];
+    }
+  ss[threadIdx.x] = s;
+  sn[threadIdx.x] = n;
+  __syncthreads();
+  for (int h = 4; h > 0; h >>= 1) {
+    if (k < h) {
+      ss[threadIdx.x] += ss[threadIdx.x + 32 * h];
+      sn[threadIdx.x] += sn[threadIdx.x + 32 * h];
+    }
+    __syncthreads();
   }
   // GradStore: count (add pullback) first, then f32(sum mask*a) (mul pullback)
-  gb[c] = __fadd_rn((float)n, __double2float_rn(s));
+  if (k == 0 && col < cols) gb[col] = __fadd_rn((float)sn[c], __double2float_rn(ss[c]));
 }
 
 }  // namespace
@@ -606,8 +632,8 @@ int b2_fused_muladd_relu_bwd(float* ga, float* gb, const float* a, const float* 
   k_muladd_relu_bwd<<<grid, kThreads, 0, st>>>(ga, psum, pcnt, a, b, rows, cols, rps);
   int rc = b2::launched("b2_fused_muladd_relu_bwd");
   if (!rc) {
-    k_muladd_relu_bwd_final<<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(gb, psum, pcnt, cols,
-                                                                           (int)splits);
+    k_muladd_relu_bwd_final<<<(unsigned)((cols + 31) / 32), 256, 0, st>>>(gb, psum, pcnt, cols,
+                                                                         (int)splits);
     rc = b2::launched("b2_fused_muladd_relu_bwd_final");
   }
   b2_free(ws, stream);
