@@ -222,54 +222,81 @@ __global__ void __launch_bounds__(256) k_rows(const float* __restrict__ x, int64
 // x: [O1, R, I] contiguous; output o = o1*I + i. Each thread owns 4
 // consecutive columns (float4; I % 4 == 0) or one column; rows unrolled x4.
 // grid = (cb * O1, S), cb = ceil(I / (256 * V)).
+// Column strips with in-CTA row lanes: a CTA owns CL*V consecutive columns
+// (CL column lanes x V columns each) and RL = 256/CL row lanes; row lane k
+// scans rows k, k+RL, ... of the CTA's row split (a warp reads 2 rows x 256 B,
+// coalesced), then a fixed shared-memory tree folds the RL lanes. Splits S
+// stay small (~8), so the second stage is cheap. grid = (strips * O1, S).
 template <int OP, int V>
-__global__ void __launch_bounds__(256, 4) k_mid(const float* __restrict__ x, int64_t O1, int64_t R,
-                                             int64_t I, int64_t Rs, float* __restrict__ out,
-                                             int64_t* __restrict__ argr, double* __restrict__ psum,
-                                             MaxAcc* __restrict__ pmax, double count, int64_t cb) {
-  const int64_t o1 = blockIdx.x / cb;
-  const int64_t i = ((blockIdx.x - o1 * cb) * (int64_t)blockDim.x + threadIdx.x) * V;
+__global__ void __launch_bounds__(256) k_strip(const float* __restrict__ x, int64_t O1, int64_t R,
+                                               int64_t I, int64_t Rs, float* __restrict__ out,
+                                               int64_t* __restrict__ argr,
+                                               double* __restrict__ psum,
+                                               MaxAcc* __restrict__ pmax, double count,
+                                               int64_t strips) {
+  constexpr int CL = V == 4 ? 16 : 32;  // column lanes
+  constexpr int RL = 256 / CL;          // row lanes
+  __shared__ double shd[256 * V];
+  __shared__ MaxAcc shm[OP == B2_RED_MAX ? 256 * V : 1];
+  const int cl = threadIdx.x % CL, rl = threadIdx.x / CL;
+  const int64_t o1 = blockIdx.x / strips;
+  const int64_t i = ((blockIdx.x - o1 * strips) * CL + cl) * V;
   const int S = gridDim.y, s = blockIdx.y;
-  if (i >= I) return;
   const int64_t r0 = s * Rs, r1 = min(R, r0 + Rs);
-  const float* base = x + o1 * R * I + i;
-  const int64_t o = o1 * I + i;
-  const int64_t O = O1 * I;
+  const bool live = i < I;
+  const float* base = x + o1 * R * I + (live ? i : 0);
   if (OP != B2_RED_MAX) {
     double a[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) a[j] = 0.0;
-    int64_t r = r0;
-    if (V == 4) {
-      for (; r + 3 < r1; r += 4) {
-        const float4 v0 = *reinterpret_cast<const float4*>(base + r * I);
-        const float4 v1 = *reinterpret_cast<const float4*>(base + (r + 1) * I);
-        const float4 v2 = *reinterpret_cast<const float4*>(base + (r + 2) * I);
-        const float4 v3 = *reinterpret_cast<const float4*>(base + (r + 3) * I);
-        a[0] += (double)v0.x + (double)v1.x + (double)v2.x + (double)v3.x;
-        a[1] += (double)v0.y + (double)v1.y + (double)v2.y + (double)v3.y;
-        a[2] += (double)v0.z + (double)v1.z + (double)v2.z + (double)v3.z;
-        a[3] += (double)v0.w + (double)v1.w + (double)v2.w + (double)v3.w;
+    if (live) {
+      int64_t r = r0 + rl;
+      for (; r + 3 * RL < r1; r += 4 * RL) {  // 4 independent loads in flight
+        if (V == 4) {
+          const float4 v0 = *reinterpret_cast<const float4*>(base + r * I);
+          const float4 v1 = *reinterpret_cast<const float4*>(base + (r + RL) * I);
+          const float4 v2 = *reinterpret_cast<const float4*>(base + (r + 2 * RL) * I);
+          const float4 v3 = *reinterpret_cast<const float4*>(base + (r + 3 * RL) * I);
+          a[0] += (double)v0.x + (double)v1.x + (double)v2.x + (double)v3.x;
+          a[V > 1 ? 1 : 0] += (double)v0.y + (double)v1.y + (double)v2.y + (double)v3.y;
+          a[V > 2 ? 2 : 0] += (double)v0.z + (double)v1.z + (double)v2.z + (double)v3.z;
+          a[V > 3 ? 3 : 0] += (double)v0.w + (double)v1.w + (double)v2.w + (double)v3.w;
+        } else {
+          a[0] += (double)base[r * I] + (double)base[(r + RL) * I] + (double)base[(r + 2 * RL) * I] +
+                  (double)base[(r + 3 * RL) * I];
+        }
       }
-      for (; r < r1; ++r) {
-        const float4 v = *reinterpret_cast<const float4*>(base + r * I);
-        a[0] += (double)v.x;
-        a[1] += (double)v.y;
-        a[2] += (double)v.z;
-        a[3] += (double)v.w;
+      for (; r < r1; r += RL) {
+        if (V == 4) {
+          const float4 v = *reinterpret_cast<const float4*>(base + r * I);
+          a[0] += (double)v.x;
+          a[V > 1 ? 1 : 0] += (double)v.y;
+          a[V > 2 ? 2 : 0] += (double)v.z;
+          a[V > 3 ? 3 : 0] += (double)v.w;
+        } else {
+          a[0] += (double)base[r * I];
+        }
       }
-    } else {
-      for (; r + 3 < r1; r += 4)
-        a[0] += (double)base[r * I] + (double)base[(r + 1) * I] + (double)base[(r + 2) * I] +
-                (double)base[(r + 3) * I];
-      for (; r < r1; ++r) a[0] += (double)base[r * I];
     }
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      if (S > 1)
-        psum[(int64_t)s * O + o + j] = a[j];
-      else
-        out[o + j] = OP == B2_RED_MEAN ? __double2float_rn(a[j] / count) : __double2float_rn(a[j]);
+    for (int j = 0; j < V; ++j) shd[(rl * CL + cl) * V + j] = a[j];
+    __syncthreads();
+    for (int h = RL / 2; h > 0; h >>= 1) {
+      if (rl < h)
+#pragma unroll
+        for (int j = 0; j < V; ++j) shd[(rl * CL + cl) * V + j] += shd[((rl + h) * CL + cl) * V + j];
+      __syncthreads();
+    }
+    if (rl == 0 && live) {
+      const int64_t o = o1 * I + i;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const double t = shd[cl * V + j];
+        if (S > 1)
+          psum[(int64_t)s * O1 * I + o + j] = t;
+        else
+          out[o + j] = OP == B2_RED_MEAN ? __double2float_rn(t / count) : __double2float_rn(t);
+      }
     }
   } else {
     float b[V];
@@ -279,30 +306,46 @@ __global__ void __launch_bounds__(256, 4) k_mid(const float* __restrict__ x, int
       b[j] = -INFINITY;
       bi[j] = kNone;
     }
-    for (int64_t r = r0; r < r1; ++r) {
-      if (V == 4) {
-        const float4 v = *reinterpret_cast<const float4*>(base + r * I);
-        max_scan(b[0], bi[0], v.x, r);
-        max_scan(b[1], bi[1], v.y, r);
-        max_scan(b[2], bi[2], v.z, r);
-        max_scan(b[3], bi[3], v.w, r);
-      } else {
-        max_scan(b[0], bi[0], base[r * I], r);
+    if (live) {
+      for (int64_t r = r0 + rl; r < r1; r += RL) {
+        if (V == 4) {
+          const float4 v = *reinterpret_cast<const float4*>(base + r * I);
+          max_scan(b[0], bi[0], v.x, r);
+          max_scan(b[V > 1 ? 1 : 0], bi[V > 1 ? 1 : 0], v.y, r);
+          max_scan(b[V > 2 ? 2 : 0], bi[V > 2 ? 2 : 0], v.z, r);
+          max_scan(b[V > 3 ? 3 : 0], bi[V > 3 ? 3 : 0], v.w, r);
+        } else {
+          max_scan(b[0], bi[0], base[r * I], r);
+        }
       }
     }
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      MaxAcc acc{b[j], bi[j]};
-      if (s == 0) {
-        const float v0 = base[j];
-        if (isnan(v0)) acc = MaxAcc{v0, 0};
-        else if (acc.i == kNone || acc.v == v0) acc = max_combine(acc, MaxAcc{v0, 0});
-      }
-      if (S > 1) {
-        pmax[(int64_t)s * O + o + j] = acc;
-      } else {
-        out[o + j] = acc.v;
-        if (argr) argr[o + j] = acc.i;
+    for (int j = 0; j < V; ++j) shm[(rl * CL + cl) * V + j] = MaxAcc{b[j], bi[j]};
+    __syncthreads();
+    for (int h = RL / 2; h > 0; h >>= 1) {
+      if (rl < h)
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          shm[(rl * CL + cl) * V + j] =
+              max_combine(shm[(rl * CL + cl) * V + j], shm[((rl + h) * CL + cl) * V + j]);
+      __syncthreads();
+    }
+    if (rl == 0 && live) {
+      const int64_t o = o1 * I + i;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        MaxAcc acc = shm[cl * V + j];
+        if (s == 0) {  // the first scanned slot of this column: NaN sticks, -inf ties at 0
+          const float v0 = base[j];
+          if (isnan(v0)) acc = MaxAcc{v0, 0};
+          else acc = max_combine(acc, MaxAcc{v0, 0});
+        }
+        if (S > 1) {
+          pmax[(int64_t)s * O1 * I + o + j] = acc;
+        } else {
+          out[o + j] = acc.v;
+          if (argr) argr[o + j] = acc.i;
+        }
       }
     }
   }
@@ -446,11 +489,12 @@ int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_
             double count, cudaStream_t st) {
   const int sms = b2::sm_count();
   const int V = (I % 4 == 0 && ((uintptr_t)x & 15) == 0) ? 4 : 1;
-  const int64_t cb = (I + 256 * V - 1) / (256 * V);
-  const int64_t ctas = cb * O1;
+  const int CL = V == 4 ? 16 : 32, RL = 256 / CL;
+  const int64_t strips = (I + CL * V - 1) / (CL * V);
+  const int64_t ctas = strips * O1;
   int64_t S = 1;
-  if (ctas < 4 * sms && R >= 64) {
-    S = std::min<int64_t>((4 * sms + ctas - 1) / ctas, R / 16);
+  if (ctas < 4 * sms) {
+    S = std::min<int64_t>((4 * sms + ctas - 1) / ctas, R / (RL * 8));
     S = std::max<int64_t>(S, 1);
   }
   int64_t Rs = (R + S - 1) / S;
@@ -466,11 +510,11 @@ int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_
     psum = (double*)ws;
     pmax = (MaxAcc*)ws;
   }
-  dim3 grid((unsigned)(cb * O1), (unsigned)S);
+  dim3 grid((unsigned)(strips * O1), (unsigned)S);
   if (V == 4)
-    k_mid<OP, 4><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, cb);
+    k_strip<OP, 4><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, strips);
   else
-    k_mid<OP, 1><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, cb);
+    k_strip<OP, 1><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, strips);
   int rc = b2::launched("b2_reduce(mid)");
   if (!rc && S > 1) {
     launch_final<OP>(O, S, psum, pmax, out, argr, count, st);
