@@ -43,6 +43,13 @@ int b2_event_elapsed_ms(void* start, void* end, float* ms);
 int b2_stream_wait_event(void* stream, void* ev);
 /* kernels launched by this library since process start (launch counter) */
 int b2_launch_count(uint64_t* n);
+/* CUDA-graph capture of the engine stream (a training step replayed as one
+ * launch). Blocks freed during capture stay private to the graph; every block
+ * the graph touches is parked until b2_graph_destroy. No host syncs inside. */
+int b2_graph_begin(void* stream);
+int b2_graph_end(void* stream, int* graph_id);
+int b2_graph_launch(int graph_id, void* stream);
+int b2_graph_destroy(int graph_id);
 
 /* ---------------------------------------------------------------- storage
  * Replaces Buffer(array('f')) per op output (core.py:68-75, 315-330): a

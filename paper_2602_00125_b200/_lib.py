@@ -42,6 +42,10 @@ _SIGS = {
     "b2_event_elapsed_ms": (c_int, [c_void_p, c_void_p, POINTER(c_float)]),
     "b2_stream_wait_event": (c_int, [c_void_p, c_void_p]),
     "b2_launch_count": (c_int, [POINTER(c_uint64)]),
+    "b2_graph_begin": (c_int, [c_void_p]),
+    "b2_graph_end": (c_int, [c_void_p, POINTER(c_int)]),
+    "b2_graph_launch": (c_int, [c_int, c_void_p]),
+    "b2_graph_destroy": (c_int, [c_int]),
     "b2_alloc": (c_int, [c_size_t, c_void_p, POINTER(c_void_p)]),
     "b2_free": (c_int, [c_void_p, c_void_p]),
     "b2_alloc_stats": (c_int, [POINTER(c_size_t), POINTER(c_size_t), POINTER(c_size_t),

@@ -730,19 +730,23 @@ def _split(t, rows, cols, ld, kind):
     """Cached split of the stored matrix region of t for a tensor-core GEMM:
     kind "tf32x" -> (bf16 hi, bf16 lo) of trunc_tf32(x) / x - trunc (2 B each),
     kind "3xtf32" -> (fp32 hi, fp32 lo). Invalidated by the buffer version."""
+    from .graph import _capturing
+
     buf = t.buffer
     key = (kind, t.offset, rows, cols, ld)
     if buf._splits is None:
         buf._splits = {}
     ent = buf._splits.get(key)
-    if ent is not None and ent[0] == buf.version:
+    cap = _capturing[0]
+    # inside a CUDA-graph capture only splits made by this capture are trusted
+    if ent is not None and ent[0] == buf.version and (not cap or ent[3] == cap):
         return ent[1], ent[2]
     n = rows * cols
     esz = 2 if kind == "tf32x" else 4
     hi, lo = Buffer(esz * n), Buffer(esz * n)
     fn = "b2_bf16x2_split" if kind == "tf32x" else "b2_tf32_split"
     L.call(fn, hi.ptr, lo.ptr, t.data_ptr, rows, cols, ld, None)
-    buf._splits[key] = (buf.version, hi, lo)
+    buf._splits[key] = (buf.version, hi, lo, cap)
     return hi, lo
 
 

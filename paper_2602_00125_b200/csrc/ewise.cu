@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fexp.cuh"
 
 namespace {
 
@@ -100,7 +101,7 @@ struct Un {
   double alpha, beta;
   __device__ __forceinline__ float operator()(float x) const {
     if constexpr (OP == B2_NEG) return -x;
-    if constexpr (OP == B2_EXP) return __double2float_rn(exp((double)x));
+    if constexpr (OP == B2_EXP) return b2::exp_f32(x);
     if constexpr (OP == B2_LOG) return __double2float_rn(log((double)x));
     if constexpr (OP == B2_SQRT) return __fsqrt_rn(x);
     if constexpr (OP == B2_ABS) return fabsf(x);
@@ -423,12 +424,17 @@ __global__ void __launch_bounds__(kThreads) k_muladd_relu_bwd(float* __restrict_
                                                               const float* __restrict__ b,
                                                               int64_t rows, int64_t cols,
                                                               int64_t rows_per_split) {
-  // grid: x = column block of 4*kThreads columns, y = row split
-  int64_t col = (blockIdx.x * (int64_t)kThreads + threadIdx.x) * 4;
-  int64_t r0 = blockIdx.y * rows_per_split;
-  int64_t r1 = min(rows, r0 + rows_per_split);
-  if (col >= cols) return;
-  const float4 vb = *reinterpret_cast<const float4*>(b + col);
+  // grid: x = strip of 64 columns (16 column lanes x float4), y = row split;
+  // 16 row lanes per CTA (a warp touches 2 rows x 256 B), folded in smem
+  constexpr int CL = 16, RL = kThreads / CL;
+  __shared__ double sh_s[kThreads * 4];
+  __shared__ int sh_n[kThreads * 4];
+  const int cl = threadIdx.x % CL, rl = threadIdx.x / CL;
+  const int64_t col = (blockIdx.x * (int64_t)CL + cl) * 4;
+  const int64_t r0 = blockIdx.y * rows_per_split;
+  const int64_t r1 = min(rows, r0 + rows_per_split);
+  const bool live = col < cols;
+  const float4 vb = live ? *reinterpret_cast<const float4*>(b + col) : make_float4(0, 0, 0, 0);
   double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
   int n0 = 0, n1 = 0, n2 = 0, n3 = 0;
   auto one = [&](const float4& va, float4* dst) {
@@ -447,23 +453,45 @@ __global__ void __launch_bounds__(kThreads) k_muladd_relu_bwd(float* __restrict_
     n2 += m2 > 0.f;
     n3 += m3 > 0.f;
   };
-  int64_t r = r0;
-  for (; r + 3 < r1; r += 4) {  // 4 independent 128-bit loads in flight
-    const float4 v0 = *reinterpret_cast<const float4*>(a + r * cols + col);
-    const float4 v1 = *reinterpret_cast<const float4*>(a + (r + 1) * cols + col);
-    const float4 v2 = *reinterpret_cast<const float4*>(a + (r + 2) * cols + col);
-    const float4 v3 = *reinterpret_cast<const float4*>(a + (r + 3) * cols + col);
-    one(v0, reinterpret_cast<float4*>(ga + r * cols + col));
-    one(v1, reinterpret_cast<float4*>(ga + (r + 1) * cols + col));
-    one(v2, reinterpret_cast<float4*>(ga + (r + 2) * cols + col));
-    one(v3, reinterpret_cast<float4*>(ga + (r + 3) * cols + col));
+  if (live) {
+    int64_t r = r0 + rl;
+    for (; r + 3 * RL < r1; r += 4 * RL) {  // 4 independent 128-bit loads in flight
+      const float4 v0 = *reinterpret_cast<const float4*>(a + r * cols + col);
+      const float4 v1 = *reinterpret_cast<const float4*>(a + (r + RL) * cols + col);
+      const float4 v2 = *reinterpret_cast<const float4*>(a + (r + 2 * RL) * cols + col);
+      const float4 v3 = *reinterpret_cast<const float4*>(a + (r + 3 * RL) * cols + col);
+      one(v0, reinterpret_cast<float4*>(ga + r * cols + col));
+      one(v1, reinterpret_cast<float4*>(ga + (r + RL) * cols + col));
+      one(v2, reinterpret_cast<float4*>(ga + (r + 2 * RL) * cols + col));
+      one(v3, reinterpret_cast<float4*>(ga + (r + 3 * RL) * cols + col));
+    }
+    for (; r < r1; r += RL)
+      one(*reinterpret_cast<const float4*>(a + r * cols + col),
+          reinterpret_cast<float4*>(ga + r * cols + col));
   }
-  for (; r < r1; ++r)
-    one(*reinterpret_cast<const float4*>(a + r * cols + col),
-        reinterpret_cast<float4*>(ga + r * cols + col));
-  int64_t o = blockIdx.y * cols + col;
-  psum[o] = s0; psum[o + 1] = s1; psum[o + 2] = s2; psum[o + 3] = s3;
-  pcnt[o] = n0; pcnt[o + 1] = n1; pcnt[o + 2] = n2; pcnt[o + 3] = n3;
+  const int me = (rl * CL + cl) * 4;
+  sh_s[me] = s0; sh_s[me + 1] = s1; sh_s[me + 2] = s2; sh_s[me + 3] = s3;
+  sh_n[me] = n0; sh_n[me + 1] = n1; sh_n[me + 2] = n2; sh_n[me + 3] = n3;
+  __syncthreads();
+  for (int h = RL / 2; h > 0; h >>= 1) {  // fixed fold order -> deterministic
+    if (rl < h) {
+      const int other = ((rl + h) * CL + cl) * 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        sh_s[me + j] += sh_s[other + j];
+        sh_n[me + j] += sh_n[other + j];
+      }
+    }
+    __syncthreads();
+  }
+  if (rl == 0 && live) {
+    const int64_t o = blockIdx.y * cols + col;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      psum[o + j] = sh_s[cl * 4 + j];
+      pcnt[o + j] = sh_n[cl * 4 + j];
+    }
+  }
 }
 
 // 32 columns per CTA x 8 split-lanes per column: lane k folds splits k, k+8,
@@ -617,9 +645,9 @@ int b2_fused_muladd_relu_bwd(float* ga, float* gb, const float* a, const float* 
   if (cols % 4 || !aligned16(a) || !aligned16(b) || !aligned16(ga))
     return b2::fail("b2_fused_muladd_relu_bwd: needs cols%4==0 and 16-B aligned rows");
   cudaStream_t st = b2::resolve(stream);
-  int64_t colblocks = (cols + 4 * kThreads - 1) / (4 * kThreads);
+  int64_t colblocks = (cols + 63) / 64;  // strips of 64 columns
   int64_t splits = std::max<int64_t>(1, (b2::sm_count() * 4) / colblocks);
-  splits = std::min<int64_t>(splits, std::max<int64_t>(rows, 1));
+  splits = std::min<int64_t>(splits, std::max<int64_t>(rows / 64, 1));
   int64_t rps = (rows + splits - 1) / splits;
   if (rps == 0) rps = 1;
   splits = std::max<int64_t>(1, (rows + rps - 1) / rps);

@@ -52,10 +52,15 @@ __device__ __forceinline__ MaxAcc max_combine(const MaxAcc& a, const MaxAcc& b) 
 }
 
 // in-order scan step: NaN never compares greater, so it is skipped
-__device__ __forceinline__ void max_scan(float& best, int64_t& bi, float v, int64_t i) {
+// indices inside a scan are 32-bit (reduced extents < 2^31, checked on the host)
+constexpr int kNone32 = INT32_MAX;
+__device__ __forceinline__ void max_scan(float& best, int& bi, float v, int64_t i) {
   const bool gt = v > best;  // predicated selects, no branch
   best = gt ? v : best;
-  bi = gt ? i : bi;
+  bi = gt ? (int)i : bi;
+}
+__device__ __forceinline__ MaxAcc mk(float b, int i) {
+  return MaxAcc{b, i == kNone32 ? kNone : (int64_t)i};
 }
 
 __device__ __forceinline__ MaxAcc shfl_max(MaxAcc a, int off) {
@@ -163,7 +168,7 @@ __global__ void __launch_bounds__(256) k_rows(const float* __restrict__ x, int64
   } else {
     // each of the 4 lanes of the unroll scans its own index sequence in order
     float b0 = -INFINITY, b1 = -INFINITY, b2 = -INFINITY, b3 = -INFINITY;
-    int64_t i0 = kNone, i1 = kNone, i2 = kNone, i3 = kNone;
+    int i0 = kNone32, i1 = kNone32, i2 = kNone32, i3 = kNone32;
     if (live) {
       if (VEC) {
         int64_t r = r0 + 4 * t;
@@ -197,8 +202,7 @@ __global__ void __launch_bounds__(256) k_rows(const float* __restrict__ x, int64
         for (int64_t r = r0 + t; r < r1; r += GROUP) max_scan(b0, i0, row[r], r);
       }
     }
-    MaxAcc acc = max_combine(max_combine(MaxAcc{b0, i0}, MaxAcc{b1, i1}),
-                             max_combine(MaxAcc{b2, i2}, MaxAcc{b3, i3}));
+    MaxAcc acc = max_combine(max_combine(mk(b0, i0), mk(b1, i1)), max_combine(mk(b2, i2), mk(b3, i3)));
     if (live && s == 0 && t == 0) {
       const float v0 = row[0];
       if (isnan(v0)) acc = MaxAcc{v0, 0};          // first-slot NaN sticks
@@ -300,27 +304,44 @@ __global__ void __launch_bounds__(256) k_strip(const float* __restrict__ x, int6
     }
   } else {
     float b[V];
-    int64_t bi[V];
+    int bi[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       b[j] = -INFINITY;
-      bi[j] = kNone;
+      bi[j] = kNone32;
     }
     if (live) {
-      for (int64_t r = r0 + rl; r < r1; r += RL) {
-        if (V == 4) {
-          const float4 v = *reinterpret_cast<const float4*>(base + r * I);
-          max_scan(b[0], bi[0], v.x, r);
-          max_scan(b[V > 1 ? 1 : 0], bi[V > 1 ? 1 : 0], v.y, r);
-          max_scan(b[V > 2 ? 2 : 0], bi[V > 2 ? 2 : 0], v.z, r);
-          max_scan(b[V > 3 ? 3 : 0], bi[V > 3 ? 3 : 0], v.w, r);
-        } else {
-          max_scan(b[0], bi[0], base[r * I], r);
+      auto scan4 = [&](const float4& v, int64_t r) {
+        max_scan(b[0], bi[0], v.x, r);
+        max_scan(b[V > 1 ? 1 : 0], bi[V > 1 ? 1 : 0], v.y, r);
+        max_scan(b[V > 2 ? 2 : 0], bi[V > 2 ? 2 : 0], v.z, r);
+        max_scan(b[V > 3 ? 3 : 0], bi[V > 3 ? 3 : 0], v.w, r);
+      };
+      int64_t r = r0 + rl;
+      if (V == 4) {
+        constexpr int U = 8;  // 8 x 128-bit loads issued before any compare
+        for (; r + (U - 1) * RL < r1; r += U * RL) {
+          float4 v[U];
+#pragma unroll
+          for (int k = 0; k < U; ++k) v[k] = __ldg(reinterpret_cast<const float4*>(base + (r + k * RL) * I));
+#pragma unroll
+          for (int k = 0; k < U; ++k) scan4(v[k], r + k * RL);
         }
+        for (; r < r1; r += RL) scan4(*reinterpret_cast<const float4*>(base + r * I), r);
+      } else {
+        for (; r + 3 * RL < r1; r += 4 * RL) {
+          const float v0 = base[r * I], v1 = base[(r + RL) * I], v2 = base[(r + 2 * RL) * I],
+                      v3 = base[(r + 3 * RL) * I];
+          max_scan(b[0], bi[0], v0, r);
+          max_scan(b[0], bi[0], v1, r + RL);
+          max_scan(b[0], bi[0], v2, r + 2 * RL);
+          max_scan(b[0], bi[0], v3, r + 3 * RL);
+        }
+        for (; r < r1; r += RL) max_scan(b[0], bi[0], base[r * I], r);
       }
     }
 #pragma unroll
-    for (int j = 0; j < V; ++j) shm[(rl * CL + cl) * V + j] = MaxAcc{b[j], bi[j]};
+    for (int j = 0; j < V; ++j) shm[(rl * CL + cl) * V + j] = mk(b[j], bi[j]);
     __syncthreads();
     for (int h = RL / 2; h > 0; h >>= 1) {
       if (rl < h)
@@ -450,8 +471,8 @@ int run_rows(const float* x, int64_t O, int64_t R, float* out, int64_t* argr, do
   const int rpc = 256 / group;
   const int64_t ctas = (O + rpc - 1) / rpc;
   int64_t S = 1;
-  if (ctas < 2 * sms && R >= 16384) {  // few long rows: split R so ~2 CTAs per SM
-    S = std::min<int64_t>((2 * sms + ctas - 1) / ctas, (R + 16383) / 16384);
+  if (ctas < 2 * sms && R >= 16384) {  // few long rows: split R so ~4 CTAs per SM
+    S = std::min<int64_t>((4 * sms + ctas - 1) / ctas, (R + 8191) / 8192);
     S = std::max<int64_t>(S, 1);
   }
   int64_t Rs = (R + S - 1) / S;
@@ -548,6 +569,8 @@ extern "C" int b2_reduce(int op, float* out, int64_t* argr, int ndim, const int6
       nkept *= shape[d];
   }
   if (nkept == 0) return 0;
+  if (op == B2_RED_MAX && nred >= INT32_MAX)
+    return b2::fail("b2_reduce: max over more than 2^31-1 elements per output");
   if (nred == 0) {
     if (op == B2_RED_MAX) return b2::fail("max over a zero-extent axis is undefined");
     float v = op == B2_RED_MEAN ? NAN : 0.0f;

@@ -59,7 +59,22 @@ struct Block {
   void* ptr;
   size_t size;
   cudaStream_t stream;  // owning stream
+  int graph = 0;        // CUDA graph that references this block (0: none)
 };
+
+// CUDA-graph capture support: while the engine stream is being captured,
+// freed blocks stay private to the capture (reusable by later allocations of
+// the same capture -- the captured stream order keeps that safe) and, once
+// the graph exists, every block it touched is parked until b2_graph_destroy,
+// so replays never race with other users of the memory.
+struct GraphState {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<Block*> parked;
+};
+static int g_capture = 0;  // id of the graph being captured (0: none)
+static int g_next_graph = 1;
+static std::multimap<size_t, Block*> g_cap_free;
+static std::map<int, GraphState> g_graphs;
 
 struct Pending {
   Block* blk;
@@ -225,6 +240,18 @@ int b2_alloc(size_t bytes, void* stream, void** out) {
   size_t sz = round_size(bytes);
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_pending.empty()) drain_pending_locked();
+  if (g_capture) {  // reuse a block this capture already freed
+    auto ci = g_cap_free.lower_bound(sz);
+    if (ci != g_cap_free.end() && ci->first - sz <= (sz < (1u << 20) ? sz : sz / 8 + (2u << 20))) {
+      Block* b = ci->second;
+      g_cap_free.erase(ci);
+      g_live[b->ptr] = b;
+      g_in_use += b->size;
+      if (g_in_use > g_peak) g_peak = g_in_use;
+      *out = b->ptr;
+      return 0;
+    }
+  }
   auto& fl = g_free[st];
   // best fit; small blocks may be up to 2x the request, large ones at most
   // 1/8 (>= 2 MiB) bigger, so steady-state reuse never balloons the footprint
@@ -233,6 +260,7 @@ int b2_alloc(size_t bytes, void* stream, void** out) {
   if (it != fl.end() && it->first - sz <= slack) {
     Block* b = it->second;
     fl.erase(it);
+    if (g_capture) b->graph = g_capture;
     g_live[b->ptr] = b;
     g_in_use += b->size;
     if (g_in_use > g_peak) g_peak = g_in_use;
@@ -254,7 +282,7 @@ int b2_alloc(size_t bytes, void* stream, void** out) {
     }
   }
   ++g_nmalloc;
-  Block* b = new Block{p, sz, st};
+  Block* b = new Block{p, sz, st, g_capture};
   g_live[p] = b;
   g_in_use += sz;
   g_cached += sz;
@@ -271,6 +299,19 @@ int b2_free(void* ptr, void* stream) {
   Block* b = it->second;
   g_live.erase(it);
   g_in_use -= b->size;
+  if (g_capture) {  // freed inside a capture: the graph may still touch it on replay
+    b->graph = g_capture;
+    g_cap_free.emplace(b->size, b);
+    return 0;
+  }
+  if (b->graph) {  // owned by a live graph: park until the graph is destroyed
+    auto gi = g_graphs.find(b->graph);
+    if (gi != g_graphs.end()) {
+      gi->second.parked.push_back(b);
+      return 0;
+    }
+    b->graph = 0;
+  }
   cudaStream_t fs = stream ? (cudaStream_t)stream : b->stream;
   if (fs == b->stream) {
     g_free[b->stream].emplace(b->size, b);
@@ -286,6 +327,79 @@ int b2_free(void* ptr, void* stream) {
       g_pending.push_back({b, ev});
     }
   }
+  return 0;
+}
+
+// ------------------------------------------------------------ CUDA graphs
+
+int b2_graph_begin(void* stream) {
+  B2_TRY(ensure_init());
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_capture) return fail("b2_graph_begin: a capture is already in progress");
+    g_capture = g_next_graph++;
+  }
+  cudaError_t e = cudaStreamBeginCapture(resolve(stream), cudaStreamCaptureModeRelaxed);
+  if (e != cudaSuccess) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_capture = 0;
+    return cuda_fail(e, "cudaStreamBeginCapture");
+  }
+  return 0;
+}
+
+static void end_capture_locked(int id, cudaGraphExec_t exec) {
+  GraphState& gs = g_graphs[id];
+  gs.exec = exec;
+  for (auto& kv : g_cap_free) gs.parked.push_back(kv.second);
+  g_cap_free.clear();
+  g_capture = 0;
+}
+
+int b2_graph_end(void* stream, int* graph_id) {
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(resolve(stream), &graph);
+  std::lock_guard<std::mutex> lk(g_mu);
+  int id = g_capture;
+  if (e != cudaSuccess || !graph) {
+    end_capture_locked(id, nullptr);  // keep the capture's blocks parked under a dead id
+    return cuda_fail(e != cudaSuccess ? e : cudaErrorStreamCaptureInvalidated, "cudaStreamEndCapture");
+  }
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  end_capture_locked(id, e == cudaSuccess ? exec : nullptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  *graph_id = id;
+  return 0;
+}
+
+int b2_graph_launch(int graph_id, void* stream) {
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_graphs.find(graph_id);
+    if (it == g_graphs.end() || !it->second.exec) return fail("b2_graph_launch: unknown graph");
+    exec = it->second.exec;
+  }
+  B2_CUDA(cudaGraphLaunch(exec, resolve(stream)));
+  count_launch();
+  return 0;
+}
+
+int b2_graph_destroy(int graph_id) {
+  B2_CUDA(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_graphs.find(graph_id);
+  if (it == g_graphs.end()) return 0;
+  if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+  for (Block* b : it->second.parked) {
+    b->graph = 0;
+    g_free[b->stream].emplace(b->size, b);
+  }
+  for (auto& kv : g_live)
+    if (kv.second->graph == graph_id) kv.second->graph = 0;
+  g_graphs.erase(it);
   return 0;
 }
 

@@ -16,6 +16,7 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "fexp.cuh"
 
 extern "C" int b2_alloc(size_t, void*, void**);
 extern "C" int b2_free(void*, void*);
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(256) k_xent_rows(double* __restrict__ row_loss
     const float* row = z + r * C;
     double m = (double)row_max(row, C, lane);
     double s = 0, c = 0;
-    for (int64_t j = lane; j < C; j += 32) neu_add(s, c, exp((double)row[j] - m));
+    for (int64_t j = lane; j < C; j += 32) neu_add(s, c, b2::exp_fast((double)row[j] - m));
     // per-lane compensated partials, then a fixed butterfly over 32 lanes
     double tot = warp_sum(s + c);
     if (lane == 0) {
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(256) k_xent_bwd(float* __restrict__ dz, const 
     int64_t r = i / C;
     int64_t j = i - r * C;
     double m = row_stats[2 * r], se = row_stats[2 * r + 1];
-    double p = exp((double)z[i] - m) / se - (j == labels[r] ? 1.0 : 0.0);
+    double p = b2::exp_fast((double)z[i] - m) / se - (j == labels[r] ? 1.0 : 0.0);
     dz[i] = __double2float_rn(p * gv);  // nn.py:500
   }
 }
@@ -139,14 +140,14 @@ __global__ void __launch_bounds__(256) k_softmax_fwd(float* __restrict__ y, floa
     float m = row_max(row, C, lane);
     double acc = 0;
     for (int64_t j = lane; j < C; j += 32) {
-      float e = __double2float_rn(exp((double)__fsub_rn(row[j], m)));  // exp(sub(z, m))
+      float e = b2::exp_f32(__fsub_rn(row[j], m));  // exp(sub(z, m))
       acc += (double)e;
     }
     acc = warp_sum(acc);
     float s = __double2float_rn(acc);  // sum(e, -1, keepdims)
     float* yr = y + r * C;
     for (int64_t j = lane; j < C; j += 32) {
-      float e = __double2float_rn(exp((double)__fsub_rn(row[j], m)));
+      float e = b2::exp_f32(__fsub_rn(row[j], m));
       yr[j] = __fdiv_rn(e, s);  // div(e, s)
     }
     if (lane == 0) {
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(256) k_softmax_bwd(float* __restrict__ gz,
     float ss = __fmul_rn(s, s);
     double acc = 0;
     for (int64_t j = lane; j < C; j += 32) {
-      float e = __double2float_rn(exp((double)__fsub_rn(row[j], m)));
+      float e = b2::exp_f32(__fsub_rn(row[j], m));
       float t = __fdiv_rn(__fmul_rn(grow[j], e), ss);  // div(mul(g, e), mul(s, s))
       acc += (double)(-t);                              // neg, then sum(axis=-1)
     }
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(256) k_softmax_bwd(float* __restrict__ gz,
     float gs = __double2float_rn(acc);
     float* out = gz + r * C;
     for (int64_t j = lane; j < C; j += 32) {
-      float e = __double2float_rn(exp((double)__fsub_rn(row[j], m)));
+      float e = b2::exp_f32(__fsub_rn(row[j], m));
       float ge = __fdiv_rn(grow[j], s);            // div(g, s) -- stored first
       float tot = __fadd_rn(ge, gs);               // GradStore add(cur, g)
       out[j] = __fmul_rn(tot, e);                  // exp pullback mul(g, out)

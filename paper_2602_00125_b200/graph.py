@@ -1,0 +1,65 @@
+"""CUDA-graph capture of engine work (b2_graph_* in include/b2.h).
+
+A small step (BASELINE config 1: ~40 kernels of a few microseconds each) is
+launch-latency bound when driven eagerly from Python; capturing it once and
+replaying the graph issues the whole step as a single launch.
+
+    g = graph.capture(step)   # runs step() once eagerly (warm-up), then captures it
+    g.replay()                 # replays every kernel of step() on the same buffers
+
+The captured function must only launch kernels: no host reads (``item()``,
+``numpy()``) and no host->device uploads inside it. Buffers it allocates stay
+owned by the graph; tensors it returns (``g.outputs``) are rewritten by every
+replay. Cached 3xTF32/TF32X operand splits made before the capture are not
+trusted inside it, so every split the step needs is part of the graph.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib as L
+
+_capturing = [0]  # id of the open capture (unique per capture), 0 when none
+_serial = [0]
+
+
+def capturing() -> bool:
+    return _capturing[0] != 0
+
+
+class CudaGraph:
+    def __init__(self, gid: int, outputs):
+        self.id = gid
+        self.outputs = outputs
+
+    def replay(self, stream=None):
+        L.call("b2_graph_launch", self.id, stream)
+
+    def __del__(self):
+        try:
+            if L._lib is not None and self.id:
+                L._lib.b2_graph_destroy(self.id)
+        except Exception:
+            pass
+        self.id = 0
+
+
+def capture(fn, *args, warmup: int = 1, **kwargs) -> CudaGraph:
+    for _ in range(warmup):
+        fn(*args, **kwargs)
+    L.synchronize()
+    L.call("b2_graph_begin", None)
+    _serial[0] += 1
+    _capturing[0] = _serial[0]
+    try:
+        out = fn(*args, **kwargs)
+    except BaseException:
+        gid = ctypes.c_int(0)
+        L.lib().b2_graph_end(None, ctypes.byref(gid))
+        raise
+    finally:
+        _capturing[0] = 0
+    gid = ctypes.c_int(0)
+    L.check(L.lib().b2_graph_end(None, ctypes.byref(gid)))
+    return CudaGraph(gid.value, out)

@@ -1,0 +1,12 @@
+"""Config-2 exp and dim-0 max on 4096x4096 (for ncu)."""
+import sys
+sys.path.insert(0, '.')
+import numpy as np
+import paper_2602_00125_b200 as P
+from paper_2602_00125_b200 import _lib as L
+a = P.from_numpy(np.random.default_rng(0).standard_normal((4096, 4096), dtype=np.float32))
+with P.no_grad():
+    for _ in range(2):
+        P.exp(a); P.max(a, axis=0)
+L.synchronize()
+print("ok")

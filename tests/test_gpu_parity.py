@@ -486,3 +486,51 @@ def test_smoke_entry_point():
     import __graft_entry__
 
     __graft_entry__.smoke()
+
+
+def test_cuda_graph_replay_matches_eager_config1():
+    from paper_2602_00125_b200 import graph
+    from paper_2602_00125_b200.data import build_mlp
+
+    params, x, labels = I.config1_inputs()
+    xs = dev(x)
+    lab = nn.labels_buffer(labels)
+
+    def make():
+        return build_mlp([(w.copy(), b.copy()) for w, b in params])
+
+    eager = make()
+    opt_e = optim.SGD(lr=0.01)
+    for _ in range(3):
+        P.reset_tape()
+        loss = nn.cross_entropy(eager(xs), lab)
+        optim.step_all(opt_e, eager.parameters(), P.backward(loss))
+
+    model = make()
+    opt_g = optim.SGD(lr=0.01)
+
+    def step():
+        P.reset_tape()
+        loss = nn.cross_entropy(model(xs), lab)
+        optim.step_all(opt_g, model.parameters(), P.backward(loss))
+        return loss
+
+    g = graph.capture(step, warmup=1)   # 1 eager step
+    g.replay()
+    g.replay()                          # + 2 replayed steps
+    for pe, pg in zip(eager.parameters(), model.parameters()):
+        assert bits_equal(host(pe), host(pg))
+    assert np.isfinite(g.outputs.item())
+
+
+def test_exp_matches_double_exp_on_wide_range():
+    rng = np.random.default_rng(12)
+    x = np.concatenate([rng.uniform(-110, 100, 1 << 20), rng.standard_normal(1 << 18) * 3,
+                        np.array([0.0, -0.0, 88.72, 88.73, -87.3, -103.9, -104.0, np.inf,
+                                  -np.inf, np.nan])]).astype(np.float32)
+    got = host(P.exp(dev(x)))
+    want = O.exp(x)
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(got), nan)
+    diff = got[~nan].view(np.int32).astype(np.int64) - want[~nan].view(np.int32).astype(np.int64)
+    assert np.abs(diff).max() <= 1 and np.count_nonzero(diff) <= 2, np.count_nonzero(diff)
