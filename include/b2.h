@@ -160,6 +160,17 @@ int b2_gemm_tf32x(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
                   const float* B, int64_t ldb, const void* B_hi16, const void* B_lo16,
                   float* C, int64_t ldc, const float* bias, int epilogue, void* stream);
 
+/* TF32X GEMM with the fused MLP epilogue stages (nn.py:78-111 chained):
+ * mask (nullable): C *= (mask > 0 ? 1 : 0) elementwise, mask [M,N] with ld = ldc
+ *   -- the ReLU pullback of the layer below, applied to x_bar in the epilogue;
+ * C_hi16/C_lo16 (nullable pair): also write C's TF32X split ([M,N] contiguous)
+ *   so the GEMMs consuming C skip the b2_bf16x2_split pass. */
+int b2_gemm_tf32x_ex(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
+                     const float* A, int64_t lda, const void* A_hi16, const void* A_lo16,
+                     const float* B, int64_t ldb, const void* B_hi16, const void* B_lo16,
+                     float* C, int64_t ldc, const float* bias, int epilogue,
+                     const float* mask, void* C_hi16, void* C_lo16, void* stream);
+
 /* ---------------------------------------------------------------- losses
  * cross_entropy (nn.py:453-503): fwd writes the mean loss (f32 scalar) and
  * per-row stats (max, sum exp) in double; bwd writes

@@ -82,6 +82,10 @@ _SIGS = {
     "b2_gemm_tf32x": (c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p,
                               c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64,
                               c_void_p, c_int, c_void_p]),
+    "b2_gemm_tf32x_ex": (c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_void_p, c_int64,
+                                 c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
+                                 c_void_p, c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+                                 c_void_p]),
     "b2_xent_fwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_double,
                             c_void_p]),
     "b2_xent_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,

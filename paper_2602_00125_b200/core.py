@@ -761,8 +761,13 @@ def set_gemm_algo(name):
                       "1xtf32": L.GEMM_1XTF32, "tf32x": L.GEMM_TF32X}[name]
 
 
-def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE):
-    """out[M,N] = x[M,K] . w[N,K]^T (+bias)(relu); x, w arbitrary 2-D views."""
+def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False):
+    """out[M,N] = x[M,K] . w[N,K]^T (+bias)(relu); x, w arbitrary 2-D views.
+
+    mask (contiguous [M,N]): multiply out by (mask > 0), the ReLU pullback --
+    fused into the TF32X epilogue, else applied by a separate pass.
+    emit_split: let the TF32X epilogue also write out's operand split into
+    out's split cache (the next GEMMs reading out skip the split pass)."""
     M, K = x.shape
     N = w.shape[0]
     ta, lda, xa = _as_A(x)
@@ -777,12 +782,28 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE):
              and lda % 4 == 0 and ldb % 4 == 0 and xa.data_ptr % 16 == 0 and wb.data_ptr % 16 == 0)
     ar, ac = (K, M) if ta else (M, K)
     br, bc = (N, K) if tb else (K, N)
+    mask_done = False
     if algo == L.GEMM_TF32X and tc_ok:
         ahi, alo = _split(xa, ar, ac, lda, "tf32x")
         bhi, blo = _split(wb, br, bc, ldb, "tf32x")
+        mptr = None
+        if mask is not None and mask.is_contiguous and mask.shape == out.shape \
+                and mask.data_ptr % 16 == 0:
+            mptr, mask_done = mask.data_ptr, True
+        shi = slo = None
+        if emit_split and N % 8 == 0 and out.is_contiguous:
+            shi, slo = Buffer(2 * M * N), Buffer(2 * M * N)
         ev = _timer_start()
-        L.call("b2_gemm_tf32x", ta, tb, M, N, K, xa.data_ptr, lda, ahi.ptr, alo.ptr, wb.data_ptr,
-               ldb, bhi.ptr, blo.ptr, out.data_ptr, N, bptr, epi, None)
+        L.call("b2_gemm_tf32x_ex", ta, tb, M, N, K, xa.data_ptr, lda, ahi.ptr, alo.ptr,
+               wb.data_ptr, ldb, bhi.ptr, blo.ptr, out.data_ptr, N, bptr, epi, mptr,
+               shi.ptr if shi else None, slo.ptr if slo else None, None)
+        if shi is not None:
+            from .graph import _capturing
+
+            buf = out.buffer
+            if buf._splits is None:
+                buf._splits = {}
+            buf._splits[("tf32x", out.offset, M, N, N)] = (buf.version, shi, slo, _capturing[0])
     elif algo == L.GEMM_3XTF32 and tc_ok:
         ahi, alo = _split(xa, ar, ac, lda, "3xtf32")
         bhi, blo = _split(wb, br, bc, ldb, "3xtf32")
@@ -799,6 +820,9 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE):
         end = L.Event()
         end.record()
         GEMM_TIMER.append((2.0 * M * N * K, ev, end))
+    if mask is not None and not mask_done:
+        L.call("b2_binary", L.RELU_BWD, out.data_ptr, 2, L.i64s(out.shape), out.data_ptr,
+               L.i64s(out.strides), mask.data_ptr, L.i64s(mask.strides), None)
     return out
 
 
@@ -843,6 +867,10 @@ def mm(a, b) -> Tensor:
     return reshape(y, lead + (b.shape[1],)) if a.ndim > 2 else y
 
 
+_RELU_OUTPUTS = weakref.WeakSet()  # outputs of relu-fused linear layers
+_PREMASKED = weakref.WeakSet()     # cotangents whose ReLU mask is already applied
+
+
 def linear(x, weight, bias=None, relu_out=False) -> Tensor:
     """Fused Dense forward: relu?(x @ W^T + b) in ONE tcgen05 GEMM whose
     epilogue adds the bias and applies the ReLU. Values are bit-identical to
@@ -864,19 +892,38 @@ def linear(x, weight, bias=None, relu_out=False) -> Tensor:
         epi = (L.EPI_BIAS_RELU if relu_out else L.EPI_BIAS) if bias is not None else \
             (L.EPI_RELU if relu_out else L.EPI_NONE)
         bc = bias if (bias is None or bias.is_contiguous) else _copy_contig(bias)
-        _gemm_into(out, x, weight, bc, epi)
+        # a hidden layer's output is the next layer's GEMM operand: let the
+        # epilogue write its TF32X split too (no separate split pass)
+        _gemm_into(out, x, weight, bc, epi, emit_split=relu_out)
     memo = [None, None]
     y = out.detach()  # no output->node->closure->output cycle (see _unary)
+    if relu_out:
+        _RELU_OUTPUTS.add(out)
+    x_is_relu = x in _RELU_OUTPUTS
 
     def pre(g):  # cotangent at the pre-activation (relu pullback, nn.py:101-103)
-        if not relu_out:
+        if not relu_out or g in _PREMASKED:  # the layer above already applied this mask
             return g
         if memo[0] is not g:
             memo[0] = g
             memo[1] = _launch_binary(L.RELU_BWD, g, y, y.shape)
         return memo[1]
 
-    pulls = [lambda g: matmul(pre(g), transpose2d(weight)),
+    def x_bar(g):
+        # matmul(g, W) (core.py:816). When x is the ReLU output of the layer
+        # below, that layer's pullback starts with g * (x > 0): apply it in this
+        # GEMM's epilogue and emit the split its own dX/dW GEMMs read.
+        gp = pre(g)
+        if not x_is_relu:
+            return matmul(gp, transpose2d(weight))
+        xm = x.detach()
+        res = _empty(x.shape)
+        if res.size:
+            _gemm_into(res, gp, transpose2d(weight), mask=xm, emit_split=True)
+        _PREMASKED.add(res)
+        return res
+
+    pulls = [x_bar,
              lambda g: matmul(transpose2d(pre(g)), transpose2d(x))]
     inputs = [x, weight]
     if bias is not None:

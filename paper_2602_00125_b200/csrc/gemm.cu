@@ -14,7 +14,8 @@ int gemm_simt(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, i
 int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const void* a0,
             const void* a1, const void* a2, int64_t lda, const void* b0, const void* b1,
             const void* b2_, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
-            cudaStream_t st);
+            cudaStream_t st, const float* mask = nullptr, void* s_hi = nullptr,
+            void* s_lo = nullptr);
 int tf32_split(float* hi, float* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
                cudaStream_t st);
 int bf16x2_split(void* hi, void* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
@@ -155,6 +156,22 @@ int b2_gemm_tf32x(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* 
     return b2::fail("b2_gemm_tf32x: operands not TMA-compatible");
   return b2::gemm_tc(ta, tb, 2, M, N, K, A, A_hi16, A_lo16, lda, B, B_hi16, B_lo16, ldb, C, ldc,
                      bias, epi, b2::resolve(stream));
+}
+
+// b2_gemm_tf32x with the fused MLP epilogue stages: optional ReLU-pullback
+// mask (C *= mask > 0, mask [M,N] with ld = ldc) and optional emission of C's
+// own TF32X split (bf16 hi/lo, [M,N] contiguous) for the GEMMs that consume C.
+int b2_gemm_tf32x_ex(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                     const void* A_hi16, const void* A_lo16, const float* B, int64_t ldb,
+                     const void* B_hi16, const void* B_lo16, float* C, int64_t ldc,
+                     const float* bias, int epi, const float* mask, void* C_hi16, void* C_lo16,
+                     void* stream) {
+  if (M == 0 || N == 0) return 0;
+  if (!b2::tc_supported(ta, tb, M, N, K, lda, ldb) || ((uintptr_t)A & 15) || ((uintptr_t)B & 15))
+    return b2::fail("b2_gemm_tf32x_ex: operands not TMA-compatible");
+  if (mask && (((uintptr_t)mask & 15) || ldc % 4)) return b2::fail("b2_gemm_tf32x_ex: mask alignment");
+  return b2::gemm_tc(ta, tb, 2, M, N, K, A, A_hi16, A_lo16, lda, B, B_hi16, B_lo16, ldb, C, ldc,
+                     bias, epi, b2::resolve(stream), mask, C_hi16, C_lo16);
 }
 
 }  // extern "C"

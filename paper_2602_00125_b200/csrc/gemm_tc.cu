@@ -207,6 +207,10 @@ struct TcParams {
   int epi;
   int tiles_n, num_tiles;  // tiles of BM*CG x BN
   int tiles_m;
+  // optional fused epilogue stages (MLP backward / forward chaining):
+  const float* mask;        // C = C * (mask > 0 ? 1 : 0), mask [M, N] with ld = ldc (ReLU pullback)
+  __nv_bfloat16* s_hi;      // emit the TF32X split of C: bf16(trunc_tf32(C)) ...
+  __nv_bfloat16* s_lo;      // ... and bf16(C - trunc_tf32(C)), both [M, N] contiguous
 };
 
 // Grouped raster: tiles walk M inside groups of kGroupN tile-columns, so the
@@ -513,7 +517,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (p.epi == B2_EPI_BIAS_RELU || p.epi == B2_EPI_RELU) x = x > 0.0f ? x : 0.0f;
           acc[j] = x;
         }
-        if (vec_ok && nb + 64 <= p.N) {
+        const bool full64 = vec_ok && nb + 64 <= p.N;
+        if (p.mask) {  // ReLU pullback of the layer below: g * (y > 0 ? 1 : 0) (nn.py:101-103)
+          const float* mrow = p.mask + m * p.ldc;
+          if (full64) {
+#pragma unroll
+            for (int j = 0; j < 64; j += 4) {
+              const float4 y = __ldg(reinterpret_cast<const float4*>(mrow + nb + j));
+              acc[j] = __fmul_rn(acc[j], y.x > 0.0f ? 1.0f : 0.0f);
+              acc[j + 1] = __fmul_rn(acc[j + 1], y.y > 0.0f ? 1.0f : 0.0f);
+              acc[j + 2] = __fmul_rn(acc[j + 2], y.z > 0.0f ? 1.0f : 0.0f);
+              acc[j + 3] = __fmul_rn(acc[j + 3], y.w > 0.0f ? 1.0f : 0.0f);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              if (nb + j < p.N) acc[j] = __fmul_rn(acc[j], mrow[nb + j] > 0.0f ? 1.0f : 0.0f);
+          }
+        }
+        if (full64) {
 #pragma unroll
           for (int j = 0; j < 64; j += 4)
             *reinterpret_cast<float4*>(crow + nb + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
@@ -521,6 +543,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 64; ++j)
             if (nb + j < p.N) crow[nb + j] = acc[j];
+        }
+        if (p.s_hi) {  // the next GEMM's TF32X operand split, without a separate pass
+          __nv_bfloat16* hrow = p.s_hi + m * (int64_t)p.N;
+          __nv_bfloat16* lrow = p.s_lo + m * (int64_t)p.N;
+          if (full64 && (p.N % 8) == 0) {
+#pragma unroll
+            for (int j = 0; j < 64; j += 8) {
+              __align__(16) __nv_bfloat16 h[8], l[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float t = __uint_as_float(__float_as_uint(acc[j + i]) & 0xFFFFE000u);
+                h[i] = __float2bfloat16_rn(t);
+                l[i] = __float2bfloat16_rn(__fsub_rn(acc[j + i], t));
+              }
+              *reinterpret_cast<uint4*>(hrow + nb + j) = *reinterpret_cast<const uint4*>(h);
+              *reinterpret_cast<uint4*>(lrow + nb + j) = *reinterpret_cast<const uint4*>(l);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              if (nb + j < p.N) {
+                const float t = __uint_as_float(__float_as_uint(acc[j]) & 0xFFFFE000u);
+                hrow[nb + j] = __float2bfloat16_rn(t);
+                lrow[nb + j] = __float2bfloat16_rn(__fsub_rn(acc[j], t));
+              }
+          }
         }
       }
     }
@@ -751,7 +799,7 @@ static int cg_mode() {
 int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const void* a0,
             const void* a1, const void* a2, int64_t lda, const void* b0, const void* b1,
             const void* b2_, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
-            cudaStream_t st) {
+            cudaStream_t st, const float* mask, void* s_hi, void* s_lo) {
   B2_TRY(get_encode());
   TcParams p;
   p.C = C;
@@ -762,6 +810,10 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   p.K = (int)K;
   p.epi = epi;
   p.tiles_n = p.num_tiles = p.tiles_m = 0;
+  p.mask = mask;
+  p.s_hi = (__nv_bfloat16*)s_hi;
+  p.s_lo = (__nv_bfloat16*)s_lo;
+  if ((s_hi == nullptr) != (s_lo == nullptr)) return fail("gemm_tc: split outputs come in pairs");
   Operands o{{a0, a1, a2}, {b0, b1, b2_}, lda, ldb};
   const bool a_mn = ta != 0, b_mn = tb == 0;
   // CTA pairs once there are enough 256-row tiles to fill the chip
