@@ -86,23 +86,47 @@ class PinnedHost:
 
 
 class PinnedFeeder:
-    """Host batch (pinned) -> device tensor + int64 label buffer, per step."""
+    """Host batch (pinned) -> device tensor + int64 label buffer, every step.
+
+    Double-buffered: while step i computes on slot i%2, the H2D copy of step
+    i+1's batch runs on a dedicated copy stream into the other slot (the
+    copy waits until the compute stream has released that slot; the compute
+    stream waits until its slot's copy has landed). Every step still moves its
+    full batch host -> device; the copy just overlaps the previous step."""
 
     def __init__(self, x, labels):
         self.hx = PinnedHost(x.shape, np.float32)
         self.hx.array[...] = x
         self.hl = PinnedHost(labels.shape, np.int64)
         self.hl.array[...] = labels
-        self.dx = T._empty(x.shape)
-        self.dl = T.Buffer(8 * max(labels.size, 1))
+        self.dx = [T._empty(x.shape) for _ in range(2)]
+        self.dl = [T.Buffer(8 * max(labels.size, 1)) for _ in range(2)]
+        s = ctypes.c_void_p()
+        L.check(L.lib().b2_stream_create(ctypes.byref(s)))
+        self.copy_stream = s.value
+        self.ready = [L.Event(), L.Event()]
+        self.released = [L.Event(), L.Event()]
+        self.i = 0
+        self._issue(0)
 
     @property
     def h2d_bytes(self):
         return self.hx.nbytes + self.hl.nbytes
 
+    def _issue(self, slot):
+        cs = self.copy_stream
+        L.call("b2_memcpy_h2d", self.dx[slot].data_ptr, self.hx.ptr, self.hx.nbytes, cs)
+        L.call("b2_memcpy_h2d", self.dl[slot].ptr, self.hl.ptr, self.hl.nbytes, cs)
+        self.ready[slot].record(cs)
+
     def next(self):
-        """Queue this step's H2D copies on the engine stream; returns (x, labels)."""
-        L.call("b2_memcpy_h2d", self.dx.data_ptr, self.hx.ptr, self.hx.nbytes, None)
-        L.call("b2_memcpy_h2d", self.dl.ptr, self.hl.ptr, self.hl.nbytes, None)
-        self.dx.buffer.version += 1
-        return self.dx, self.dl
+        """Returns this step's (x, labels); queues the next step's copy."""
+        cur, nxt = self.i % 2, (self.i + 1) % 2
+        L.call("b2_stream_wait_event", None, self.ready[cur].h)  # this slot's batch landed
+        # the previous step (already queued) was the last user of `nxt`
+        self.released[nxt].record(None)
+        L.call("b2_stream_wait_event", self.copy_stream, self.released[nxt].h)
+        self._issue(nxt)
+        self.i += 1
+        self.dx[cur].buffer.version += 1  # a new batch: cached operand splits are stale
+        return self.dx[cur], self.dl[cur]

@@ -78,14 +78,25 @@ def nccl_unique_id() -> bytes:
 
 
 class Communicator:
-    """libb2's NCCL communicator for this process's GPU."""
+    """libb2's NCCL communicator for this process's GPU.
 
-    def __init__(self, env: Env, store=None):
+    ``active`` is True when NCCL is in use: always for world > 1, and for a
+    single process when ``force_nccl`` is set (exercises the exact N>1 code
+    path -- uid exchange, comm stream, in-place ncclAvg -- on one GPU)."""
+
+    def __init__(self, env: Env, store=None, force_nccl=False):
         self.env = env
         L.ensure_device(env.local_rank)
         self.comm_stream = None
-        if env.world > 1:
-            store = store or make_store(env)
+        self.active = env.world > 1 or force_nccl
+        if self.active:
+            if store is None:
+                if env.world > 1:
+                    store = make_store(env)
+                else:
+                    from torch.distributed import HashStore
+
+                    store = HashStore()
             self._store = store
             uid = exchange_unique_id(store, env.rank, nccl_unique_id)
             L.check(L.lib().b2_comm_init(env.rank, env.world, uid))
@@ -98,12 +109,12 @@ class Communicator:
         return self.env.world
 
     def allreduce_(self, t, op=AVG, stream=None):
-        if self.env.world > 1 and t.size:
+        if self.active and t.size:
             L.call("b2_allreduce_f32", t.data_ptr, t.size, op, stream)
         return t
 
     def barrier(self):
-        if self.env.world > 1:
+        if self.active:
             from . import core as T
 
             t = T.ones((1,))
@@ -112,7 +123,7 @@ class Communicator:
 
     def max_scalar(self, v: float) -> float:
         """Max of a host float over ranks (device NCCL allreduce)."""
-        if self.env.world == 1:
+        if not self.active:
             return v
         from . import core as T
 
@@ -125,28 +136,30 @@ class GradReducer:
     """Overlapped gradient averaging for one backward pass.
 
     Pass ``hook`` as ``backward(loss, on_leaf_ready=reducer.hook)``; call
-    ``finish()`` before the optimizer step."""
+    ``finish()`` before the optimizer step. Each leaf gradient is averaged
+    in place on the communication stream as soon as backward has queued its
+    last contribution, so the all-reduces of the upper layers overlap the
+    GEMMs of the lower ones. (Leaf gradients of Dense layers are fresh
+    tensors; an aliased leaf gradient would be averaged in place too.)"""
 
-    def __init__(self, comm: Communicator, params):
+    def __init__(self, comm: Communicator, params=None):
         self.comm = comm
-        self._ids = {}
-        self._params = list(params)
         self._pending = []
 
     def hook(self, node_id, grad):
-        if self.comm.world == 1:
+        if not self.comm.active:
             return
         s = self.comm.comm_stream
         ev = L.Event()
         ev.record(None)  # grad produced on the compute stream
         L.call("b2_stream_wait_event", s, ev.h)
         self.comm.allreduce_(grad, AVG, s)
-        self._pending.append(ev)
+        self._pending.append((ev, grad))
 
     def finish(self):
-        if self.comm.world == 1:
+        if not self.comm.active:
             return
         done = L.Event()
         done.record(self.comm.comm_stream)
-        L.call("b2_stream_wait_event", None, done.h)  # optimizer waits for the reduces
+        L.call("b2_stream_wait_event", None, done.h)  # the optimizer waits for the reduces
         self._pending.clear()

@@ -534,3 +534,35 @@ def test_exp_matches_double_exp_on_wide_range():
     assert np.array_equal(np.isnan(got), nan)
     diff = got[~nan].view(np.int32).astype(np.int64) - want[~nan].view(np.int32).astype(np.int64)
     assert np.abs(diff).max() <= 1 and np.count_nonzero(diff) <= 2, np.count_nonzero(diff)
+
+
+def test_nccl_gradient_path_single_rank_matches_plain_step():
+    """The N>1 data-parallel code path (NCCL uid exchange, comm stream,
+    overlapped in-place ncclAvg, optimizer waiting on the comm stream) with a
+    1-rank communicator: averaging over one rank is the identity, so the
+    parameters must match a plain step bit for bit."""
+    from paper_2602_00125_b200 import dist
+    from paper_2602_00125_b200.data import build_mlp, mlp_config5
+
+    params = mlp_config5(0, width=256, classes=10, depth=2)
+    x = dev(np.random.default_rng(1).standard_normal((512, 256)))
+    lab = nn.labels_buffer(np.arange(512) % 10)
+    comm = dist.Communicator(dist.Env(), force_nccl=True)
+    assert comm.active
+
+    def run(use_comm):
+        model = build_mlp([(w.copy(), b.copy()) for w, b in params])
+        opt = optim.Adam(lr=1e-3)
+        for _ in range(2):
+            P.reset_tape()
+            loss = nn.cross_entropy(model(x), lab, denom=512)
+            red = dist.GradReducer(comm if use_comm else dist.Communicator(dist.Env()))
+            store = P.backward(loss, on_leaf_ready=red.hook)
+            red.finish()
+            optim.step_all(opt, model.parameters(), store)
+        return [host(p) for p in model.parameters()]
+
+    for a, b in zip(run(True), run(False)):
+        assert bits_equal(a, b)
+    assert comm.max_scalar(3.5) == 3.5
+    comm.barrier()
