@@ -330,6 +330,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-ops", action="store_true", help="skip the config 2-4 op benchmarks")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--no-bf16", action="store_true", help="skip the bf16-variant measurement")
+    ap.add_argument("--gemm", default="auto", choices=["auto", "tf32x", "3xbf16", "3xtf32"],
+                    help="fp32-accurate GEMM algorithm for the headline run")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -355,6 +358,27 @@ def main():
     del x_np
 
     gemm_log = []
+    if args.gemm != "auto":
+        P.set_gemm_algo(args.gemm)
+    g_algo = C.get_gemm_algo()
+    if g_algo is None:
+        import ctypes
+
+        sel = ctypes.c_int()
+        L.check(L.lib().b2_gemm_select(0, 1, rows, WIDTH, WIDTH, WIDTH, WIDTH, ctypes.byref(sel)))
+        g_algo = sel.value
+    ALGO_INFO = {
+        L.GEMM_TF32X: ("k_gemm_tc<TF32X> (tcgen05 kind::tf32 hi*hi + 2x kind::f16 bf16 cross terms)",
+                       4.0, "TF32X = 1 tf32 MMA (half the bf16 rate) + 2 bf16 MMAs per fp32 MAC: "
+                            "ceiling = bf16/4",
+                       "TF32X tcgen05 (tf32 main + bf16 cross terms, fp32 accuracy ~2e-6)"),
+        L.GEMM_3XBF16: ("k_gemm_tc<3xBF16> (tcgen05 kind::f16: hi*hi + hi*lo + lo*hi)", 3.0,
+                        "3xBF16 = 3 bf16 MMAs per fp32 MAC: ceiling = bf16/3",
+                        "3xBF16 tcgen05 (bf16 hi/lo split, 3 MMAs, fp32 accuracy ~4e-6)"),
+        L.GEMM_3XTF32: ("k_gemm_tc<3xTF32>", 6.0, "3xTF32 = 3 tf32 MMAs per MAC: ceiling = bf16/6",
+                        "3xTF32 tcgen05 (fp32 accuracy ~1e-6)"),
+    }
+    a_kernel, a_div, a_note, a_desc = ALGO_INFO[g_algo]
 
     def step(x, labels, read_loss=False):
         P.reset_tape()
@@ -419,14 +443,48 @@ def main():
     roof = {
         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
         "frac": achieved / peak, "traffic": traffic,
-        "kernel": "k_gemm_tc<TF32X> (tcgen05 kind::tf32 hi*hi + 2x kind::f16 bf16 cross terms)",
+        "kernel": a_kernel,
         "algorithmic_flops_per_step": g_flops, "gemm_launches_per_step": n_gemm,
         "gemm_ms_per_step": g_ms, "gemm_share_of_step": g_ms / ms,
         "peak_source": f"{src} bf16 dense sustained (MEASURED_PEAKS.json)",
-        "frac_of_tf32x_ceiling": achieved / (peak / 4.0),
-        "note": "TF32X = 1 tf32 MMA (half the bf16 rate) + 2 bf16 MMAs per fp32 MAC: "
-                "ceiling = bf16/4 (3xTF32 would be bf16/6)",
+        "frac_of_algo_ceiling": achieved / (peak / a_div),
+        "note": a_note,
     }
+
+    # BASELINE's bf16 variant of config 5: bf16 GEMM operands (one kind::f16
+    # MMA per MAC), fp32 accumulation, fp32 master weights / Adam / loss
+    bf16 = None
+    if not args.no_bf16:
+        P.set_gemm_algo("bf16")
+        try:
+            for _ in range(max(args.warmup, 0)):
+                step(x_dev, y_dev)
+            comm.barrier()
+            b0, b1 = L.Event(), L.Event()
+            b0.record()
+            for _ in range(args.steps):
+                lb = step(x_dev, y_dev)
+            b1.record()
+            L.synchronize()
+            comm.barrier()
+            ms_b = comm.max_scalar(b0.elapsed_ms(b1) / args.steps)
+            blog = []
+            C.GEMM_TIMER = blog
+            step(x_dev, y_dev)
+            L.synchronize()
+            C.GEMM_TIMER = None
+        finally:
+            P.set_gemm_algo(None if args.gemm == "auto" else args.gemm)
+        bf_flops = sum(f for f, _, _ in blog)
+        bf_ms = sum(s.elapsed_ms(e) for _, s, e in blog)
+        bf_ach = bf_flops / (bf_ms / 1000.0) / 1e12
+        bf16 = {"value": GLOBAL_BATCH / (ms_b / 1000.0), "unit": "samples/s", "ms_per_step": ms_b,
+                "dtype": "bf16 GEMM operands, fp32 accumulate/master weights/Adam",
+                "final_loss": lb.item(),
+                "roofline": {"bound": "tensor", "achieved": bf_ach, "peak": peak,
+                             "unit": "TFLOP/s", "frac": bf_ach / peak,
+                             "kernel": "k_gemm_tc<BF16> (tcgen05 kind::f16, cta_group::2)",
+                             "gemm_ms_per_step": bf_ms, "gemm_share_of_step": bf_ms / ms_b}}
 
     ops = None
     cpu = None
@@ -449,7 +507,7 @@ def main():
                        "global_batch": GLOBAL_BATCH, "per_gpu_batch": rows,
                        "layers": "4xLinear(4096,4096)+ReLU, Linear(4096,1000)",
                        "optimizer": "Adam lr=1e-3 betas=(0.9,0.999) eps=1e-8",
-                       "gemm": "TF32X tcgen05 (tf32 main + bf16 cross terms, fp32 accuracy ~2e-6)",
+                       "gemm": a_desc,
                        "parallelism": f"dp{world}", "l2": "inputs > L2 (1 GiB/rank at N=1)"},
             "e2e": {"value": GLOBAL_BATCH / (ms_e2e / 1000.0), "unit": "samples/s",
                     "h2d_bytes_per_step": feeder.h2d_bytes, "d2h_bytes_per_step": 4},
@@ -461,6 +519,7 @@ def main():
             "launches_per_step": launches / args.steps,
             "tflops_per_gpu": flops_per_step(rows) / (ms / 1000.0) / 1e12,
             "final_loss": loss_val,
+            "bf16_variant": bf16,
             "ops": ops,
         }
         print(json.dumps(line), flush=True)

@@ -128,10 +128,14 @@ int b2_max_scatter(float* gx, int ndim, const int64_t* shape, uint32_t reduce_ma
  * algo: 0 auto, 1 FP32 SIMT (FFMA), 2 3xTF32 on tcgen05 (fp32 accuracy),
  *       3 1xTF32 on tcgen05 (fast, ~1e-3 rel; never chosen by auto),
  *       4 TF32X: tf32 main product + the two cross terms as bf16 MMAs
- *         (2 tf32-equivalent MMAs per fp32 MAC, fp32-grade accuracy).
+ *         (2 tf32-equivalent MMAs per fp32 MAC, fp32-grade accuracy),
+ *       5 3xBF16: hi = bf16_rn(x), lo = bf16_rn(x - hi); hi*hi + hi*lo + lo*hi
+ *         as bf16 MMAs (1.5 tf32-equivalents per MAC, half TF32X's operand
+ *         bytes, normwise error ~4e-6: inside the 1e-4 fp32 contract).
  */
 enum b2_gemm_algo { B2_GEMM_AUTO = 0, B2_GEMM_SIMT = 1, B2_GEMM_3XTF32 = 2,
-                    B2_GEMM_1XTF32 = 3, B2_GEMM_TF32X = 4 /* tf32 hi*hi + bf16 hi*lo + lo*hi */ };
+                    B2_GEMM_1XTF32 = 3, B2_GEMM_TF32X = 4 /* tf32 hi*hi + bf16 hi*lo + lo*hi */,
+                    B2_GEMM_3XBF16 = 5 };
 enum b2_epilogue { B2_EPI_NONE = 0, B2_EPI_BIAS = 1, B2_EPI_BIAS_RELU = 2, B2_EPI_RELU = 3 };
 int b2_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
             const float* A, int64_t lda, const float* B, int64_t ldb,
@@ -170,6 +174,26 @@ int b2_gemm_tf32x_ex(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
                      const float* B, int64_t ldb, const void* B_hi16, const void* B_lo16,
                      float* C, int64_t ldc, const float* bias, int epilogue,
                      const float* mask, void* C_hi16, void* C_lo16, void* stream);
+
+/* 3xBF16 split (hi = bf16_rn(x), lo = bf16_rn(x - hi), contiguous; cols % 8 == 0)
+ * and the GEMM on such splits, with the same fused epilogue as
+ * b2_gemm_tf32x_ex (C_hi16/C_lo16 receive C's own 3xBF16 split). */
+int b2_bf16x3_split(void* hi16, void* lo16, const float* x, int64_t rows, int64_t cols,
+                    int64_t ld, void* stream);
+int b2_gemm_3xbf16(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
+                   const void* A_hi16, const void* A_lo16, const void* B_hi16,
+                   const void* B_lo16, float* C, int64_t ldc, const float* bias, int epilogue,
+                   const float* mask, void* C_hi16, void* C_lo16, void* stream);
+
+/* BF16 variant (explicitly requested precision only; bf16 tolerance 2e-2):
+ * contiguous round-to-nearest bf16 cast of a [rows, cols] (ld) matrix, and a
+ * GEMM on such casts (one kind::f16 MMA per MAC, fp32 accumulation) with the
+ * same fused epilogue; C16 (nullable) receives C's own bf16 cast. */
+int b2_bf16_cast(void* out16, const float* x, int64_t rows, int64_t cols, int64_t ld,
+                 void* stream);
+int b2_gemm_bf16(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const void* A16,
+                 const void* B16, float* C, int64_t ldc, const float* bias, int epilogue,
+                 const float* mask, void* C16, void* stream);
 
 /* ---------------------------------------------------------------- losses
  * cross_entropy (nn.py:453-503): fwd writes the mean loss (f32 scalar) and

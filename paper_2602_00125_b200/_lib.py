@@ -86,6 +86,13 @@ _SIGS = {
                                  c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
                                  c_void_p, c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
                                  c_void_p]),
+    "b2_bf16x3_split": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
+    "b2_gemm_3xbf16": (c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                               c_void_p, c_void_p, c_int64, c_void_p, c_int, c_void_p, c_void_p,
+                               c_void_p, c_void_p]),
+    "b2_bf16_cast": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
+    "b2_gemm_bf16": (c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                             c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "b2_xent_fwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_double,
                             c_void_p]),
     "b2_xent_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
@@ -106,7 +113,8 @@ _SIGS = {
 ADD, SUB, MUL, DIV, RELU_BWD, SIGN_MUL = range(6)
 NEG, EXP, LOG, SQRT, ABS, RELU, RELU_MASK, COPY, CLAMP, SCALE, DIV_SCALAR, CLAMP_MASK = range(12)
 RED_SUM, RED_MEAN, RED_MAX = range(3)
-GEMM_AUTO, GEMM_SIMT, GEMM_3XTF32, GEMM_1XTF32, GEMM_TF32X = range(5)
+GEMM_AUTO, GEMM_SIMT, GEMM_3XTF32, GEMM_1XTF32, GEMM_TF32X, GEMM_3XBF16 = range(6)
+GEMM_BF16 = 6  # host-side selector for b2_gemm_bf16 (bf16 variant; never auto-selected)
 EPI_NONE, EPI_BIAS, EPI_BIAS_RELU, EPI_RELU = range(4)
 
 _lib = None

@@ -729,7 +729,9 @@ def _as_B(t):
 def _split(t, rows, cols, ld, kind):
     """Cached split of the stored matrix region of t for a tensor-core GEMM:
     kind "tf32x" -> (bf16 hi, bf16 lo) of trunc_tf32(x) / x - trunc (2 B each),
-    kind "3xtf32" -> (fp32 hi, fp32 lo). Invalidated by the buffer version."""
+    kind "3xbf16" -> (bf16 hi, bf16 lo) of bf16_rn(x) / bf16_rn(x - hi),
+    kind "3xtf32" -> (fp32 hi, fp32 lo), kind "bf16" -> (bf16 cast, None).
+    Invalidated by the buffer version."""
     from .graph import _capturing
 
     buf = t.buffer
@@ -742,9 +744,14 @@ def _split(t, rows, cols, ld, kind):
     if ent is not None and ent[0] == buf.version and (not cap or ent[3] == cap):
         return ent[1], ent[2]
     n = rows * cols
-    esz = 2 if kind == "tf32x" else 4
+    if kind == "bf16":  # bf16 variant: one RN cast, no low part
+        hi, lo = Buffer(2 * n), None
+        L.call("b2_bf16_cast", hi.ptr, t.data_ptr, rows, cols, ld, None)
+        buf._splits[key] = (buf.version, hi, lo, cap)
+        return hi, lo
+    esz = 4 if kind == "3xtf32" else 2
     hi, lo = Buffer(esz * n), Buffer(esz * n)
-    fn = "b2_bf16x2_split" if kind == "tf32x" else "b2_tf32_split"
+    fn = {"tf32x": "b2_bf16x2_split", "3xbf16": "b2_bf16x3_split", "3xtf32": "b2_tf32_split"}[kind]
     L.call(fn, hi.ptr, lo.ptr, t.data_ptr, rows, cols, ld, None)
     buf._splits[key] = (buf.version, hi, lo, cap)
     return hi, lo
@@ -755,10 +762,18 @@ GEMM_TIMER = None  # bench/profiling: a list receiving (flops, start_event, end_
 
 
 def set_gemm_algo(name):
-    """Force 'simt' | '3xtf32' | '1xtf32' | None (auto) for subsequent matmuls."""
+    """Force 'simt' | '3xtf32' | '1xtf32' | 'tf32x' | 'bf16' | None (auto) for
+    subsequent matmuls. 'bf16' is the reduced-precision variant (bf16 operands,
+    fp32 accumulation, fp32 master values everywhere else) and is only ever
+    used when asked for."""
     global _ALGO_OVERRIDE
     _ALGO_OVERRIDE = {None: None, "auto": None, "simt": L.GEMM_SIMT, "3xtf32": L.GEMM_3XTF32,
-                      "1xtf32": L.GEMM_1XTF32, "tf32x": L.GEMM_TF32X}[name]
+                      "1xtf32": L.GEMM_1XTF32, "tf32x": L.GEMM_TF32X, "3xbf16": L.GEMM_3XBF16,
+                      "bf16": L.GEMM_BF16}[name]
+
+
+def get_gemm_algo():
+    return _ALGO_OVERRIDE
 
 
 def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False):
@@ -804,6 +819,47 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
             if buf._splits is None:
                 buf._splits = {}
             buf._splits[("tf32x", out.offset, M, N, N)] = (buf.version, shi, slo, _capturing[0])
+    elif algo == L.GEMM_3XBF16 and tc_ok:
+        ahi, alo = _split(xa, ar, ac, lda, "3xbf16")
+        bhi, blo = _split(wb, br, bc, ldb, "3xbf16")
+        mptr = None
+        if mask is not None and mask.is_contiguous and mask.shape == out.shape \
+                and mask.data_ptr % 16 == 0:
+            mptr, mask_done = mask.data_ptr, True
+        shi = slo = None
+        if emit_split and N % 8 == 0 and out.is_contiguous:
+            shi, slo = Buffer(2 * M * N), Buffer(2 * M * N)
+        ev = _timer_start()
+        L.call("b2_gemm_3xbf16", ta, tb, M, N, K, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr,
+               out.data_ptr, N, bptr, epi, mptr, shi.ptr if shi else None,
+               slo.ptr if slo else None, None)
+        if shi is not None:
+            from .graph import _capturing
+
+            buf = out.buffer
+            if buf._splits is None:
+                buf._splits = {}
+            buf._splits[("3xbf16", out.offset, M, N, N)] = (buf.version, shi, slo, _capturing[0])
+    elif algo == L.GEMM_BF16 and tc_ok:
+        a16, _ = _split(xa, ar, ac, lda, "bf16")
+        b16, _ = _split(wb, br, bc, ldb, "bf16")
+        mptr = None
+        if mask is not None and mask.is_contiguous and mask.shape == out.shape \
+                and mask.data_ptr % 16 == 0:
+            mptr, mask_done = mask.data_ptr, True
+        c16 = None
+        if emit_split and N % 8 == 0 and out.is_contiguous:
+            c16 = Buffer(2 * M * N)
+        ev = _timer_start()
+        L.call("b2_gemm_bf16", ta, tb, M, N, K, a16.ptr, b16.ptr, out.data_ptr, N, bptr, epi,
+               mptr, c16.ptr if c16 else None, None)
+        if c16 is not None:
+            from .graph import _capturing
+
+            buf = out.buffer
+            if buf._splits is None:
+                buf._splits = {}
+            buf._splits[("bf16", out.offset, M, N, N)] = (buf.version, c16, None, _capturing[0])
     elif algo == L.GEMM_3XTF32 and tc_ok:
         ahi, alo = _split(xa, ar, ac, lda, "3xtf32")
         bhi, blo = _split(wb, br, bc, ldb, "3xtf32")
@@ -811,7 +867,7 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
         L.call("b2_gemm_presplit", ta, tb, M, N, K, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr,
                out.data_ptr, N, bptr, epi, None)
     else:
-        if algo in (L.GEMM_3XTF32, L.GEMM_TF32X):
+        if algo in (L.GEMM_3XTF32, L.GEMM_TF32X, L.GEMM_3XBF16, L.GEMM_BF16):
             algo = L.GEMM_SIMT
         ev = _timer_start()
         L.call("b2_gemm", ta, tb, M, N, K, xa.data_ptr, lda, wb.data_ptr, ldb, out.data_ptr, N,

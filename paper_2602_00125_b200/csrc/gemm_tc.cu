@@ -41,7 +41,7 @@ namespace {
 
 constexpr int BM = 128, BN = 256, BK = 32;  // BK fp32 = 128 bytes = one swizzle row
 constexpr int kThreads = 640;  // 4 control warps + 16 epilogue warps
-constexpr int KC = 8;          // k-blocks per accumulation chunk (K = 256)
+constexpr int KC_BASE = 8;     // k-blocks per accumulation chunk (K = 256)
 constexpr int kTmemCols = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -233,6 +233,11 @@ __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& tm, i
 //         to tf32: hi = trunc(x), probed on B200) and the two cross terms
 //         hi*lo + lo*hi run as kind::f16 MMAs on bf16(hi), bf16(lo) at twice the
 //         tf32 rate -- 2 tf32-equivalents per fp32 MAC instead of 3.
+// MODE 4: BF16 (explicit bf16 variant) tiles Ah16 | Bh16, one kind::f16 MMA per MAC.
+// MODE 5: 3xBF16            tiles Ah16 | Al16 | Bh16 | Bl16 with hi = bf16_rn(x),
+//         lo = bf16_rn(x - hi) (16 significant bits): hi*hi + hi*lo + lo*hi, all
+//         kind::f16 -- 3 bf16 MMAs per fp32 MAC (1.5 tf32-equivalents) on half
+//         MODE 2's operand bytes; normwise error ~4e-6 against the 1e-4 contract.
 // CG 1: one CTA computes a 128x256 tile. CG 2: a CTA pair (cluster of 2)
 //         computes 256x256 with tcgen05 cta_group::2: each CTA holds its 128
 //         rows of A and HALF (128 rows) of B, the leader issues M=256 MMAs that
@@ -244,19 +249,24 @@ struct Cfg {
   static constexpr int B32 = BNL * BK * 4;
   static constexpr int A16 = BM * BK * 2;
   static constexpr int B16 = BNL * BK * 2;
-  static constexpr int STAGE_BYTES = MODE == 1 ? A32 + B32 : (MODE == 3 ? 2 * (A32 + B32)
-                                                                       : A32 + B32 + 2 * (A16 + B16));
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGE_BYTES =
+      MODE == 1 ? A32 + B32
+      : MODE == 3 ? 2 * (A32 + B32)
+      : MODE == 4 ? A16 + B16
+      : MODE == 5 ? 2 * (A16 + B16)
+                  : A32 + B32 + 2 * (A16 + B16);
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   // byte offsets inside a stage
   static constexpr int OFF_A = 0;
   static constexpr int OFF_ALO = A32;                                 // MODE 3
   static constexpr int OFF_B = MODE == 3 ? 2 * A32 : A32;
   static constexpr int OFF_BLO = 2 * A32 + B32;                       // MODE 3
-  static constexpr int OFF_AH16 = A32 + B32;                          // MODE 2
-  static constexpr int OFF_AL16 = A32 + B32 + A16;
-  static constexpr int OFF_BH16 = A32 + B32 + 2 * A16;
-  static constexpr int OFF_BL16 = A32 + B32 + 2 * A16 + B16;
+  static constexpr int F32 = (MODE == 4 || MODE == 5) ? 0 : A32 + B32;  // fp32 part (MODE 2)
+  static constexpr int OFF_AH16 = F32;                                // MODE 2 / 4 / 5
+  static constexpr int OFF_AL16 = F32 + A16;                          // MODE 2 / 5
+  static constexpr int OFF_BH16 = MODE == 4 ? A16 : F32 + 2 * A16;
+  static constexpr int OFF_BL16 = F32 + 2 * A16 + B16;
 };
 
 // Loads a tile into this CTA's smem, counting bytes on `bar` (a local
@@ -308,6 +318,21 @@ __device__ __forceinline__ uint64_t desc16(uint32_t base, bool mn, int ks) {
   return mn ? umma_desc(base + ks * 2048, 4096, 1024, 2) : umma_desc(base + ks * 32, 16, 512, 4);
 }
 
+// operand split written by the epilogue for the next GEMM: TF32X (MODE 2)
+// = bf16(trunc_tf32(x)), bf16(x - trunc_tf32(x)); 3xBF16 (MODE 5) = hi =
+// bf16_rn(x), lo = bf16_rn(x - hi). Same arithmetic as the split kernels.
+template <int MODE>
+__device__ __forceinline__ void split_pair(float x, __nv_bfloat16& h, __nv_bfloat16& l) {
+  if (MODE == 5) {
+    h = __float2bfloat16_rn(x);
+    l = __float2bfloat16_rn(__fsub_rn(x, __bfloat162float(h)));
+  } else {
+    const float t = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    h = __float2bfloat16_rn(t);
+    l = __float2bfloat16_rn(__fsub_rn(x, t));
+  }
+}
+
 template <bool A_MN, bool B_MN, int MODE, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -316,6 +341,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               const TcParams p) {
   using CF = Cfg<MODE, CG>;
   constexpr int STAGES = CF::STAGES;
+  // bf16 operands carry 2^-9 relative error: promote every K = 1024 instead
+  constexpr int KC = MODE == 4 ? 4 * KC_BASE : KC_BASE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + STAGES * CF::STAGE_BYTES);
@@ -381,8 +408,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t fb_cl = CG == 2 ? mapa(smem_u32(fb), 0) : 0;
           if (leader) mbar_expect_tx(fb, CF::STAGE_BYTES * CG);
           const int k0 = kb * BK;
-          load32<A_MN, BM, CG>(st + CF::OFF_A, &tmA, fb, fb_cl, m0, k0);
-          load32<B_MN, CF::BNL, CG>(st + CF::OFF_B, &tmB, fb, fb_cl, n0, k0);
+          if (MODE == 4 || MODE == 5) {  // bf16 operands only
+            load16<A_MN, BM, CG>(st + CF::OFF_AH16, &tmA, fb, fb_cl, m0, k0);
+            load16<B_MN, CF::BNL, CG>(st + CF::OFF_BH16, &tmB, fb, fb_cl, n0, k0);
+            if (MODE == 5) {
+              load16<A_MN, BM, CG>(st + CF::OFF_AL16, &tmA2, fb, fb_cl, m0, k0);
+              load16<B_MN, CF::BNL, CG>(st + CF::OFF_BL16, &tmB2, fb, fb_cl, n0, k0);
+            }
+          } else {
+            load32<A_MN, BM, CG>(st + CF::OFF_A, &tmA, fb, fb_cl, m0, k0);
+            load32<B_MN, CF::BNL, CG>(st + CF::OFF_B, &tmB, fb, fb_cl, n0, k0);
+          }
           if (MODE == 3) {
             load32<A_MN, BM, CG>(st + CF::OFF_ALO, &tmA2, fb, fb_cl, m0, k0);
             load32<B_MN, CF::BNL, CG>(st + CF::OFF_BLO, &tmB2, fb, fb_cl, n0, k0);
@@ -424,8 +460,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           if (lane == 0) {
             const uint32_t s0 = smem_u32(smem + stage * CF::STAGE_BYTES);
+            if (MODE == 4) {
 #pragma unroll
-            for (int ks = 0; ks < BK / 8; ++ks) {
+              for (int ks = 0; ks < BK / 16; ++ks)
+                tc_mma<CG>(d_tmem, desc16(s0 + CF::OFF_AH16, A_MN, ks),
+                           desc16(s0 + CF::OFF_BH16, B_MN, ks), id16, (kc | ks) ? 1u : 0u, true);
+            }
+            if (MODE == 5) {
+#pragma unroll
+              for (int ks = 0; ks < BK / 16; ++ks) {
+                const uint64_t ah = desc16(s0 + CF::OFF_AH16, A_MN, ks);
+                const uint64_t bh = desc16(s0 + CF::OFF_BH16, B_MN, ks);
+                tc_mma<CG>(d_tmem, ah, bh, id16, (kc | ks) ? 1u : 0u, true);
+                tc_mma<CG>(d_tmem, ah, desc16(s0 + CF::OFF_BL16, B_MN, ks), id16, 1u, true);
+                tc_mma<CG>(d_tmem, desc16(s0 + CF::OFF_AL16, A_MN, ks), bh, id16, 1u, true);
+              }
+            }
+#pragma unroll
+            for (int ks = 0; ks < ((MODE == 4 || MODE == 5) ? 0 : BK / 8); ++ks) {
               const uint64_t a = desc32(s0 + CF::OFF_A, A_MN, ks);
               const uint64_t b = desc32(s0 + CF::OFF_B, B_MN, ks);
               tc_mma<CG>(d_tmem, a, b, id32, (kc | ks) ? 1u : 0u, false);
@@ -544,7 +596,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 64; ++j)
             if (nb + j < p.N) crow[nb + j] = acc[j];
         }
-        if (p.s_hi) {  // the next GEMM's TF32X operand split, without a separate pass
+        if (MODE == 4 && p.s_hi) {  // BF16 mode: the next GEMM's bf16 operand (RN cast)
+          __nv_bfloat16* hrow = p.s_hi + m * (int64_t)p.N;
+          if (full64 && (p.N % 8) == 0) {
+#pragma unroll
+            for (int j = 0; j < 64; j += 8) {
+              __align__(16) __nv_bfloat16 h[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) h[i] = __float2bfloat16_rn(acc[j + i]);
+              *reinterpret_cast<uint4*>(hrow + nb + j) = *reinterpret_cast<const uint4*>(h);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              if (nb + j < p.N) hrow[nb + j] = __float2bfloat16_rn(acc[j]);
+          }
+        } else if (p.s_hi) {  // the next GEMM's operand split (TF32X / 3xBF16), no separate pass
           __nv_bfloat16* hrow = p.s_hi + m * (int64_t)p.N;
           __nv_bfloat16* lrow = p.s_lo + m * (int64_t)p.N;
           if (full64 && (p.N % 8) == 0) {
@@ -552,22 +619,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 64; j += 8) {
               __align__(16) __nv_bfloat16 h[8], l[8];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const float t = __uint_as_float(__float_as_uint(acc[j + i]) & 0xFFFFE000u);
-                h[i] = __float2bfloat16_rn(t);
-                l[i] = __float2bfloat16_rn(__fsub_rn(acc[j + i], t));
-              }
+              for (int i = 0; i < 8; ++i) split_pair<MODE>(acc[j + i], h[i], l[i]);
               *reinterpret_cast<uint4*>(hrow + nb + j) = *reinterpret_cast<const uint4*>(h);
               *reinterpret_cast<uint4*>(lrow + nb + j) = *reinterpret_cast<const uint4*>(l);
             }
           } else {
 #pragma unroll
             for (int j = 0; j < 64; ++j)
-              if (nb + j < p.N) {
-                const float t = __uint_as_float(__float_as_uint(acc[j]) & 0xFFFFE000u);
-                hrow[nb + j] = __float2bfloat16_rn(t);
-                lrow[nb + j] = __float2bfloat16_rn(__fsub_rn(acc[j], t));
-              }
+              if (nb + j < p.N) split_pair<MODE>(acc[j], hrow[nb + j], lrow[nb + j]);
           }
         }
       }
@@ -621,14 +680,9 @@ __global__ void k_tf32_split_vec(float* __restrict__ hi, float* __restrict__ lo,
   }
 }
 
-// TF32 + 2xBF16: t = trunc_tf32(x) (what the tensor core uses), hi16 = bf16(t),
-// lo16 = bf16(x - t). 8 elements per thread-iteration (32 B in, 2 x 16 B out).
-__device__ __forceinline__ void bf16x2_pair(float v, __nv_bfloat16& h, __nv_bfloat16& l) {
-  const float t = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-  h = __float2bfloat16_rn(t);
-  l = __float2bfloat16_rn(__fsub_rn(v, t));
-}
-
+// Operand split (split_pair<MODE>): TF32X (MODE 2) or 3xBF16 (MODE 5).
+// 8 elements per thread-iteration (32 B in, 2 x 16 B out).
+template <int MODE>
 __global__ void k_bf16x2_split(__nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
                                const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ld) {
   const int64_t c8 = cols >> 3;  // cols % 8 == 0 (checked on the host)
@@ -647,9 +701,33 @@ __global__ void k_bf16x2_split(__nv_bfloat16* __restrict__ hi, __nv_bfloat16* __
     }
     __align__(16) __nv_bfloat16 h[8], l[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) bf16x2_pair(v[j], h[j], l[j]);
+    for (int j = 0; j < 8; ++j) split_pair<MODE>(v[j], h[j], l[j]);
     *reinterpret_cast<uint4*>(hi + r * cols + c) = *reinterpret_cast<const uint4*>(h);
     *reinterpret_cast<uint4*>(lo + r * cols + c) = *reinterpret_cast<const uint4*>(l);
+  }
+}
+
+// BF16 mode operand: contiguous bf16 round-to-nearest copy of a [rows, cols] (ld) matrix
+__global__ void k_bf16_cast(__nv_bfloat16* __restrict__ out, const float* __restrict__ x,
+                            int64_t rows, int64_t cols, int64_t ld) {
+  const int64_t c8 = cols >> 3;  // cols % 8 == 0 (checked on the host)
+  const int64_t n8 = rows * c8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / c8, c = (i - r * c8) * 8;
+    const float* src = x + r * ld + c;
+    __align__(16) __nv_bfloat16 h[8];
+    if (((uintptr_t)src & 15) == 0) {
+      const float4 a = reinterpret_cast<const float4*>(src)[0], b = reinterpret_cast<const float4*>(src)[1];
+      h[0] = __float2bfloat16_rn(a.x); h[1] = __float2bfloat16_rn(a.y);
+      h[2] = __float2bfloat16_rn(a.z); h[3] = __float2bfloat16_rn(a.w);
+      h[4] = __float2bfloat16_rn(b.x); h[5] = __float2bfloat16_rn(b.y);
+      h[6] = __float2bfloat16_rn(b.z); h[7] = __float2bfloat16_rn(b.w);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) h[j] = __float2bfloat16_rn(src[j]);
+    }
+    *reinterpret_cast<uint4*>(out + r * cols + c) = *reinterpret_cast<const uint4*>(h);
   }
 }
 
@@ -692,7 +770,7 @@ int make_map(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int6
 }
 
 struct Operands {
-  const void* a[3];   // MODE 1: {A}; MODE 3: {Ahi, Alo}; MODE 2: {A, Ah16, Al16}
+  const void* a[3];   // MODE 1: {A}; MODE 3/5: {Ahi, Alo}; MODE 2: {A, Ah16, Al16}; MODE 4: {A16}
   const void* b[3];
   int64_t lda, ldb;   // leading dims of a[0], b[0]; the other arrays are contiguous
 };
@@ -705,10 +783,15 @@ int launch_tc(const Operands& o, TcParams p, cudaStream_t st) {
   const int64_t ar = A_MN ? p.K : p.M, ac = A_MN ? p.M : p.K;
   const int64_t br = B_MN ? p.K : p.N, bc = B_MN ? p.N : p.K;
   const int abox = A_MN ? 32 : BM, bbox = B_MN ? 32 : CF::BNL;
-  B2_TRY(make_map(&m[0], o.a[0], ar, ac, o.lda, abox, A_MN, false));
-  B2_TRY(make_map(&m[1], o.b[0], br, bc, o.ldb, bbox, B_MN, false));
+  // MODE 4 / 5 read bf16 operand arrays (contiguous casts / splits) through bf16 maps
+  constexpr bool kB16 = MODE == 4 || MODE == 5;
+  B2_TRY(make_map(&m[0], o.a[0], ar, ac, o.lda, abox, A_MN, kB16));
+  B2_TRY(make_map(&m[1], o.b[0], br, bc, o.ldb, bbox, B_MN, kB16));
   m[2] = m[0]; m[3] = m[1]; m[4] = m[0]; m[5] = m[1];
-  if (MODE == 3) {
+  if (MODE == 5) {
+    B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, true));
+    B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, true));
+  } else if (MODE == 3) {
     B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, false));
     B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, false));
   } else if (MODE == 2) {
@@ -763,16 +846,30 @@ int tf32_split(float* hi, float* lo, const float* x, int64_t rows, int64_t cols,
   return launched("b2_tf32_split");
 }
 
-// split a [rows, cols] (ld) matrix into contiguous bf16(trunc_tf32(x)), bf16(x - trunc)
+// split a [rows, cols] (ld) matrix into contiguous bf16 hi/lo arrays:
+// mode 2 (TF32X) bf16(trunc_tf32(x)), bf16(x - trunc); mode 5 (3xBF16)
+// bf16_rn(x), bf16_rn(x - hi)
 int bf16x2_split(void* hi, void* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
-                 cudaStream_t st) {
+                 cudaStream_t st, int mode) {
   int64_t n = rows * cols;
   if (n == 0) return 0;
   if (cols % 8 || ((uintptr_t)hi & 15) || ((uintptr_t)lo & 15))
     return fail("b2_bf16x2_split: cols must be a multiple of 8 and outputs 16-B aligned");
-  k_bf16x2_split<<<grid_for(n / 8, 256 * 4, 8), 256, 0, st>>>(
-      (__nv_bfloat16*)hi, (__nv_bfloat16*)lo, x, rows, cols, ld);
-  return launched("b2_bf16x2_split");
+  if (mode == 5)
+    k_bf16x2_split<5><<<grid_for(n / 8, 256 * 4, 8), 256, 0, st>>>(
+        (__nv_bfloat16*)hi, (__nv_bfloat16*)lo, x, rows, cols, ld);
+  else
+    k_bf16x2_split<2><<<grid_for(n / 8, 256 * 4, 8), 256, 0, st>>>(
+        (__nv_bfloat16*)hi, (__nv_bfloat16*)lo, x, rows, cols, ld);
+  return launched(mode == 5 ? "b2_bf16x3_split" : "b2_bf16x2_split");
+}
+
+int bf16_cast(void* out, const float* x, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st) {
+  int64_t n = rows * cols;
+  if (n == 0) return 0;
+  if (cols % 8 || ((uintptr_t)out & 15)) return fail("b2_bf16_cast: cols % 8 and 16-B output needed");
+  k_bf16_cast<<<grid_for(n / 8, 256 * 4, 8), 256, 0, st>>>((__nv_bfloat16*)out, x, rows, cols, ld);
+  return launched("b2_bf16_cast");
 }
 
 bool tc_supported(int ta, int tb, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb) {
@@ -795,7 +892,8 @@ static int cg_mode() {
 }
 
 // mode 1: a0/b0 raw; mode 3: a0/b0 = hi arrays, a1/b1 = lo arrays (contiguous);
-// mode 2: a0/b0 raw fp32 (lda/ldb), a1/b1 = bf16 hi, a2/b2 = bf16 lo (contiguous)
+// mode 2: a0/b0 raw fp32 (lda/ldb), a1/b1 = bf16 hi, a2/b2 = bf16 lo (contiguous);
+// mode 4: a0/b0 = bf16 casts; mode 5: a0/b0 = bf16 hi, a1/b1 = bf16 lo (contiguous)
 int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const void* a0,
             const void* a1, const void* a2, int64_t lda, const void* b0, const void* b1,
             const void* b2_, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
@@ -813,7 +911,9 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   p.mask = mask;
   p.s_hi = (__nv_bfloat16*)s_hi;
   p.s_lo = (__nv_bfloat16*)s_lo;
-  if ((s_hi == nullptr) != (s_lo == nullptr)) return fail("gemm_tc: split outputs come in pairs");
+  if ((s_hi == nullptr) != (s_lo == nullptr) && mode != 4)
+    return fail("gemm_tc: split outputs come in pairs");
+  if (mode == 4) p.s_lo = nullptr;  // BF16 mode emits a single bf16 cast
   Operands o{{a0, a1, a2}, {b0, b1, b2_}, lda, ldb};
   const bool a_mn = ta != 0, b_mn = tb == 0;
   // CTA pairs once there are enough 256-row tiles to fill the chip
@@ -826,10 +926,14 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   if (a_mn == AMN && b_mn == BMN) {                                                 \
     if (cg == 2) {                                                                  \
       if (mode == 3) return launch_tc<AMN, BMN, 3, 2>(o, p, st);                    \
+      if (mode == 4) return launch_tc<AMN, BMN, 4, 2>(o, p, st);                    \
+      if (mode == 5) return launch_tc<AMN, BMN, 5, 2>(o, p, st);                    \
       if (mode == 2) return launch_tc<AMN, BMN, 2, 2>(o, p, st);                    \
       return launch_tc<AMN, BMN, 1, 2>(o, p, st);                                   \
     }                                                                               \
     if (mode == 3) return launch_tc<AMN, BMN, 3, 1>(o, p, st);                      \
+    if (mode == 4) return launch_tc<AMN, BMN, 4, 1>(o, p, st);                      \
+    if (mode == 5) return launch_tc<AMN, BMN, 5, 1>(o, p, st);                      \
     if (mode == 2) return launch_tc<AMN, BMN, 2, 1>(o, p, st);                      \
     return launch_tc<AMN, BMN, 1, 1>(o, p, st);                                     \
   }
