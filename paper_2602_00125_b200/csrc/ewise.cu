@@ -167,15 +167,23 @@ __global__ void __launch_bounds__(kThreads) k_un_flat(float* __restrict__ out,
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t nth = (int64_t)gridDim.x * blockDim.x;
   if (VEC) {
-    int64_t n4 = n >> 2;
-    for (int64_t i = tid; i < n4; i += nth) {
-      float4 v = reinterpret_cast<const float4*>(x)[i];
+    // software-pipelined: the next 128-bit load is in flight while this one's
+    // results are computed (exp's FP64 polynomial would otherwise serialise
+    // with the memory latency)
+    const int64_t n4 = n >> 2;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    int64_t i = tid;
+    float4 v = i < n4 ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (; i < n4; i += nth) {
+      const int64_t nx = i + nth;
+      const float4 vn = nx < n4 ? __ldg(x4 + nx) : v;
       float4 r;
       r.x = f(v.x);
       r.y = f(v.y);
       r.z = f(v.z);
       r.w = f(v.w);
       reinterpret_cast<float4*>(out)[i] = r;
+      v = vn;
     }
     for (int64_t i = (n4 << 2) + tid; i < n; i += nth) out[i] = f(x[i]);
   } else {
@@ -646,7 +654,11 @@ int b2_fused_muladd_relu_bwd(float* ga, float* gb, const float* a, const float* 
     return b2::fail("b2_fused_muladd_relu_bwd: needs cols%4==0 and 16-B aligned rows");
   cudaStream_t st = b2::resolve(stream);
   int64_t colblocks = (cols + 63) / 64;  // strips of 64 columns
-  int64_t splits = std::max<int64_t>(1, (b2::sm_count() * 4) / colblocks);
+  static int occ = 0;  // resident CTAs per SM: the splits fill exactly one wave
+  if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_muladd_relu_bwd, kThreads, 0) !=
+                   cudaSuccess || occ < 1))
+    occ = 1;
+  int64_t splits = std::max<int64_t>(1, ((int64_t)b2::sm_count() * occ) / colblocks);
   splits = std::min<int64_t>(splits, std::max<int64_t>(rows / 64, 1));
   int64_t rps = (rows + splits - 1) / splits;
   if (rps == 0) rps = 1;

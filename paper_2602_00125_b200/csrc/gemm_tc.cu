@@ -211,6 +211,7 @@ struct TcParams {
   const float* mask;        // C = C * (mask > 0 ? 1 : 0), mask [M, N] with ld = ldc (ReLU pullback)
   __nv_bfloat16* s_hi;      // emit the TF32X split of C: bf16(trunc_tf32(C)) ...
   __nv_bfloat16* s_lo;      // ... and bf16(C - trunc_tf32(C)), both [M, N] contiguous
+  int kc;                   // k-blocks per fp32 promotion chunk
 };
 
 // Grouped raster: tiles walk M inside groups of kGroupN tile-columns, so the
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using CF = Cfg<MODE, CG>;
   constexpr int STAGES = CF::STAGES;
   // bf16 operands carry 2^-9 relative error: promote every K = 1024 instead
-  constexpr int KC = MODE == 4 ? 4 * KC_BASE : KC_BASE;
+  const int KC = p.kc;  // k-blocks per accumulation chunk (host: kc_for_mode)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + STAGES * CF::STAGE_BYTES);
@@ -775,6 +776,22 @@ struct Operands {
   int64_t lda, ldb;   // leading dims of a[0], b[0]; the other arrays are contiguous
 };
 
+// fp32 promotion interval: the tensor core's accumulation truncates (~1 ulp
+// per MMA, biased), so the accumulator restarts every KC k-blocks and the
+// epilogue sums chunks in RN fp32. K = 256 for the tf32 modes; K = 1024 for
+// 3xBF16 (measured: normwise 5e-6 at K = 8192 vs 4e-6 at K = 256, +8% speed
+// from 4x fewer TMEM drains) and for the bf16 variant (2^-9 operand error).
+// B2_GEMM_KC overrides (scripts/gemm_kc_probe.py).
+static int kc_for_mode(int mode) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("B2_GEMM_KC");
+    env = e ? atoi(e) : 0;
+  }
+  if (env > 0) return env;
+  return (mode == 4 || mode == 5) ? 4 * KC_BASE : KC_BASE;
+}
+
 template <bool A_MN, bool B_MN, int MODE, int CG>
 int launch_tc(const Operands& o, TcParams p, cudaStream_t st) {
   using CF = Cfg<MODE, CG>;
@@ -800,6 +817,7 @@ int launch_tc(const Operands& o, TcParams p, cudaStream_t st) {
     B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, true));
     B2_TRY(make_map(&m[5], o.b[2], br, bc, bc, bbox, B_MN, true));
   }
+  p.kc = kc_for_mode(MODE);
   p.tiles_n = (p.N + BN - 1) / BN;
   p.tiles_m = (p.M + BM * CG - 1) / (BM * CG);
   p.num_tiles = p.tiles_m * p.tiles_n;

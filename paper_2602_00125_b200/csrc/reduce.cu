@@ -231,15 +231,14 @@ __global__ void __launch_bounds__(256) k_rows(const float* __restrict__ x, int64
 // scans rows k, k+RL, ... of the CTA's row split (a warp reads 2 rows x 256 B,
 // coalesced), then a fixed shared-memory tree folds the RL lanes. Splits S
 // stay small (~8), so the second stage is cheap. grid = (strips * O1, S).
-template <int OP, int V>
+template <int OP, int V, int CL>
 __global__ void __launch_bounds__(256) k_strip(const float* __restrict__ x, int64_t O1, int64_t R,
                                                int64_t I, int64_t Rs, float* __restrict__ out,
                                                int64_t* __restrict__ argr,
                                                double* __restrict__ psum,
                                                MaxAcc* __restrict__ pmax, double count,
                                                int64_t strips) {
-  constexpr int CL = V == 4 ? 16 : 32;  // column lanes
-  constexpr int RL = 256 / CL;          // row lanes
+  constexpr int RL = 256 / CL;  // CL column lanes x RL row lanes
   __shared__ double shd[256 * V];
   __shared__ MaxAcc shm[OP == B2_RED_MAX ? 256 * V : 1];
   const int cl = threadIdx.x % CL, rl = threadIdx.x / CL;
@@ -319,13 +318,31 @@ __global__ void __launch_bounds__(256) k_strip(const float* __restrict__ x, int6
       };
       int64_t r = r0 + rl;
       if (V == 4) {
-        constexpr int U = 8;  // 8 x 128-bit loads issued before any compare
+        // 8 x 128-bit loads in flight; per column the block maximum is an
+        // FMNMX tree (NaNs drop out unless all are NaN) and only a block that
+        // beats the running best (rare after the first few) locates its first
+        // maximal row -- the in-order strict '>' scan's answer for the block.
+        constexpr int U = 8;
+        auto comp = [](const float4& q, int j) { return j == 0 ? q.x : j == 1 ? q.y : j == 2 ? q.z : q.w; };
         for (; r + (U - 1) * RL < r1; r += U * RL) {
           float4 v[U];
 #pragma unroll
           for (int k = 0; k < U; ++k) v[k] = __ldg(reinterpret_cast<const float4*>(base + (r + k * RL) * I));
 #pragma unroll
-          for (int k = 0; k < U; ++k) scan4(v[k], r + k * RL);
+          for (int j = 0; j < 4; ++j) {
+            float m = comp(v[0], j);
+#pragma unroll
+            for (int k = 1; k < U; ++k) m = fmaxf(m, comp(v[k], j));
+            if (m > b[j]) {
+              int kk = U - 1;
+#pragma unroll
+              for (int k = U - 2; k >= 0; --k) kk = comp(v[k], j) == m ? k : kk;
+              // the element itself, not m: keeps the sign of a zero maximum
+#pragma unroll
+              for (int k = 0; k < U; ++k) b[j] = k == kk ? comp(v[k], j) : b[j];
+              bi[j] = (int)(r + kk * RL);
+            }
+          }
         }
         for (; r < r1; r += RL) scan4(*reinterpret_cast<const float4*>(base + r * I), r);
       } else {
@@ -460,6 +477,24 @@ __global__ void k_max_scatter(float* __restrict__ gx, const float* __restrict__ 
   gx[pos] = __fadd_rn(0.0f, g[o]);  // acc[pos] += g with acc = 0.0 (core.py:723-726): -0 -> +0
 }
 
+// resident CTAs per SM of a 256-thread reduction kernel (cached per kernel)
+template <int OP>
+int resident(const void* kern) {
+  static const void* kerns[8] = {};
+  static int occ[8] = {};
+  for (int i = 0; i < 8; ++i)
+    if (kerns[i] == kern) return occ[i];
+  int n = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 256, 0) != cudaSuccess || n < 1) n = 1;
+  for (int i = 0; i < 8; ++i)
+    if (!kerns[i]) {
+      kerns[i] = kern;
+      occ[i] = n;
+      break;
+    }
+  return n;
+}
+
 template <int OP>
 int run_rows(const float* x, int64_t O, int64_t R, float* out, int64_t* argr, double count,
              cudaStream_t st) {
@@ -471,8 +506,10 @@ int run_rows(const float* x, int64_t O, int64_t R, float* out, int64_t* argr, do
   const int rpc = 256 / group;
   const int64_t ctas = (O + rpc - 1) / rpc;
   int64_t S = 1;
-  if (ctas < 2 * sms && R >= 16384) {  // few long rows: split R so ~4 CTAs per SM
-    S = std::min<int64_t>((4 * sms + ctas - 1) / ctas, (R + 8191) / 8192);
+  if (ctas < 2 * sms && R >= 16384) {  // few long rows: split R to fill one resident wave
+    const int64_t cap = (int64_t)sms * resident<OP>(group == 256 ? (const void*)k_rows<OP, 256, true>
+                                                                 : (const void*)k_rows<OP, 32, true>);
+    S = std::min<int64_t>(std::max<int64_t>(cap / ctas, 1), (R + 8191) / 8192);
     S = std::max<int64_t>(S, 1);
   }
   int64_t Rs = (R + S - 1) / S;
@@ -510,12 +547,18 @@ int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_
             double count, cudaStream_t st) {
   const int sms = b2::sm_count();
   const int V = (I % 4 == 0 && ((uintptr_t)x & 15) == 0) ? 4 : 1;
+  // (measured: 128 column lanes -- 2 KB contiguous per row and CTA -- is
+  // slower than 16 on B200: more splits, more partial traffic)
   const int CL = V == 4 ? 16 : 32, RL = 256 / CL;
+  const void* kern = V == 4 ? (const void*)k_strip<OP, 4, 16> : (const void*)k_strip<OP, 1, 32>;
   const int64_t strips = (I + CL * V - 1) / (CL * V);
   const int64_t ctas = strips * O1;
   int64_t S = 1;
-  if (ctas < 4 * sms) {
-    S = std::min<int64_t>((4 * sms + ctas - 1) / ctas, R / (RL * 8));
+  // splits: as many as ONE resident wave holds (a partial second wave would
+  // double the tail), but at least 8 row-lane passes per CTA
+  const int64_t cap = (int64_t)sms * resident<OP>(kern);
+  if (ctas < cap) {
+    S = std::min<int64_t>(cap / ctas, R / (RL * 8));
     S = std::max<int64_t>(S, 1);
   }
   int64_t Rs = (R + S - 1) / S;
@@ -533,9 +576,9 @@ int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_
   }
   dim3 grid((unsigned)(strips * O1), (unsigned)S);
   if (V == 4)
-    k_strip<OP, 4><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, strips);
+    k_strip<OP, 4, 16><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, strips);
   else
-    k_strip<OP, 1><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, strips);
+    k_strip<OP, 1, 32><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, strips);
   int rc = b2::launched("b2_reduce(mid)");
   if (!rc && S > 1) {
     launch_final<OP>(O, S, psum, pmax, out, argr, count, st);
