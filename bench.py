@@ -6,7 +6,7 @@
 One step = forward of 4 x Linear(4096,4096)+ReLU + Linear(4096,1000) over the
 rank's shard of the 65536-sample global batch, mean cross-entropy, backward,
 gradient all-reduce over NCCL (N > 1), one fused Adam(lr=1e-3) update. fp32
-everywhere (TF32X tcgen05 GEMMs = fp32 accuracy). Global batch fixed ->
+everywhere (3xBF16 tcgen05 GEMMs = fp32 accuracy). Global batch fixed ->
 strong scaling. Timing: W warm-up steps, barrier + device sync, CUDA events on
 the engine stream around exactly K steps, max over ranks. Inputs (1 GiB per
 rank at N=1) are larger than L2, so no explicit flush.
@@ -14,7 +14,7 @@ rank at N=1) are larger than L2, so no explicit flush.
 Keys beyond the base contract:
   e2e         same metric through the public API with the batch copied
               host(pinned)->device every step and the loss read back
-  roofline    dominant kernel (tcgen05 3xTF32 GEMM): algorithmic FLOPs per
+  roofline    dominant kernel (tcgen05 3xBF16 GEMM): algorithmic FLOPs per
               launch / its CUDA-event duration inside a real step
   cpu_baseline  the NumPy oracle port of the reference on this host's cores
   ops         the per-op benchmarks of configs 2-4 (1 GPU, rank 0)
@@ -382,7 +382,7 @@ def main():
 
     def step(x, labels, read_loss=False):
         P.reset_tape()
-        x.buffer.version += 1  # a new batch each step: its 3xTF32 split is redone
+        x.buffer.version += 1  # a new batch each step: its operand split is redone
         logits = model(x)
         loss = nn.cross_entropy(logits, labels, denom=rows)
         red = dist.GradReducer(comm, params)

@@ -14,7 +14,7 @@ place (strided / broadcast operands, transposed GEMM operands).
 
 Numerics: + - * / are IEEE fp32 (== the reference's
 f32(double op)); exp/log are f32(double libm); sums accumulate in fp64;
-max keeps the first maximum; matmul is fp32-accurate (3xTF32 on tcgen05
+max keeps the first maximum; matmul is fp32-accurate (3xBF16 on tcgen05
 or FFMA) and lands within the 1e-4 tolerance of the reference's double
 dot products.
 """
@@ -52,7 +52,7 @@ class Buffer:
         self.ptr = p.value
         self.nbytes = int(nbytes)
         self.version = 0
-        self._splits = None  # {(offset, rows, cols, ld): (version, hi, lo)} 3xTF32 operand cache
+        self._splits = None  # {(kind, offset, rows, cols, ld): (version, hi, lo, capture)} GEMM operand splits
 
     def __del__(self):
         try:
@@ -780,8 +780,8 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
     """out[M,N] = x[M,K] . w[N,K]^T (+bias)(relu); x, w arbitrary 2-D views.
 
     mask (contiguous [M,N]): multiply out by (mask > 0), the ReLU pullback --
-    fused into the TF32X epilogue, else applied by a separate pass.
-    emit_split: let the TF32X epilogue also write out's operand split into
+    fused into the tensor-core epilogue, else applied by a separate pass.
+    emit_split: let the tensor-core epilogue also write out's operand split into
     out's split cache (the next GEMMs reading out skip the split pass)."""
     M, K = x.shape
     N = w.shape[0]
@@ -949,7 +949,7 @@ def linear(x, weight, bias=None, relu_out=False) -> Tensor:
             (L.EPI_RELU if relu_out else L.EPI_NONE)
         bc = bias if (bias is None or bias.is_contiguous) else _copy_contig(bias)
         # a hidden layer's output is the next layer's GEMM operand: let the
-        # epilogue write its TF32X split too (no separate split pass)
+        # epilogue write its operand split too (no separate split pass)
         _gemm_into(out, x, weight, bc, epi, emit_split=relu_out)
     memo = [None, None]
     y = out.detach()  # no output->node->closure->output cycle (see _unary)

@@ -212,19 +212,21 @@ struct TcParams {
   __nv_bfloat16* s_hi;      // emit the TF32X split of C: bf16(trunc_tf32(C)) ...
   __nv_bfloat16* s_lo;      // ... and bf16(C - trunc_tf32(C)), both [M, N] contiguous
   int kc;                   // k-blocks per fp32 promotion chunk
+  int group_n;              // raster group width in tile-columns
 };
 
 // Grouped raster: tiles walk M inside groups of kGroupN tile-columns, so the
 // ~74-148 tiles resident at once cover a ~9 x 8 block of the output and the
 // B panels of a group stay in L2 across waves (the plain row-major order
 // re-read all of B from DRAM every wave: 12.8 GB/launch for 3.4 GB of data).
-constexpr int kGroupN = 8;
+constexpr int kGroupN = 8;  // default group width (B2_GEMM_GROUPN overrides, p.group_n)
 __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& tm, int& tn) {
-  const int group = kGroupN * p.tiles_m;
+  const int gn = p.group_n;
+  const int group = gn * p.tiles_m;
   const int g = t / group, r = t - g * group;
-  const int w = min(kGroupN, p.tiles_n - g * kGroupN);
+  const int w = min(gn, p.tiles_n - g * gn);
   tm = r / w;
-  tn = g * kGroupN + (r - tm * w);
+  tn = g * gn + (r - tm * w);
 }
 
 // MODE 1: 1xTF32            tiles A32 | B32
@@ -818,6 +820,15 @@ int launch_tc(const Operands& o, TcParams p, cudaStream_t st) {
     B2_TRY(make_map(&m[5], o.b[2], br, bc, bc, bbox, B_MN, true));
   }
   p.kc = kc_for_mode(MODE);
+  {
+    static int gn = -1;
+    if (gn < 0) {
+      const char* e = getenv("B2_GEMM_GROUPN");
+      gn = e ? atoi(e) : 0;
+      if (gn <= 0) gn = kGroupN;
+    }
+    p.group_n = gn;
+  }
   p.tiles_n = (p.N + BN - 1) / BN;
   p.tiles_m = (p.M + BM * CG - 1) / (BM * CG);
   p.num_tiles = p.tiles_m * p.tiles_n;
