@@ -121,33 +121,40 @@ def ncu_traffic():
 
 def cpu_oracle_step_rate(sample_rows=512, width=WIDTH, seed=0, budget_s=25.0):
     """The NumPy f64 restatement of the reference (oracle/tensorlite_np.py) on
-    this host: fwd+bwd over `sample_rows` rows of the config-5 workload and one
-    Adam step over all 71.2M parameters; extrapolated to the 65536 batch as
-    65536 / (t_fwdbwd * 65536/rows + t_adam) (the optimizer is
-    charged once per step)."""
+    this host, extrapolated per SURVEY 8d: fwd+bwd timed at two batch sizes
+    (rows/2 and rows) and fit t = fixed + slope*rows, evaluated at 65536; one
+    Adam step over all 71.2M parameters charged once per step."""
     from oracle import tensorlite_np as O
     from paper_2602_00125_b200.data import mlp_config5
 
     params = mlp_config5(seed, WIDTH, CLASSES, DEPTH)
     rng = np.random.default_rng(1)
-    x = rng.standard_normal((sample_rows, width), dtype=np.float32)
-    labels = rng.integers(0, CLASSES, sample_rows)
 
     class _NoOpt:
         def step(self, key, th, g):
             return th
 
-    t0 = time.perf_counter()
-    r = O.mlp_train_step(params, x, labels, _NoOpt())
-    t_fb = time.perf_counter() - t0
+    def fwdbwd(rows):
+        x = rng.standard_normal((rows, width), dtype=np.float32)
+        labels = rng.integers(0, CLASSES, rows)
+        t0 = time.perf_counter()
+        r = O.mlp_train_step(params, x, labels, _NoOpt())
+        return time.perf_counter() - t0, r
+
+    half = max(sample_rows // 2, 1)
+    t_half, _ = fwdbwd(half)
+    t_fb, r = fwdbwd(sample_rows)
+    slope = max((t_fb - t_half) / (sample_rows - half), 0.0) if sample_rows > half else t_fb / sample_rows
+    fixed = max(t_half - slope * half, 0.0)
     adam = O.Adam(lr=1e-3)
     t0 = time.perf_counter()
     for i, ((w, b), (gw, gb)) in enumerate(zip(params, r["grads"])):
         adam.step(("w", i), w, gw)
         adam.step(("b", i), b, gb)
     t_adam = time.perf_counter() - t0
-    step_s = t_fb * (GLOBAL_BATCH / sample_rows) + t_adam
-    return GLOBAL_BATCH / step_s, {"t_fwdbwd_s": t_fb, "t_adam_s": t_adam, "rows": sample_rows}
+    step_s = fixed + slope * GLOBAL_BATCH + t_adam
+    return GLOBAL_BATCH / step_s, {"t_fwdbwd_s": t_fb, "t_half_s": t_half, "fixed_s": fixed,
+                                   "t_adam_s": t_adam, "rows": sample_rows}
 
 
 def run_reference(args):
@@ -171,12 +178,53 @@ def run_reference(args):
         "config": {"workload": "config5_mlp_4x4096_1000_b65536_adam", "global_batch": GLOBAL_BATCH,
                    "parallelism": "cpu"},
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
-                         "sample": f"{info['rows']} rows fwd+bwd + full Adam per step, "
-                                   f"extrapolated to 65536 (oracle/tensorlite_np.py, numpy BLAS "
-                                   f"threads={cores})"},
+                         "sample": f"fwd+bwd at {info['rows'] // 2} and {info['rows']} rows fit as "
+                                   f"fixed + slope*rows, evaluated at 65536, + one full Adam step "
+                                   f"(oracle/tensorlite_np.py, numpy BLAS threads={cores}); "
+                                   f"extrapolated"},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_ops_baseline():
+    """The per-op figures of `op_benchmarks` for the NumPy oracle port on the
+    host cores (configs 1, 2 and 3 at 1024 at full size), same
+    units: GB/s of algorithmic bytes, TFLOP/s, us/step."""
+    from oracle import tensorlite_np as O
+
+    def best(fn, reps=3):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+
+    out = {"kind": "port", "cores": os.cpu_count(), "note": "oracle/tensorlite_np.py (f64 NumPy), best of 3"}
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((4096, 4096), dtype=np.float32)
+    b = rng.uniform(-1, 1, (1, 4096)).astype(np.float32)
+    n = a.size
+    out["config2_fused_fwd_gbs"] = 8 * n / best(lambda: O.relu(O.add(O.mul(a, b), b))) / 1e9
+    out["config2_exp_gbs"] = 8 * n / best(lambda: O.exp(a)) / 1e9
+    out["config2_mul_bcast_gbs"] = 8 * n / best(lambda: O.mul(a, b)) / 1e9
+    for ax in (0, 1):
+        out[f"config2_sum_dim{ax}_gbs"] = 4 * n / best(lambda: O.axis_sum(a, ax)) / 1e9
+        out[f"config2_max_dim{ax}_gbs"] = 4 * n / best(lambda: O.axis_max(a, ax)) / 1e9
+    out["config2_sum_all_gbs"] = 4 * n / best(lambda: O.axis_sum(a, None)) / 1e9
+    A = rng.uniform(-1, 1, (1024, 1024)).astype(np.float32)
+    B = rng.uniform(-1, 1, (1024, 1024)).astype(np.float32)
+    dC = rng.standard_normal((1024, 1024), dtype=np.float32)
+    out["config3_n1024_fwdbwd_tflops"] = 6 * 1024 ** 3 / best(lambda: O.matmul_fwd_bwd(A, B, dC)) / 1e12
+    from paper_2602_00125_b200.data import linear_params
+
+    r1 = np.random.default_rng(0)
+    params = [linear_params(r1, 784, 256), linear_params(r1, 256, 10)]
+    x1 = r1.standard_normal((256, 784), dtype=np.float32)
+    l1 = r1.integers(0, 10, 256)
+    out["config1_us_per_step"] = best(lambda: O.mlp_train_step(params, x1, l1, O.SGD(lr=0.01))) * 1e6
+    return out
 
 
 # --------------------------------------------------------------------- op benchmarks (configs 2-4)
@@ -488,14 +536,18 @@ def main():
 
     ops = None
     cpu = None
+    ops_cpu = None
     if rank == 0 and world == 1:
         if not args.no_ops:
             ops = op_benchmarks()
         if not args.no_cpu:
             v_cpu, info = cpu_oracle_step_rate()
             cpu = {"value": v_cpu, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
-                   "sample": f"{info['rows']} rows fwd+bwd ({info['t_fwdbwd_s']:.2f}s) + full Adam "
-                             f"({info['t_adam_s']:.2f}s), extrapolated to 65536 rows"}
+                   "sample": f"fwd+bwd at {info['rows'] // 2} rows ({info['t_half_s']:.2f}s) and "
+                             f"{info['rows']} rows ({info['t_fwdbwd_s']:.2f}s) fit as fixed + "
+                             f"slope*rows at 65536, + full Adam ({info['t_adam_s']:.2f}s); "
+                             f"extrapolated"}
+            ops_cpu = cpu_ops_baseline()
 
     if rank == 0:
         line = {
@@ -521,6 +573,7 @@ def main():
             "final_loss": loss_val,
             "bf16_variant": bf16,
             "ops": ops,
+            "ops_cpu_baseline": ops_cpu,
         }
         print(json.dumps(line), flush=True)
 

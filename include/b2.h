@@ -72,11 +72,19 @@ int b2_fill_f32(float* dst, float value, int64_t n, void* stream);
  */
 enum b2_binary_op { B2_ADD = 0, B2_SUB = 1, B2_MUL = 2, B2_DIV = 3,
                     B2_RELU_BWD = 4 /* a * (b > 0 ? 1 : 0), nn.py:101-103 */,
-                    B2_SIGN_MUL = 5 /* a * sign(b), core.py:533-546 */ };
+                    B2_SIGN_MUL = 5 /* a * sign(b), core.py:533-546 */,
+                    /* activation pullbacks (nn.py:95-144 _pointwise): a * f32(dfn(b)),
+                       dfn in double on the saved value b */
+                    B2_SIGMOID_BWD = 6 /* b = y: y * (1 - y) */,
+                    B2_TANH_BWD = 7 /* b = y: 1 - y * y */,
+                    B2_GELU_BWD = 8 /* b = x: Phi(x) + x * phi(x) */ };
 enum b2_unary_op { B2_NEG = 0, B2_EXP = 1, B2_LOG = 2, B2_SQRT = 3, B2_ABS = 4,
                    B2_RELU = 5, B2_RELU_MASK = 6, B2_COPY = 7, B2_CLAMP = 8,
                    B2_SCALE = 9 /* x * alpha */, B2_DIV_SCALAR = 10 /* x / f32(alpha) */,
-                   B2_CLAMP_MASK = 11 /* alpha <= x <= beta ? 1 : 0 */ };
+                   B2_CLAMP_MASK = 11 /* alpha <= x <= beta ? 1 : 0 */,
+                   /* activations: f32(fn(double x)) (nn.py:114-144) */
+                   B2_SIGMOID = 12 /* sign-split 1/(1+e^-x) | e^x/(1+e^x) */,
+                   B2_TANH = 13, B2_GELU = 14 /* 0.5 x (1 + erf(x / sqrt 2)) */ };
 int b2_binary(int op, float* out, int ndim, const int64_t* shape,
               const float* a, const int64_t* a_strides,
               const float* b, const int64_t* b_strides, void* stream);
@@ -233,6 +241,10 @@ int b2_sgd_multi(const b2_opt_tensor* tensors, int count, double lr, double mome
                  double weight_decay, void* stream);
 int b2_adam_multi(const b2_opt_tensor* tensors, int count, double lr, double beta1,
                   double beta2, double eps, double weight_decay, void* stream);
+/* RMSprop (optim.py:103-122): v = rho*v + (1-rho)*g*g; theta -= lr*g/sqrt(v+eps);
+ * slot0 = v (fp64) */
+int b2_rmsprop_multi(const b2_opt_tensor* tensors, int count, double lr, double rho, double eps,
+                     double weight_decay, void* stream);
 
 /* ---------------------------------------------------------------- collectives
  * Data-parallel gradient exchange (new; the reference is single-process).

@@ -419,6 +419,84 @@ class Adam:
         return f32(th - self.lr * (m / bc1) / (np.sqrt(v / bc2) + self.eps))
 
 
+class RMSprop:
+    """v = rho*v + (1-rho)*g*g; theta = f32(theta - lr*g/sqrt(v + eps)) (optim.py:103-122)."""
+
+    def __init__(self, lr=0.01, rho=0.99, eps=1e-8, weight_decay=0.0):
+        self.lr, self.rho, self.eps, self.weight_decay = lr, rho, eps, weight_decay
+        self.state = {}
+
+    def step(self, key, theta, grad):
+        th = _d(theta)
+        g = _d(grad)
+        if self.weight_decay:
+            g = g + self.weight_decay * th
+        v = self.state.get(key)
+        if v is None:
+            v = np.zeros_like(th)
+        v = self.rho * v + (1.0 - self.rho) * g * g
+        self.state[key] = v
+        return f32(th - self.lr * g / np.sqrt(v + self.eps))
+
+
+# ---------------------------------------------------------------------------
+# pointwise activations (nn.py:95-144): out = f32(fn(double x)); the pullback
+# multiplies g by f32(dfn(v)), v the saved input or output
+
+
+def _map(fn, x):
+    flat = [fn(float(v)) for v in np.asarray(x, np.float32).ravel()]
+    return f32(np.array(flat, np.float64).reshape(np.shape(x)))
+
+
+def _sigmoid_scalar(v):  # nn.py:114-119, split on sign
+    if v >= 0.0:
+        return 1.0 / (1.0 + math.exp(-v))
+    e = math.exp(v)
+    return e / (1.0 + e)
+
+
+_SQRT2 = math.sqrt(2.0)
+_INV_SQRT_2PI = 1.0 / math.sqrt(2.0 * math.pi)
+
+
+def _gelu_scalar(v):  # nn.py:132-133
+    return 0.5 * v * (1.0 + math.erf(v / _SQRT2))
+
+
+def _gelu_deriv(v):  # nn.py:136-139
+    cdf = 0.5 * (1.0 + math.erf(v / _SQRT2))
+    pdf = _INV_SQRT_2PI * math.exp(-0.5 * v * v)
+    return cdf + v * pdf
+
+
+def _math_tanh(v):
+    return math.tanh(v)
+
+
+def sigmoid(x):
+    return _map(_sigmoid_scalar, x)
+
+
+def tanh(x):
+    return _map(_math_tanh, x)
+
+
+def gelu(x):
+    return _map(_gelu_scalar, x)
+
+
+def activation_grad(kind, g, x, y):
+    """g * f32(dfn(v)) with v = y for sigmoid/tanh, x for gelu (nn.py:101-103)."""
+    if kind == "sigmoid":
+        d = _map(lambda v: v * (1.0 - v), y)
+    elif kind == "tanh":
+        d = _map(lambda v: 1.0 - v * v, y)
+    else:
+        d = _map(_gelu_deriv, x)
+    return mul(g, d)
+
+
 # ---------------------------------------------------------------------------
 # composed hot paths (BASELINE configs)
 

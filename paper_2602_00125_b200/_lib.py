@@ -103,6 +103,8 @@ _SIGS = {
     "b2_sgd_multi": (c_int, [POINTER(OptTensor), c_int, c_double, c_double, c_double, c_void_p]),
     "b2_adam_multi": (c_int, [POINTER(OptTensor), c_int, c_double, c_double, c_double, c_double,
                               c_double, c_void_p]),
+    "b2_rmsprop_multi": (c_int, [POINTER(OptTensor), c_int, c_double, c_double, c_double, c_double,
+                                 c_void_p]),
     "b2_comm_unique_id": (c_int, [ctypes.c_char_p]),
     "b2_comm_init": (c_int, [c_int, c_int, ctypes.c_char_p]),
     "b2_comm_destroy": (c_int, []),
@@ -110,8 +112,9 @@ _SIGS = {
 }
 
 # enum values (include/b2.h)
-ADD, SUB, MUL, DIV, RELU_BWD, SIGN_MUL = range(6)
-NEG, EXP, LOG, SQRT, ABS, RELU, RELU_MASK, COPY, CLAMP, SCALE, DIV_SCALAR, CLAMP_MASK = range(12)
+ADD, SUB, MUL, DIV, RELU_BWD, SIGN_MUL, SIGMOID_BWD, TANH_BWD, GELU_BWD = range(9)
+(NEG, EXP, LOG, SQRT, ABS, RELU, RELU_MASK, COPY, CLAMP, SCALE, DIV_SCALAR, CLAMP_MASK, SIGMOID, TANH,
+ GELU) = range(15)
 RED_SUM, RED_MEAN, RED_MAX = range(3)
 GEMM_AUTO, GEMM_SIMT, GEMM_3XTF32, GEMM_1XTF32, GEMM_TF32X, GEMM_3XBF16 = range(6)
 GEMM_BF16 = 6  # host-side selector for b2_gemm_bf16 (bf16 variant; never auto-selected)

@@ -534,6 +534,34 @@ def relu(x) -> Tensor:
     return record("relu", (x,), out, (pull,), saved=(x,))
 
 
+def _activation(kind, op, bwd_op, x, from_input):
+    """nn._pointwise (nn.py:95-105): out = f32(fn(x)); pullback g * f32(dfn(v))
+    with v the saved input (from_input) or output -- one kernel each way."""
+    x = _as_tensor(_as_operand(x))
+    out = _launch_unary(op, x)
+    v = x if from_input else out.detach()
+
+    def pull(g):
+        return _launch_binary(bwd_op, g, v, broadcast_shapes(g.shape, v.shape))
+
+    return record(kind, (x,), out, (pull,), saved=(v,))
+
+
+def sigmoid(x) -> Tensor:
+    """nn.sigmoid (nn.py:114-124): sign-split logistic; grad y * (1 - y)."""
+    return _activation("sigmoid", L.SIGMOID, L.SIGMOID_BWD, x, False)
+
+
+def tanh(x) -> Tensor:
+    """nn.tanh (nn.py:127-129): math.tanh; grad 1 - y * y."""
+    return _activation("tanh", L.TANH, L.TANH_BWD, x, False)
+
+
+def gelu(x) -> Tensor:
+    """nn.gelu (nn.py:132-144): 0.5 x (1 + erf(x / sqrt 2)); grad Phi(x) + x phi(x)."""
+    return _activation("gelu", L.GELU, L.GELU_BWD, x, True)
+
+
 def clamp(x, low, high) -> Tensor:
     """min(max(x, low), high). Not a reference op (the BASELINE config-2 clamp
     happens on the host there); gradient passes where low<=x<=high."""
@@ -661,6 +689,23 @@ def max(x, axis=None, keepdims=False) -> Tensor:
         return gx
 
     return record("max", (x,), out, (pull,), saved=(x,))
+
+
+def argmax(x, axis=-1) -> np.ndarray:
+    """First-maximum indices along one axis (the max reduction's routing
+    index, core.py:709-713 scan order), read back to the host as int64 -- for
+    callers' metrics such as the demos' accuracy (demos.py:85-96)."""
+    x = _as_tensor(_as_operand(x))
+    axes = _normalize_axes(axis, x.ndim)
+    if len(axes) != 1:
+        raise ShapeError("argmax takes exactly one axis")
+    if x.shape[axes[0]] == 0:
+        raise ShapeError("max over a zero-extent axis is undefined")
+    _, oshape = _reduced_shapes(x.shape, axes, False)
+    out, arg = _reduce(L.RED_MAX, x, axes, oshape, want_arg=True)
+    idx = np.empty(_py_max(out.size, 1), np.int64)
+    L.call("b2_memcpy_d2h", idx.ctypes.data, arg.ptr, 8 * idx.size, None)
+    return idx[:out.size].reshape(oshape)
 
 
 # ---------------------------------------------------------------------------

@@ -83,6 +83,22 @@ __device__ __forceinline__ float sign_of(float v) {
   return v > 0.0f ? 1.0f : (v < 0.0f ? -1.0f : 0.0f);  // core.py:533-538
 }
 
+// activations and their derivatives in double, like the reference's
+// math.* on Python floats (nn.py:114-144); one f32 rounding at the store
+__device__ __forceinline__ double sigmoid_d(double v) {
+  if (v >= 0.0) return 1.0 / (1.0 + b2::exp_fast(-v));  // split on sign: exp never overflows
+  const double e = b2::exp_fast(v);
+  return e / (1.0 + e);
+}
+constexpr double kSqrt2 = 1.4142135623730951;          // math.sqrt(2.0)
+constexpr double kInvSqrt2Pi = 0.3989422804014327;     // 1 / math.sqrt(2 pi)
+__device__ __forceinline__ double gelu_d(double v) { return 0.5 * v * (1.0 + erf(v / kSqrt2)); }
+__device__ __forceinline__ double gelu_deriv_d(double v) {
+  const double cdf = 0.5 * (1.0 + erf(v / kSqrt2));
+  const double pdf = kInvSqrt2Pi * b2::exp_fast(-0.5 * v * v);
+  return cdf + v * pdf;
+}
+
 template <int OP>
 struct Bin {
   __device__ __forceinline__ float operator()(float a, float b) const {
@@ -92,6 +108,15 @@ struct Bin {
     if constexpr (OP == B2_DIV) return __fdiv_rn(a, b);
     if constexpr (OP == B2_RELU_BWD) return __fmul_rn(a, b > 0.0f ? 1.0f : 0.0f);
     if constexpr (OP == B2_SIGN_MUL) return __fmul_rn(a, sign_of(b));
+    if constexpr (OP == B2_SIGMOID_BWD) {
+      const double y = b;
+      return __fmul_rn(a, __double2float_rn(__dmul_rn(y, __dsub_rn(1.0, y))));
+    }
+    if constexpr (OP == B2_TANH_BWD) {
+      const double y = b;
+      return __fmul_rn(a, __double2float_rn(__dsub_rn(1.0, __dmul_rn(y, y))));
+    }
+    if constexpr (OP == B2_GELU_BWD) return __fmul_rn(a, __double2float_rn(gelu_deriv_d(b)));
     return 0.0f;
   }
 };
@@ -112,6 +137,9 @@ struct Un {
     if constexpr (OP == B2_SCALE) return __fmul_rn(x, (float)alpha);
     if constexpr (OP == B2_DIV_SCALAR) return __fdiv_rn(x, (float)alpha);
     if constexpr (OP == B2_CLAMP_MASK) return (x >= (float)alpha && x <= (float)beta) ? 1.0f : 0.0f;
+    if constexpr (OP == B2_SIGMOID) return __double2float_rn(sigmoid_d(x));
+    if constexpr (OP == B2_TANH) return __double2float_rn(tanh((double)x));
+    if constexpr (OP == B2_GELU) return __double2float_rn(gelu_d(x));
     return x;
   }
 };
@@ -562,6 +590,9 @@ int b2_binary(int op, float* out, int ndim, const int64_t* shape, const float* a
     case B2_DIV: return launch_binary(out, nd, a, b, Bin<B2_DIV>{}, st);
     case B2_RELU_BWD: return launch_binary(out, nd, a, b, Bin<B2_RELU_BWD>{}, st);
     case B2_SIGN_MUL: return launch_binary(out, nd, a, b, Bin<B2_SIGN_MUL>{}, st);
+    case B2_SIGMOID_BWD: return launch_binary(out, nd, a, b, Bin<B2_SIGMOID_BWD>{}, st);
+    case B2_TANH_BWD: return launch_binary(out, nd, a, b, Bin<B2_TANH_BWD>{}, st);
+    case B2_GELU_BWD: return launch_binary(out, nd, a, b, Bin<B2_GELU_BWD>{}, st);
   }
   return b2::fail("b2_binary: unknown op");
 }
@@ -610,6 +641,9 @@ int b2_unary(int op, float* out, int ndim, const int64_t* shape, const float* x,
     case B2_SCALE: return launch_unary(out, nd, x, Un<B2_SCALE>{alpha, beta}, st);
     case B2_DIV_SCALAR: return launch_unary(out, nd, x, Un<B2_DIV_SCALAR>{alpha, beta}, st);
     case B2_CLAMP_MASK: return launch_unary(out, nd, x, Un<B2_CLAMP_MASK>{alpha, beta}, st);
+    case B2_SIGMOID: return launch_unary(out, nd, x, Un<B2_SIGMOID>{alpha, beta}, st);
+    case B2_TANH: return launch_unary(out, nd, x, Un<B2_TANH>{alpha, beta}, st);
+    case B2_GELU: return launch_unary(out, nd, x, Un<B2_GELU>{alpha, beta}, st);
   }
   return b2::fail("b2_unary: unknown op");
 }

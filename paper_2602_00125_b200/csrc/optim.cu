@@ -1,4 +1,4 @@
-// Multi-tensor fused SGD / Adam: one launch updates every parameter.
+// Multi-tensor fused SGD / Adam / RMSprop: one launch updates every parameter.
 //
 // Replaces Optimizer.step/_update and step_all (tensorlite/optim.py:39-136).
 // Slot arithmetic is double and mirrors the reference expression order
@@ -72,6 +72,26 @@ __global__ void __launch_bounds__(kThreads) k_adam(const __grid_constant__ Table
   }
 }
 
+__global__ void __launch_bounds__(kThreads) k_rmsprop(const __grid_constant__ Table tb, double lr,
+                                                      double rho, double omrho, double eps,
+                                                      double wd) {
+  int ti = find_tensor(tb, blockIdx.x);
+  const b2_opt_tensor& T = tb.t[ti];
+  int64_t base = (blockIdx.x - tb.prefix[ti]) * (int64_t)kChunk;
+  int64_t end = min(T.n, base + kChunk);
+  for (int64_t i = base + threadIdx.x; i < end; i += kThreads) {
+    double th = (double)T.param[i];
+    double g = (double)T.grad[i];
+    if (wd != 0.0) g = __dadd_rn(g, __dmul_rn(wd, th));
+    // vi = rho * v + (1.0 - rho) * gi * gi (left to right)                     optim.py:118
+    double v = __dadd_rn(__dmul_rn(rho, T.slot0[i]), __dmul_rn(__dmul_rn(omrho, g), g));
+    T.slot0[i] = v;
+    // theta - lr * gi / sqrt(vi + eps)                                           optim.py:120
+    T.param[i] = __double2float_rn(
+        __dsub_rn(th, __ddiv_rn(__dmul_rn(lr, g), __dsqrt_rn(__dadd_rn(v, eps)))));
+  }
+}
+
 template <class Launch>
 int run_multi(const b2_opt_tensor* ts, int count, Launch launch) {
   for (int off = 0; off < count; off += kMaxT) {
@@ -113,6 +133,16 @@ int b2_adam_multi(const b2_opt_tensor* ts, int count, double lr, double b1, doub
   return run_multi(ts, count, [&](const Table& tb, unsigned grid) {
     k_adam<<<grid, kThreads, 0, st>>>(tb, lr, b1, b2, omb1, omb2, eps, wd);
     return b2::launched("b2_adam_multi");
+  });
+}
+
+int b2_rmsprop_multi(const b2_opt_tensor* ts, int count, double lr, double rho, double eps,
+                     double wd, void* stream) {
+  cudaStream_t st = b2::resolve(stream);
+  double omrho = 1.0 - rho;
+  return run_multi(ts, count, [&](const Table& tb, unsigned grid) {
+    k_rmsprop<<<grid, kThreads, 0, st>>>(tb, lr, rho, omrho, eps, wd);
+    return b2::launched("b2_rmsprop_multi");
   });
 }
 

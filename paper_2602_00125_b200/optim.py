@@ -1,4 +1,4 @@
-"""SGD / Adam as single multi-tensor kernel launches (tensorlite/optim.py).
+"""SGD / Adam / RMSprop as single multi-tensor kernel launches (tensorlite/optim.py).
 
 Semantics follow optim.py:16-136: per-parameter slots keyed by identity,
 coupled weight decay, SGD momentum ``v = mu*v + g``, Adam debiased with eps
@@ -112,6 +112,19 @@ class Adam(Optimizer):
     def _launch(self, table, count):
         L.call("b2_adam_multi", table, count, float(self.lr), float(self.beta1),
                float(self.beta2), float(self.eps), float(self.weight_decay), None)
+
+
+class RMSprop(Optimizer):
+    """v = rho*v + (1-rho)*g^2; theta -= lr*g/sqrt(v + eps) (optim.py:103-122)."""
+
+    def __init__(self, lr=0.01, rho=0.99, eps=1e-8, weight_decay=0.0):
+        super().__init__(lr, weight_decay)
+        self.rho = rho
+        self.eps = eps
+
+    def _launch(self, table, count):
+        L.call("b2_rmsprop_multi", table, count, float(self.lr), float(self.rho), float(self.eps),
+               float(self.weight_decay), None)
 
 
 def step_all(optimizer: Optimizer, parameters, grad_store):

@@ -239,7 +239,46 @@ def gen_configs():
     save("config5_small.npz", **out)
 
 
+def gen_next_rows():
+    """activations (nn.py:95-144), RMSprop (optim.py:103-122)
+    and the demo training callers' logs (demos.py:42-130)."""
+    from tensorlite import demos as tdemos
+
+    out = {}
+    u = unary_values()
+    out["act_x"] = u
+    g = np.random.default_rng(12).standard_normal(u.shape).astype(np.float32)
+    out["act_g"] = g
+    for name in ("sigmoid", "tanh", "gelu"):
+        tl.reset_tape()
+        x = T(u, grad=True)
+        y = getattr(tnn, name)(x)
+        store = tl.backward(y, seed=T(g))
+        out[f"act_{name}"] = A(y)
+        out[f"act_{name}_grad"] = A(store[x])
+    rng = np.random.default_rng(13)
+    theta0 = rng.standard_normal(257).astype(np.float32)
+    grads = rng.standard_normal((4, 257)).astype(np.float32)
+    out["opt_theta0"], out["opt_grads"] = theta0, grads
+    for name, opt in (("rmsprop", topt.RMSprop(lr=0.01)),
+                      ("rmsprop_wd", topt.RMSprop(lr=3e-3, rho=0.9, eps=1e-6, weight_decay=0.05))):
+        p = T(theta0)
+        seq = []
+        for k in range(4):
+            opt.step(p, T(grads[k]))
+            seq.append(A(p))
+        out[f"opt_{name}"] = np.stack(seq)
+    xor = tdemos.run_xor(seed=0, epochs=300)
+    blobs = tdemos.run_blobs(seed=0, epochs=60)
+    out["xor_lines"] = np.array(xor.lines)
+    out["blobs_lines"] = np.array(blobs.lines)
+    blobs_rms = tdemos.run_blobs(seed=3, epochs=30, lr=0.01, optimizer="rmsprop")
+    out["blobs_rms_lines"] = np.array(blobs_rms.lines)
+    save("next_rows.npz", **out)
+
+
 if __name__ == "__main__":
+    gen_next_rows()
     gen_elementwise()
     gen_reductions()
     gen_matmul()

@@ -1,0 +1,65 @@
+"""Device parity for the SURVEY 8f rows: pointwise activations and their
+pullbacks (nn.py:95-144), multi-tensor RMSprop (optim.py:103-122), and the
+reference's training callers with their log contract (demos.py:42-130) --
+against goldens produced by running the reference (tests/golden/next_rows.npz)."""
+
+import numpy as np
+import pytest
+
+import paper_2602_00125_b200 as P
+from paper_2602_00125_b200 import demos, optim
+from tests.golden.load import bits_equal, load, normwise
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a, grad=False):
+    return P.from_numpy(np.asarray(a, np.float32), requires_grad=grad)
+
+
+@pytest.mark.parametrize("name", ["sigmoid", "tanh", "gelu"])
+def test_activations_and_pullbacks_bit_exact(name):
+    g = load("next_rows.npz")
+    P.reset_tape()
+    x = dev(g["act_x"], True)
+    y = getattr(P, name)(x)
+    assert bits_equal(y.numpy(), g[f"act_{name}"])
+    store = P.backward(y, seed=dev(g["act_g"]))
+    assert bits_equal(store[x].numpy(), g[f"act_{name}_grad"])
+
+
+@pytest.mark.parametrize("name,ctor", [
+    ("rmsprop", lambda: optim.RMSprop(lr=0.01)),
+    ("rmsprop_wd", lambda: optim.RMSprop(lr=3e-3, rho=0.9, eps=1e-6, weight_decay=0.05)),
+])
+def test_rmsprop_multi_tensor_bit_exact(name, ctor):
+    g = load("next_rows.npz")
+    opt = ctor()
+    p = dev(g["opt_theta0"])
+    for k in range(4):
+        opt.step(p, dev(g["opt_grads"][k]))
+        assert bits_equal(p.numpy(), g[f"opt_{name}"][k]), (name, k)
+
+
+def _parse(lines):
+    rows = [l.split(",") for l in lines]
+    return [r[0] for r in rows], np.array([[float(v) for v in r[1:]] for r in rows])
+
+
+@pytest.mark.parametrize("key,run", [
+    ("xor_lines", lambda: demos.run_xor(seed=0, epochs=300)),
+    ("blobs_lines", lambda: demos.run_blobs(seed=0, epochs=60)),
+    ("blobs_rms_lines", lambda: demos.run_blobs(seed=3, epochs=30, lr=0.01, optimizer="rmsprop")),
+])
+def test_demo_training_logs_match_reference(key, run):
+    """Same seeds, init streams and log format; losses within the fp32
+    tolerance (GEMMs accumulate in fp32, the reference in double), accuracies
+    equal up to one sample."""
+    want_ep, want = _parse(load("next_rows.npz")[key])
+    res = run()
+    got_ep, got = _parse(res.lines)
+    assert got_ep == want_ep
+    assert res.diverged_at is None
+    assert normwise(got[:, 0], want[:, 0]) <= 1e-4
+    if want.shape[1] > 1:
+        assert np.max(np.abs(got[:, 1] - want[:, 1])) <= 1.0 / 200 + 1e-12

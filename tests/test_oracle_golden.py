@@ -140,3 +140,37 @@ def test_config4_small_bit_exact():
     assert bits_equal(r["dX"].reshape(-1, 64), g["dX"])
     assert bits_equal(r["dW"], g["dW"])
     assert bits_equal(r["dbias"], g["dbias"])
+
+
+# ---------------------------------------------------------------- SURVEY 8f rows
+
+
+@pytest.mark.parametrize("name", ["sigmoid", "tanh", "gelu"])
+def test_activations_and_grads_bit_exact(name):
+    g = load("next_rows.npz")
+    x, gy = g["act_x"], g["act_g"]
+    y = getattr(O, name)(x)
+    assert bits_equal(y, g[f"act_{name}"])
+    assert bits_equal(O.activation_grad(name, gy, x, y), g[f"act_{name}_grad"])
+
+
+@pytest.mark.parametrize("name,ctor", [
+    ("rmsprop", lambda: O.RMSprop(lr=0.01)),
+    ("rmsprop_wd", lambda: O.RMSprop(lr=3e-3, rho=0.9, eps=1e-6, weight_decay=0.05)),
+])
+def test_rmsprop_sequences_bit_exact(name, ctor):
+    g = load("next_rows.npz")
+    opt = ctor()
+    th = g["opt_theta0"]
+    for k in range(4):
+        th = opt.step("p", th, g["opt_grads"][k])
+        assert bits_equal(th, g[f"opt_{name}"][k]), (name, k)
+
+
+def test_demo_logs_have_the_reference_format():
+    """The demos' `epoch,loss[,acc]` log contract (demos.py:59, 116)."""
+    g = load("next_rows.npz")
+    xor, blobs = list(g["xor_lines"]), list(g["blobs_lines"])
+    assert len(xor) == 301 and xor[0].startswith("0,") and xor[-1].startswith("final,")
+    assert all(len(l.split(",")) == 3 for l in blobs)
+    assert blobs[-1].startswith("final,")
