@@ -63,3 +63,28 @@ def test_demo_training_logs_match_reference(key, run):
     assert normwise(got[:, 0], want[:, 0]) <= 1e-4
     if want.shape[1] > 1:
         assert np.max(np.abs(got[:, 1] - want[:, 1])) <= 1.0 / 200 + 1e-12
+
+
+def test_gradcheck_suite_on_device():
+    """the reference's finite-difference suite
+    (gradcheck.py:317-344) over the device ops; both sides run on the B200."""
+    from paper_2602_00125_b200 import gradcheck
+
+    ok, text = gradcheck.run_suite(seeds=(0, 1, 2))
+    assert ok, text
+    assert text.splitlines()[-1] == "OVERALL PASS"
+    assert text.count("== ") == len(gradcheck.STANDARD_CHECKS)
+
+
+def test_gradcheck_catches_a_wrong_pullback():
+    from paper_2602_00125_b200 import gradcheck
+    from paper_2602_00125_b200.autograd import record
+
+    def bad_square(x):  # value x*x, pullback claims 3x
+        out = P.mul(x, x).detach()
+        return record("bad_square", (x,), out, (lambda g: P.mul(g, P.mul(x, 3.0)),))
+
+    x = P.uniform((3, 4), -1, 1, rng=0, requires_grad=True)
+    c = P.uniform((3, 4), -1, 1, rng=1)
+    rep = gradcheck.check_function(lambda: P.sum(P.mul(bad_square(x), c)), {"x": x})
+    assert not rep.passed
