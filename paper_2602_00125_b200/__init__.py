@@ -13,7 +13,7 @@ from . import nn, optim
 from .autograd import (GradStore, backward, is_recording, no_grad, record, reset_tape, tape,
                        zero_grad)
 from .core import (Buffer, Tensor, abs_, absolute, add, broadcast_shapes, broadcast_to, clamp, div,
-                   exp, from_buffer, from_flat, from_numpy, full, fused_muladd_relu, gelu, linear,
+                   exp, from_buffer, from_dlpack, from_flat, from_numpy, full, fused_muladd_relu, gelu, linear,
                    log, matmul, max, mean, mm, mul, muladd_relu_sum_grads, neg, ones, ones_like,
                    reduce_to_shape, relu, reshape, set_gemm_algo, sigmoid, softmax, sqrt, sub, sum,
                    tanh, tensor, transpose2d, uniform, zeros, zeros_like)
@@ -22,7 +22,8 @@ from .errors import BroadcastError, DeterminismError, GradError, ShapeError
 __version__ = "0.1.0"
 
 __all__ = [
-    "Tensor", "Buffer", "tensor", "from_flat", "from_buffer", "from_numpy", "zeros", "ones",
+    "Tensor", "Buffer", "tensor", "from_flat", "from_buffer", "from_numpy", "from_dlpack", "zeros",
+    "ones",
     "full", "uniform", "zeros_like", "ones_like",
     "add", "sub", "mul", "div", "neg", "exp", "log", "sqrt", "absolute", "abs_", "relu", "clamp",
     "sigmoid", "tanh", "gelu",

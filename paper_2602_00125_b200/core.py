@@ -63,6 +63,32 @@ class Buffer:
         self.ptr = 0
 
 
+class ExternalBuffer(Buffer):
+    """Device memory owned by another framework (a DLPack import): never
+    returned to the engine's allocator; the producer's deleter runs when the
+    last engine view dies."""
+
+    __slots__ = ("_owner",)
+
+    def __init__(self, ptr: int, nbytes: int, owner=None):
+        self.ptr = ptr
+        self.nbytes = int(nbytes)
+        self.version = 0
+        self._splits = None
+        self._owner = owner
+
+    def __del__(self):
+        try:
+            if self._owner is not None:
+                from . import dlpack
+
+                dlpack.release(self._owner)
+        except Exception:
+            pass
+        self._owner = None
+        self.ptr = 0
+
+
 def _contig_strides(shape):
     st = [0] * len(shape)
     acc = 1
@@ -192,6 +218,17 @@ class Tensor:
     def detach(self) -> "Tensor":
         return Tensor(self.buffer, self.shape, self.strides, self.offset)
 
+    # -- DLPack (zero-copy device exchange, dlpack.py)
+    def __dlpack__(self, stream=None):
+        from . import dlpack
+
+        return dlpack.to_capsule(self, stream)
+
+    def __dlpack_device__(self):
+        from . import dlpack
+
+        return (dlpack.kDLCUDA, dlpack.device_id())
+
     def copy(self) -> "Tensor":
         return _copy_contig(self)
 
@@ -211,6 +248,16 @@ def _copy_contig(t: Tensor) -> Tensor:
 
 # ---------------------------------------------------------------------------
 # constructors (core.py:254-357)
+
+
+def from_dlpack(obj, requires_grad=False) -> Tensor:
+    """Wrap a CUDA float32 tensor from any DLPack producer (torch, CuPy, ...)
+    without a copy; the engine's ops read and write its memory in place."""
+    from . import dlpack
+
+    t = dlpack.from_dlpack(obj)
+    t.requires_grad = requires_grad
+    return t
 
 
 def from_numpy(arr, requires_grad=False) -> Tensor:

@@ -88,3 +88,48 @@ def test_gradcheck_catches_a_wrong_pullback():
     c = P.uniform((3, 4), -1, 1, rng=1)
     rep = gradcheck.check_function(lambda: P.sum(P.mul(bad_square(x), c)), {"x": x})
     assert not rep.passed
+
+
+def test_dlpack_zero_copy_exchange_with_torch():
+    """device-side zero-copy exchange (the HBM analogue of
+    the reference's aliasing wrap_host_array / to_host_array)."""
+    torch = pytest.importorskip("torch")
+    base = np.arange(12, dtype=np.float32).reshape(3, 4)
+    x = P.from_numpy(base)
+    tx = torch.from_dlpack(x)
+    assert tx.device.type == "cuda" and tuple(tx.shape) == (3, 4)
+    assert tx.data_ptr() == x.data_ptr
+    assert bits_equal(tx.cpu().numpy(), base)
+    tx.mul_(2.0)  # torch writes, the engine sees them
+    torch.cuda.synchronize()
+    assert bits_equal(x.numpy(), 2 * base)
+    tv = torch.from_dlpack(P.transpose2d(x))  # strided view: no copy, strides kept
+    assert tuple(tv.stride()) == (1, 4) and bits_equal(tv.cpu().numpy(), 2 * base.T)
+
+    t = torch.randn(64, 48, device="cuda")
+    e = P.from_dlpack(t)  # engine ops on torch's memory
+    assert e.data_ptr == t.data_ptr() and e.shape == (64, 48)
+    from oracle import tensorlite_np as O
+
+    host = t.cpu().numpy()
+    assert bits_equal(P.sum(e, axis=0).numpy(), O.axis_sum(host, 0))
+    assert bits_equal(P.exp(P.transpose2d(e)).numpy(), O.exp(host.T))
+    e.fill_(1.0)  # engine writes, torch sees them
+    L_sync = P.ones((1,)).numpy()  # noqa: F841 (orders the engine stream)
+    assert float(t.sum().item()) == 64 * 48
+    del e
+    import gc
+
+    gc.collect()
+    assert float(t.sum().item()) == 64 * 48  # torch's storage outlives the engine view
+
+
+def test_tlnp_dlpack_roundtrip():
+    torch = pytest.importorskip("torch")
+    from paper_2602_00125_b200 import tlnp
+
+    t = torch.arange(6, dtype=torch.float32, device="cuda").reshape(2, 3)
+    h = tlnp.from_dlpack(t)
+    y = (h * 2.0).relu()
+    back = torch.from_dlpack(y)
+    assert torch.equal(back, t * 2.0)
