@@ -9,7 +9,12 @@
 // axis to keep shared-memory reads conflict-free), register double buffering.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
+
+extern "C" int b2_alloc(size_t, void*, void**);
+extern "C" int b2_free(void*, void*);
 
 namespace {
 
@@ -104,6 +109,107 @@ __global__ void __launch_bounds__(256) k_gemm_simt(int64_t M, int64_t N, int64_t
   }
 }
 
+// ---------------------------------------------------------------- small / skinny GEMMs
+// Latency path for problems whose 128x128 tiling leaves most SMs idle (BASELINE
+// config 1: 256x256x784, 256x10x256, ...): 64x64x16 tiles, 4x4 outputs per
+// thread, and the K loop split over S CTAs (grid.z). S > 1 writes fp32 partials
+// [S][M][N] that k_splitk_reduce sums in fixed order s = 0..S-1 (deterministic)
+// before the bias/ReLU epilogue.
+constexpr int SBM = 64, SBN = 64, SBK = 16;
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) k_gemm_small(int64_t M, int64_t N, int64_t K, int64_t kslice,
+                                                    const float* __restrict__ A, int64_t lda,
+                                                    const float* __restrict__ B, int64_t ldb,
+                                                    float* __restrict__ C, int64_t ldc,
+                                                    const float* __restrict__ bias, int epi,
+                                                    float* __restrict__ part) {
+  __shared__ __align__(16) float As[2][SBK][SBM];
+  __shared__ __align__(16) float Bs[2][SBK][SBN];
+  const int t = threadIdx.x, tx = t % 16, ty = t / 16;
+  const int64_t m0 = blockIdx.y * (int64_t)SBM, n0 = blockIdx.x * (int64_t)SBN;
+  const int64_t kb = blockIdx.z * kslice, ke = min(K, kb + kslice);
+  float acc[4][4] = {};
+  float ra[4], rb[4];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int64_t m, k;
+      if (!TA) { m = m0 + t / 4; k = k0 + (t % 4) * 4 + i; }
+      else     { k = k0 + t / 16; m = m0 + (t % 16) * 4 + i; }
+      ra[i] = (m < M && k < ke) ? (TA ? A[k * lda + m] : A[m * lda + k]) : 0.0f;
+      int64_t n, kk;
+      if (TB) { n = n0 + t / 4; kk = k0 + (t % 4) * 4 + i; }
+      else    { kk = k0 + t / 16; n = n0 + (t % 16) * 4 + i; }
+      rb[i] = (n < N && kk < ke) ? (TB ? B[n * ldb + kk] : B[kk * ldb + n]) : 0.0f;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (!TA) As[buf][(t % 4) * 4 + i][t / 4] = ra[i];
+      else     As[buf][t / 16][(t % 16) * 4 + i] = ra[i];
+      if (TB)  Bs[buf][(t % 4) * 4 + i][t / 4] = rb[i];
+      else     Bs[buf][t / 16][(t % 16) * 4 + i] = rb[i];
+    }
+  };
+  const int nk = (int)((ke - kb + SBK - 1) / SBK);
+  if (nk > 0) {
+    load(kb);
+    store(0);
+  }
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    const int cur = kt & 1;
+    if (kt + 1 < nk) load(kb + (int64_t)(kt + 1) * SBK);
+#pragma unroll
+    for (int k = 0; k < SBK; ++k) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[cur][k][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[cur][k][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    if (kt + 1 < nk) {
+      store(cur ^ 1);
+      __syncthreads();
+    }
+  }
+  const bool split = gridDim.z > 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      float v = acc[i][j];
+      if (split) {
+        part[(blockIdx.z * M + m) * N + n] = v;
+        continue;
+      }
+      if (epi == B2_EPI_BIAS || epi == B2_EPI_BIAS_RELU) v = __fadd_rn(v, bias[n]);
+      if (epi == B2_EPI_BIAS_RELU || epi == B2_EPI_RELU) v = v > 0.0f ? v : 0.0f;
+      C[m * ldc + n] = v;
+    }
+  }
+}
+
+__global__ void k_splitk_reduce(float* __restrict__ C, int64_t ldc, const float* __restrict__ part,
+                                int64_t M, int64_t N, int S, const float* __restrict__ bias, int epi) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= M * N) return;
+  const int64_t m = i / N, n = i - m * N;
+  float v = 0.0f;
+  for (int s = 0; s < S; ++s) v = __fadd_rn(v, part[s * M * N + i]);  // fixed order
+  if (epi == B2_EPI_BIAS || epi == B2_EPI_BIAS_RELU) v = __fadd_rn(v, bias[n]);
+  if (epi == B2_EPI_BIAS_RELU || epi == B2_EPI_RELU) v = v > 0.0f ? v : 0.0f;
+  C[m * ldc + n] = v;
+}
+
 __global__ void k_fill_bias(float* C, int64_t M, int64_t N, int64_t ldc, const float* bias, int epi) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= M * N) return;
@@ -125,6 +231,34 @@ int gemm_simt(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, i
   if (K == 0) {  // empty inner dimension: zeros (core.py matmul of (m,0)x(d,0))
     k_fill_bias<<<(unsigned)((M * N + 255) / 256), 256, 0, st>>>(C, M, N, ldc, bias, epi);
     return launched("b2_gemm(empty-K)");
+  }
+  const int64_t big_tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
+  if (big_tiles < sm_count() / 2) {
+    // latency path: 64x64 tiles, K split so the grid covers ~2 CTAs per SM
+    const int64_t tiles = ((N + SBN - 1) / SBN) * ((M + SBM - 1) / SBM);
+    int64_t S = std::max<int64_t>(1, std::min<int64_t>((2 * sm_count()) / tiles, K / (4 * SBK)));
+    S = std::min<int64_t>(S, 32);
+    int64_t kslice = (K + S - 1) / S;
+    kslice = (kslice + SBK - 1) / SBK * SBK;
+    S = (K + kslice - 1) / kslice;
+    dim3 g((unsigned)((N + SBN - 1) / SBN), (unsigned)((M + SBM - 1) / SBM), (unsigned)S);
+    void* ws = nullptr;
+    if (S > 1) B2_TRY(b2_alloc((size_t)S * M * N * sizeof(float), st, &ws));
+    float* part = (float*)ws;
+#define B2_SMALL(TA_, TB_) \
+  k_gemm_small<TA_, TB_><<<g, 256, 0, st>>>(M, N, K, kslice, A, lda, B, ldb, C, ldc, bias, epi, part)
+    if (!ta && !tb) B2_SMALL(false, false);
+    else if (!ta && tb) B2_SMALL(false, true);
+    else if (ta && !tb) B2_SMALL(true, false);
+    else B2_SMALL(true, true);
+#undef B2_SMALL
+    int rc = launched("b2_gemm(simt-small)");
+    if (!rc && S > 1) {
+      k_splitk_reduce<<<(unsigned)((M * N + 255) / 256), 256, 0, st>>>(C, ldc, part, M, N, (int)S, bias, epi);
+      rc = launched("b2_gemm(splitk-reduce)");
+    }
+    if (ws) b2_free(ws, st);
+    return rc;
   }
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
   if (grid.y > 65535) return fail("b2_gemm(simt): M too large for the SIMT grid");

@@ -10,17 +10,20 @@
 // search over the per-tensor chunk prefix.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace {
 
 constexpr int kMaxT = 48;
-constexpr int kChunk = 8192;  // elements per CTA
+constexpr int kChunk = 8192;  // max elements per CTA (small steps use less: more CTAs)
 constexpr int kThreads = 256;
 
 struct Table {
   b2_opt_tensor t[kMaxT];
   int64_t prefix[kMaxT + 1];  // chunk prefix sums
+  int64_t chunk;              // elements per CTA
   int count;
 };
 
@@ -37,8 +40,8 @@ __global__ void __launch_bounds__(kThreads) k_sgd(const __grid_constant__ Table 
                                                   double mu, double wd) {
   int ti = find_tensor(tb, blockIdx.x);
   const b2_opt_tensor& T = tb.t[ti];
-  int64_t base = (blockIdx.x - tb.prefix[ti]) * (int64_t)kChunk;
-  int64_t end = min(T.n, base + kChunk);
+  int64_t base = (blockIdx.x - tb.prefix[ti]) * tb.chunk;
+  int64_t end = min(T.n, base + tb.chunk);
   for (int64_t i = base + threadIdx.x; i < end; i += kThreads) {
     double th = (double)T.param[i];
     double g = (double)T.grad[i];
@@ -54,8 +57,8 @@ __global__ void __launch_bounds__(kThreads) k_adam(const __grid_constant__ Table
                                                    double eps, double wd) {
   int ti = find_tensor(tb, blockIdx.x);
   const b2_opt_tensor& T = tb.t[ti];
-  int64_t base = (blockIdx.x - tb.prefix[ti]) * (int64_t)kChunk;
-  int64_t end = min(T.n, base + kChunk);
+  int64_t base = (blockIdx.x - tb.prefix[ti]) * tb.chunk;
+  int64_t end = min(T.n, base + tb.chunk);
   double bc1 = T.bc1, bc2 = T.bc2;
   for (int64_t i = base + threadIdx.x; i < end; i += kThreads) {
     double th = (double)T.param[i];
@@ -77,8 +80,8 @@ __global__ void __launch_bounds__(kThreads) k_rmsprop(const __grid_constant__ Ta
                                                       double wd) {
   int ti = find_tensor(tb, blockIdx.x);
   const b2_opt_tensor& T = tb.t[ti];
-  int64_t base = (blockIdx.x - tb.prefix[ti]) * (int64_t)kChunk;
-  int64_t end = min(T.n, base + kChunk);
+  int64_t base = (blockIdx.x - tb.prefix[ti]) * tb.chunk;
+  int64_t end = min(T.n, base + tb.chunk);
   for (int64_t i = base + threadIdx.x; i < end; i += kThreads) {
     double th = (double)T.param[i];
     double g = (double)T.grad[i];
@@ -97,12 +100,17 @@ int run_multi(const b2_opt_tensor* ts, int count, Launch launch) {
   for (int off = 0; off < count; off += kMaxT) {
     Table tb;
     int k = 0;
-    int64_t chunks = 0;
+    int64_t chunks = 0, total = 0;
+    for (int i = off; i < count && i < off + kMaxT; ++i) total += ts[i].n > 0 ? ts[i].n : 0;
+    // about 4 CTAs per SM for small steps (config 1: 203K params), 8K elements each for large
+    int64_t chunk = total / (4 * (int64_t)b2::sm_count());
+    chunk = std::max<int64_t>(1024, std::min<int64_t>(kChunk, (chunk + 255) / 256 * 256));
+    tb.chunk = chunk;
     for (int i = off; i < count && k < kMaxT; ++i) {
       if (ts[i].n <= 0) continue;
       tb.t[k] = ts[i];
       tb.prefix[k] = chunks;
-      chunks += (ts[i].n + kChunk - 1) / kChunk;
+      chunks += (ts[i].n + chunk - 1) / chunk;
       ++k;
     }
     if (k == 0) continue;

@@ -377,6 +377,27 @@ def test_config5_small_bf16_variant_adam_losses():
     assert normwise(losses, golden["loss"]) <= 2e-2
 
 
+@pytest.mark.parametrize("ta,tb", [(0, 1), (0, 0), (1, 0), (1, 1)])
+@pytest.mark.parametrize("shape", [(2048, 1056, 72), (256, 256, 784), (256, 10, 256), (10, 784, 256),
+                                   (3, 5, 1000), (70, 130, 17)])
+def test_gemm_simt_paths(ta, tb, shape):
+    """FP32 FFMA paths: the 128x128 tile kernel (many tiles) and the
+    64x64 split-K latency kernel (config-1 shapes, ragged, K split 1..32)."""
+    from paper_2602_00125_b200 import _lib as L
+
+    M, N, K = shape
+    rng = np.random.default_rng(M * 7 + N + K + ta + 2 * tb)
+    A = rng.uniform(-1, 1, (K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.uniform(-1, 1, (N, K) if tb else (K, N)).astype(np.float32)
+    bias = rng.uniform(-1, 1, N).astype(np.float32)
+    ref = np.maximum(_ref_gemm(A, B, ta, tb) + bias.astype(np.float64), 0)
+    At, Bt, bt = dev(A), dev(B), dev(bias)  # keep the operands alive across the call
+    C = P.zeros((M, N))
+    L.call("b2_gemm", ta, tb, M, N, K, At.data_ptr, A.shape[1], Bt.data_ptr, B.shape[1],
+           C.data_ptr, N, bt.data_ptr, L.EPI_BIAS_RELU, L.GEMM_SIMT, None)
+    assert normwise(host(C), ref) <= 5e-6, (ta, tb, shape)
+
+
 def test_gemm_accuracy_long_k():
     """K-chunk promotion keeps 3xTF32 at sgemm accuracy for the config-3 K."""
     from paper_2602_00125_b200 import _lib as L
