@@ -31,11 +31,15 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "common.cuh"
+
+extern "C" int b2_alloc(size_t, void*, void**);
+extern "C" int b2_free(void*, void*);
 
 namespace {
 
@@ -213,7 +217,21 @@ struct TcParams {
   __nv_bfloat16* s_lo;      // ... and bf16(C - trunc_tf32(C)), both [M, N] contiguous
   int kc;                   // k-blocks per fp32 promotion chunk
   int group_n;              // raster group width in tile-columns
+  int splits;               // split-K slices (1: none); slice s covers k-blocks [s*kbps, (s+1)*kbps)
+  int kbps;                 // k-blocks per slice
+  int64_t split_stride;     // elements between the partial C slices (M*N) when splits > 1
 };
+
+// tile t -> (slice, output tile, k-block range); slices are the slowest index
+__device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& tm, int& tn);
+__device__ __forceinline__ void tile_info(const TcParams& p, int t, int nkb, int& tm, int& tn,
+                                          int& kb0, int& kb1, int& ks) {
+  const int per = p.tiles_m * p.tiles_n;
+  ks = t / per;
+  tile_coords(p, t - ks * per, tm, tn);
+  kb0 = ks * p.kbps;
+  kb1 = min(nkb, kb0 + p.kbps);
+}
 
 // Grouped raster: tiles walk M inside groups of kGroupN tile-columns, so the
 // ~74-148 tiles resident at once cover a ~9 x 8 block of the output and the
@@ -400,11 +418,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cl_id; tile < p.num_tiles; tile += cl_num) {
-        int tm, tn;
-        tile_coords(p, tile, tm, tn);
+        int tm, tn, kb0, kb1, ks;
+        tile_info(p, tile, nkb, tm, tn, kb0, kb1, ks);
         const int m0 = tm * (BM * CG) + (int)rank * BM;
         const int n0 = tn * BN + (int)rank * CF::BNL;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * CF::STAGE_BYTES;
           uint64_t* fb = &full[stage];
@@ -451,8 +469,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int chunk = 0;
       uint32_t d_tmem = tmem_base;
       for (int tile = cl_id; tile < p.num_tiles; tile += cl_num) {
-        for (int kb = 0; kb < nkb; ++kb) {
-          const int kc = kb % KC;
+        int tm, tn, kb0, kb1, ks_;
+        tile_info(p, tile, nkb, tm, tn, kb0, kb1, ks_);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const int kc = (kb - kb0) % KC;
           if (kc == 0) {  // claim the next chunk accumulator (ping-pong)
             const int cb = chunk & 1;
             mbar_wait(&tempty[cb], ((chunk >> 1) & 1) ^ 1);
@@ -499,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             // smem slot free (in both CTAs) once these MMAs retire; chunk ready
-            const bool last = kc == KC - 1 || kb == nkb - 1;
+            const bool last = kc == KC - 1 || kb == kb1 - 1;
             if (CG == 1) {
               tc_commit(&empty[stage]);
               if (last) tc_commit(&tfull[chunk & 1]);
@@ -509,7 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           __syncwarp();
-          if (kc == KC - 1 || kb == nkb - 1) ++chunk;
+          if (kc == KC - 1 || kb == kb1 - 1) ++chunk;
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -525,12 +545,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int cg = (warp - 4) >> 2;
     const int row = q * 32 + lane;
-    const int nch = (nkb + KC - 1) / KC;
     const bool vec_ok = (p.ldc % 4) == 0 && (((uintptr_t)p.C) & 15) == 0;
     int chunk = 0;
     for (int tile = cl_id; tile < p.num_tiles; tile += cl_num) {
-      int tm, tn;
-      tile_coords(p, tile, tm, tn);
+      int tm, tn, kb0, kb1, ks;
+      tile_info(p, tile, nkb, tm, tn, kb0, kb1, ks);
+      const int nch = (kb1 - kb0 + KC - 1) / KC;
+      float* const Cs = p.C + (int64_t)ks * p.split_stride;  // this slice's partial (or C)
       const int m0 = tm * (BM * CG) + (int)rank * BM;
       const int n0 = tn * BN;
       float acc[64];
@@ -560,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int64_t m = m0 + row;
       if (m < p.M) {
-        float* crow = p.C + m * p.ldc;
+        float* crow = Cs + m * p.ldc;
         const int nb = n0 + cg * 64;
 #pragma unroll
         for (int j = 0; j < 64; ++j) {
@@ -734,6 +755,33 @@ __global__ void k_bf16_cast(__nv_bfloat16* __restrict__ out, const float* __rest
   }
 }
 
+// Split-K second stage: C = epilogue(sum_s part[s]) in fixed slice order
+// (deterministic), with the same epilogue stages as the GEMM kernel: bias,
+// ReLU, the ReLU-pullback mask, and emission of C's operand split (EMIT = the
+// GEMM mode: 2 TF32X split, 5 3xBF16 split, 4 bf16 cast, 0 none).
+template <int EMIT>
+__global__ void __launch_bounds__(256) k_splitk_epilogue(float* __restrict__ C, int64_t ldc,
+                                                         const float* __restrict__ part, int M, int N,
+                                                         int S, const float* __restrict__ bias, int epi,
+                                                         const float* __restrict__ mask,
+                                                         __nv_bfloat16* __restrict__ s_hi,
+                                                         __nv_bfloat16* __restrict__ s_lo) {
+  const int64_t total = (int64_t)M * N;
+  const int64_t MN = total;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / N, n = i - m * N;
+    float x = 0.0f;
+    for (int sl = 0; sl < S; ++sl) x = __fadd_rn(x, part[sl * MN + i]);
+    if (epi == B2_EPI_BIAS || epi == B2_EPI_BIAS_RELU) x = __fadd_rn(x, bias[n]);
+    if (epi == B2_EPI_BIAS_RELU || epi == B2_EPI_RELU) x = x > 0.0f ? x : 0.0f;
+    if (mask) x = __fmul_rn(x, mask[m * ldc + n] > 0.0f ? 1.0f : 0.0f);
+    C[m * ldc + n] = x;
+    if (EMIT == 4 && s_hi) s_hi[i] = __float2bfloat16_rn(x);
+    if ((EMIT == 2 || EMIT == 5) && s_hi) split_pair<EMIT>(x, s_hi[i], s_lo[i]);
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -831,7 +879,7 @@ int launch_tc(const Operands& o, TcParams p, cudaStream_t st) {
   }
   p.tiles_n = (p.N + BN - 1) / BN;
   p.tiles_m = (p.M + BM * CG - 1) / (BM * CG);
-  p.num_tiles = p.tiles_m * p.tiles_n;
+  p.num_tiles = p.tiles_m * p.tiles_n * p.splits;
   auto kern = k_gemm_tc<A_MN, B_MN, MODE, CG>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -911,6 +959,15 @@ bool tc_supported(int ta, int tb, int64_t M, int64_t N, int64_t K, int64_t lda, 
   return true;
 }
 
+static int splitk_enabled() {
+  static int v = -1;  // B2_GEMM_SPLITK=0 disables split-K (A/B measurements)
+  if (v < 0) {
+    const char* e = getenv("B2_GEMM_SPLITK");
+    v = !(e && e[0] == '0');
+  }
+  return v;
+}
+
 static int cg_mode() {
   static int v = -1;
   if (v < 0) {
@@ -945,12 +1002,40 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   if (mode == 4) p.s_lo = nullptr;  // BF16 mode emits a single bf16 cast
   Operands o{{a0, a1, a2}, {b0, b1, b2_}, lda, ldb};
   const bool a_mn = ta != 0, b_mn = tb == 0;
+  const int sms = sm_count();
   // CTA pairs once there are enough 256-row tiles to fill the chip
   int cg = cg_mode();
   if (cg != 1 && cg != 2) {
     int64_t pair_tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
-    cg = pair_tiles >= sm_count() / 2 ? 2 : 1;
+    cg = pair_tiles >= sms / 2 ? 2 : 1;
   }
+  // split-K when the output tiles leave most SMs idle and K is long enough
+  // (dW GEMMs: [1024 x 1024] over K = 32768; square n = 1024): slices of >= 8
+  // k-blocks, fp32 partials, a fixed-order second stage with the fused epilogue
+  const int nkb = (int)((K + BK - 1) / BK);
+  const int64_t tiles = ((M + (int64_t)BM * cg - 1) / ((int64_t)BM * cg)) * ((N + BN - 1) / BN);
+  int S = 1;
+  if (tiles * cg <= sms / 2 && nkb >= 16 && splitk_enabled())  // slices of >= 8 k-blocks (K 256)
+    S = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms / (tiles * cg), nkb / 8, 16}));
+  p.splits = 1;
+  p.kbps = nkb;
+  p.split_stride = 0;
+  void* part = nullptr;
+  if (S > 1) {
+    p.kbps = (nkb + S - 1) / S;
+    S = (nkb + p.kbps - 1) / p.kbps;
+  }
+  if (S > 1) {
+    B2_TRY(b2_alloc((size_t)S * M * N * sizeof(float), st, &part));
+    p.splits = S;
+    p.split_stride = M * N;
+    p.C = (float*)part;
+    p.ldc = N;
+    p.epi = B2_EPI_NONE;
+    p.mask = nullptr;
+    p.s_hi = p.s_lo = nullptr;
+  }
+  auto run = [&]() -> int {
 #define B2_TC(AMN, BMN)                                                             \
   if (a_mn == AMN && b_mn == BMN) {                                                 \
     if (cg == 2) {                                                                  \
@@ -966,12 +1051,30 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
     if (mode == 2) return launch_tc<AMN, BMN, 2, 1>(o, p, st);                      \
     return launch_tc<AMN, BMN, 1, 1>(o, p, st);                                     \
   }
-  B2_TC(false, false)
-  B2_TC(false, true)
-  B2_TC(true, false)
-  B2_TC(true, true)
+    B2_TC(false, false)
+    B2_TC(false, true)
+    B2_TC(true, false)
+    B2_TC(true, true)
 #undef B2_TC
-  return fail("gemm_tc: unreachable");
+    return fail("gemm_tc: unreachable");
+  };
+  int rc = run();
+  if (!rc && S > 1) {
+    const int64_t total = M * N;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+    __nv_bfloat16* hi = (__nv_bfloat16*)s_hi;
+    __nv_bfloat16* lo = mode == 4 ? nullptr : (__nv_bfloat16*)s_lo;
+#define B2_SKE(E) \
+  k_splitk_epilogue<E><<<grid, 256, 0, st>>>(C, ldc, (const float*)part, (int)M, (int)N, S, bias, epi, mask, hi, lo)
+    if (!hi) B2_SKE(0);
+    else if (mode == 4) B2_SKE(4);
+    else if (mode == 5) B2_SKE(5);
+    else B2_SKE(2);
+#undef B2_SKE
+    rc = launched("b2_gemm(tcgen05 split-K epilogue)");
+  }
+  if (part) b2_free(part, st);
+  return rc;
 }
 
 }  // namespace b2

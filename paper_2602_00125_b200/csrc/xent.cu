@@ -189,6 +189,130 @@ __global__ void __launch_bounds__(256) k_softmax_bwd(float* __restrict__ gz,
   }
 }
 
+// Register-resident variants for rows of up to 128*NV floats (C % 4 == 0,
+// 16-B aligned rows): a warp loads its row once with NV 128-bit loads in
+// flight per lane, computes each exp ONCE, and writes with 128-bit stores.
+// Same arithmetic and rounding sequence as the looped kernels above.
+__device__ __forceinline__ float f4get(const float4& q, int k) {
+  return k == 0 ? q.x : k == 1 ? q.y : k == 2 ? q.z : q.w;
+}
+__device__ __forceinline__ void f4set(float4& q, int k, float v) {
+  if (k == 0) q.x = v; else if (k == 1) q.y = v; else if (k == 2) q.z = v; else q.w = v;
+}
+
+template <int NV>
+__device__ __forceinline__ float row_max_regs(const float4 (&v)[NV], int64_t C, int lane) {
+  float m = -INFINITY;
+  bool any = false;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t idx = (int64_t)(i * 32 + lane) * 4 + k;
+      const float x = f4get(v[i], k);
+      if (idx < C && !isnan(x)) {
+        m = any ? (x > m ? x : m) : x;
+        any = true;
+      }
+    }
+  m = warp_max_first(any ? m : -INFINITY);
+  const float v0 = __shfl_sync(0xffffffffu, v[0].x, 0);  // the first scanned slot
+  return isnan(v0) ? v0 : m;
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256) k_softmax_fwd_v(float* __restrict__ y, float* __restrict__ rs,
+                                                       float* __restrict__ rm,
+                                                       const float* __restrict__ z, int64_t B,
+                                                       int64_t C) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < B; r += nw) {
+    const float4* row = reinterpret_cast<const float4*>(z + r * C);
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      v[i] = q * 4 < C ? __ldg(row + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float m = row_max_regs<NV>(v, C, lane);
+    double acc = 0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float e = b2::exp_f32(__fsub_rn(f4get(v[i], k), m));  // exp(sub(z, m))
+        f4set(v[i], k, e);
+        if ((int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)e;
+      }
+    const float s = __double2float_rn(warp_sum(acc));  // sum(e, -1, keepdims)
+    float4* yr = reinterpret_cast<float4*>(y + r * C);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      if (q * 4 < C)
+        yr[q] = make_float4(__fdiv_rn(v[i].x, s), __fdiv_rn(v[i].y, s), __fdiv_rn(v[i].z, s),
+                            __fdiv_rn(v[i].w, s));  // div(e, s)
+    }
+    if (lane == 0) {
+      rs[r] = s;
+      rm[r] = m;
+    }
+  }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256) k_softmax_bwd_v(float* __restrict__ gz,
+                                                       const float* __restrict__ gy,
+                                                       const float* __restrict__ z,
+                                                       const float* __restrict__ rs,
+                                                       const float* __restrict__ rm, int64_t B,
+                                                       int64_t C) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < B; r += nw) {
+    const float4* zr = reinterpret_cast<const float4*>(z + r * C);
+    const float4* gr = reinterpret_cast<const float4*>(gy + r * C);
+    float4 ev[NV], gv[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      const bool in = q * 4 < C;
+      ev[i] = in ? __ldg(zr + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      gv[i] = in ? __ldg(gr + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float s = rs[r], m = rm[r];
+    const float ss = __fmul_rn(s, s);
+    double acc = 0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float e = b2::exp_f32(__fsub_rn(f4get(ev[i], k), m));
+        f4set(ev[i], k, e);
+        const float t = __fdiv_rn(__fmul_rn(f4get(gv[i], k), e), ss);  // div(mul(g, e), mul(s, s))
+        if ((int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)(-t);  // neg, then sum(axis=-1)
+      }
+    const float gs = __double2float_rn(warp_sum(acc));
+    float4* out = reinterpret_cast<float4*>(gz + r * C);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      if (q * 4 < C) {
+        float4 o;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float ge = __fdiv_rn(f4get(gv[i], k), s);  // div(g, s) -- stored first
+          f4set(o, k, __fmul_rn(__fadd_rn(ge, gs), f4get(ev[i], k)));  // GradStore add, exp pullback
+        }
+        out[q] = o;
+      }
+    }
+  }
+}
+
 int rows_grid(int64_t B) {
   int64_t warps = B;
   int64_t ctas = (warps + 7) / 8;
@@ -229,7 +353,19 @@ int b2_softmax_fwd(float* y, float* row_s, float* row_m, const float* z, int64_t
                    int64_t cols, void* stream) {
   if (rows <= 0 || cols <= 0) return 0;
   cudaStream_t st = b2::resolve(stream);
-  k_softmax_fwd<<<rows_grid(rows), 256, 0, st>>>(y, row_s, row_m, z, rows, cols);
+  const bool vec = cols % 4 == 0 && cols <= 2048 && ((uintptr_t)z & 15) == 0 && ((uintptr_t)y & 15) == 0;
+  if (vec) {
+    const int nv = (int)((cols + 127) / 128);
+#define B2_SMF(NV) k_softmax_fwd_v<NV><<<rows_grid(rows), 256, 0, st>>>(y, row_s, row_m, z, rows, cols)
+    if (nv <= 1) B2_SMF(1);
+    else if (nv <= 2) B2_SMF(2);
+    else if (nv <= 4) B2_SMF(4);
+    else if (nv <= 8) B2_SMF(8);
+    else B2_SMF(16);
+#undef B2_SMF
+  } else {
+    k_softmax_fwd<<<rows_grid(rows), 256, 0, st>>>(y, row_s, row_m, z, rows, cols);
+  }
   return b2::launched("b2_softmax_fwd");
 }
 
@@ -237,7 +373,20 @@ int b2_softmax_bwd(float* gz, const float* gy, const float* z, const float* row_
                    const float* row_m, int64_t rows, int64_t cols, void* stream) {
   if (rows <= 0 || cols <= 0) return 0;
   cudaStream_t st = b2::resolve(stream);
-  k_softmax_bwd<<<rows_grid(rows), 256, 0, st>>>(gz, gy, z, row_s, row_m, rows, cols);
+  const bool vec = cols % 4 == 0 && cols <= 2048 && ((uintptr_t)z & 15) == 0 &&
+                   ((uintptr_t)gy & 15) == 0 && ((uintptr_t)gz & 15) == 0;
+  if (vec) {
+    const int nv = (int)((cols + 127) / 128);
+#define B2_SMB(NV) k_softmax_bwd_v<NV><<<rows_grid(rows), 256, 0, st>>>(gz, gy, z, row_s, row_m, rows, cols)
+    if (nv <= 1) B2_SMB(1);
+    else if (nv <= 2) B2_SMB(2);
+    else if (nv <= 4) B2_SMB(4);
+    else if (nv <= 8) B2_SMB(8);
+    else B2_SMB(16);
+#undef B2_SMB
+  } else {
+    k_softmax_bwd<<<rows_grid(rows), 256, 0, st>>>(gz, gy, z, row_s, row_m, rows, cols);
+  }
   return b2::launched("b2_softmax_bwd");
 }
 

@@ -398,6 +398,55 @@ def test_gemm_simt_paths(ta, tb, shape):
     assert normwise(host(C), ref) <= 5e-6, (ta, tb, shape)
 
 
+@pytest.mark.parametrize("ta,tb", [(0, 1), (1, 0), (1, 1)])
+def test_gemm_split_k_few_tiles_long_k(ta, tb):
+    """Few output tiles and a long K (the dW GEMMs of configs 4/5) take the
+    split-K path: fp32 partial slices + a fixed-order second stage carrying
+    the fused epilogue. Every tensor-core scheme, against fp64."""
+    from paper_2602_00125_b200 import _lib as L
+
+    M, N, K = 256, 384, 16384
+    rng = np.random.default_rng(21 + ta + 2 * tb)
+    A = rng.uniform(-1, 1, (K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.uniform(-1, 1, (N, K) if tb else (K, N)).astype(np.float32)
+    bias = rng.uniform(-1, 1, N).astype(np.float32) * 8
+    ref = np.maximum(_ref_gemm(A, B, ta, tb) + bias.astype(np.float64), 0)
+    At, Bt, bt = dev(A), dev(B), dev(bias)
+    for algo, tol in ((L.GEMM_3XBF16, 1e-5), (L.GEMM_TF32X, 5e-6), (L.GEMM_3XTF32, 5e-6),
+                      (L.GEMM_1XTF32, 3e-3)):
+        C = P.zeros((M, N))
+        L.call("b2_gemm", ta, tb, M, N, K, At.data_ptr, A.shape[1], Bt.data_ptr, B.shape[1],
+               C.data_ptr, N, bt.data_ptr, L.EPI_BIAS_RELU, algo, None)
+        assert normwise(host(C), ref) <= tol, (algo, ta, tb)
+
+
+def test_gemm_split_k_fused_epilogue_mask_and_emission():
+    """Split-K second stage applies the ReLU-pullback mask and emits C's own
+    3xBF16 split exactly like the single-pass epilogue."""
+    from paper_2602_00125_b200 import _lib as L
+    from paper_2602_00125_b200.core import Buffer
+
+    M, N, K = 256, 256, 16384
+    rng = np.random.default_rng(5)
+    A = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    B = rng.uniform(-1, 1, (N, K)).astype(np.float32)
+    mask = (rng.uniform(-1, 1, (M, N)) > 0).astype(np.float32)
+    At, Bt, mt = dev(A), dev(B), dev(mask)
+    ah, al, bh, bl = (Buffer(2 * M * K), Buffer(2 * M * K), Buffer(2 * N * K), Buffer(2 * N * K))
+    L.call("b2_bf16x3_split", ah.ptr, al.ptr, At.data_ptr, M, K, K, None)
+    L.call("b2_bf16x3_split", bh.ptr, bl.ptr, Bt.data_ptr, N, K, K, None)
+    C = P.zeros((M, N))
+    ch, cl = Buffer(2 * M * N), Buffer(2 * M * N)
+    L.call("b2_gemm_3xbf16", 0, 1, M, N, K, ah.ptr, al.ptr, bh.ptr, bl.ptr, C.data_ptr, N, None,
+           L.EPI_NONE, mt.data_ptr, ch.ptr, cl.ptr, None)
+    got = host(C)
+    assert normwise(got, _ref_gemm(A, B, 0, 1) * mask) <= 1e-5
+    hi = _bf16_rn(got)
+    lo = _bf16_rn((got - hi).astype(np.float32))
+    assert bits_equal(_bf16_bits(ch.ptr, M * N).reshape(M, N), hi)
+    assert bits_equal(_bf16_bits(cl.ptr, M * N).reshape(M, N), lo)
+
+
 def test_gemm_accuracy_long_k():
     """K-chunk promotion keeps 3xTF32 at sgemm accuracy for the config-3 K."""
     from paper_2602_00125_b200 import _lib as L
@@ -455,10 +504,17 @@ def test_cross_entropy_label_validation():
         nn.cross_entropy(z, [0])
 
 
-def test_softmax_matches_composed_reference_bit_exact():
-    rng = np.random.default_rng(4)
-    z = (rng.standard_normal((33, 1024)) * 3).astype(np.float32)
-    gy = rng.standard_normal((33, 1024)).astype(np.float32)
+@pytest.mark.parametrize("cols", [1024, 1000, 2048, 64, 130, 3000])
+def test_softmax_matches_composed_reference_bit_exact(cols):
+    """Register-resident row kernels (cols % 4 == 0, <= 2048) and the looped
+    ones (other widths), incl. a NaN first slot and -inf entries."""
+    rng = np.random.default_rng(4 + cols)
+    z = (rng.standard_normal((33, cols)) * 3).astype(np.float32)
+    z[3, 0] = np.nan
+    z[5, 7] = np.nan
+    z[6, :] = -np.inf
+    z[6, 1] = 0.0
+    gy = rng.standard_normal((33, cols)).astype(np.float32)
     zt = dev(z, True)
     y = P.softmax(zt)
     yo, e, s = O.softmax_rows_composed(z)
