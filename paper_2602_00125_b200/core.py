@@ -675,9 +675,10 @@ def _reduce(op, x, axes, oshape, want_arg=False):
 
 
 def _sum_pullback(x, axes, kshape):
+    # the cotangent of a sum is g broadcast over the reduced axes: returned as
+    # a stride-0 view (no HBM write); consumers read it through their strides
     def pull(g):
-        g = reshape(g, kshape)
-        return _copy_contig(_expand_view(g, x.shape))
+        return _expand_view(reshape(g, kshape), x.shape)
 
     return pull
 
@@ -703,13 +704,15 @@ def mean(x, axis=None, keepdims=False) -> Tensor:
     fcount = _Scalar(float(count))
 
     def pull(g):
-        # div(expand(g), float(count)) in one pass (the expand copy is exact)
+        # div(expand(g), float(count)): every element of a broadcast row is the
+        # same f32(g / count), so divide the kept-shape cotangent once and
+        # return it as a stride-0 view (bit-identical, no full-size write)
         gk = reshape(g, kshape)
-        res = _empty(x.shape)
-        if res.size:
-            L.call("b2_binary_scalar", L.DIV, res.data_ptr, x.ndim, L.i64s(x.shape), gk.data_ptr,
-                   L.i64s(_expand_strides(gk, x.shape)), fcount.value, 0, None)
-        return res
+        q = _empty(kshape)
+        if q.size:
+            L.call("b2_binary_scalar", L.DIV, q.data_ptr, len(kshape), L.i64s(kshape), gk.data_ptr,
+                   L.i64s(gk.strides), fcount.value, 0, None)
+        return _expand_view(q, x.shape)
 
     return record("mean", (x,), out, (pull,))
 
