@@ -35,10 +35,13 @@ __device__ __forceinline__ double exp_fast(double x) {
   const double kInv = 0x1.71547652b82fep+6;      // 64 / ln 2
   const double kHi = 0x1.62e42fef00000p-7;       // ln2/64, 33 bits: n*kHi exact
   const double kLo = 0x1.473de6af278edp-40;
-  const double n = rint(x * kInv);
+  // round-to-integer by the 1.5*2^52 shift (n lands in the low mantissa bits):
+  // no FRND/F2I conversions, which issue at a fraction of the FMA rate
+  const double t_ = fma(x, kInv, 0x1.8p52);
+  const double n = t_ - 0x1.8p52;
+  const int ni = __double2loint(t_);
   double r = fma(-n, kHi, x);
   r = fma(-n, kLo, r);
-  const int ni = (int)n;
   const int j = ni & 63, m = (ni - j) >> 6;
   double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
   p = fma(r, p, 1.0 / 24.0);
@@ -55,17 +58,19 @@ __device__ __forceinline__ double exp_fast(double x) {
   return ldexp(y, m);                              // subnormal results (x < -708)
 }
 
-// f32(exp(double(x))) for a float x: the same table algorithm with the
-// range reduction index formed in fp32 (any rounding of n only moves r
-// within the polynomial's margin) and the 2^m scaling done on the exponent
-// bits. Out-of-range inputs short-circuit: the f32 result is inf above
+// f32(exp(double(x))) for a float x: the same table algorithm, the 2^m
+// scaling done on the exponent bits (one f64->f32 conversion at the end). Out-of-range inputs short-circuit: the f32 result is inf above
 // 88.8, +0 below -104.5 (exp < 2^-150), NaN propagates.
 __device__ __forceinline__ float exp_f32(float x) {
-  if (!(x < 88.8f)) return x != x ? x : INFINITY;
-  if (!(x > -104.5f)) return 0.0f;
-  const int ni = __float2int_rn(x * 92.33248261689366f);  // 64 / ln 2
-  const double n = (double)ni;
-  double r = fma(-n, 0x1.62e42fef00000p-7, (double)x);
+  // branch-free: evaluate on a clamped input, then select the special cases
+  // (inf above 88.8, +0 below -104.5, NaN propagates) -- no divergent
+  // control flow in the elementwise / softmax loops
+  const float xc = fminf(fmaxf(x, -104.5f), 88.8f);
+  const double xd = (double)xc;
+  const double t_ = fma(xd, 0x1.71547652b82fep+6, 0x1.8p52);  // 64/ln2; rint via the shift
+  const double n = t_ - 0x1.8p52;
+  const int ni = __double2loint(t_);
+  double r = fma(-n, 0x1.62e42fef00000p-7, xd);
   r = fma(-n, 0x1.473de6af278edp-40, r);
   const int j = ni & 63, m = (ni - j) >> 6;
   double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
@@ -76,7 +81,10 @@ __device__ __forceinline__ float exp_f32(float x) {
   p = p * r;
   const double t = __ldg(&kExp2Tab[j]);
   const double y = fma(t, p, t);  // in [1, 2): adding m to the exponent is exact, m in [-151, 128]
-  return __double2float_rn(__longlong_as_double(__double_as_longlong(y) + ((long long)m << 52)));
+  float v = __double2float_rn(__longlong_as_double(__double_as_longlong(y) + ((long long)m << 52)));
+  v = x < 88.8f ? v : INFINITY;
+  v = x > -104.5f ? v : 0.0f;
+  return x == x ? v : x;
 }
 
 }  // namespace b2

@@ -547,17 +547,22 @@ int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_
             double count, cudaStream_t st) {
   const int sms = b2::sm_count();
   const int V = (I % 4 == 0 && ((uintptr_t)x & 15) == 0) ? 4 : 1;
-  // (measured: 128 column lanes -- 2 KB contiguous per row and CTA -- is
-  // slower than 16 on B200: more splits, more partial traffic)
-  const int CL = V == 4 ? 16 : 32, RL = 256 / CL;
-  const void* kern = V == 4 ? (const void*)k_strip<OP, 4, 16> : (const void*)k_strip<OP, 1, 32>;
+  // Column lanes and split policy (measured on 4096x4096, scripts/red_bench.py):
+  // sums use 8 column lanes x 4 columns (128 B per row segment) and split rows
+  // to fill one wave; max uses 4 x 4 (64 B segments, 4x more strips) and does
+  // not split once the strips alone cover the SMs -- its 16-B (value, index)
+  // partials and second stage cost more than the narrower segments.
+  const int CL = V == 4 ? (OP == B2_RED_MAX ? 4 : 8) : 32, RL = 256 / CL;
+  const bool single = OP == B2_RED_MAX;
+  const void* kern = V == 4 ? (CL == 4 ? (const void*)k_strip<OP, 4, 4> : (const void*)k_strip<OP, 4, 8>)
+                            : (const void*)k_strip<OP, 1, 32>;
   const int64_t strips = (I + CL * V - 1) / (CL * V);
   const int64_t ctas = strips * O1;
   int64_t S = 1;
   // splits: as many as ONE resident wave holds (a partial second wave would
   // double the tail), but at least 8 row-lane passes per CTA
   const int64_t cap = (int64_t)sms * resident<OP>(kern);
-  if (ctas < cap) {
+  if (ctas < cap && !(single && ctas >= sms)) {
     S = std::min<int64_t>(cap / ctas, R / (RL * 8));
     S = std::max<int64_t>(S, 1);
   }
@@ -575,8 +580,10 @@ int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_
     pmax = (MaxAcc*)ws;
   }
   dim3 grid((unsigned)(strips * O1), (unsigned)S);
-  if (V == 4)
-    k_strip<OP, 4, 16><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, strips);
+  if (V == 4 && CL == 4)
+    k_strip<OP, 4, 4><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, strips);
+  else if (V == 4)
+    k_strip<OP, 4, 8><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, strips);
   else
     k_strip<OP, 1, 32><<<grid, 256, 0, st>>>(x, O1, R, I, Rs, out, argr, psum, pmax, count, strips);
   int rc = b2::launched("b2_reduce(mid)");
