@@ -451,6 +451,11 @@ __global__ void __launch_bounds__(kThreads) k_muladd_relu_fwd(float* __restrict_
   }
 }
 
+#ifndef B2_MULADD_CL
+#define B2_MULADD_CL 32
+#endif
+constexpr int kMuladdCL = B2_MULADD_CL;  // column lanes per CTA (x4 columns each)
+
 // backward of sum(relu(a*b + b)): ga = f32(mask*b); partial column sums of
 // mask*a (fp64) and mask counts per row-split.
 __global__ void __launch_bounds__(kThreads) k_muladd_relu_bwd(float* __restrict__ ga,
@@ -460,9 +465,9 @@ __global__ void __launch_bounds__(kThreads) k_muladd_relu_bwd(float* __restrict_
                                                               const float* __restrict__ b,
                                                               int64_t rows, int64_t cols,
                                                               int64_t rows_per_split) {
-  // grid: x = strip of 64 columns (16 column lanes x float4), y = row split;
-  // 16 row lanes per CTA (a warp touches 2 rows x 256 B), folded in smem
-  constexpr int CL = 16, RL = kThreads / CL;
+  // grid: x = strip of 4*CL columns (CL column lanes x float4), y = row split;
+  // 256/CL row lanes per CTA (a warp touches 32/CL rows x 16*CL B), folded in smem
+  constexpr int CL = kMuladdCL, RL = kThreads / CL;
   __shared__ double sh_s[kThreads * 4];
   __shared__ int sh_n[kThreads * 4];
   const int cl = threadIdx.x % CL, rl = threadIdx.x / CL;
@@ -687,7 +692,7 @@ int b2_fused_muladd_relu_bwd(float* ga, float* gb, const float* a, const float* 
   if (cols % 4 || !aligned16(a) || !aligned16(b) || !aligned16(ga))
     return b2::fail("b2_fused_muladd_relu_bwd: needs cols%4==0 and 16-B aligned rows");
   cudaStream_t st = b2::resolve(stream);
-  int64_t colblocks = (cols + 63) / 64;  // strips of 64 columns
+  int64_t colblocks = (cols + 4 * kMuladdCL - 1) / (4 * kMuladdCL);  // strips of 4*CL columns
   static int occ = 0;  // resident CTAs per SM: the splits fill exactly one wave
   if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_muladd_relu_bwd, kThreads, 0) !=
                    cudaSuccess || occ < 1))
