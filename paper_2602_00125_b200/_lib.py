@@ -14,7 +14,9 @@ from ctypes import (POINTER, Structure, c_char_p, c_double, c_float, c_int, c_in
                     c_size_t, c_uint32, c_uint64, c_void_p)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libb2.so")
+# B2_LIB_PATH: an alternative in-tree build of the same library (A/B kernel
+# experiments); the product path is always libb2.so next to this file
+LIB_PATH = os.environ.get("B2_LIB_PATH") or os.path.join(HERE, "libb2.so")
 
 i64p = POINTER(c_int64)
 
