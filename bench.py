@@ -364,6 +364,17 @@ def op_benchmarks():
     out["config1_graph_us_per_step"] = ms * 1000
     out["config1_graph_samples_per_s"] = 256 / (ms / 1000)
     P.reset_tape()
+    # roofline fractions: HBM-bound config-2 ops against the measured copy
+    # bandwidth; GEMM-bound configs against the 3xBF16 ceiling (bf16 sustained / 3)
+    peaks, _ = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6457.0)
+    tc = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1422.1)) / 3.0
+    frac = {k.replace("_gbs", "_frac_hbm"): v / hbm for k, v in out.items()
+            if k.startswith("config2_") and k.endswith("_gbs")}
+    for k in ("config3_n1024_fwdbwd_tflops", "config3_n4096_fwdbwd_tflops",
+              "config3_n8192_fwdbwd_tflops", "config4_gemm_tflops_effective"):
+        frac[k.replace("_tflops", "_frac_3xbf16_ceiling")] = out[k] / tc
+    out["roofline_fractions"] = frac
     return out
 
 
