@@ -999,6 +999,8 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   p.s_lo = (__nv_bfloat16*)s_lo;
   if ((s_hi == nullptr) != (s_lo == nullptr) && mode != 4)
     return fail("gemm_tc: split outputs come in pairs");
+  if (((uintptr_t)s_hi & 15) || ((uintptr_t)s_lo & 15) || ((uintptr_t)C & 3))
+    return fail("gemm_tc: C must be 4-B and the emitted split arrays 16-B aligned");
   if (mode == 4) p.s_lo = nullptr;  // BF16 mode emits a single bf16 cast
   Operands o{{a0, a1, a2}, {b0, b1, b2_}, lda, ldb};
   const bool a_mn = ta != 0, b_mn = tb == 0;

@@ -855,3 +855,28 @@ def test_nccl_gradient_path_single_rank_matches_plain_step():
         assert bits_equal(a, b)
     assert comm.max_scalar(3.5) == 3.5
     comm.barrier()
+
+
+def test_c_abi_rejects_bad_arguments_loudly():
+    """The boundary validates before launching: misaligned split outputs, a
+    bias epilogue without a bias, bad enums -- non-zero status + message."""
+    import ctypes
+
+    from paper_2602_00125_b200 import _lib as L
+    from paper_2602_00125_b200.core import Buffer
+
+    lib = L.lib()
+    M = N = K = 128
+    a, b = Buffer(2 * M * K), Buffer(2 * N * K)
+    c, hi, lo = P.zeros((M, N)), Buffer(2 * M * N + 64), Buffer(2 * M * N + 64)
+    rc = lib.b2_gemm_3xbf16(0, 1, M, N, K, a.ptr, a.ptr, b.ptr, b.ptr, c.data_ptr, N, None, 0,
+                            None, hi.ptr + 2, lo.ptr, None)
+    assert rc != 0 and b"aligned" in lib.b2_last_error()
+    x = P.zeros((M, K))
+    rc = lib.b2_gemm(0, 1, M, N, K, x.data_ptr, K, x.data_ptr, K, c.data_ptr, N, None,
+                     L.EPI_BIAS, L.GEMM_SIMT, None)
+    assert rc != 0 and b"bias" in lib.b2_last_error()
+    rc = lib.b2_unary(99, c.data_ptr, 2, L.i64s((M, N)), c.data_ptr, L.i64s((N, 1)), 0.0, 0.0, None)
+    assert rc != 0
+    with pytest.raises(RuntimeError):
+        L.call("b2_reduce", 7, c.data_ptr, None, 2, L.i64s((M, N)), c.data_ptr, L.i64s((N, 1)), 1, None)
