@@ -203,6 +203,19 @@ int b2_gemm_bf16(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, cons
                  const void* B16, float* C, int64_t ldc, const float* bias, int epilogue,
                  const float* mask, void* C16, void* stream);
 
+/* ---------------------------------------------------------------- conv2d
+ * im2col / col2im of tensorlite's conv2d (nn.py:191-303); the GEMMs between
+ * them run on b2_gemm*. x: (B, C, H, W) contiguous; patches: (B*OH*OW, C*KH*KW)
+ * with rows = output positions (b, i, j), cols = taps (c, u, v), zero padding.
+ * col2im gathers each input element's taps in increasing output-row order,
+ * accumulating in double (the reference's scatter order), one f32 rounding. */
+int b2_im2col(float* patches, const float* x, int64_t B, int64_t C, int64_t H, int64_t W,
+              int64_t KH, int64_t KW, int64_t stride, int64_t pad, int64_t OH, int64_t OW,
+              void* stream);
+int b2_col2im(float* dx, const float* dpatches, int64_t B, int64_t C, int64_t H, int64_t W,
+              int64_t KH, int64_t KW, int64_t stride, int64_t pad, int64_t OH, int64_t OW,
+              void* stream);
+
 /* ---------------------------------------------------------------- losses
  * cross_entropy (nn.py:453-503): fwd writes the mean loss (f32 scalar) and
  * per-row stats (max, sum exp) in double; bwd writes

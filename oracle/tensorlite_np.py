@@ -498,6 +498,56 @@ def activation_grad(kind, g, x, y):
 
 
 # ---------------------------------------------------------------------------
+# conv2d (nn.py:191-303): im2col (+ ones column for the bias, folded into the
+# same double dot), permute, col2im scatter in row order with double sums
+
+
+def _im2col(x, kh, kw, s, p):
+    b, c, h, w = x.shape
+    oh, ow = (h + 2 * p - kh) // s + 1, (w + 2 * p - kw) // s + 1
+    xp = np.zeros((b, c, h + 2 * p, w + 2 * p), np.float64)
+    xp[:, :, p:p + h, p:p + w] = x
+    cols = np.empty((b, oh, ow, c, kh, kw), np.float64)
+    for u in range(kh):
+        for v in range(kw):
+            cols[:, :, :, :, u, v] = xp[:, :, u:u + s * oh:s, v:v + s * ow:s].transpose(0, 2, 3, 1)
+    return cols.reshape(b * oh * ow, c * kh * kw), oh, ow
+
+
+def conv2d(x, w, bias, stride=1, padding=0):
+    """Returns (y, pullback(g) -> (dx, dw, db))."""
+    x = np.asarray(x, np.float32)
+    b, c, h, wd = x.shape
+    cout, _, kh, kw = w.shape
+    pt, oh, ow = _im2col(x, kh, kw, stride, padding)
+    wf = _d(w).reshape(cout, -1)
+    if bias is not None:  # the reference's trailing ones column (nn.py:222-246)
+        y = f32(np.concatenate([pt, np.ones((pt.shape[0], 1))], 1)
+                @ np.concatenate([wf, _d(bias)[:, None]], 1).T)
+    else:
+        y = f32(pt @ wf.T)
+    out = y.reshape(b, oh * ow, cout).transpose(0, 2, 1).reshape(b, cout, oh, ow)
+
+    def pull(g):
+        gr = np.asarray(g, np.float32).reshape(b, cout, oh * ow).transpose(0, 2, 1).reshape(-1, cout)
+        dp = f32(_d(gr) @ wf)  # (rows, cols)
+        dx = np.zeros((b, c, h + 2 * padding, wd + 2 * padding), np.float64)
+        dpv = dp.astype(np.float64).reshape(b, oh, ow, c, kh, kw)
+        # rows in increasing order per pixel == accumulate taps by output position
+        for i in range(oh):
+            for j in range(ow):
+                for u in range(kh):
+                    for v in range(kw):
+                        dx[:, :, i * stride + u, j * stride + v] += dpv[:, i, j, :, u, v]
+        dx = f32(dx[:, :, padding:padding + h, padding:padding + wd])
+        dw = f32(_d(gr).T @ pt).reshape(w.shape)
+        db = None if bias is None else axis_sum(np.asarray(g, np.float32), (0, 2, 3))
+        return dx, dw, db
+
+    return out, pull
+
+
+# ---------------------------------------------------------------------------
 # composed hot paths (BASELINE configs)
 
 

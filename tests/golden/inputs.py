@@ -156,3 +156,14 @@ def ce_cases():
     # huge logits stay finite (tests/test_nn.py:450-455)
     out.append((_f32([[1.0e4, -1.0e4, 0.0], [5.0e3, 5.0e3, -5.0e3]]), np.array([0, 1], np.int64)))
     return out
+
+
+# Conv2D cases of tests/golden/catalog.npz:
+# (B, C_in, H, W, C_out, (kh, kw), stride, padding, bias)
+CONV_CASES = [
+    (2, 3, 7, 7, 4, (3, 3), 1, 1, True),
+    (2, 2, 5, 5, 2, (3, 3), 2, 1, True),
+    (1, 3, 6, 5, 5, (2, 3), 1, 0, False),
+    (3, 4, 4, 4, 8, (1, 1), 1, 0, True),
+    (2, 1, 9, 8, 3, (4, 4), 3, 2, True),
+]

@@ -32,7 +32,7 @@ from tensorlite import nn as tnn, optim as topt  # noqa: E402
 from tests.golden.inputs import (  # noqa: E402
     config1_inputs, config2_inputs, config3_inputs, config4_inputs,
     config5_inputs, broadcast_cases, reduction_cases, matmul_cases,
-    unary_values, ce_cases,
+    unary_values, ce_cases, CONV_CASES,
 )
 
 
@@ -277,7 +277,58 @@ def gen_next_rows():
     save("next_rows.npz", **out)
 
 
+
+
+def gen_catalog():
+    """Conv2D (nn.py:191-325), BatchNorm (nn.py:366-412),
+    dropout (nn.py:415-437) on the reference."""
+    out = {}
+    rng = np.random.default_rng(41)
+    for i, (b, cin, h, w, cout, k, s, p, bias) in enumerate(CONV_CASES):
+        layer = tnn.Conv2D(cin, cout, k, stride=s, padding=p, bias=bias, rng=100 + i)
+        x = rng.standard_normal((b, cin, h, w)).astype(np.float32)
+        tl.reset_tape()
+        xt = T(x, grad=True)
+        y = layer(xt)
+        g = rng.standard_normal(y.shape).astype(np.float32)
+        store = tl.backward(y, seed=T(g))
+        out[f"conv{i}_x"], out[f"conv{i}_g"] = x, g
+        out[f"conv{i}_w"] = A(layer.weight)
+        out[f"conv{i}_y"] = A(y)
+        out[f"conv{i}_dx"] = A(store[xt])
+        out[f"conv{i}_dw"] = A(store[layer.weight])
+        if bias:
+            out[f"conv{i}_b"] = A(layer.bias)
+            out[f"conv{i}_db"] = A(store[layer.bias])
+    # batchnorm: two train steps (output, grads, running buffers), then eval
+    bn = tnn.BatchNorm(6, eps=1e-5, momentum=0.1)
+    for k in range(2):
+        x = (rng.standard_normal((16, 6)) * (k + 1) + k).astype(np.float32)
+        g = rng.standard_normal((16, 6)).astype(np.float32)
+        tl.reset_tape()
+        xt = T(x, grad=True)
+        y = bn(xt)
+        store = tl.backward(y, seed=T(g))
+        out[f"bn{k}_x"], out[f"bn{k}_g"] = x, g
+        out[f"bn{k}_y"], out[f"bn{k}_dx"] = A(y), A(store[xt])
+        out[f"bn{k}_dgamma"], out[f"bn{k}_dbeta"] = A(store[bn.gamma]), A(store[bn.beta])
+        out[f"bn{k}_rmean"], out[f"bn{k}_rvar"] = A(bn.running_mean), A(bn.running_var)
+    bn.set_mode("eval")
+    xe = rng.standard_normal((5, 6)).astype(np.float32)
+    with tl.no_grad():
+        out["bn_eval_x"], out["bn_eval_y"] = xe, A(bn(T(xe)))
+    # dropout with a seeded stream
+    xd = rng.standard_normal((7, 9)).astype(np.float32)
+    tl.reset_tape()
+    xt = T(xd, grad=True)
+    y = tnn.dropout(xt, 0.3, "train", rng=random.Random(5))
+    store = tl.backward(tl.sum(y))
+    out["drop_x"], out["drop_y"], out["drop_dx"] = xd, A(y), A(store[xt])
+    save("catalog.npz", **out)
+
+
 if __name__ == "__main__":
+    gen_catalog()
     gen_next_rows()
     gen_elementwise()
     gen_reductions()

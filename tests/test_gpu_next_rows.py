@@ -133,3 +133,68 @@ def test_tlnp_dlpack_roundtrip():
     y = (h * 2.0).relu()
     back = torch.from_dlpack(y)
     assert torch.equal(back, t * 2.0)
+
+
+# ---------------------------------------------------------------- catalog
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_conv2d_against_reference(i):
+    """im2col -> GEMM engine -> permute; col2im in the reference's order.
+    Same seeded init as the reference's Conv2D; GEMM tolerance 1e-4
+    normwise (the patch GEMMs accumulate in fp32), db bit-exact."""
+    from paper_2602_00125_b200 import nn
+    from tests.golden import inputs as I
+
+    g = load("catalog.npz")
+    b, cin, h, w, cout, k, s, p, bias = I.CONV_CASES[i]
+    layer = nn.Conv2D(cin, cout, k, stride=s, padding=p, bias=bias, rng=100 + i)
+    assert bits_equal(layer.weight.numpy(), g[f"conv{i}_w"])  # same init stream
+    P.reset_tape()
+    x = dev(g[f"conv{i}_x"], True)
+    y = layer(x)
+    assert y.shape == g[f"conv{i}_y"].shape
+    assert normwise(y.numpy(), g[f"conv{i}_y"]) <= 1e-4
+    store = P.backward(y, seed=dev(g[f"conv{i}_g"]))
+    assert normwise(store[x].numpy(), g[f"conv{i}_dx"]) <= 1e-4
+    assert normwise(store[layer.weight].numpy(), g[f"conv{i}_dw"]) <= 1e-4
+    if bias:
+        assert bits_equal(store[layer.bias].numpy(), g[f"conv{i}_db"])
+
+
+def test_batchnorm_train_eval_bit_exact():
+    """Composed from the device ops in the reference's order: outputs,
+    gradients and running buffers bit-exact over two train steps + eval."""
+    from paper_2602_00125_b200 import nn
+
+    g = load("catalog.npz")
+    bn = nn.BatchNorm(6, eps=1e-5, momentum=0.1)
+    for k in range(2):
+        P.reset_tape()
+        x = dev(g[f"bn{k}_x"], True)
+        y = bn(x)
+        store = P.backward(y, seed=dev(g[f"bn{k}_g"]))
+        assert bits_equal(y.numpy(), g[f"bn{k}_y"]), k
+        assert bits_equal(store[x].numpy(), g[f"bn{k}_dx"]), k
+        assert bits_equal(store[bn.gamma].numpy(), g[f"bn{k}_dgamma"]), k
+        assert bits_equal(store[bn.beta].numpy(), g[f"bn{k}_dbeta"]), k
+        assert bits_equal(bn.running_mean.numpy(), g[f"bn{k}_rmean"]), k
+        assert bits_equal(bn.running_var.numpy(), g[f"bn{k}_rvar"]), k
+    bn.set_mode("eval")
+    with P.no_grad():
+        assert bits_equal(bn(dev(g["bn_eval_x"])).numpy(), g["bn_eval_y"])
+
+
+def test_dropout_same_stream_bit_exact():
+    import random
+
+    from paper_2602_00125_b200 import nn
+
+    g = load("catalog.npz")
+    P.reset_tape()
+    x = dev(g["drop_x"], True)
+    y = nn.dropout(x, 0.3, "train", rng=random.Random(5))
+    store = P.backward(P.sum(y))
+    assert bits_equal(y.numpy(), g["drop_y"])
+    assert bits_equal(store[x].numpy(), g["drop_dx"])
+    assert nn.dropout(x, 0.3, "eval") is x

@@ -174,3 +174,19 @@ def test_demo_logs_have_the_reference_format():
     assert len(xor) == 301 and xor[0].startswith("0,") and xor[-1].startswith("final,")
     assert all(len(l.split(",")) == 3 for l in blobs)
     assert blobs[-1].startswith("final,")
+
+
+# ---------------------------------------------------------------- catalog
+
+
+def test_conv2d_oracle_against_reference():
+    g = load("catalog.npz")
+    for i, (b, cin, h, w, cout, k, s, p, bias) in enumerate(I.CONV_CASES):
+        bv = g[f"conv{i}_b"] if bias else None
+        y, pull = O.conv2d(g[f"conv{i}_x"], g[f"conv{i}_w"], bv, s, p)
+        assert bits_equal(y, g[f"conv{i}_y"]), i
+        dx, dw, db = pull(g[f"conv{i}_g"])
+        assert bits_equal(dx, g[f"conv{i}_dx"]), i
+        assert bits_equal(dw, g[f"conv{i}_dw"]), i
+        if bias:
+            assert bits_equal(db, g[f"conv{i}_db"]), i
