@@ -98,21 +98,35 @@ __device__ __forceinline__ void cluster_sync() {
 // 2-SM TMA: data lands in this CTA's smem, the transaction bytes are counted on
 // the mbarrier at `bar_cluster` (the leader CTA's barrier)
 __device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* tm, uint32_t bar_cluster,
-                                                int c0, int c1) {
+                                                int c0, int c1, uint64_t pol) {
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"((uint64_t)tm), "r"(bar_cluster), "r"(c0), "r"(c1)
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)tm), "r"(bar_cluster), "r"(c0), "r"(c1), "l"(pol)
       : "memory");
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0,
-                                            int c1) {
+                                            int c1, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"((uint64_t)tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(pol)
       : "memory");
+}
+
+// L2 cache policies for the operand streams: the raster keeps a group of B
+// panels hot across every wave of the group sweep (evict_last), A panels are
+// shared only by the tiles of one wave (evict_normal)
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -220,6 +234,7 @@ struct TcParams {
   int splits;               // split-K slices (1: none); slice s covers k-blocks [s*kbps, (s+1)*kbps)
   int kbps;                 // k-blocks per slice
   int64_t split_stride;     // elements between the partial C slices (M*N) when splits > 1
+  int l2hint;               // B operand loads with L2 evict_last (B2_GEMM_L2HINT=0 disables)
 };
 
 // tile t -> (slice, output tile, k-block range); slices are the slowest index
@@ -294,34 +309,34 @@ struct Cfg {
 // barrier for CG 1, the leader's barrier as a shared::cluster address for CG 2).
 template <int CG>
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t* bar, uint32_t bar_cl,
-                                      int c0, int c1) {
+                                      int c0, int c1, uint64_t pol) {
   if (CG == 1)
-    tma_load_2d(dst, tm, bar, c0, c1);
+    tma_load_2d(dst, tm, bar, c0, c1, pol);
   else
-    tma_load_2d_cg2(dst, tm, bar_cl, c0, c1);
+    tma_load_2d_cg2(dst, tm, bar_cl, c0, c1, pol);
 }
 
 // fp32 tile (tf32 consumption): K-major = one box {32 K, rows}; MN-major = 32x32 boxes
 template <bool MN, int ROWS, int CG>
 __device__ __forceinline__ void load32(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
-                                       uint32_t bar_cl, int mn0, int k0) {
+                                       uint32_t bar_cl, int mn0, int k0, uint64_t pol) {
   if (MN) {
 #pragma unroll
-    for (int j = 0; j < ROWS / 32; ++j) tma2d<CG>(dst + j * 4096, tm, bar, bar_cl, mn0 + 32 * j, k0);
+    for (int j = 0; j < ROWS / 32; ++j) tma2d<CG>(dst + j * 4096, tm, bar, bar_cl, mn0 + 32 * j, k0, pol);
   } else {
-    tma2d<CG>(dst, tm, bar, bar_cl, k0, mn0);
+    tma2d<CG>(dst, tm, bar, bar_cl, k0, mn0, pol);
   }
 }
 
 // bf16 tile: K-major = one box {32 K (64 B), rows}; MN-major = boxes {64 MN (128 B), 32 K}
 template <bool MN, int ROWS, int CG>
 __device__ __forceinline__ void load16(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
-                                       uint32_t bar_cl, int mn0, int k0) {
+                                       uint32_t bar_cl, int mn0, int k0, uint64_t pol) {
   if (MN) {
 #pragma unroll
-    for (int j = 0; j < ROWS / 64; ++j) tma2d<CG>(dst + j * 4096, tm, bar, bar_cl, mn0 + 64 * j, k0);
+    for (int j = 0; j < ROWS / 64; ++j) tma2d<CG>(dst + j * 4096, tm, bar, bar_cl, mn0 + 64 * j, k0, pol);
   } else {
-    tma2d<CG>(dst, tm, bar, bar_cl, k0, mn0);
+    tma2d<CG>(dst, tm, bar, bar_cl, k0, mn0, pol);
   }
 }
 
@@ -417,6 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t pa = l2_policy_normal();
+      const uint64_t pb = p.l2hint ? l2_policy_last() : pa;
       for (int tile = cl_id; tile < p.num_tiles; tile += cl_num) {
         int tm, tn, kb0, kb1, ks;
         tile_info(p, tile, nkb, tm, tn, kb0, kb1, ks);
@@ -430,24 +447,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (leader) mbar_expect_tx(fb, CF::STAGE_BYTES * CG);
           const int k0 = kb * BK;
           if (MODE == 4 || MODE == 5) {  // bf16 operands only
-            load16<A_MN, BM, CG>(st + CF::OFF_AH16, &tmA, fb, fb_cl, m0, k0);
-            load16<B_MN, CF::BNL, CG>(st + CF::OFF_BH16, &tmB, fb, fb_cl, n0, k0);
+            load16<A_MN, BM, CG>(st + CF::OFF_AH16, &tmA, fb, fb_cl, m0, k0, pa);
+            load16<B_MN, CF::BNL, CG>(st + CF::OFF_BH16, &tmB, fb, fb_cl, n0, k0, pb);
             if (MODE == 5) {
-              load16<A_MN, BM, CG>(st + CF::OFF_AL16, &tmA2, fb, fb_cl, m0, k0);
-              load16<B_MN, CF::BNL, CG>(st + CF::OFF_BL16, &tmB2, fb, fb_cl, n0, k0);
+              load16<A_MN, BM, CG>(st + CF::OFF_AL16, &tmA2, fb, fb_cl, m0, k0, pa);
+              load16<B_MN, CF::BNL, CG>(st + CF::OFF_BL16, &tmB2, fb, fb_cl, n0, k0, pb);
             }
           } else {
-            load32<A_MN, BM, CG>(st + CF::OFF_A, &tmA, fb, fb_cl, m0, k0);
-            load32<B_MN, CF::BNL, CG>(st + CF::OFF_B, &tmB, fb, fb_cl, n0, k0);
+            load32<A_MN, BM, CG>(st + CF::OFF_A, &tmA, fb, fb_cl, m0, k0, pa);
+            load32<B_MN, CF::BNL, CG>(st + CF::OFF_B, &tmB, fb, fb_cl, n0, k0, pb);
           }
           if (MODE == 3) {
-            load32<A_MN, BM, CG>(st + CF::OFF_ALO, &tmA2, fb, fb_cl, m0, k0);
-            load32<B_MN, CF::BNL, CG>(st + CF::OFF_BLO, &tmB2, fb, fb_cl, n0, k0);
+            load32<A_MN, BM, CG>(st + CF::OFF_ALO, &tmA2, fb, fb_cl, m0, k0, pa);
+            load32<B_MN, CF::BNL, CG>(st + CF::OFF_BLO, &tmB2, fb, fb_cl, n0, k0, pb);
           } else if (MODE == 2) {
-            load16<A_MN, BM, CG>(st + CF::OFF_AH16, &tmA2, fb, fb_cl, m0, k0);
-            load16<A_MN, BM, CG>(st + CF::OFF_AL16, &tmA3, fb, fb_cl, m0, k0);
-            load16<B_MN, CF::BNL, CG>(st + CF::OFF_BH16, &tmB2, fb, fb_cl, n0, k0);
-            load16<B_MN, CF::BNL, CG>(st + CF::OFF_BL16, &tmB3, fb, fb_cl, n0, k0);
+            load16<A_MN, BM, CG>(st + CF::OFF_AH16, &tmA2, fb, fb_cl, m0, k0, pa);
+            load16<A_MN, BM, CG>(st + CF::OFF_AL16, &tmA3, fb, fb_cl, m0, k0, pa);
+            load16<B_MN, CF::BNL, CG>(st + CF::OFF_BH16, &tmB2, fb, fb_cl, n0, k0, pb);
+            load16<B_MN, CF::BNL, CG>(st + CF::OFF_BL16, &tmB3, fb, fb_cl, n0, k0, pb);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -1019,6 +1036,14 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   int S = 1;
   if (tiles * cg <= sms / 2 && nkb >= 16 && splitk_enabled())  // slices of >= 8 k-blocks (K 256)
     S = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms / (tiles * cg), nkb / 8, 16}));
+  {
+    static int h = -1;
+    if (h < 0) {
+      const char* e = getenv("B2_GEMM_L2HINT");
+      h = !(e && e[0] == '0');
+    }
+    p.l2hint = h;
+  }
   p.splits = 1;
   p.kbps = nkb;
   p.split_stride = 0;
