@@ -281,10 +281,15 @@ __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& tm, i
 template <int MODE, int CG>
 struct Cfg {
   static constexpr int BNL = BN / CG;      // B rows loaded per CTA
+  // k-block depth: 32 for every mode that stages fp32 tiles (128-B rows), 64
+  // for the pure-bf16 modes (128-B rows of bf16, SW128): twice the MMAs per
+  // barrier round trip
+  static constexpr bool W64 = MODE == 4 || MODE == 5;
+  static constexpr int BKM = W64 ? 64 : BK;
   static constexpr int A32 = BM * BK * 4;  // 16 KB
   static constexpr int B32 = BNL * BK * 4;
-  static constexpr int A16 = BM * BK * 2;
-  static constexpr int B16 = BNL * BK * 2;
+  static constexpr int A16 = BM * BKM * 2;
+  static constexpr int B16 = BNL * BKM * 2;
   static constexpr int STAGE_BYTES =
       MODE == 1 ? A32 + B32
       : MODE == 3 ? 2 * (A32 + B32)
@@ -328,13 +333,15 @@ __device__ __forceinline__ void load32(uint8_t* dst, const CUtensorMap* tm, uint
   }
 }
 
-// bf16 tile: K-major = one box {32 K (64 B), rows}; MN-major = boxes {64 MN (128 B), 32 K}
-template <bool MN, int ROWS, int CG>
+// bf16 tile: K-major = one box {KB K, rows}; MN-major = boxes {64 MN (128 B), KB K}
+// (KB = 32 with 64-B rows in MODE 2, 64 with 128-B rows in the pure-bf16 modes)
+template <bool MN, int ROWS, int CG, int KB = 32>
 __device__ __forceinline__ void load16(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
                                        uint32_t bar_cl, int mn0, int k0, uint64_t pol) {
   if (MN) {
 #pragma unroll
-    for (int j = 0; j < ROWS / 64; ++j) tma2d<CG>(dst + j * 4096, tm, bar, bar_cl, mn0 + 64 * j, k0, pol);
+    for (int j = 0; j < ROWS / 64; ++j)
+      tma2d<CG>(dst + j * (KB * 128), tm, bar, bar_cl, mn0 + 64 * j, k0, pol);
   } else {
     tma2d<CG>(dst, tm, bar, bar_cl, k0, mn0, pol);
   }
@@ -347,11 +354,14 @@ __device__ __forceinline__ uint64_t desc32(uint32_t base, bool mn, int ks) {
   // 32-element box (4 KB), SBO = next 4-row atom (512 B).
   return mn ? umma_desc(base + ks * 1024, 4096, 512, 1) : umma_desc(base + ks * 32, 16, 1024, 2);
 }
+template <int KB = 32>
 __device__ __forceinline__ uint64_t desc16(uint32_t base, bool mn, int ks) {
-  // bf16, K=16 per MMA. K-major: 64-B swizzle (rows of 32 bf16), +32 B per
-  // k-step, SBO 8 rows x 64 B. MN-major: 128-B swizzle, +16 rows x 128 B per
-  // k-step, LBO = next 64-element box (4 KB), SBO 8 rows x 128 B.
-  return mn ? umma_desc(base + ks * 2048, 4096, 1024, 2) : umma_desc(base + ks * 32, 16, 512, 4);
+  // bf16, K=16 per MMA. KB = 32: K-major 64-B swizzle (rows of 32 bf16), +32 B
+  // per k-step, SBO 8 rows x 64 B. KB = 64: K-major 128-B swizzle (rows of 64
+  // bf16), +32 B per k-step, SBO 8 rows x 128 B. MN-major: 128-B swizzle, +16
+  // rows x 128 B per k-step, LBO = next 64-element box (KB x 128 B), SBO 8 x 128 B.
+  if (mn) return umma_desc(base + ks * 2048, KB * 128, 1024, 2);
+  return KB == 64 ? umma_desc(base + ks * 32, 16, 1024, 2) : umma_desc(base + ks * 32, 16, 512, 4);
 }
 
 // operand split written by the epilogue for the next GEMM: TF32X (MODE 2)
@@ -389,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkb = (p.K + BK - 1) / BK;
+  const int nkb = (p.K + CF::BKM - 1) / CF::BKM;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const bool leader = rank == 0;
   const int cl_id = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
@@ -445,13 +455,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint64_t* fb = &full[stage];
           const uint32_t fb_cl = CG == 2 ? mapa(smem_u32(fb), 0) : 0;
           if (leader) mbar_expect_tx(fb, CF::STAGE_BYTES * CG);
-          const int k0 = kb * BK;
+          const int k0 = kb * CF::BKM;
           if (MODE == 4 || MODE == 5) {  // bf16 operands only
-            load16<A_MN, BM, CG>(st + CF::OFF_AH16, &tmA, fb, fb_cl, m0, k0, pa);
-            load16<B_MN, CF::BNL, CG>(st + CF::OFF_BH16, &tmB, fb, fb_cl, n0, k0, pb);
+            load16<A_MN, BM, CG, CF::BKM>(st + CF::OFF_AH16, &tmA, fb, fb_cl, m0, k0, pa);
+            load16<B_MN, CF::BNL, CG, CF::BKM>(st + CF::OFF_BH16, &tmB, fb, fb_cl, n0, k0, pb);
             if (MODE == 5) {
-              load16<A_MN, BM, CG>(st + CF::OFF_AL16, &tmA2, fb, fb_cl, m0, k0, pa);
-              load16<B_MN, CF::BNL, CG>(st + CF::OFF_BL16, &tmB2, fb, fb_cl, n0, k0, pb);
+              load16<A_MN, BM, CG, CF::BKM>(st + CF::OFF_AL16, &tmA2, fb, fb_cl, m0, k0, pa);
+              load16<B_MN, CF::BNL, CG, CF::BKM>(st + CF::OFF_BL16, &tmB2, fb, fb_cl, n0, k0, pb);
             }
           } else {
             load32<A_MN, BM, CG>(st + CF::OFF_A, &tmA, fb, fb_cl, m0, k0, pa);
@@ -502,18 +512,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t s0 = smem_u32(smem + stage * CF::STAGE_BYTES);
             if (MODE == 4) {
 #pragma unroll
-              for (int ks = 0; ks < BK / 16; ++ks)
-                tc_mma<CG>(d_tmem, desc16(s0 + CF::OFF_AH16, A_MN, ks),
-                           desc16(s0 + CF::OFF_BH16, B_MN, ks), id16, (kc | ks) ? 1u : 0u, true);
+              for (int ks = 0; ks < CF::BKM / 16; ++ks)
+                tc_mma<CG>(d_tmem, desc16<CF::BKM>(s0 + CF::OFF_AH16, A_MN, ks),
+                           desc16<CF::BKM>(s0 + CF::OFF_BH16, B_MN, ks), id16, (kc | ks) ? 1u : 0u,
+                           true);
             }
             if (MODE == 5) {
 #pragma unroll
-              for (int ks = 0; ks < BK / 16; ++ks) {
-                const uint64_t ah = desc16(s0 + CF::OFF_AH16, A_MN, ks);
-                const uint64_t bh = desc16(s0 + CF::OFF_BH16, B_MN, ks);
+              for (int ks = 0; ks < CF::BKM / 16; ++ks) {
+                const uint64_t ah = desc16<CF::BKM>(s0 + CF::OFF_AH16, A_MN, ks);
+                const uint64_t bh = desc16<CF::BKM>(s0 + CF::OFF_BH16, B_MN, ks);
                 tc_mma<CG>(d_tmem, ah, bh, id16, (kc | ks) ? 1u : 0u, true);
-                tc_mma<CG>(d_tmem, ah, desc16(s0 + CF::OFF_BL16, B_MN, ks), id16, 1u, true);
-                tc_mma<CG>(d_tmem, desc16(s0 + CF::OFF_AL16, A_MN, ks), bh, id16, 1u, true);
+                tc_mma<CG>(d_tmem, ah, desc16<CF::BKM>(s0 + CF::OFF_BL16, B_MN, ks), id16, 1u, true);
+                tc_mma<CG>(d_tmem, desc16<CF::BKM>(s0 + CF::OFF_AL16, A_MN, ks), bh, id16, 1u, true);
               }
             }
 #pragma unroll
@@ -821,14 +832,19 @@ int get_encode() {
 //     128-B swizzle with 32-B atoms (UMMA SWIZZLE_128B_BASE32B).
 //   bf16 operand: K-major box {32 (64 B), box_rows} with 64-B swizzle; MN-major
 //     box {64 (128 B), 32} with 128-B swizzle.
+//   wide (pure-bf16 modes): K-major box {64 (128 B), box_rows} with 128-B
+//     swizzle; MN-major box {64, 64}.
 int make_map(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
-             bool mn_major, bool bf16) {
+             bool mn_major, bool bf16, bool wide = false) {
   const int esz = bf16 ? 2 : 4;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * esz};
-  cuuint32_t box[2] = {(cuuint32_t)(bf16 && mn_major ? 64 : 32), (cuuint32_t)box_rows};
+  const int kb = bf16 && wide ? 64 : 32;  // k extent of a box
+  // box = {inner (contiguous) extent, outer extent}; for MN-major tiles the
+  // inner extent is 64 MN elements and box_rows carries the k extent
+  cuuint32_t box[2] = {(cuuint32_t)(bf16 && mn_major ? 64 : kb), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUtensorMapSwizzle sw = bf16 ? (mn_major ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)
+  CUtensorMapSwizzle sw = bf16 ? ((mn_major || wide) ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)
                                : (mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B);
   CUresult r = g_encode(tm, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                         (void*)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
@@ -856,7 +872,7 @@ static int kc_for_mode(int mode) {
     env = e ? atoi(e) : 0;
   }
   if (env > 0) return env;
-  return (mode == 4 || mode == 5) ? 4 * KC_BASE : KC_BASE;
+  return (mode == 4 || mode == 5) ? 2 * KC_BASE : KC_BASE;  // K = 1024 (BK 64) / 256 (BK 32)
 }
 
 template <bool A_MN, bool B_MN, int MODE, int CG>
@@ -866,15 +882,15 @@ int launch_tc(const Operands& o, TcParams p, cudaStream_t st) {
   // A is [M,K] (K-major) or stored [K,M] (MN-major); B is [N,K] or stored [K,N]
   const int64_t ar = A_MN ? p.K : p.M, ac = A_MN ? p.M : p.K;
   const int64_t br = B_MN ? p.K : p.N, bc = B_MN ? p.N : p.K;
-  const int abox = A_MN ? 32 : BM, bbox = B_MN ? 32 : CF::BNL;
+  const int abox = A_MN ? CF::BKM : BM, bbox = B_MN ? CF::BKM : CF::BNL;
   // MODE 4 / 5 read bf16 operand arrays (contiguous casts / splits) through bf16 maps
   constexpr bool kB16 = MODE == 4 || MODE == 5;
-  B2_TRY(make_map(&m[0], o.a[0], ar, ac, o.lda, abox, A_MN, kB16));
-  B2_TRY(make_map(&m[1], o.b[0], br, bc, o.ldb, bbox, B_MN, kB16));
+  B2_TRY(make_map(&m[0], o.a[0], ar, ac, o.lda, abox, A_MN, kB16, CF::W64));
+  B2_TRY(make_map(&m[1], o.b[0], br, bc, o.ldb, bbox, B_MN, kB16, CF::W64));
   m[2] = m[0]; m[3] = m[1]; m[4] = m[0]; m[5] = m[1];
   if (MODE == 5) {
-    B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, true));
-    B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, true));
+    B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, true, CF::W64));
+    B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, true, CF::W64));
   } else if (MODE == 3) {
     B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, false));
     B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, false));
@@ -1031,7 +1047,8 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   // split-K when the output tiles leave most SMs idle and K is long enough
   // (dW GEMMs: [1024 x 1024] over K = 32768; square n = 1024): slices of >= 8
   // k-blocks, fp32 partials, a fixed-order second stage with the fused epilogue
-  const int nkb = (int)((K + BK - 1) / BK);
+  const int bk = (mode == 4 || mode == 5) ? 64 : BK;  // Cfg::BKM
+  const int nkb = (int)((K + bk - 1) / bk);
   const int64_t tiles = ((M + (int64_t)BM * cg - 1) / ((int64_t)BM * cg)) * ((N + BN - 1) / BN);
   int S = 1;
   if (tiles * cg <= sms / 2 && nkb >= 16 && splitk_enabled())  // slices of >= 8 k-blocks (K 256)

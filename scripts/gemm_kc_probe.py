@@ -1,5 +1,6 @@
 """Speed and accuracy of the 3xBF16 / BF16 GEMM for one B2_GEMM_KC setting
-(promotion interval in k-blocks of 32; read once per process).
+(promotion interval in k-blocks: 64 deep for the bf16 modes, 32 for the tf32
+modes; read once per process).
 
     B2_GEMM_KC=16 python scripts/gemm_kc_probe.py
 """
