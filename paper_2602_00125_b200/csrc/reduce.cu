@@ -129,6 +129,18 @@ __global__ void __launch_bounds__(256) k_rows(const float* __restrict__ x, int64
     if (live) {
       if (VEC) {
         int64_t r = r0 + 4 * t;
+        for (; r + 28 * GROUP + 3 < r1; r += 32 * GROUP) {  // 8 x 128-bit loads in flight
+          float4 v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float4*>(row + r + 4 * k * GROUP));
+#pragma unroll
+          for (int k = 0; k < 8; k += 4) {
+            a0 += (double)v[k].x + (double)v[k].y + (double)v[k].z + (double)v[k].w;
+            a1 += (double)v[k + 1].x + (double)v[k + 1].y + (double)v[k + 1].z + (double)v[k + 1].w;
+            a2 += (double)v[k + 2].x + (double)v[k + 2].y + (double)v[k + 2].z + (double)v[k + 2].w;
+            a3 += (double)v[k + 3].x + (double)v[k + 3].y + (double)v[k + 3].z + (double)v[k + 3].w;
+          }
+        }
         for (; r + 12 * GROUP + 3 < r1; r += 16 * GROUP) {  // 4 x 128-bit loads in flight
           const float4 v0 = *reinterpret_cast<const float4*>(row + r);
           const float4 v1 = *reinterpret_cast<const float4*>(row + r + 4 * GROUP);
@@ -254,6 +266,20 @@ __global__ void __launch_bounds__(256) k_strip(const float* __restrict__ x, int6
     for (int j = 0; j < V; ++j) a[j] = 0.0;
     if (live) {
       int64_t r = r0 + rl;
+      if (V == 4) {  // 8 independent 128-bit loads in flight, then fold
+        for (; r + 7 * RL < r1; r += 8 * RL) {
+          float4 v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float4*>(base + (r + k * RL) * I));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            a[0] += (double)v[k].x;
+            a[V > 1 ? 1 : 0] += (double)v[k].y;
+            a[V > 2 ? 2 : 0] += (double)v[k].z;
+            a[V > 3 ? 3 : 0] += (double)v[k].w;
+          }
+        }
+      }
       for (; r + 3 * RL < r1; r += 4 * RL) {  // 4 independent loads in flight
         if (V == 4) {
           const float4 v0 = *reinterpret_cast<const float4*>(base + r * I);
