@@ -880,3 +880,22 @@ def test_c_abi_rejects_bad_arguments_loudly():
     assert rc != 0
     with pytest.raises(RuntimeError):
         L.call("b2_reduce", 7, c.data_ptr, None, 2, L.i64s((M, N)), c.data_ptr, L.i64s((N, 1)), 1, None)
+
+
+def test_beyond_2_31_elements_int64_indexing():
+    """Maximum-size edge: a tensor of 2^31 + 5 elements (8 GiB) through the
+    flat elementwise kernel, a full fp64 sum and a column sum -- every index
+    path is 64-bit. Size-independent properties: exact values of constant
+    fills and of their sums."""
+    n = 2 ** 31 + 5
+    x = P.full((n,), 1.5)
+    y = P.add(x, 2.25)  # 3.75 exactly
+    assert P.sum(y).item() == np.float32(n * 3.75)
+    last = P.Tensor(y.buffer, (5,), offset=n - 5)  # a view of the last elements (offset > 2^31)
+    assert np.all(last.numpy() == np.float32(3.75))
+    del x, y, last
+    m = P.full((2 ** 20 + 3, 2048), 0.5)  # 2^31 + 6144 elements, column sums
+    cs = P.sum(m, axis=0).numpy()
+    assert np.all(cs == np.float32((2 ** 20 + 3) * 0.5))
+    with pytest.raises(RuntimeError):
+        P.max(P.reshape(m, (-1,)))  # max over >= 2^31 elements per output is rejected loudly
