@@ -330,6 +330,18 @@ def op_benchmarks():
     ms = timed(c4, 5)
     out["config4_ms_per_step"] = ms
     out["config4_gemm_tflops_effective"] = 3 * 2 * 32768 * 1024 * 1024 / ms / 1e9
+    # the same step written with the fused Linear layer: X @ W + b as one GEMM
+    # whose epilogue adds the bias (bit-identical to the separate add)
+    X2 = P.reshape(X, (-1, 1024))
+
+    def c4_fused():
+        P.reset_tape()
+        X.buffer.version += 1
+        W.buffer.version += 1
+        Y = P.softmax(P.linear(X2, P.transpose2d(W), bias))
+        P.backward(P.mean(P.mul(Y, P.reshape(Tt, (-1, 1024)))))
+
+    out["config4_fused_linear_ms_per_step"] = timed(c4_fused, 5)
     P.reset_tape()
     del X, W, bias, Tt
 
