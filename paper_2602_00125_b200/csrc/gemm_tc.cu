@@ -5,27 +5,33 @@
 // output as one double dot rounded to f32; the fp32 tolerance (1e-4, SURVEY
 // 8a.3) rules out plain TF32 (~2.5e-4 normwise), so operands are split
 // x = hi + lo and the tensor cores accumulate hi*hi + hi*lo + lo*hi:
-//   3xTF32 (MODE 3): three kind::tf32 MMAs on fp32 hi/lo arrays;
-//   TF32X  (MODE 2, default): the tf32 MMA reads the raw fp32 operand (the
-//          hardware truncates to tf32, so hi = trunc(x)) and the two cross
-//          terms run as kind::f16 MMAs on bf16(hi), bf16(lo) at twice the tf32
-//          rate: 2 tf32-equivalents per fp32 MAC, ~2e-6 normwise error.
+//   3xBF16 (MODE 5, default): hi = bf16_rn(x), lo = bf16_rn(x - hi), three
+//          kind::f16 MMAs per fp32 MAC (1.5 tf32-equivalents), ~5e-6 normwise;
+//   TF32X  (MODE 2): the tf32 MMA reads the raw fp32 operand (the hardware
+//          truncates to tf32, so hi = trunc(x)) and the two cross terms run as
+//          kind::f16 MMAs on bf16(hi), bf16(lo): 2 tf32-equivalents, ~2e-6;
+//   3xTF32 (MODE 3): three kind::tf32 MMAs on fp32 hi/lo arrays, ~1e-6;
+//   1xTF32 (MODE 1, TF32 accuracy) and BF16 (MODE 4, the explicit bf16
+//          variant) are single-MMA modes.
 //
 // Structure (persistent; one CTA per SM, CTA pairs for big problems):
 //   warp 0      TMA producer: per k-block loads the mode's operand tiles
-//               (cp.async.bulk.tensor, 128/64-byte swizzles) into a ring
+//               (cp.async.bulk.tensor, 128/64-byte swizzles, L2 cache hints)
+//               into a ring of up to 8 stages
 //   warp 1      MMA issuer (leader CTA): one thread issues the tcgen05.mma's
 //               (M=128 per CTA or 256 per pair, N=256, K=8/16), tcgen05.commit
 //               frees smem slots and hands K-chunks to the epilogue
 //   warp 2      TMEM allocator (512 columns = two 128x256 fp32 accumulators,
-//               ping-ponged per K-chunk of 256)
+//               ping-ponged per K-chunk: K = 1024 for the bf16 modes, 256 for tf32)
 //   warps 4..19 epilogue: drain each K-chunk (tcgen05.ld) into RN fp32
 //               running sums in registers while the MMAs fill the other
-//               accumulator; after the last chunk +bias -> relu -> stores
-// Operand majorness comes from the reference's three layouts: NT (forward,
-// x.w^T), NN (x_bar = g.w), TN (w_bar = g^T.x): K-major tiles are one TMA box
-// per operand; MN-major tiles are 128-byte-wide boxes laid side by side
-// (UMMA LBO = box bytes).
+//               accumulator; after the last chunk +bias -> relu -> ReLU-pullback
+//               mask -> stores (+ the result's own operand split for the next GEMM)
+// Few-tile long-K problems split K over CTAs (fp32 partial slices, fixed-order
+// second stage, k_splitk_epilogue). Operand majorness comes from the
+// reference's three layouts: NT (forward, x.w^T), NN (x_bar = g.w), TN (w_bar
+// = g^T.x): K-major tiles are one TMA box per operand; MN-major tiles are
+// 128-byte-wide boxes laid side by side (UMMA LBO = box bytes).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -45,7 +51,7 @@ namespace {
 
 constexpr int BM = 128, BN = 256, BK = 32;  // BK fp32 = 128 bytes = one swizzle row
 constexpr int kThreads = 640;  // 4 control warps + 16 epilogue warps
-constexpr int KC_BASE = 8;     // k-blocks per accumulation chunk (K = 256)
+constexpr int KC_BASE = 8;     // k-blocks per accumulation chunk for the tf32 modes (K = 256)
 constexpr int kTmemCols = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -485,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (leader CTA only)
-    // The accumulator restarts every KC k-blocks (K = 256): the tensor core's
+    // The accumulator restarts every KC k-blocks (kc_for_mode): the tensor core's
     // fp32 accumulation loses ~1 ulp per MMA step (2e-5 normwise at K=8192 with
     // exact inputs), so the epilogue promotes each chunk into RN fp32 sums.
     if (leader) {
