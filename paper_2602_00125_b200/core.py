@@ -262,7 +262,8 @@ def from_dlpack(obj, requires_grad=False) -> Tensor:
 
 def from_numpy(arr, requires_grad=False) -> Tensor:
     """Upload a host array (any float dtype is rounded to f32 once)."""
-    a = np.ascontiguousarray(arr, dtype=np.float32)
+    # np.require keeps 0-d arrays 0-d (ascontiguousarray would return shape (1,))
+    a = np.require(np.asarray(arr, dtype=np.float32), requirements="C")
     t = _empty(a.shape)
     if a.size:
         L.call("b2_memcpy_h2d", t.data_ptr, a.ctypes.data, a.nbytes, None)
