@@ -198,3 +198,38 @@ def test_dropout_same_stream_bit_exact():
     assert bits_equal(y.numpy(), g["drop_y"])
     assert bits_equal(store[x].numpy(), g["drop_dx"])
     assert nn.dropout(x, 0.3, "eval") is x
+
+
+def test_checkpoint_resume_bit_identical(tmp_path):
+    """Train 2 steps, save (params, buffers, Adam slots and step counts),
+    resume in a fresh model/optimizer for 1 more step == 3 uninterrupted steps."""
+    from paper_2602_00125_b200 import checkpoint, nn
+
+    rng = np.random.default_rng(3)
+    x = dev(rng.standard_normal((64, 32)).astype(np.float32))
+    labels = nn.labels_buffer(rng.integers(0, 10, 64))
+
+    def make():
+        return nn.Sequential(nn.Dense(32, 48, rng=1), nn.ReLU(), nn.BatchNorm(48),
+                             nn.Dense(48, 10, rng=2))
+
+    def step(model, opt):
+        P.reset_tape()
+        store = P.backward(nn.cross_entropy(model(x), labels))
+        optim.step_all(opt, model.parameters(), store)
+
+    ref, ropt = make(), optim.Adam(lr=1e-2)
+    for _ in range(3):
+        step(ref, ropt)
+    a, aopt = make(), optim.Adam(lr=1e-2)
+    for _ in range(2):
+        step(a, aopt)
+    path = str(tmp_path / "ck.npz")
+    checkpoint.save(path, a, aopt)
+    b, bopt = make(), optim.Adam(lr=1e-2)
+    checkpoint.load(path, b, bopt)
+    step(b, bopt)
+    for (n1, p1), (n2, p2) in zip(ref.named_parameters(), b.named_parameters()):
+        assert n1 == n2 and bits_equal(p1.numpy(), p2.numpy()), n1
+    for (n1, b1), (n2, b2) in zip(ref.named_buffers(), b.named_buffers()):
+        assert n1 == n2 and bits_equal(b1.numpy(), b2.numpy()), n1
