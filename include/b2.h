@@ -268,6 +268,12 @@ int b2_comm_init(int rank, int nranks, const unsigned char* uid128);
 int b2_comm_destroy(void);
 /* in-place sum (op=0) / average (op=1) / max (op=2) over all ranks, fp32 */
 int b2_allreduce_f32(float* buf, int64_t n, int op, void* stream);
+/* failure detection: the communicator's asynchronous NCCL error (0 = ok),
+ * abort, and a host wait for a stream with a deadline that polls the async
+ * error and aborts the communicator on error or timeout */
+int b2_comm_async_error(int* err);
+int b2_comm_abort(void);
+int b2_stream_wait_timeout(void* stream, double timeout_ms);
 
 #ifdef __cplusplus
 }

@@ -7,9 +7,11 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 
 #include "common.cuh"
 
@@ -23,6 +25,8 @@ struct Nccl {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 
 Nccl g_nccl;
@@ -42,6 +46,9 @@ int load_nccl() {
   g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(g_nccl.h, "ncclCommDestroy");
   g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(g_nccl.h, "ncclAllReduce");
   g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(g_nccl.h, "ncclGetErrorString");
+  g_nccl.CommGetAsyncError =
+      (decltype(g_nccl.CommGetAsyncError))dlsym(g_nccl.h, "ncclCommGetAsyncError");
+  g_nccl.CommAbort = (decltype(g_nccl.CommAbort))dlsym(g_nccl.h, "ncclCommAbort");
   if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce)
     return b2::fail("libnccl is missing required symbols");
   return 0;
@@ -93,6 +100,65 @@ int b2_allreduce_f32(float* buf, int64_t n, int op, void* stream) {
   ncclResult_t r = g_nccl.AllReduce(buf, buf, (size_t)n, ncclFloat32, rop, g_comm, b2::resolve(stream));
   if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
   return 0;
+}
+
+// Failure detection: the communicator's asynchronous error state
+// (0 = ok; a peer that died or a network fault shows up here, not as a hang)
+int b2_comm_async_error(int* err) {
+  *err = 0;
+  if (!g_comm || !g_nccl.CommGetAsyncError) return 0;
+  ncclResult_t r = ncclSuccess;
+  ncclResult_t q = g_nccl.CommGetAsyncError(g_comm, &r);
+  if (q != ncclSuccess) return nccl_fail(q, "ncclCommGetAsyncError");
+  *err = (int)r;
+  return 0;
+}
+
+int b2_comm_abort(void) {
+  if (g_comm && g_nccl.CommAbort) g_nccl.CommAbort(g_comm);
+  g_comm = nullptr;
+  return 0;
+}
+
+// Host wait for `stream` with a deadline, polling the communicator's async
+// error: returns 0 when the stream drained, fails (and aborts the
+// communicator so no rank blocks forever) on an NCCL error or a timeout.
+int b2_stream_wait_timeout(void* stream, double timeout_ms) {
+  cudaStream_t st = b2::resolve(stream);
+  cudaEvent_t ev;
+  B2_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  cudaError_t e = cudaEventRecord(ev, st);
+  if (e != cudaSuccess) {
+    cudaEventDestroy(ev);
+    return b2::cuda_fail(e, "cudaEventRecord");
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc = 0;
+  for (;;) {
+    e = cudaEventQuery(ev);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) {
+      rc = b2::cuda_fail(e, "b2_stream_wait_timeout");
+      break;
+    }
+    int err = 0;
+    if (b2_comm_async_error(&err) == 0 && err != 0 && err != (int)ncclInProgress) {
+      b2_comm_abort();
+      rc = b2::fail("NCCL asynchronous error " + std::to_string(err) + "; communicator aborted");
+      break;
+    }
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > timeout_ms) {
+      b2_comm_abort();
+      rc = b2::fail("stream did not drain within " + std::to_string(timeout_ms) +
+                    " ms; communicator aborted");
+      break;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  cudaEventDestroy(ev);
+  return rc;
 }
 
 }  // extern "C"

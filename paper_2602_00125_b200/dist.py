@@ -113,6 +113,22 @@ class Communicator:
             L.call("b2_allreduce_f32", t.data_ptr, t.size, op, stream)
         return t
 
+    def check(self):
+        """Raise if the communicator reports an asynchronous NCCL error."""
+        if not self.active:
+            return
+        err = ctypes.c_int(0)
+        L.check(L.lib().b2_comm_async_error(ctypes.byref(err)))
+        if err.value not in (0, 7):  # 7 = ncclInProgress
+            raise RuntimeError(f"NCCL asynchronous error {err.value}")
+
+    def wait(self, timeout_s: float):
+        """Host wait for the communication stream with a deadline; on an NCCL
+        error or a timeout the communicator is aborted and RuntimeError raised
+        (a dead peer fails the step instead of hanging it)."""
+        if self.active:
+            L.check(L.lib().b2_stream_wait_timeout(self.comm_stream, float(timeout_s) * 1000.0))
+
     def barrier(self):
         if self.active:
             from . import core as T
@@ -142,9 +158,13 @@ class GradReducer:
     GEMMs of the lower ones. (Leaf gradients of Dense layers are fresh
     tensors; an aliased leaf gradient would be averaged in place too.)"""
 
-    def __init__(self, comm: Communicator, params=None):
+    def __init__(self, comm: Communicator, params=None, timeout_s=None):
         self.comm = comm
         self._pending = []
+        if timeout_s is None:
+            env = os.environ.get("B2_COMM_TIMEOUT_S")
+            timeout_s = float(env) if env else None
+        self.timeout_s = timeout_s  # None: stay asynchronous (no host wait)
 
     def hook(self, node_id, grad):
         if not self.comm.active:
@@ -159,6 +179,8 @@ class GradReducer:
     def finish(self):
         if not self.comm.active:
             return
+        if self.timeout_s is not None:
+            self.comm.wait(self.timeout_s)  # failure detection: error/timeout -> abort + raise
         done = L.Event()
         done.record(self.comm.comm_stream)
         L.call("b2_stream_wait_event", None, done.h)  # the optimizer waits for the reduces

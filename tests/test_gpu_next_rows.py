@@ -233,3 +233,29 @@ def test_checkpoint_resume_bit_identical(tmp_path):
         assert n1 == n2 and bits_equal(p1.numpy(), p2.numpy()), n1
     for (n1, b1), (n2, b2) in zip(ref.named_buffers(), b.named_buffers()):
         assert n1 == n2 and bits_equal(b1.numpy(), b2.numpy()), n1
+
+
+def test_comm_failure_detection_and_timeout_abort():
+    """SURVEY 5 failure detection: the communicator's async error is polled;
+    a comm stream that does not drain within the deadline aborts the
+    communicator and raises (a dead peer fails the step instead of hanging it)."""
+    from paper_2602_00125_b200 import _lib as L
+    from paper_2602_00125_b200 import dist, nn
+
+    comm = dist.Communicator(dist.Env(), force_nccl=True)
+    comm.check()
+    g = P.ones((1000,))
+    red = dist.GradReducer(comm, timeout_s=60.0)  # timed host wait, healthy path
+    red.hook(0, g)
+    red.finish()
+    assert bits_equal(g.numpy(), np.ones(1000, np.float32))
+    n = 8192
+    a = P.zeros((n, n))
+    c = P.zeros((n, n))
+    L.call("b2_gemm", 0, 1, n, n, n, a.data_ptr, n, a.data_ptr, n, c.data_ptr, n, None, 0,
+           L.GEMM_3XBF16, comm.comm_stream)  # ~ms of work on the comm stream
+    with pytest.raises(RuntimeError, match="aborted"):
+        comm.wait(1e-6)
+    with pytest.raises(RuntimeError):
+        comm.allreduce_(P.ones((4,)))  # the aborted communicator fails loudly
+    L.synchronize()
