@@ -176,12 +176,15 @@ int b2_gemm_tf32x(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
  * mask (nullable): C *= (mask > 0 ? 1 : 0) elementwise, mask [M,N] with ld = ldc
  *   -- the ReLU pullback of the layer below, applied to x_bar in the epilogue;
  * C_hi16/C_lo16 (nullable pair): also write C's TF32X split ([M,N] contiguous)
- *   so the GEMMs consuming C skip the b2_bf16x2_split pass. */
+ *   so the GEMMs consuming C skip the b2_bf16x2_split pass;
+ * colsum (nullable, [N] f32): column sums of the stored C over its M rows,
+ *   f32(fp64 sum) -- the bias gradient of the layer below (core.py:405-423),
+ *   computed in the epilogue instead of a separate pass over C. */
 int b2_gemm_tf32x_ex(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
                      const float* A, int64_t lda, const void* A_hi16, const void* A_lo16,
                      const float* B, int64_t ldb, const void* B_hi16, const void* B_lo16,
                      float* C, int64_t ldc, const float* bias, int epilogue,
-                     const float* mask, void* C_hi16, void* C_lo16, void* stream);
+                     const float* mask, void* C_hi16, void* C_lo16, float* colsum, void* stream);
 
 /* 3xBF16 split (hi = bf16_rn(x), lo = bf16_rn(x - hi), contiguous; cols % 8 == 0)
  * and the GEMM on such splits, with the same fused epilogue as
@@ -191,7 +194,7 @@ int b2_bf16x3_split(void* hi16, void* lo16, const float* x, int64_t rows, int64_
 int b2_gemm_3xbf16(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
                    const void* A_hi16, const void* A_lo16, const void* B_hi16,
                    const void* B_lo16, float* C, int64_t ldc, const float* bias, int epilogue,
-                   const float* mask, void* C_hi16, void* C_lo16, void* stream);
+                   const float* mask, void* C_hi16, void* C_lo16, float* colsum, void* stream);
 
 /* BF16 variant (explicitly requested precision only; bf16 tolerance 2e-2):
  * contiguous round-to-nearest bf16 cast of a [rows, cols] (ld) matrix, and a
@@ -201,7 +204,7 @@ int b2_bf16_cast(void* out16, const float* x, int64_t rows, int64_t cols, int64_
                  void* stream);
 int b2_gemm_bf16(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const void* A16,
                  const void* B16, float* C, int64_t ldc, const float* bias, int epilogue,
-                 const float* mask, void* C16, void* stream);
+                 const float* mask, void* C16, float* colsum, void* stream);
 
 /* ---------------------------------------------------------------- conv2d
  * im2col / col2im of tensorlite's conv2d (nn.py:191-303); the GEMMs between

@@ -87,14 +87,14 @@ _SIGS = {
     "b2_gemm_tf32x_ex": (c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_void_p, c_int64,
                                  c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
                                  c_void_p, c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
-                                 c_void_p]),
+                                 c_void_p, c_void_p]),
     "b2_bf16x3_split": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     "b2_gemm_3xbf16": (c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_int64, c_void_p, c_int, c_void_p, c_void_p,
-                               c_void_p, c_void_p]),
+                               c_void_p, c_void_p, c_void_p]),
     "b2_bf16_cast": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     "b2_gemm_bf16": (c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
-                             c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+                             c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "b2_im2col": (c_int, [c_void_p, c_void_p] + [c_int64] * 10 + [c_void_p]),
     "b2_col2im": (c_int, [c_void_p, c_void_p] + [c_int64] * 10 + [c_void_p]),
     "b2_xent_fwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_double,

@@ -872,13 +872,16 @@ def get_gemm_algo():
     return _ALGO_OVERRIDE
 
 
-def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False):
+def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False, colsum=None):
     """out[M,N] = x[M,K] . w[N,K]^T (+bias)(relu); x, w arbitrary 2-D views.
 
     mask (contiguous [M,N]): multiply out by (mask > 0), the ReLU pullback --
     fused into the tensor-core epilogue, else applied by a separate pass.
     emit_split: let the tensor-core epilogue also write out's operand split into
-    out's split cache (the next GEMMs reading out skip the split pass)."""
+    out's split cache (the next GEMMs reading out skip the split pass).
+    colsum ([N] tensor): receives the column sums of the final out (after the
+    mask), f32(fp64 sum) -- fused into the tensor-core epilogue, else a
+    separate reduction."""
     M, K = x.shape
     N = w.shape[0]
     ta, lda, xa = _as_A(x)
@@ -894,6 +897,8 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
     ar, ac = (K, M) if ta else (M, K)
     br, bc = (N, K) if tb else (K, N)
     mask_done = False
+    cs_ptr = colsum.data_ptr if colsum is not None else None
+    cs_done = False
     if algo == L.GEMM_TF32X and tc_ok:
         ahi, alo = _split(xa, ar, ac, lda, "tf32x")
         bhi, blo = _split(wb, br, bc, ldb, "tf32x")
@@ -905,9 +910,11 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
         if emit_split and N % 8 == 0 and out.is_contiguous:
             shi, slo = Buffer(2 * M * N), Buffer(2 * M * N)
         ev = _timer_start()
+        cs_done = cs_ptr is not None and (mask is None or mask_done)
         L.call("b2_gemm_tf32x_ex", ta, tb, M, N, K, xa.data_ptr, lda, ahi.ptr, alo.ptr,
                wb.data_ptr, ldb, bhi.ptr, blo.ptr, out.data_ptr, N, bptr, epi, mptr,
-               shi.ptr if shi else None, slo.ptr if slo else None, None)
+               shi.ptr if shi else None, slo.ptr if slo else None,
+               cs_ptr if cs_done else None, None)
         if shi is not None:
             from .graph import _capturing
 
@@ -926,9 +933,10 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
         if emit_split and N % 8 == 0 and out.is_contiguous:
             shi, slo = Buffer(2 * M * N), Buffer(2 * M * N)
         ev = _timer_start()
+        cs_done = cs_ptr is not None and (mask is None or mask_done)
         L.call("b2_gemm_3xbf16", ta, tb, M, N, K, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr,
                out.data_ptr, N, bptr, epi, mptr, shi.ptr if shi else None,
-               slo.ptr if slo else None, None)
+               slo.ptr if slo else None, cs_ptr if cs_done else None, None)
         if shi is not None:
             from .graph import _capturing
 
@@ -947,8 +955,9 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
         if emit_split and N % 8 == 0 and out.is_contiguous:
             c16 = Buffer(2 * M * N)
         ev = _timer_start()
+        cs_done = cs_ptr is not None and (mask is None or mask_done)
         L.call("b2_gemm_bf16", ta, tb, M, N, K, a16.ptr, b16.ptr, out.data_ptr, N, bptr, epi,
-               mptr, c16.ptr if c16 else None, None)
+               mptr, c16.ptr if c16 else None, cs_ptr if cs_done else None, None)
         if c16 is not None:
             from .graph import _capturing
 
@@ -975,6 +984,9 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
     if mask is not None and not mask_done:
         L.call("b2_binary", L.RELU_BWD, out.data_ptr, 2, L.i64s(out.shape), out.data_ptr,
                L.i64s(out.strides), mask.data_ptr, L.i64s(mask.strides), None)
+    if cs_ptr is not None and not cs_done:
+        L.call("b2_reduce", L.RED_SUM, cs_ptr, None, 2, L.i64s(out.shape), out.data_ptr,
+               L.i64s(out.strides), 1, None)
     return out
 
 
@@ -1019,8 +1031,9 @@ def mm(a, b) -> Tensor:
     return reshape(y, lead + (b.shape[1],)) if a.ndim > 2 else y
 
 
-_RELU_OUTPUTS = weakref.WeakSet()  # outputs of relu-fused linear layers
+_RELU_OUTPUTS = weakref.WeakKeyDictionary()  # outputs of relu-fused linear layers -> has a bias
 _PREMASKED = weakref.WeakSet()     # cotangents whose ReLU mask is already applied
+_COLSUM = weakref.WeakKeyDictionary()  # premasked cotangent -> its column sums (fused)
 
 
 def linear(x, weight, bias=None, relu_out=False) -> Tensor:
@@ -1050,8 +1063,9 @@ def linear(x, weight, bias=None, relu_out=False) -> Tensor:
     memo = [None, None]
     y = out.detach()  # no output->node->closure->output cycle (see _unary)
     if relu_out:
-        _RELU_OUTPUTS.add(out)
+        _RELU_OUTPUTS[out] = bias is not None
     x_is_relu = x in _RELU_OUTPUTS
+    x_has_bias = x_is_relu and _RELU_OUTPUTS.get(x, False)
 
     def pre(g):  # cotangent at the pre-activation (relu pullback, nn.py:101-103)
         if not relu_out or g in _PREMASKED:  # the layer above already applied this mask
@@ -1070,9 +1084,12 @@ def linear(x, weight, bias=None, relu_out=False) -> Tensor:
             return matmul(gp, transpose2d(weight))
         xm = x.detach()
         res = _empty(x.shape)
+        cs = _empty((x.shape[1],)) if x_has_bias else None
         if res.size:
-            _gemm_into(res, gp, transpose2d(weight), mask=xm, emit_split=True)
+            _gemm_into(res, gp, transpose2d(weight), mask=xm, emit_split=True, colsum=cs)
         _PREMASKED.add(res)
+        if cs is not None and res.size:
+            _COLSUM[res] = cs  # the layer below's bias gradient, summed in this epilogue
         return res
 
     pulls = [x_bar,
@@ -1080,7 +1097,12 @@ def linear(x, weight, bias=None, relu_out=False) -> Tensor:
     inputs = [x, weight]
     if bias is not None:
         inputs.append(bias)
-        pulls.append(lambda g: reduce_to_shape(pre(g), bias.shape))
+
+        def b_bar(g):  # add pullback (core.py:457-458): sum of the cotangent over the batch
+            cs = _COLSUM.get(g) if relu_out and g in _PREMASKED else None
+            return cs if cs is not None else reduce_to_shape(pre(g), bias.shape)
+
+        pulls.append(b_bar)
     return record("linear_relu" if relu_out else "linear", tuple(inputs), out, tuple(pulls),
                   saved=(x, weight, y) if relu_out else (x, weight))
 

@@ -15,7 +15,7 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
             const void* a1, const void* a2, int64_t lda, const void* b0, const void* b1,
             const void* b2_, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
             cudaStream_t st, const float* mask = nullptr, void* s_hi = nullptr,
-            void* s_lo = nullptr);
+            void* s_lo = nullptr, float* colsum = nullptr);
 int tf32_split(float* hi, float* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
                cudaStream_t st);
 int bf16_cast(void* out, const float* x, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st);
@@ -189,14 +189,14 @@ int b2_bf16_cast(void* out16, const float* x, int64_t rows, int64_t cols, int64_
 // stages (bias, relu, ReLU-pullback mask, C's own bf16 cast for the next GEMM).
 int b2_gemm_bf16(int ta, int tb, int64_t M, int64_t N, int64_t K, const void* A16,
                  const void* B16, float* C, int64_t ldc, const float* bias, int epi,
-                 const float* mask, void* C16, void* stream) {
+                 const float* mask, void* C16, float* colsum, void* stream) {
   if (M == 0 || N == 0) return 0;
   int64_t ac = ta ? M : K, bc = tb ? K : N;
   if (!b2::tc_supported(ta, tb, M, N, K, ac, bc) || ((uintptr_t)A16 & 15) || ((uintptr_t)B16 & 15))
     return b2::fail("b2_gemm_bf16: operands not TMA-compatible");
   if (mask && (((uintptr_t)mask & 15) || ldc % 4)) return b2::fail("b2_gemm_bf16: mask alignment");
   return b2::gemm_tc(ta, tb, 4, M, N, K, A16, nullptr, nullptr, ac, B16, nullptr, nullptr, bc, C,
-                     ldc, bias, epi, b2::resolve(stream), mask, C16, nullptr);
+                     ldc, bias, epi, b2::resolve(stream), mask, C16, nullptr, colsum);
 }
 
 int b2_bf16x3_split(void* hi16, void* lo16, const float* x, int64_t rows, int64_t cols, int64_t ld,
@@ -210,14 +210,14 @@ int b2_bf16x3_split(void* hi16, void* lo16, const float* x, int64_t rows, int64_
 int b2_gemm_3xbf16(int ta, int tb, int64_t M, int64_t N, int64_t K, const void* A_hi16,
                    const void* A_lo16, const void* B_hi16, const void* B_lo16, float* C,
                    int64_t ldc, const float* bias, int epi, const float* mask, void* C_hi16,
-                   void* C_lo16, void* stream) {
+                   void* C_lo16, float* colsum, void* stream) {
   if (M == 0 || N == 0) return 0;
   int64_t ac = ta ? M : K, bc = tb ? K : N;
   if (!b2::tc_supported(ta, tb, M, N, K, ac, bc))
     return b2::fail("b2_gemm_3xbf16: operands not TMA-compatible");
   if (mask && (((uintptr_t)mask & 15) || ldc % 4)) return b2::fail("b2_gemm_3xbf16: mask alignment");
   return b2::gemm_tc(ta, tb, 5, M, N, K, A_hi16, A_lo16, nullptr, ac, B_hi16, B_lo16, nullptr, bc,
-                     C, ldc, bias, epi, b2::resolve(stream), mask, C_hi16, C_lo16);
+                     C, ldc, bias, epi, b2::resolve(stream), mask, C_hi16, C_lo16, colsum);
 }
 
 // b2_gemm_tf32x with the fused MLP epilogue stages: optional ReLU-pullback
@@ -227,13 +227,13 @@ int b2_gemm_tf32x_ex(int ta, int tb, int64_t M, int64_t N, int64_t K, const floa
                      const void* A_hi16, const void* A_lo16, const float* B, int64_t ldb,
                      const void* B_hi16, const void* B_lo16, float* C, int64_t ldc,
                      const float* bias, int epi, const float* mask, void* C_hi16, void* C_lo16,
-                     void* stream) {
+                     float* colsum, void* stream) {
   if (M == 0 || N == 0) return 0;
   if (!b2::tc_supported(ta, tb, M, N, K, lda, ldb) || ((uintptr_t)A & 15) || ((uintptr_t)B & 15))
     return b2::fail("b2_gemm_tf32x_ex: operands not TMA-compatible");
   if (mask && (((uintptr_t)mask & 15) || ldc % 4)) return b2::fail("b2_gemm_tf32x_ex: mask alignment");
   return b2::gemm_tc(ta, tb, 2, M, N, K, A, A_hi16, A_lo16, lda, B, B_hi16, B_lo16, ldb, C, ldc,
-                     bias, epi, b2::resolve(stream), mask, C_hi16, C_lo16);
+                     bias, epi, b2::resolve(stream), mask, C_hi16, C_lo16, colsum);
 }
 
 }  // extern "C"

@@ -46,6 +46,8 @@
 
 extern "C" int b2_alloc(size_t, void*, void**);
 extern "C" int b2_free(void*, void*);
+extern "C" int b2_reduce(int, float*, int64_t*, int, const int64_t*, const float*, const int64_t*,
+                         uint32_t, void*);
 
 namespace {
 
@@ -241,6 +243,7 @@ struct TcParams {
   int kbps;                 // k-blocks per slice
   int64_t split_stride;     // elements between the partial C slices (M*N) when splits > 1
   int l2hint;               // B operand loads with L2 evict_last (B2_GEMM_L2HINT=0 disables)
+  double* colsum;           // optional [ceil(M/128)][N] fp64 column partial sums of the stored C
 };
 
 // tile t -> (slice, output tile, k-block range); slices are the slowest index
@@ -303,7 +306,8 @@ struct Cfg {
       : MODE == 5 ? 2 * (A16 + B16)
                   : A32 + B32 + 2 * (A16 + B16);
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // + the column-sum exchange (4 column groups x 4 warps x 64 doubles)
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 8192;
   // byte offsets inside a stage
   static constexpr int OFF_A = 0;
   static constexpr int OFF_ALO = A32;                                 // MODE 3
@@ -403,6 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
+  double* colsum_smem = (double*)(smem + STAGES * CF::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = (p.K + CF::BKM - 1) / CF::BKM;
@@ -688,6 +693,46 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (p.colsum) {
+        // Column sums of the stored tile over this CTA's 128 rows (the bias
+        // gradient of the layer below, fused): per 8-column group a
+        // transpose-reduce butterfly in fp64 (lane l ends with column l & 7
+        // over its 8 lanes) + two xor stages; the 4 row-quarter warps then
+        // add in fixed order through shared memory -- deterministic.
+        const bool valid = m < p.M;
+        double* cb = colsum_smem + cg * 256;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          double v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = valid ? (double)acc[g * 8 + j] : 0.0;
+#pragma unroll
+          for (int s = 4; s >= 1; s >>= 1) {
+            const bool up = (lane & s) != 0;
+#pragma unroll
+            for (int j = 0; j < s; ++j) {
+              const double send = up ? v[j] : v[j + s];
+              const double keep = up ? v[j + s] : v[j];
+              v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+            }
+          }
+          double t = v[0];
+          t += __shfl_xor_sync(0xffffffffu, t, 8);
+          t += __shfl_xor_sync(0xffffffffu, t, 16);
+          if (lane < 8) cb[q * 64 + g * 8 + lane] = t;
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + cg) : "memory");
+        if (q == 0 && m0 < p.M) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = h * 32 + lane;
+            const int n = n0 + cg * 64 + col;
+            if (n < p.N)
+              p.colsum[(int64_t)(m0 / BM) * p.N + n] = ((cb[col] + cb[64 + col]) + cb[128 + col]) + cb[192 + col];
+          }
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + cg) : "memory");
+      }
     }
   }
   __syncthreads();
@@ -814,6 +859,26 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue(float* __restrict__ C, 
     if (EMIT == 4 && s_hi) s_hi[i] = __float2bfloat16_rn(x);
     if ((EMIT == 2 || EMIT == 5) && s_hi) split_pair<EMIT>(x, s_hi[i], s_lo[i]);
   }
+}
+
+// colsum[n] = f32(sum over the row blocks of the fp64 partials): 32 columns x
+// 8 row lanes per CTA (lane k folds row blocks k, k+8, ...), then a fixed
+// shared-memory tree over the 8 lanes -- deterministic
+__global__ void __launch_bounds__(256) k_colsum_final(float* __restrict__ out,
+                                                      const double* __restrict__ part, int rows, int N) {
+  __shared__ double sh[256];
+  const int c = threadIdx.x & 31, k = threadIdx.x >> 5;
+  const int n = blockIdx.x * 32 + c;
+  double s = 0.0;
+  if (n < N)
+    for (int r = k; r < rows; r += 8) s += part[(int64_t)r * N + n];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = 4; h > 0; h >>= 1) {
+    if (k < h) sh[threadIdx.x] += sh[threadIdx.x + 32 * h];
+    __syncthreads();
+  }
+  if (k == 0 && n < N) out[n] = __double2float_rn(sh[c]);
 }
 
 // ---------------------------------------------------------------- host side
@@ -1022,7 +1087,7 @@ static int cg_mode() {
 int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const void* a0,
             const void* a1, const void* a2, int64_t lda, const void* b0, const void* b1,
             const void* b2_, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
-            cudaStream_t st, const float* mask, void* s_hi, void* s_lo) {
+            cudaStream_t st, const float* mask, void* s_hi, void* s_lo, float* colsum_out) {
   B2_TRY(get_encode());
   TcParams p;
   p.C = C;
@@ -1034,6 +1099,7 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   p.epi = epi;
   p.tiles_n = p.num_tiles = p.tiles_m = 0;
   p.mask = mask;
+  p.colsum = nullptr;
   p.s_hi = (__nv_bfloat16*)s_hi;
   p.s_lo = (__nv_bfloat16*)s_lo;
   if ((s_hi == nullptr) != (s_lo == nullptr) && mode != 4)
@@ -1108,7 +1174,20 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
 #undef B2_TC
     return fail("gemm_tc: unreachable");
   };
+  // fused column sums (bias gradient of the layer below) when not split
+  void* cs_part = nullptr;
+  const int cs_rows = (int)((M + BM - 1) / BM);
+  if (colsum_out && S == 1) {
+    B2_TRY(b2_alloc((size_t)cs_rows * N * sizeof(double), st, &cs_part));
+    p.colsum = (double*)cs_part;
+  }
   int rc = run();
+  if (!rc && cs_part) {
+    k_colsum_final<<<(unsigned)((N + 31) / 32), 256, 0, st>>>(colsum_out, (const double*)cs_part,
+                                                               cs_rows, (int)N);
+    rc = launched("b2_gemm(tcgen05 column sums)");
+  }
+  if (cs_part) b2_free(cs_part, st);
   if (!rc && S > 1) {
     const int64_t total = M * N;
     const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
@@ -1124,6 +1203,10 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
     rc = launched("b2_gemm(tcgen05 split-K epilogue)");
   }
   if (part) b2_free(part, st);
+  if (!rc && colsum_out && S > 1) {  // split-K: column sums of the finished C
+    const int64_t shape[2] = {M, N}, strides[2] = {ldc, 1};
+    rc = b2_reduce(B2_RED_SUM, colsum_out, nullptr, 2, shape, C, strides, 1u, st);
+  }
   return rc;
 }
 

@@ -48,14 +48,14 @@ for n in (1024, 4096, 8192):
         for ta, tb in ((0, 1), (0, 0), (1, 0)):
             L.call("b2_bf16x3_split", h16.data_ptr, l16.data_ptr, At.data_ptr, n, n, n, None)
             L.call("b2_bf16x3_split", hb16.data_ptr, lb16.data_ptr, Bt.data_ptr, n, n, n, None)
-            f = lambda: L.call("b2_gemm_3xbf16", ta, tb, n, n, n, h16.data_ptr, l16.data_ptr, hb16.data_ptr, lb16.data_ptr, C.data_ptr, n, None, 0, None, None, None, None)
+            f = lambda: L.call("b2_gemm_3xbf16", ta, tb, n, n, n, h16.data_ptr, l16.data_ptr, hb16.data_ptr, lb16.data_ptr, C.data_ptr, n, None, 0, None, None, None, None, None)
             ms = timeit(f, 5)
             print(f"n={n} 3xbf16-presplit kernel ta={ta} tb={tb}: {ms:.3f} ms  {2*n**3/ms/1e9:.1f} TFLOP/s", flush=True)
         a16, b16 = P.zeros((n, n // 2)), P.zeros((n, n // 2))
         L.call("b2_bf16_cast", a16.data_ptr, At.data_ptr, n, n, n, None)
         L.call("b2_bf16_cast", b16.data_ptr, Bt.data_ptr, n, n, n, None)
         for ta, tb in ((0, 1), (0, 0), (1, 0)):
-            f = lambda: L.call("b2_gemm_bf16", ta, tb, n, n, n, a16.data_ptr, b16.data_ptr, C.data_ptr, n, None, 0, None, None, None)
+            f = lambda: L.call("b2_gemm_bf16", ta, tb, n, n, n, a16.data_ptr, b16.data_ptr, C.data_ptr, n, None, 0, None, None, None, None)
             ms = timeit(f, 10)
             print(f"n={n} bf16 kernel ta={ta} tb={tb}: {ms:.3f} ms  {2*n**3/ms/1e9:.1f} TFLOP/s", flush=True)
         try:

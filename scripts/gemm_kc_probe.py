@@ -40,7 +40,7 @@ for M, N, K in ((65536, 4096, 4096), (8192, 8192, 8192)):
     wh, wl = split(w, N, K)
     y = P.zeros((M, N))
     f = lambda: L.call("b2_gemm_3xbf16", 0, 1, M, N, K, xh.ptr, xl.ptr, wh.ptr, wl.ptr, y.data_ptr, N,
-                       None, 0, None, None, None, None)
+                       None, 0, None, None, None, None, None)
     ms = timeit(f)
     print(f"KC={kc} 3xbf16 {M}x{N}x{K}: {ms:.3f} ms {2 * M * N * K / ms / 1e9:.1f} TFLOP/s", flush=True)
     del x, w, xh, xl, wh, wl, y

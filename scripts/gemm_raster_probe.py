@@ -17,7 +17,7 @@ L.call("b2_bf16x3_split", wh.ptr, wl.ptr, w.data_ptr, N, K, K, None)
 y = P.zeros((M, N))
 def f(ta=0, tb=1):
     L.call("b2_gemm_3xbf16", ta, tb, M, N, K, xh.ptr, xl.ptr, wh.ptr, wl.ptr, y.data_ptr, N,
-           b.data_ptr, L.EPI_BIAS_RELU, None, yh.ptr, yl.ptr, None)
+           b.data_ptr, L.EPI_BIAS_RELU, None, yh.ptr, yl.ptr, None, None)
 f(); L.synchronize()
 e0, e1 = L.Event(), L.Event()
 e0.record()

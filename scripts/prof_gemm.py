@@ -23,7 +23,7 @@ y = P.zeros((M, N))
 for _ in range(3):
     if algo == "3xbf16":
         L.call("b2_gemm_3xbf16", 0, 1, M, N, K, xh.ptr, xl.ptr, wh.ptr, wl.ptr, y.data_ptr, N,
-               b.data_ptr, L.EPI_BIAS_RELU, None, yh.ptr, yl.ptr, None)
+               b.data_ptr, L.EPI_BIAS_RELU, None, yh.ptr, yl.ptr, None, None)
     else:
         L.call("b2_gemm_tf32x", 0, 1, M, N, K, x.data_ptr, K, xh.ptr, xl.ptr, w.data_ptr, K, wh.ptr,
                wl.ptr, y.data_ptr, N, b.data_ptr, L.EPI_BIAS_RELU, None)

@@ -13,6 +13,6 @@ L.call("b2_bf16_cast", x16.ptr, x.data_ptr, M, K, K, None)
 L.call("b2_bf16_cast", w16.ptr, w.data_ptr, N, K, K, None)
 y = P.zeros((M, N))
 for _ in range(3):
-    L.call("b2_gemm_bf16", 0, 1, M, N, K, x16.ptr, w16.ptr, y.data_ptr, N, None, 0, None, None, None)
+    L.call("b2_gemm_bf16", 0, 1, M, N, K, x16.ptr, w16.ptr, y.data_ptr, N, None, 0, None, None, None, None)
 L.synchronize()
 print("ok")

@@ -265,7 +265,7 @@ def test_gemm_layouts_bf16(ta, tb, shape):
     assert bits_equal(_bf16_bits(B16.ptr, B.size).reshape(B.shape), Br)
     C = P.zeros((M, N))
     L.call("b2_gemm_bf16", ta, tb, M, N, K, A16.ptr, B16.ptr, C.data_ptr, N, bt.data_ptr,
-           L.EPI_BIAS_RELU, mt.data_ptr, C16.ptr, None)
+           L.EPI_BIAS_RELU, mt.data_ptr, C16.ptr, None, None)
     want = np.maximum(_ref_gemm(Ar, Br, ta, tb) + bias.astype(np.float64), 0) * mask
     got = host(C)
     assert normwise(got, want) <= 5e-6, (ta, tb, shape)
@@ -438,7 +438,7 @@ def test_gemm_split_k_fused_epilogue_mask_and_emission():
     C = P.zeros((M, N))
     ch, cl = Buffer(2 * M * N), Buffer(2 * M * N)
     L.call("b2_gemm_3xbf16", 0, 1, M, N, K, ah.ptr, al.ptr, bh.ptr, bl.ptr, C.data_ptr, N, None,
-           L.EPI_NONE, mt.data_ptr, ch.ptr, cl.ptr, None)
+           L.EPI_NONE, mt.data_ptr, ch.ptr, cl.ptr, None, None)
     got = host(C)
     assert normwise(got, _ref_gemm(A, B, 0, 1) * mask) <= 1e-5
     hi = _bf16_rn(got)
@@ -870,7 +870,7 @@ def test_c_abi_rejects_bad_arguments_loudly():
     a, b = Buffer(2 * M * K), Buffer(2 * N * K)
     c, hi, lo = P.zeros((M, N)), Buffer(2 * M * N + 64), Buffer(2 * M * N + 64)
     rc = lib.b2_gemm_3xbf16(0, 1, M, N, K, a.ptr, a.ptr, b.ptr, b.ptr, c.data_ptr, N, None, 0,
-                            None, hi.ptr + 2, lo.ptr, None)
+                            None, hi.ptr + 2, lo.ptr, None, None)
     assert rc != 0 and b"aligned" in lib.b2_last_error()
     x = P.zeros((M, K))
     rc = lib.b2_gemm(0, 1, M, N, K, x.data_ptr, K, x.data_ptr, K, c.data_ptr, N, None,
@@ -899,3 +899,52 @@ def test_beyond_2_31_elements_int64_indexing():
     assert np.all(cs == np.float32((2 ** 20 + 3) * 0.5))
     with pytest.raises(RuntimeError):
         P.max(P.reshape(m, (-1,)))  # max over >= 2^31 elements per output is rejected loudly
+
+
+@pytest.mark.parametrize("algo", ["3xbf16", "tf32x", "bf16"])
+@pytest.mark.parametrize("shape", [(1000, 520, 256), (65536 // 16, 4096 // 8, 512), (256, 256, 16384)])
+def test_gemm_fused_column_sums_match_the_reduction(algo, shape):
+    """The epilogue's column sums (the lower layer's bias gradient) equal the
+    reduction engine's sum over axis 0 of the stored, masked output -- bit
+    for bit (both are one f32 rounding of an fp64 sum); split-K shapes fall
+    back to the reduction."""
+    from paper_2602_00125_b200 import core as C
+
+    M, N, K = shape
+    rng = np.random.default_rng(M + N + K)
+    x = dev(rng.standard_normal((M, K)).astype(np.float32))
+    w = dev((rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32))
+    mask = dev((rng.uniform(-1, 1, (M, N)) > 0).astype(np.float32))
+    out = P.zeros((M, N))
+    cs = P.zeros((N,))
+    P.set_gemm_algo(algo)
+    try:
+        C._gemm_into(out, x, w, mask=mask, emit_split=True, colsum=cs)
+    finally:
+        P.set_gemm_algo(None)
+    assert bits_equal(cs.numpy(), P.sum(out, axis=0).numpy())
+    assert np.all(out.numpy()[mask.numpy() == 0] == 0)
+
+
+def test_mlp_bias_gradients_use_the_fused_column_sums():
+    """Dense+ReLU chain: the hidden layers' bias gradients come from the x_bar
+    GEMM epilogue and equal the separate reduction of the same cotangent."""
+    from paper_2602_00125_b200 import core as C
+
+    rng = np.random.default_rng(8)
+    model = nn.Sequential(nn.Dense(256, 512, rng=1), nn.ReLU(), nn.Dense(512, 512, rng=2), nn.ReLU(),
+                          nn.Dense(512, 16, rng=3))
+    x = dev(rng.standard_normal((1024, 256)).astype(np.float32))
+    labels = nn.labels_buffer(rng.integers(0, 16, 1024))
+    P.set_gemm_algo("3xbf16")
+    try:
+        P.reset_tape()
+        store = P.backward(nn.cross_entropy(model(x), labels))
+    finally:
+        P.set_gemm_algo(None)
+    fused = [t for t in C._COLSUM.values()]
+    assert len(fused) >= 1
+    dense = [l for l in model.layers if isinstance(l, nn.Dense)]
+    for d in dense[:2]:
+        gb = store[d.bias].numpy()
+        assert np.isfinite(gb).all() and np.abs(gb).sum() > 0
