@@ -200,6 +200,20 @@ __device__ __forceinline__ void f4set(float4& q, int k, float v) {
   if (k == 0) q.x = v; else if (k == 1) q.y = v; else if (k == 2) q.z = v; else q.w = v;
 }
 
+// a / b rounded to nearest, for many a with one row-constant b: rb = RN(1/b)
+// once per row, then Markstein's correction q' = RN(q + RN(a - b q) rb) with
+// q = RN(a rb) -- exactly RN(a/b) whenever no intermediate under/overflows
+// (Markstein 1990; Muller et al., Handbook of FP Arithmetic, Thm 4.10), which
+// `ok` (b finite, >= 1) and the |a| window guarantee; anything else takes the
+// IEEE division. Three FMA-pipe ops instead of __fdiv_rn's MUFU + fixups.
+__device__ __forceinline__ float div_by(float a, float b, float rb, bool ok) {
+  const float q = __fmul_rn(a, rb);
+  const float r = __fmaf_rn(-q, b, a);
+  const float q1 = __fmaf_rn(r, rb, q);
+  const float aa = fabsf(a);
+  return (ok && aa >= 0x1p-100f && aa <= 0x1p100f) ? q1 : __fdiv_rn(a, b);
+}
+
 template <int NV>
 __device__ __forceinline__ float row_max_regs(const float4 (&v)[NV], int64_t C, int lane) {
   float m = -INFINITY;
@@ -247,13 +261,15 @@ __global__ void __launch_bounds__(256) k_softmax_fwd_v(float* __restrict__ y, fl
         if ((int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)e;
       }
     const float s = __double2float_rn(warp_sum(acc));  // sum(e, -1, keepdims)
+    const bool ok = s >= 1.0f && s <= 0x1p100f;        // s >= 1 unless the row is NaN/-inf
+    const float rs_ = __frcp_rn(s);
     float4* yr = reinterpret_cast<float4*>(y + r * C);
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int64_t q = i * 32 + lane;
       if (q * 4 < C)
-        yr[q] = make_float4(__fdiv_rn(v[i].x, s), __fdiv_rn(v[i].y, s), __fdiv_rn(v[i].z, s),
-                            __fdiv_rn(v[i].w, s));  // div(e, s)
+        yr[q] = make_float4(div_by(v[i].x, s, rs_, ok), div_by(v[i].y, s, rs_, ok),
+                            div_by(v[i].z, s, rs_, ok), div_by(v[i].w, s, rs_, ok));  // div(e, s)
     }
     if (lane == 0) {
       rs[r] = s;
@@ -285,6 +301,8 @@ __global__ void __launch_bounds__(256) k_softmax_bwd_v(float* __restrict__ gz,
     }
     const float s = rs[r], m = rm[r];
     const float ss = __fmul_rn(s, s);
+    const bool ok = s >= 1.0f && ss <= 0x1p100f;
+    const float rs_ = __frcp_rn(s), rss = __frcp_rn(ss);
     double acc = 0;
 #pragma unroll
     for (int i = 0; i < NV; ++i)
@@ -292,7 +310,7 @@ __global__ void __launch_bounds__(256) k_softmax_bwd_v(float* __restrict__ gz,
       for (int k = 0; k < 4; ++k) {
         const float e = b2::exp_f32(__fsub_rn(f4get(ev[i], k), m));
         f4set(ev[i], k, e);
-        const float t = __fdiv_rn(__fmul_rn(f4get(gv[i], k), e), ss);  // div(mul(g, e), mul(s, s))
+        const float t = div_by(__fmul_rn(f4get(gv[i], k), e), ss, rss, ok);  // div(mul(g, e), mul(s, s))
         if ((int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)(-t);  // neg, then sum(axis=-1)
       }
     const float gs = __double2float_rn(warp_sum(acc));
@@ -304,7 +322,7 @@ __global__ void __launch_bounds__(256) k_softmax_bwd_v(float* __restrict__ gz,
         float4 o;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const float ge = __fdiv_rn(f4get(gv[i], k), s);  // div(g, s) -- stored first
+          const float ge = div_by(f4get(gv[i], k), s, rs_, ok);  // div(g, s) -- stored first
           f4set(o, k, __fmul_rn(__fadd_rn(ge, gs), f4get(ev[i], k)));  // GradStore add, exp pullback
         }
         out[q] = o;
