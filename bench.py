@@ -456,10 +456,12 @@ def main():
         x.buffer.version += 1  # a new batch each step: its operand split is redone
         logits = model(x)
         loss = nn.cross_entropy(logits, labels, denom=rows)
-        red = dist.GradReducer(comm, params)
+        # all-reduce + Adam per layer on a side stream as soon as its last
+        # gradient is queued: the updates overlap the remaining backward GEMMs
+        red = dist.GradReducer(comm, params, optimizer=opt)
         store = P.backward(loss, on_leaf_ready=red.hook)
         red.finish()
-        optim.step_all(opt, params, store)
+        red.step_rest(store)
         return loss.item() if read_loss else loss
 
     for _ in range(max(args.warmup, 0)):

@@ -149,39 +149,89 @@ class Communicator:
 
 
 class GradReducer:
-    """Overlapped gradient averaging for one backward pass.
+    """Overlapped gradient averaging -- and optionally the optimizer update --
+    for one backward pass.
 
     Pass ``hook`` as ``backward(loss, on_leaf_ready=reducer.hook)``; call
-    ``finish()`` before the optimizer step. Each leaf gradient is averaged
-    in place on the communication stream as soon as backward has queued its
-    last contribution, so the all-reduces of the upper layers overlap the
-    GEMMs of the lower ones. (Leaf gradients of Dense layers are fresh
-    tensors; an aliased leaf gradient would be averaged in place too.)"""
+    ``finish()`` before the next use of the parameters. Each leaf gradient is
+    averaged in place on the communication stream as soon as backward has
+    queued its last contribution, so the all-reduces of the upper layers
+    overlap the GEMMs of the lower ones. With ``optimizer`` (and ``params``),
+    the parameter's update is launched on the same side stream right after
+    its all-reduce (or right away for a single process): a layer's weights
+    are no longer read once its last gradient is queued, so the HBM-bound
+    update kernels overlap the remaining tensor-core GEMMs of the backward.
+    (Leaf gradients of Dense layers are fresh tensors; an aliased leaf
+    gradient would be averaged in place too.)"""
 
-    def __init__(self, comm: Communicator, params=None, timeout_s=None):
+    _side = None  # per-process side stream for single-process optimizer overlap
+
+    def __init__(self, comm: Communicator, params=None, timeout_s=None, optimizer=None):
         self.comm = comm
         self._pending = []
         if timeout_s is None:
             env = os.environ.get("B2_COMM_TIMEOUT_S")
             timeout_s = float(env) if env else None
         self.timeout_s = timeout_s  # None: stay asynchronous (no host wait)
+        self.optimizer = optimizer
+        self.params = list(params) if params is not None else []
+        self._by_node = None
+        self._used = False
+        self._updated = set()
+        if optimizer is not None and not params:
+            raise ValueError("GradReducer(optimizer=...) needs the parameter list")
+
+    def _stream(self):
+        if self.comm.active:
+            return self.comm.comm_stream
+        if GradReducer._side is None:
+            s = ctypes.c_void_p()
+            L.check(L.lib().b2_stream_create(ctypes.byref(s)))
+            GradReducer._side = s.value
+        return GradReducer._side
+
+    def _param(self, node_id):
+        if self._by_node is None:
+            self._by_node = {p.node.id: p for p in self.params if p.node is not None}
+        return self._by_node.get(node_id)
 
     def hook(self, node_id, grad):
-        if not self.comm.active:
+        if not self.comm.active and self.optimizer is None:
             return
-        s = self.comm.comm_stream
+        handle = None
+        if self.optimizer is not None:
+            p = self._param(node_id)
+            if p is not None:
+                # slot creation / contiguity copies go on the engine stream
+                # BEFORE the event the side stream waits on
+                handle = self.optimizer.prepare([(p, grad)])
+                self._updated.add(id(p))
+        s = self._stream()
         ev = L.Event()
         ev.record(None)  # grad produced on the compute stream
         L.call("b2_stream_wait_event", s, ev.h)
-        self.comm.allreduce_(grad, AVG, s)
-        self._pending.append((ev, grad))
+        if self.comm.active:
+            self.comm.allreduce_(grad, AVG, s)
+        if handle is not None:
+            self.optimizer.launch(handle, stream=s)
+        self._pending.append((ev, grad, handle))
+        self._used = True
 
     def finish(self):
-        if not self.comm.active:
+        if not self._used:
             return
-        if self.timeout_s is not None:
+        if self.comm.active and self.timeout_s is not None:
             self.comm.wait(self.timeout_s)  # failure detection: error/timeout -> abort + raise
         done = L.Event()
-        done.record(self.comm.comm_stream)
-        L.call("b2_stream_wait_event", None, done.h)  # the optimizer waits for the reduces
+        done.record(self._stream())
+        L.call("b2_stream_wait_event", None, done.h)  # the next user of the params waits
         self._pending.clear()
+
+    def step_rest(self, store):
+        """Optimizer step (engine stream) for parameters that have a gradient
+        but were not updated by the hook; returns how many."""
+        if self.optimizer is None:
+            return 0
+        rest = [(p, store.get(p)) for p in self.params
+                if id(p) not in self._updated and store.get(p) is not None]
+        return self.optimizer.step_many(rest)

@@ -60,24 +60,37 @@ class Optimizer:
     def _bias_corrections(self, t):
         return 1.0, 1.0
 
-    def _launch(self, table, count):
+    def _launch(self, table, count, stream=None):
         raise NotImplementedError
 
-    def step_many(self, pairs):
-        """Update every (param, grad) pair with one kernel launch."""
+    def prepare(self, pairs):
+        """Host-side half of a step: validate, make gradients contiguous and
+        create slots (both enqueue work on the engine stream), bump the step
+        counts and build the tensor table. Returns an opaque handle for
+        `launch`."""
         pairs = list(pairs)
-        if not pairs:
-            return 0
         entries, keep = [], []
         for p, g in pairs:
             e, gg = self._entry(p, g)
             entries.append(e)
             keep.append(gg)
-        table = (L.OptTensor * len(entries))(*entries)
-        self._launch(table, len(entries))
+        table = (L.OptTensor * len(entries))(*entries) if entries else None
+        return pairs, table, keep
+
+    def launch(self, handle, stream=None):
+        """Device half: one multi-tensor kernel on `stream` (None: the engine
+        stream), which must be ordered after everything `prepare` enqueued."""
+        pairs, table, _ = handle
+        if not pairs:
+            return 0
+        self._launch(table, len(pairs), stream)
         for p, _ in pairs:
             p.buffer.version += 1  # in-place write, like param.write_flat
         return len(pairs)
+
+    def step_many(self, pairs):
+        """Update every (param, grad) pair with one kernel launch."""
+        return self.launch(self.prepare(pairs))
 
     def step(self, param, grad):
         self.step_many([(param, grad)])
@@ -91,9 +104,9 @@ class SGD(Optimizer):
         super().__init__(lr, weight_decay)
         self.momentum = momentum
 
-    def _launch(self, table, count):
+    def _launch(self, table, count, stream=None):
         L.call("b2_sgd_multi", table, count, float(self.lr), float(self.momentum),
-               float(self.weight_decay), None)
+               float(self.weight_decay), stream)
 
 
 class Adam(Optimizer):
@@ -109,9 +122,9 @@ class Adam(Optimizer):
     def _bias_corrections(self, t):
         return 1.0 - self.beta1 ** t, 1.0 - self.beta2 ** t  # optim.py:90-91
 
-    def _launch(self, table, count):
+    def _launch(self, table, count, stream=None):
         L.call("b2_adam_multi", table, count, float(self.lr), float(self.beta1),
-               float(self.beta2), float(self.eps), float(self.weight_decay), None)
+               float(self.beta2), float(self.eps), float(self.weight_decay), stream)
 
 
 class RMSprop(Optimizer):
@@ -122,9 +135,9 @@ class RMSprop(Optimizer):
         self.rho = rho
         self.eps = eps
 
-    def _launch(self, table, count):
+    def _launch(self, table, count, stream=None):
         L.call("b2_rmsprop_multi", table, count, float(self.lr), float(self.rho), float(self.eps),
-               float(self.weight_decay), None)
+               float(self.weight_decay), stream)
 
 
 def step_all(optimizer: Optimizer, parameters, grad_store):

@@ -965,3 +965,36 @@ def test_softmax_row_constant_division_exact_at_scale():
     assert bits_equal(host(y), yo)
     store = P.backward(y, seed=dev(gy))
     assert bits_equal(host(store[zt]), O.softmax_backward_composed(gy, e, s))
+
+
+@pytest.mark.parametrize("force_nccl", [False, True])
+def test_optimizer_overlapped_in_backward_matches_plain_step(force_nccl):
+    """GradReducer(optimizer=...) launches each layer's Adam update on a side
+    stream as soon as its gradient is final (after its all-reduce with NCCL):
+    three steps give bit-identical parameters to backward-then-step_all."""
+    from paper_2602_00125_b200 import dist
+    from paper_2602_00125_b200.data import build_mlp, mlp_config5
+
+    params0 = mlp_config5(0, width=256, classes=10, depth=3)
+    x = dev(np.random.default_rng(4).standard_normal((512, 256)))
+    lab = nn.labels_buffer(np.arange(512) % 10)
+    comm = dist.Communicator(dist.Env(), force_nccl=force_nccl)
+
+    def run(overlap):
+        model = build_mlp([(w.copy(), b.copy()) for w, b in params0])
+        ps = model.parameters()
+        opt = optim.Adam(lr=1e-3)
+        for _ in range(3):
+            P.reset_tape()
+            loss = nn.cross_entropy(model(x), lab, denom=512)
+            red = dist.GradReducer(comm, ps, optimizer=opt if overlap else None)
+            store = P.backward(loss, on_leaf_ready=red.hook)
+            red.finish()
+            if overlap:
+                assert red.step_rest(store) == 0
+            else:
+                optim.step_all(opt, ps, store)
+        return [host(p) for p in ps]
+
+    for a, b in zip(run(True), run(False)):
+        assert bits_equal(a, b)
