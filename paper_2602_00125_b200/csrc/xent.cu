@@ -331,6 +331,84 @@ __global__ void __launch_bounds__(256) k_softmax_bwd_v(float* __restrict__ gz,
   }
 }
 
+// Row form of the cross-entropy pullback for C % 4 == 0, 16-B aligned rows:
+// a warp per row, the row's (m, se) and label loaded once, 128-bit loads and
+// stores, no per-element 64-bit index division. Same per-element arithmetic
+// as k_xent_bwd (bit-identical).
+template <int NV>
+__global__ void __launch_bounds__(256) k_xent_bwd_v(float* __restrict__ dz, const float* __restrict__ g,
+                                                    const double* __restrict__ row_stats,
+                                                    const float* __restrict__ z,
+                                                    const int64_t* __restrict__ labels, int64_t B,
+                                                    int64_t C, double denom) {
+  const double gv = (double)g[0] / denom;  // nn.py:489
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < B; r += nw) {
+    const double m = row_stats[2 * r], se = row_stats[2 * r + 1];
+    const int64_t lab = labels[r];
+    const float4* zr = reinterpret_cast<const float4*>(z + r * C);
+    float4* out = reinterpret_cast<float4*>(dz + r * C);
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      v[i] = q * 4 < C ? __ldg(zr + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      if (q * 4 < C) {
+        float4 o;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t j = q * 4 + k;
+          const double pr = b2::exp_fast((double)f4get(v[i], k) - m) / se - (j == lab ? 1.0 : 0.0);
+          f4set(o, k, __double2float_rn(pr * gv));  // nn.py:500
+        }
+        out[q] = o;
+      }
+    }
+  }
+}
+
+// Row form of the cross-entropy forward (C % 4 == 0, 16-B aligned rows): the
+// row held in registers, one pass for the max and one for the compensated
+// sum of exp(v - m) in double (each lane a Neumaier pair, fixed butterfly).
+template <int NV>
+__global__ void __launch_bounds__(256) k_xent_rows_v(double* __restrict__ row_loss,
+                                                     double* __restrict__ row_stats,
+                                                     const float* __restrict__ z,
+                                                     const int64_t* __restrict__ labels, int64_t B,
+                                                     int64_t C) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < B; r += nw) {
+    const float4* zr = reinterpret_cast<const float4*>(z + r * C);
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      v[i] = q * 4 < C ? __ldg(zr + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const double m = (double)row_max_regs<NV>(v, C, lane);
+    double sum = 0, comp = 0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((int64_t)(i * 32 + lane) * 4 + k < C) neu_add(sum, comp, b2::exp_fast((double)f4get(v[i], k) - m));
+    const double tot = warp_sum(sum + comp);
+    if (lane == 0) {
+      row_stats[2 * r] = m;
+      row_stats[2 * r + 1] = tot;
+      row_loss[r] = m + log(tot) - (double)z[r * C + labels[r]];
+    }
+  }
+}
+
 int rows_grid(int64_t B) {
   int64_t warps = B;
   int64_t ctas = (warps + 7) / 8;
@@ -348,7 +426,20 @@ int b2_xent_fwd(float* loss, double* row_stats, const float* logits, const int64
   cudaStream_t st = b2::resolve(stream);
   void* ws = nullptr;
   B2_TRY(b2_alloc((size_t)rows * sizeof(double), st, &ws));
-  k_xent_rows<<<rows_grid(rows), 256, 0, st>>>((double*)ws, row_stats, logits, labels, rows, cols);
+  const bool vec = cols % 4 == 0 && cols <= 2048 && ((uintptr_t)logits & 15) == 0;
+  if (vec) {
+    const int nv = (int)((cols + 127) / 128);
+#define B2_XF(NV) \
+  k_xent_rows_v<NV><<<rows_grid(rows), 256, 0, st>>>((double*)ws, row_stats, logits, labels, rows, cols)
+    if (nv <= 1) B2_XF(1);
+    else if (nv <= 2) B2_XF(2);
+    else if (nv <= 4) B2_XF(4);
+    else if (nv <= 8) B2_XF(8);
+    else B2_XF(16);
+#undef B2_XF
+  } else {
+    k_xent_rows<<<rows_grid(rows), 256, 0, st>>>((double*)ws, row_stats, logits, labels, rows, cols);
+  }
   int rc = b2::launched("b2_xent_fwd(rows)");
   if (!rc) {
     k_xent_final<<<1, 1024, 0, st>>>(loss, (const double*)ws, rows, denom);
@@ -362,6 +453,20 @@ int b2_xent_bwd(float* dlogits, const float* g, const double* row_stats, const f
                 const int64_t* labels, int64_t rows, int64_t cols, double denom, void* stream) {
   if (rows <= 0 || cols <= 0) return 0;
   cudaStream_t st = b2::resolve(stream);
+  const bool vec = cols % 4 == 0 && cols <= 2048 && ((uintptr_t)logits & 15) == 0 &&
+                   ((uintptr_t)dlogits & 15) == 0;
+  if (vec) {
+    const int nv = (int)((cols + 127) / 128);
+#define B2_XB(NV) \
+  k_xent_bwd_v<NV><<<rows_grid(rows), 256, 0, st>>>(dlogits, g, row_stats, logits, labels, rows, cols, denom)
+    if (nv <= 1) B2_XB(1);
+    else if (nv <= 2) B2_XB(2);
+    else if (nv <= 4) B2_XB(4);
+    else if (nv <= 8) B2_XB(8);
+    else B2_XB(16);
+#undef B2_XB
+    return b2::launched("b2_xent_bwd");
+  }
   int grid = b2::grid_for(rows * cols, 256 * 8, 8);
   k_xent_bwd<<<grid, 256, 0, st>>>(dlogits, g, row_stats, logits, labels, rows, cols, denom);
   return b2::launched("b2_xent_bwd");
