@@ -196,6 +196,38 @@ int b2_gemm_3xbf16(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
                    const void* B_lo16, float* C, int64_t ldc, const float* bias, int epilogue,
                    const float* mask, void* C_hi16, void* C_lo16, float* colsum, void* stream);
 
+/* The fused tensor-core GEMM of the MLP chain, one descriptor for every
+ * epilogue stage (C = opA(A) . opB(B) as b2_gemm):
+ *   algo B2_GEMM_3XBF16: a = {A_hi16, A_lo16}, b = {B_hi16, B_lo16} (contiguous splits);
+ *   algo B2_GEMM_TF32X:  a = {A, A_hi16, A_lo16} (A with lda), b likewise;
+ *   algo B2_GEMM_BF16_VARIANT: a = {A16}, b = {B16} (contiguous bf16 casts).
+ * Epilogue, in order: + bias, ReLU, then the ReLU pullback of the layer below
+ * (mask_bits: 1 bit per element as written by relu_bits_out, else mask: a
+ * float tensor read as > 0), stores, C's own operand split (c_hi/c_lo; c_hi
+ * alone = bf16 cast for BF16_VARIANT), relu_bits_out (C > 0 as bits, words
+ * of 64 columns, ceil(N/64) words per row; needs a ReLU epilogue), colsum
+ * (column sums of C, f32(fp64)). All pointers nullable except operands/C. */
+enum { B2_GEMM_BF16_VARIANT = 6 };
+typedef struct b2_gemm_desc {
+  int algo, trans_a, trans_b;
+  int64_t M, N, K;
+  const void* a[3];
+  int64_t lda;
+  const void* b[3];
+  int64_t ldb;
+  float* C;
+  int64_t ldc;
+  const float* bias;
+  int epilogue;
+  const float* mask;
+  const uint64_t* mask_bits;
+  void* c_hi;
+  void* c_lo;
+  uint64_t* relu_bits_out;
+  float* colsum;
+} b2_gemm_desc;
+int b2_gemm_fused(const b2_gemm_desc* desc, void* stream);
+
 /* BF16 variant (explicitly requested precision only; bf16 tolerance 2e-2):
  * contiguous round-to-nearest bf16 cast of a [rows, cols] (ld) matrix, and a
  * GEMM on such casts (one kind::f16 MMA per MAC, fp32 accumulation) with the

@@ -21,6 +21,16 @@ LIB_PATH = os.environ.get("B2_LIB_PATH") or os.path.join(HERE, "libb2.so")
 i64p = POINTER(c_int64)
 
 
+class GemmDesc(Structure):
+    """include/b2.h b2_gemm_desc."""
+    _fields_ = [("algo", c_int), ("trans_a", c_int), ("trans_b", c_int), ("M", c_int64),
+                ("N", c_int64), ("K", c_int64), ("a", c_void_p * 3), ("lda", c_int64),
+                ("b", c_void_p * 3), ("ldb", c_int64), ("C", c_void_p), ("ldc", c_int64),
+                ("bias", c_void_p), ("epilogue", c_int), ("mask", c_void_p),
+                ("mask_bits", c_void_p), ("c_hi", c_void_p), ("c_lo", c_void_p),
+                ("relu_bits_out", c_void_p), ("colsum", c_void_p)]
+
+
 class OptTensor(Structure):
     _fields_ = [("param", c_void_p), ("grad", c_void_p), ("slot0", c_void_p),
                 ("slot1", c_void_p), ("n", c_int64), ("bc1", c_double), ("bc2", c_double)]
@@ -92,6 +102,7 @@ _SIGS = {
     "b2_gemm_3xbf16": (c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_int64, c_void_p, c_int, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_void_p]),
+    "b2_gemm_fused": (c_int, [c_void_p, c_void_p]),
     "b2_bf16_cast": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     "b2_gemm_bf16": (c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                              c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import random
 import weakref
 
@@ -872,7 +873,8 @@ def get_gemm_algo():
     return _ALGO_OVERRIDE
 
 
-def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False, colsum=None):
+def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False, colsum=None,
+               mask_bits=None, bits_out=None):
     """out[M,N] = x[M,K] . w[N,K]^T (+bias)(relu); x, w arbitrary 2-D views.
 
     mask (contiguous [M,N]): multiply out by (mask > 0), the ReLU pullback --
@@ -881,7 +883,11 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
     out's split cache (the next GEMMs reading out skip the split pass).
     colsum ([N] tensor): receives the column sums of the final out (after the
     mask), f32(fp64 sum) -- fused into the tensor-core epilogue, else a
-    separate reduction."""
+    separate reduction.
+    mask_bits (Buffer): the same ReLU pullback from the bits a forward ReLU
+    GEMM wrote (only passed together with mask, the fallback); bits_out
+    (Buffer, [M][ceil(N/64)] words): record out > 0 as bits. Returns whether
+    bits_out was written (tensor-core path only)."""
     M, K = x.shape
     N = w.shape[0]
     ta, lda, xa = _as_A(x)
@@ -899,72 +905,45 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
     mask_done = False
     cs_ptr = colsum.data_ptr if colsum is not None else None
     cs_done = False
-    if algo == L.GEMM_TF32X and tc_ok:
-        ahi, alo = _split(xa, ar, ac, lda, "tf32x")
-        bhi, blo = _split(wb, br, bc, ldb, "tf32x")
-        mptr = None
-        if mask is not None and mask.is_contiguous and mask.shape == out.shape \
+    fused = {L.GEMM_TF32X: ("tf32x", L.GEMM_TF32X), L.GEMM_3XBF16: ("3xbf16", L.GEMM_3XBF16),
+             L.GEMM_BF16: ("bf16", L.GEMM_BF16)}.get(algo) if tc_ok else None
+    if fused is not None:
+        kind, dalgo = fused
+        ahi, alo = _split(xa, ar, ac, lda, kind)
+        bhi, blo = _split(wb, br, bc, ldb, kind)
+        d = L.GemmDesc()
+        d.algo, d.trans_a, d.trans_b, d.M, d.N, d.K = dalgo, ta, tb, M, N, K
+        if kind == "tf32x":
+            d.a[0], d.a[1], d.a[2] = xa.data_ptr, ahi.ptr, alo.ptr
+            d.b[0], d.b[1], d.b[2] = wb.data_ptr, bhi.ptr, blo.ptr
+        else:
+            d.a[0], d.a[1] = ahi.ptr, (alo.ptr if alo is not None else None)
+            d.b[0], d.b[1] = bhi.ptr, (blo.ptr if blo is not None else None)
+        d.lda, d.ldb, d.C, d.ldc, d.bias, d.epilogue = lda, ldb, out.data_ptr, N, bptr, epi
+        if mask_bits is not None:
+            d.mask_bits, mask_done = mask_bits.ptr, True
+        elif mask is not None and mask.is_contiguous and mask.shape == out.shape \
                 and mask.data_ptr % 16 == 0:
-            mptr, mask_done = mask.data_ptr, True
+            d.mask, mask_done = mask.data_ptr, True
         shi = slo = None
         if emit_split and N % 8 == 0 and out.is_contiguous:
-            shi, slo = Buffer(2 * M * N), Buffer(2 * M * N)
-        ev = _timer_start()
+            shi = Buffer(2 * M * N)
+            slo = Buffer(2 * M * N) if kind != "bf16" else None
+            d.c_hi, d.c_lo = shi.ptr, (slo.ptr if slo is not None else None)
+        if bits_out is not None:
+            d.relu_bits_out = bits_out.ptr
         cs_done = cs_ptr is not None and (mask is None or mask_done)
-        L.call("b2_gemm_tf32x_ex", ta, tb, M, N, K, xa.data_ptr, lda, ahi.ptr, alo.ptr,
-               wb.data_ptr, ldb, bhi.ptr, blo.ptr, out.data_ptr, N, bptr, epi, mptr,
-               shi.ptr if shi else None, slo.ptr if slo else None,
-               cs_ptr if cs_done else None, None)
+        if cs_done:
+            d.colsum = cs_ptr
+        ev = _timer_start()
+        L.call("b2_gemm_fused", ctypes.byref(d), None)
         if shi is not None:
             from .graph import _capturing
 
             buf = out.buffer
             if buf._splits is None:
                 buf._splits = {}
-            buf._splits[("tf32x", out.offset, M, N, N)] = (buf.version, shi, slo, _capturing[0])
-    elif algo == L.GEMM_3XBF16 and tc_ok:
-        ahi, alo = _split(xa, ar, ac, lda, "3xbf16")
-        bhi, blo = _split(wb, br, bc, ldb, "3xbf16")
-        mptr = None
-        if mask is not None and mask.is_contiguous and mask.shape == out.shape \
-                and mask.data_ptr % 16 == 0:
-            mptr, mask_done = mask.data_ptr, True
-        shi = slo = None
-        if emit_split and N % 8 == 0 and out.is_contiguous:
-            shi, slo = Buffer(2 * M * N), Buffer(2 * M * N)
-        ev = _timer_start()
-        cs_done = cs_ptr is not None and (mask is None or mask_done)
-        L.call("b2_gemm_3xbf16", ta, tb, M, N, K, ahi.ptr, alo.ptr, bhi.ptr, blo.ptr,
-               out.data_ptr, N, bptr, epi, mptr, shi.ptr if shi else None,
-               slo.ptr if slo else None, cs_ptr if cs_done else None, None)
-        if shi is not None:
-            from .graph import _capturing
-
-            buf = out.buffer
-            if buf._splits is None:
-                buf._splits = {}
-            buf._splits[("3xbf16", out.offset, M, N, N)] = (buf.version, shi, slo, _capturing[0])
-    elif algo == L.GEMM_BF16 and tc_ok:
-        a16, _ = _split(xa, ar, ac, lda, "bf16")
-        b16, _ = _split(wb, br, bc, ldb, "bf16")
-        mptr = None
-        if mask is not None and mask.is_contiguous and mask.shape == out.shape \
-                and mask.data_ptr % 16 == 0:
-            mptr, mask_done = mask.data_ptr, True
-        c16 = None
-        if emit_split and N % 8 == 0 and out.is_contiguous:
-            c16 = Buffer(2 * M * N)
-        ev = _timer_start()
-        cs_done = cs_ptr is not None and (mask is None or mask_done)
-        L.call("b2_gemm_bf16", ta, tb, M, N, K, a16.ptr, b16.ptr, out.data_ptr, N, bptr, epi,
-               mptr, c16.ptr if c16 else None, cs_ptr if cs_done else None, None)
-        if c16 is not None:
-            from .graph import _capturing
-
-            buf = out.buffer
-            if buf._splits is None:
-                buf._splits = {}
-            buf._splits[("bf16", out.offset, M, N, N)] = (buf.version, c16, None, _capturing[0])
+            buf._splits[(kind, out.offset, M, N, N)] = (buf.version, shi, slo, _capturing[0])
     elif algo == L.GEMM_3XTF32 and tc_ok:
         ahi, alo = _split(xa, ar, ac, lda, "3xtf32")
         bhi, blo = _split(wb, br, bc, ldb, "3xtf32")
@@ -987,7 +966,7 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
     if cs_ptr is not None and not cs_done:
         L.call("b2_reduce", L.RED_SUM, cs_ptr, None, 2, L.i64s(out.shape), out.data_ptr,
                L.i64s(out.strides), 1, None)
-    return out
+    return fused is not None and bits_out is not None
 
 
 def _timer_start():
@@ -1034,6 +1013,8 @@ def mm(a, b) -> Tensor:
 _RELU_OUTPUTS = weakref.WeakKeyDictionary()  # outputs of relu-fused linear layers -> has a bias
 _PREMASKED = weakref.WeakSet()     # cotangents whose ReLU mask is already applied
 _COLSUM = weakref.WeakKeyDictionary()  # premasked cotangent -> its column sums (fused)
+_RELU_BITS = weakref.WeakKeyDictionary()  # relu-fused output -> (buffer version, y > 0 bits)
+_RELU_BITS_ON = os.environ.get("B2_RELU_BITS", "1") != "0"  # 0: read the fp32 outputs instead
 
 
 def linear(x, weight, bias=None, relu_out=False) -> Tensor:
@@ -1059,7 +1040,9 @@ def linear(x, weight, bias=None, relu_out=False) -> Tensor:
         bc = bias if (bias is None or bias.is_contiguous) else _copy_contig(bias)
         # a hidden layer's output is the next layer's GEMM operand: let the
         # epilogue write its operand split too (no separate split pass)
-        _gemm_into(out, x, weight, bc, epi, emit_split=relu_out)
+        bits = Buffer(8 * m * ((d + 63) // 64)) if relu_out and _RELU_BITS_ON else None
+        if _gemm_into(out, x, weight, bc, epi, emit_split=relu_out, bits_out=bits):
+            _RELU_BITS[out] = (out.buffer.version, bits)
     memo = [None, None]
     y = out.detach()  # no output->node->closure->output cycle (see _unary)
     if relu_out:
@@ -1086,7 +1069,10 @@ def linear(x, weight, bias=None, relu_out=False) -> Tensor:
         res = _empty(x.shape)
         cs = _empty((x.shape[1],)) if x_has_bias else None
         if res.size:
-            _gemm_into(res, gp, transpose2d(weight), mask=xm, emit_split=True, colsum=cs)
+            vb = _RELU_BITS.get(x)
+            bits = vb[1] if vb is not None and vb[0] == x.buffer.version else None
+            _gemm_into(res, gp, transpose2d(weight), mask=xm, emit_split=True, colsum=cs,
+                       mask_bits=bits)
         _PREMASKED.add(res)
         if cs is not None and res.size:
             _COLSUM[res] = cs  # the layer below's bias gradient, summed in this epilogue

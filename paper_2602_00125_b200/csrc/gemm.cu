@@ -15,7 +15,8 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
             const void* a1, const void* a2, int64_t lda, const void* b0, const void* b1,
             const void* b2_, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
             cudaStream_t st, const float* mask = nullptr, void* s_hi = nullptr,
-            void* s_lo = nullptr, float* colsum = nullptr);
+            void* s_lo = nullptr, float* colsum = nullptr, const uint64_t* mask_bits = nullptr,
+            uint64_t* bits_out = nullptr);
 int tf32_split(float* hi, float* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
                cudaStream_t st);
 int bf16_cast(void* out, const float* x, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st);
@@ -234,6 +235,35 @@ int b2_gemm_tf32x_ex(int ta, int tb, int64_t M, int64_t N, int64_t K, const floa
   if (mask && (((uintptr_t)mask & 15) || ldc % 4)) return b2::fail("b2_gemm_tf32x_ex: mask alignment");
   return b2::gemm_tc(ta, tb, 2, M, N, K, A, A_hi16, A_lo16, lda, B, B_hi16, B_lo16, ldb, C, ldc,
                      bias, epi, b2::resolve(stream), mask, C_hi16, C_lo16, colsum);
+}
+
+// The fused tensor-core GEMM behind one descriptor (include/b2.h
+// b2_gemm_desc): every epilogue stage of the MLP chain in one launch.
+int b2_gemm_fused(const b2_gemm_desc* d, void* stream) {
+  if (!d) return b2::fail("b2_gemm_fused: null descriptor");
+  if (d->M == 0 || d->N == 0) return 0;
+  const int ta = d->trans_a, tb = d->trans_b;
+  const int64_t M = d->M, N = d->N, K = d->K;
+  const int64_t ac = ta ? M : K, bc = tb ? K : N;
+  int mode;
+  int64_t lda = d->lda, ldb = d->ldb;
+  switch (d->algo) {
+    case B2_GEMM_3XBF16: mode = 5; lda = ac; ldb = bc; break;
+    case B2_GEMM_TF32X: mode = 2; break;
+    case B2_GEMM_BF16_VARIANT: mode = 4; lda = ac; ldb = bc; break;
+    default: return b2::fail("b2_gemm_fused: algo must be 3XBF16, TF32X or BF16_VARIANT");
+  }
+  if (!b2::tc_supported(ta, tb, M, N, K, lda, ldb))
+    return b2::fail("b2_gemm_fused: operands not TMA-compatible");
+  if (d->mask && (((uintptr_t)d->mask & 15) || d->ldc % 4))
+    return b2::fail("b2_gemm_fused: mask alignment");
+  if (d->relu_bits_out && !(d->epilogue == B2_EPI_RELU || d->epilogue == B2_EPI_BIAS_RELU))
+    return b2::fail("b2_gemm_fused: relu_bits_out needs a ReLU epilogue");
+  const void* a2 = mode == 2 ? d->a[2] : nullptr;
+  const void* b2p = mode == 2 ? d->b[2] : nullptr;
+  return b2::gemm_tc(ta, tb, mode, M, N, K, d->a[0], d->a[1], a2, lda, d->b[0], d->b[1], b2p, ldb,
+                     d->C, d->ldc, d->bias, d->epilogue, b2::resolve(stream), d->mask, d->c_hi,
+                     mode == 4 ? nullptr : d->c_lo, d->colsum, d->mask_bits, d->relu_bits_out);
 }
 
 }  // extern "C"

@@ -244,6 +244,9 @@ struct TcParams {
   int64_t split_stride;     // elements between the partial C slices (M*N) when splits > 1
   int l2hint;               // B operand loads with L2 evict_last (B2_GEMM_L2HINT=0 disables)
   double* colsum;           // optional [ceil(M/128)][N] fp64 column partial sums of the stored C
+  const uint64_t* mask_bits;  // ReLU-pullback mask as bits ([M][bits_ld] words, bit j = column 64w+j)
+  uint64_t* bits_out;         // emit C > 0 as bits (ReLU forward): the next backward's mask
+  int bits_ld;                // words per row of both bit arrays = ceil(N / 64)
 };
 
 // tile t -> (slice, output tile, k-block range); slices are the slowest index
@@ -633,7 +636,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           acc[j] = x;
         }
         const bool full64 = vec_ok && nb + 64 <= p.N;
-        if (p.mask) {  // ReLU pullback of the layer below: g * (y > 0 ? 1 : 0) (nn.py:101-103)
+        if (p.bits_out) {  // ReLU forward: record y > 0 as 64 bits per (row, column group)
+          uint32_t lo = 0, hi = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            lo |= (acc[j] > 0.0f ? 1u : 0u) << j;
+            hi |= (acc[32 + j] > 0.0f ? 1u : 0u) << j;
+          }
+          if (nb < p.N) p.bits_out[m * p.bits_ld + (nb >> 6)] = ((uint64_t)hi << 32) | lo;
+        }
+        if (p.mask_bits) {  // ReLU pullback from the forward's bits: g * (y > 0 ? 1 : 0)
+          const uint64_t b = __ldg(reinterpret_cast<const unsigned long long*>(p.mask_bits) +
+                                   m * p.bits_ld + (nb >> 6));
+#pragma unroll
+          for (int j = 0; j < 64; ++j) acc[j] = __fmul_rn(acc[j], (b >> j) & 1 ? 1.0f : 0.0f);
+        } else if (p.mask) {  // ReLU pullback of the layer below: g * (y > 0 ? 1 : 0) (nn.py:101-103)
           const float* mrow = p.mask + m * p.ldc;
           if (full64) {
 #pragma unroll
@@ -844,7 +861,10 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue(float* __restrict__ C, 
                                                          int S, const float* __restrict__ bias, int epi,
                                                          const float* __restrict__ mask,
                                                          __nv_bfloat16* __restrict__ s_hi,
-                                                         __nv_bfloat16* __restrict__ s_lo) {
+                                                         __nv_bfloat16* __restrict__ s_lo,
+                                                         const uint64_t* __restrict__ mask_bits,
+                                                         unsigned long long* __restrict__ bits_out,
+                                                         int bits_ld) {
   const int64_t total = (int64_t)M * N;
   const int64_t MN = total;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -854,7 +874,11 @@ __global__ void __launch_bounds__(256) k_splitk_epilogue(float* __restrict__ C, 
     for (int sl = 0; sl < S; ++sl) x = __fadd_rn(x, part[sl * MN + i]);
     if (epi == B2_EPI_BIAS || epi == B2_EPI_BIAS_RELU) x = __fadd_rn(x, bias[n]);
     if (epi == B2_EPI_BIAS_RELU || epi == B2_EPI_RELU) x = x > 0.0f ? x : 0.0f;
-    if (mask) x = __fmul_rn(x, mask[m * ldc + n] > 0.0f ? 1.0f : 0.0f);
+    if (bits_out && x > 0.0f) atomicOr(bits_out + m * bits_ld + (n >> 6), 1ull << (n & 63));
+    if (mask_bits)
+      x = __fmul_rn(x, (mask_bits[m * bits_ld + (n >> 6)] >> (n & 63)) & 1 ? 1.0f : 0.0f);
+    else if (mask)
+      x = __fmul_rn(x, mask[m * ldc + n] > 0.0f ? 1.0f : 0.0f);
     C[m * ldc + n] = x;
     if (EMIT == 4 && s_hi) s_hi[i] = __float2bfloat16_rn(x);
     if ((EMIT == 2 || EMIT == 5) && s_hi) split_pair<EMIT>(x, s_hi[i], s_lo[i]);
@@ -1087,7 +1111,8 @@ static int cg_mode() {
 int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const void* a0,
             const void* a1, const void* a2, int64_t lda, const void* b0, const void* b1,
             const void* b2_, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
-            cudaStream_t st, const float* mask, void* s_hi, void* s_lo, float* colsum_out) {
+            cudaStream_t st, const float* mask, void* s_hi, void* s_lo, float* colsum_out,
+            const uint64_t* mask_bits, uint64_t* bits_out) {
   B2_TRY(get_encode());
   TcParams p;
   p.C = C;
@@ -1100,6 +1125,11 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   p.tiles_n = p.num_tiles = p.tiles_m = 0;
   p.mask = mask;
   p.colsum = nullptr;
+  p.mask_bits = mask_bits;
+  p.bits_out = bits_out;
+  p.bits_ld = (int)((N + 63) / 64);
+  if (((uintptr_t)mask_bits & 7) || ((uintptr_t)bits_out & 7))
+    return fail("gemm_tc: bit masks need 8-B aligned word arrays");
   p.s_hi = (__nv_bfloat16*)s_hi;
   p.s_lo = (__nv_bfloat16*)s_lo;
   if ((s_hi == nullptr) != (s_lo == nullptr) && mode != 4)
@@ -1149,6 +1179,8 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
     p.ldc = N;
     p.epi = B2_EPI_NONE;
     p.mask = nullptr;
+    p.mask_bits = nullptr;
+    p.bits_out = nullptr;
     p.s_hi = p.s_lo = nullptr;
   }
   auto run = [&]() -> int {
@@ -1193,8 +1225,13 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
     const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
     __nv_bfloat16* hi = (__nv_bfloat16*)s_hi;
     __nv_bfloat16* lo = mode == 4 ? nullptr : (__nv_bfloat16*)s_lo;
+    if (bits_out) {  // the epilogue ORs bits in: start from zero words
+      rc = cudaMemsetAsync(bits_out, 0, (size_t)M * p.bits_ld * 8, st) ? fail("gemm_tc: memset") : 0;
+      if (rc) { if (part) b2_free(part, st); return rc; }
+    }
 #define B2_SKE(E) \
-  k_splitk_epilogue<E><<<grid, 256, 0, st>>>(C, ldc, (const float*)part, (int)M, (int)N, S, bias, epi, mask, hi, lo)
+  k_splitk_epilogue<E><<<grid, 256, 0, st>>>(C, ldc, (const float*)part, (int)M, (int)N, S, bias, epi, mask, hi, lo, \
+                                          mask_bits, (unsigned long long*)bits_out, p.bits_ld)
     if (!hi) B2_SKE(0);
     else if (mode == 4) B2_SKE(4);
     else if (mode == 5) B2_SKE(5);

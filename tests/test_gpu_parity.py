@@ -16,6 +16,7 @@ from paper_2602_00125_b200 import nn, optim
 from oracle import tensorlite_np as O
 from tests.golden import inputs as I
 from tests.golden.load import bits_equal, load, normwise
+from paper_2602_00125_b200 import _lib as L
 
 pytestmark = pytest.mark.gpu
 
@@ -924,6 +925,99 @@ def test_gemm_fused_column_sums_match_the_reduction(algo, shape):
         P.set_gemm_algo(None)
     assert bits_equal(cs.numpy(), P.sum(out, axis=0).numpy())
     assert np.all(out.numpy()[mask.numpy() == 0] == 0)
+
+
+def _pack_bits(y):
+    """y > 0 as [M][ceil(N/64)] little-endian uint64 words (bit j of word w =
+    column 64 w + j) -- the layout b2_gemm_fused's relu_bits_out writes."""
+    M, N = y.shape
+    W = (N + 63) // 64
+    b = np.zeros((M, W * 64), np.uint8)
+    b[:, :N] = y > 0
+    return np.packbits(b.reshape(M, W, 64), axis=2, bitorder="little").view(np.uint64).reshape(M, W)
+
+
+def _read_words(buf, M, W):
+    import ctypes
+
+    out = np.empty((M, W), np.uint64)
+    L.call("b2_memcpy_d2h", out.ctypes.data_as(ctypes.c_void_p), buf.ptr, out.nbytes, None)
+    return out
+
+
+@pytest.mark.parametrize("algo", ["3xbf16", "tf32x", "bf16"])
+@pytest.mark.parametrize("shape", [(1000, 520, 256), (4096, 512, 512), (256, 256, 16384), (300, 72, 64)])
+def test_gemm_relu_bits_and_bitmask_pullback(algo, shape):
+    """Forward: relu_bits_out records exactly y > 0 of the stored output.
+    Backward: the pullback read from those bits gives the same bits as the
+    fp32-mask pullback -- output, emitted split and fused column sums -- also
+    on long-K shapes (split-K's second stage reads and writes the bits too)."""
+    from paper_2602_00125_b200 import core as C
+
+    M, N, K = shape
+    rng = np.random.default_rng(M * 7 + N + K)
+    x = dev(rng.standard_normal((M, K)).astype(np.float32))
+    w = dev((rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32))
+    bias = dev(rng.standard_normal(N).astype(np.float32) * 0.1)
+    g = dev(rng.standard_normal((M, K)).astype(np.float32))
+    y = P.zeros((M, N))
+    bits = P.Buffer(8 * M * ((N + 63) // 64))
+    P.set_gemm_algo(algo)
+    try:
+        assert C._gemm_into(y, x, w, bias, L.EPI_BIAS_RELU, bits_out=bits)
+        yv = y.numpy()
+        assert np.array_equal(_read_words(bits, M, (N + 63) // 64), _pack_bits(yv))
+        # dX of the layer above: [M,K] . [K,N] masked by y > 0
+        wt = dev((rng.standard_normal((K, N)) / np.sqrt(K)).astype(np.float32))
+        outs = []
+        for mb in (None, bits):
+            out, cs = P.zeros((M, N)), P.zeros((N,))
+            C._gemm_into(out, g, P.transpose2d(wt), mask=y, emit_split=True, colsum=cs, mask_bits=mb)
+            outs.append((out.numpy(), cs.numpy(), out.buffer._splits))
+    finally:
+        P.set_gemm_algo(None)
+    (o0, c0, s0), (o1, c1, s1) = outs
+    assert bits_equal(o0, o1) and bits_equal(c0, c1)
+    assert np.all(o1[yv == 0] == 0)
+    k0, k1 = next(iter(s0.values())), next(iter(s1.values()))
+    n = 2 * M * N
+    for a, b in zip(k0[1:3], k1[1:3]):
+        if a is not None:
+            assert np.array_equal(_read_bytes(a, n), _read_bytes(b, n))
+
+
+def _read_bytes(buf, n):
+    import ctypes
+
+    out = np.empty(n, np.uint8)
+    L.call("b2_memcpy_d2h", out.ctypes.data_as(ctypes.c_void_p), buf.ptr, n, None)
+    return out
+
+
+def test_mlp_relu_bits_path_matches_the_fp32_mask_path():
+    """A Dense+ReLU chain trained one step with the bitmask pullback (default)
+    and with the fp32-mask pullback (B2_RELU_BITS=0) is bit-identical."""
+    from paper_2602_00125_b200 import core as C
+
+    rng = np.random.default_rng(81)
+    x = rng.standard_normal((2048, 256)).astype(np.float32)
+    labels = nn.labels_buffer(rng.integers(0, 16, 2048))
+    res = []
+    for on in (True, False):
+        C._RELU_BITS_ON = on
+        model = nn.Sequential(nn.Dense(256, 512, rng=1), nn.ReLU(), nn.Dense(512, 384, rng=2),
+                              nn.ReLU(), nn.Dense(384, 16, rng=3))
+        P.set_gemm_algo("3xbf16")
+        try:
+            P.reset_tape()
+            store = P.backward(nn.cross_entropy(model(dev(x)), labels))
+            if on:
+                assert len(C._RELU_BITS) >= 2
+        finally:
+            P.set_gemm_algo(None)
+            C._RELU_BITS_ON = True
+        res.append(np.concatenate([store[p].numpy().ravel() for p in model.parameters()]))
+    assert bits_equal(res[0], res[1])
 
 
 def test_mlp_bias_gradients_use_the_fused_column_sums():
