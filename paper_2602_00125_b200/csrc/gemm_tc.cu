@@ -27,8 +27,8 @@
 //               running sums in registers while the MMAs fill the other
 //               accumulator; after the last chunk +bias -> relu -> ReLU-pullback
 //               mask -> stores (+ the result's own operand split for the next GEMM)
-// Few-tile long-K problems split K over CTAs (fp32 partial slices, fixed-order
-// second stage, k_splitk_epilogue). Operand majorness comes from the
+// The partial last wave (and few-tile long-K problems) split K over CTAs:
+// fp32 partial slices, fixed-order second stage k_tail_epilogue. Operand majorness comes from the
 // reference's three layouts: NT (forward, x.w^T), NN (x_bar = g.w), TN (w_bar
 // = g^T.x): K-major tiles are one TMA box per operand; MN-major tiles are
 // 128-byte-wide boxes laid side by side (UMMA LBO = box bytes).
@@ -239,9 +239,15 @@ struct TcParams {
   __nv_bfloat16* s_lo;      // ... and bf16(C - trunc_tf32(C)), both [M, N] contiguous
   int kc;                   // k-blocks per fp32 promotion chunk
   int group_n;              // raster group width in tile-columns
-  int splits;               // split-K slices (1: none); slice s covers k-blocks [s*kbps, (s+1)*kbps)
-  int kbps;                 // k-blocks per slice
-  int64_t split_stride;     // elements between the partial C slices (M*N) when splits > 1
+  // work units: units [0, full_tiles) are whole tiles (all of K); the rest
+  // split the remaining tail tiles into `splits` K slices of kbps k-blocks
+  // (slices slowest), whose fp32 partials go to ws (tile-local, BM*CG x BN
+  // each) for k_tail_epilogue. full_tiles = whole waves of the persistent
+  // grid, so the last, partial wave runs on all SMs in thinner K slices.
+  int full_tiles;
+  int splits;
+  int kbps;
+  float* ws;
   int l2hint;               // B operand loads with L2 evict_last (B2_GEMM_L2HINT=0 disables)
   double* colsum;           // optional [ceil(M/128)][N] fp64 column partial sums of the stored C
   const uint64_t* mask_bits;  // ReLU-pullback mask as bits ([M][bits_ld] words, bit j = column 64w+j)
@@ -249,13 +255,22 @@ struct TcParams {
   int bits_ld;                // words per row of both bit arrays = ceil(N / 64)
 };
 
-// tile t -> (slice, output tile, k-block range); slices are the slowest index
+// unit u -> (output tile, k-block range, partial slot); slot -1 = a whole
+// tile finished in the fused epilogue, else the unit's index into ws
 __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& tm, int& tn);
-__device__ __forceinline__ void tile_info(const TcParams& p, int t, int nkb, int& tm, int& tn,
-                                          int& kb0, int& kb1, int& ks) {
-  const int per = p.tiles_m * p.tiles_n;
-  ks = t / per;
-  tile_coords(p, t - ks * per, tm, tn);
+__device__ __forceinline__ void tile_info(const TcParams& p, int u, int nkb, int& tm, int& tn,
+                                          int& kb0, int& kb1, int& slot) {
+  if (u < p.full_tiles) {
+    tile_coords(p, u, tm, tn);
+    kb0 = 0;
+    kb1 = nkb;
+    slot = -1;
+    return;
+  }
+  const int tail = p.tiles_m * p.tiles_n - p.full_tiles;
+  slot = u - p.full_tiles;
+  const int ks = slot / tail;
+  tile_coords(p, p.full_tiles + (slot - ks * tail), tm, tn);
   kb0 = ks * p.kbps;
   kb1 = min(nkb, kb0 + p.kbps);
 }
@@ -593,7 +608,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       int tm, tn, kb0, kb1, ks;
       tile_info(p, tile, nkb, tm, tn, kb0, kb1, ks);
       const int nch = (kb1 - kb0 + KC - 1) / KC;
-      float* const Cs = p.C + (int64_t)ks * p.split_stride;  // this slice's partial (or C)
       const int m0 = tm * (BM * CG) + (int)rank * BM;
       const int n0 = tn * BN;
       float acc[64];
@@ -621,9 +635,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive_remote(mapa(smem_u32(&tempty[cb]), 0));  // the leader's barrier
         }
       }
+      if (ks >= 0) {  // a K slice of a tail tile: raw partial sums, tile-local
+        float* w = p.ws + ((int64_t)ks * (BM * CG) + (int)rank * BM + row) * BN + cg * 64;
+#pragma unroll
+        for (int j = 0; j < 64; j += 4)
+          *reinterpret_cast<float4*>(w + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        continue;
+      }
       const int64_t m = m0 + row;
       if (m < p.M) {
-        float* crow = Cs + m * p.ldc;
+        float* crow = p.C + m * p.ldc;
         const int nb = n0 + cg * 64;
 #pragma unroll
         for (int j = 0; j < 64; ++j) {
@@ -851,38 +872,61 @@ __global__ void k_bf16_cast(__nv_bfloat16* __restrict__ out, const float* __rest
   }
 }
 
-// Split-K second stage: C = epilogue(sum_s part[s]) in fixed slice order
-// (deterministic), with the same epilogue stages as the GEMM kernel: bias,
-// ReLU, the ReLU-pullback mask, and emission of C's operand split (EMIT = the
-// GEMM mode: 2 TF32X split, 5 3xBF16 split, 4 bf16 cast, 0 none).
+// Tail second stage: for each split tail tile, C = epilogue(sum_s ws[s]) in
+// fixed slice order (deterministic) with the GEMM epilogue's stages: bias,
+// ReLU, relu bits (ballot per 32 columns), the ReLU-pullback mask (bits or
+// fp32), the stores, C's operand split (EMIT = GEMM mode: 2 TF32X, 5 3xBF16,
+// 4 bf16 cast, 0 none) and the fp64 column partial sums of its 128-row block.
+// grid (tail tiles, CG row blocks of 128, BN/128 column halves), 128 x 4
+// threads: x = 128 consecutive columns, y = 32-row quarter walked in order;
+// the quarters' fp64 column sums are added in fixed order.
 template <int EMIT>
-__global__ void __launch_bounds__(256) k_splitk_epilogue(float* __restrict__ C, int64_t ldc,
-                                                         const float* __restrict__ part, int M, int N,
-                                                         int S, const float* __restrict__ bias, int epi,
-                                                         const float* __restrict__ mask,
-                                                         __nv_bfloat16* __restrict__ s_hi,
-                                                         __nv_bfloat16* __restrict__ s_lo,
-                                                         const uint64_t* __restrict__ mask_bits,
-                                                         unsigned long long* __restrict__ bits_out,
-                                                         int bits_ld) {
-  const int64_t total = (int64_t)M * N;
-  const int64_t MN = total;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = i / N, n = i - m * N;
+__global__ void __launch_bounds__(512) k_tail_epilogue(const TcParams p) {
+  __shared__ double csum[4][128];
+  const int i = blockIdx.x, cg = (int)gridDim.y;
+  const int tail = p.tiles_m * p.tiles_n - p.full_tiles;
+  int tm, tn;
+  tile_coords(p, p.full_tiles + i, tm, tn);
+  const int r0 = blockIdx.y * BM + threadIdx.y * 32;
+  const int c = blockIdx.z * 128 + threadIdx.x;
+  const int64_t n = (int64_t)tn * BN + c;
+  const int64_t mb = (int64_t)tm * (BM * cg) + blockIdx.y * BM;
+  const bool col_ok = n < p.N;
+  const float bias = (col_ok && (p.epi == B2_EPI_BIAS || p.epi == B2_EPI_BIAS_RELU)) ? p.bias[n] : 0.0f;
+  const int64_t slice = (int64_t)tail * (BM * cg) * BN;
+  const float* w = p.ws + ((int64_t)i * (BM * cg) + r0) * BN + c;
+  uint32_t* bits32 = reinterpret_cast<uint32_t*>(p.bits_out);
+  const uint32_t* mbits32 = reinterpret_cast<const uint32_t*>(p.mask_bits);
+  const bool word_ok = (n >> 5) < 2 * (int64_t)p.bits_ld;  // the words cover N rounded up to 64
+  double cs = 0.0;
+#pragma unroll 4
+  for (int r = 0; r < 32; ++r) {
+    const int64_t m = (int64_t)tm * (BM * cg) + r0 + r;
+    if (m >= p.M) break;
     float x = 0.0f;
-    for (int sl = 0; sl < S; ++sl) x = __fadd_rn(x, part[sl * MN + i]);
-    if (epi == B2_EPI_BIAS || epi == B2_EPI_BIAS_RELU) x = __fadd_rn(x, bias[n]);
-    if (epi == B2_EPI_BIAS_RELU || epi == B2_EPI_RELU) x = x > 0.0f ? x : 0.0f;
-    if (bits_out && x > 0.0f) atomicOr(bits_out + m * bits_ld + (n >> 6), 1ull << (n & 63));
-    if (mask_bits)
-      x = __fmul_rn(x, (mask_bits[m * bits_ld + (n >> 6)] >> (n & 63)) & 1 ? 1.0f : 0.0f);
-    else if (mask)
-      x = __fmul_rn(x, mask[m * ldc + n] > 0.0f ? 1.0f : 0.0f);
-    C[m * ldc + n] = x;
-    if (EMIT == 4 && s_hi) s_hi[i] = __float2bfloat16_rn(x);
-    if ((EMIT == 2 || EMIT == 5) && s_hi) split_pair<EMIT>(x, s_hi[i], s_lo[i]);
+    for (int sl = 0; sl < p.splits; ++sl) x = __fadd_rn(x, w[sl * slice + (int64_t)r * BN]);
+    if (p.epi == B2_EPI_BIAS || p.epi == B2_EPI_BIAS_RELU) x = __fadd_rn(x, bias);
+    if (p.epi == B2_EPI_BIAS_RELU || p.epi == B2_EPI_RELU) x = x > 0.0f ? x : 0.0f;
+    if (bits32) {
+      const uint32_t word = __ballot_sync(0xffffffffu, col_ok && x > 0.0f);
+      if ((threadIdx.x & 31) == 0 && word_ok) bits32[m * 2 * p.bits_ld + (n >> 5)] = word;
+    }
+    if (!col_ok) continue;
+    if (mbits32)
+      x = __fmul_rn(x, (mbits32[m * 2 * p.bits_ld + (n >> 5)] >> (n & 31)) & 1 ? 1.0f : 0.0f);
+    else if (p.mask)
+      x = __fmul_rn(x, p.mask[m * p.ldc + n] > 0.0f ? 1.0f : 0.0f);
+    p.C[m * p.ldc + n] = x;
+    if (EMIT == 4 && p.s_hi) p.s_hi[m * p.N + n] = __float2bfloat16_rn(x);
+    if ((EMIT == 2 || EMIT == 5) && p.s_hi) split_pair<EMIT>(x, p.s_hi[m * p.N + n], p.s_lo[m * p.N + n]);
+    cs += (double)x;
   }
+  if (!p.colsum) return;
+  csum[threadIdx.y][threadIdx.x] = cs;
+  __syncthreads();
+  if (threadIdx.y == 0 && col_ok && mb < p.M)
+    p.colsum[(mb / BM) * p.N + n] = ((csum[0][threadIdx.x] + csum[1][threadIdx.x]) + csum[2][threadIdx.x]) +
+                                    csum[3][threadIdx.x];
 }
 
 // colsum[n] = f32(sum over the row blocks of the fp64 partials): 32 columns x
@@ -971,7 +1015,7 @@ static int kc_for_mode(int mode) {
 }
 
 template <bool A_MN, bool B_MN, int MODE, int CG>
-int launch_tc(const Operands& o, TcParams p, cudaStream_t st) {
+int launch_tc(const Operands& o, TcParams& p, cudaStream_t st) {
   using CF = Cfg<MODE, CG>;
   CUtensorMap m[6];
   // A is [M,K] (K-major) or stored [K,M] (MN-major); B is [N,K] or stored [K,N]
@@ -1007,7 +1051,7 @@ int launch_tc(const Operands& o, TcParams p, cudaStream_t st) {
   }
   p.tiles_n = (p.N + BN - 1) / BN;
   p.tiles_m = (p.M + BM * CG - 1) / (BM * CG);
-  p.num_tiles = p.tiles_m * p.tiles_n * p.splits;
+  p.num_tiles = p.full_tiles + (p.tiles_m * p.tiles_n - p.full_tiles) * p.splits;  // units
   auto kern = k_gemm_tc<A_MN, B_MN, MODE, CG>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1146,15 +1190,32 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
     int64_t pair_tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
     cg = pair_tiles >= sms / 2 ? 2 : 1;
   }
-  // split-K when the output tiles leave most SMs idle and K is long enough
-  // (dW GEMMs: [1024 x 1024] over K = 32768; square n = 1024): slices of >= 8
-  // k-blocks, fp32 partials, a fixed-order second stage with the fused epilogue
+  // Work units (TcParams): whole waves of whole tiles, then the tail tiles
+  // split into S K slices so the last wave fills the chip. Taken where it
+  // pays for the partials' round trip and the second stage (measured,
+  // scripts/tail_probe.py): few-tile long-K GEMMs (every tile split: dW
+  // [1024 x 1024] over K = 32768, square n = 1024) and a short run of waves
+  // whose last wave is at most half full (dW [4096 x 4096] over K = 65536:
+  // 3 waves + 34 of 74 tiles). Slices >= 8 k-blocks, S <= 16. Deterministic:
+  // the partition depends only on the shape and the SM count, partials are
+  // summed in slice order.
   const int bk = (mode == 4 || mode == 5) ? 64 : BK;  // Cfg::BKM
   const int nkb = (int)((K + bk - 1) / bk);
   const int64_t tiles = ((M + (int64_t)BM * cg - 1) / ((int64_t)BM * cg)) * ((N + BN - 1) / BN);
+  const int64_t P = sms / cg;
+  int64_t full = tiles, T = 0;
   int S = 1;
-  if (tiles * cg <= sms / 2 && nkb >= 16 && splitk_enabled())  // slices of >= 8 k-blocks (K 256)
-    S = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)sms / (tiles * cg), nkb / 8, 16}));
+  if (nkb >= 16 && splitk_enabled()) {
+    if (tiles * cg <= sms / 2) {
+      full = 0;
+      T = tiles;
+    } else if (tiles >= P && tiles < 8 * P && 2 * (tiles % P) <= P) {
+      full = (tiles / P) * P;
+      T = tiles - full;
+    }
+    if (T > 0) S = (int)std::max<int64_t>(1, std::min<int64_t>({P / T, nkb / 8, 16}));
+    if (S == 1) full = tiles;
+  }
   {
     static int h = -1;
     if (h < 0) {
@@ -1163,25 +1224,16 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
     }
     p.l2hint = h;
   }
-  p.splits = 1;
+  p.full_tiles = (int)full;
+  p.splits = S;
   p.kbps = nkb;
-  p.split_stride = 0;
+  p.ws = nullptr;
   void* part = nullptr;
   if (S > 1) {
     p.kbps = (nkb + S - 1) / S;
-    S = (nkb + p.kbps - 1) / p.kbps;
-  }
-  if (S > 1) {
-    B2_TRY(b2_alloc((size_t)S * M * N * sizeof(float), st, &part));
-    p.splits = S;
-    p.split_stride = M * N;
-    p.C = (float*)part;
-    p.ldc = N;
-    p.epi = B2_EPI_NONE;
-    p.mask = nullptr;
-    p.mask_bits = nullptr;
-    p.bits_out = nullptr;
-    p.s_hi = p.s_lo = nullptr;
+    S = p.splits = (nkb + p.kbps - 1) / p.kbps;
+    B2_TRY(b2_alloc((size_t)S * T * (BM * cg) * BN * sizeof(float), st, &part));
+    p.ws = (float*)part;
   }
   auto run = [&]() -> int {
 #define B2_TC(AMN, BMN)                                                             \
@@ -1206,44 +1258,33 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
 #undef B2_TC
     return fail("gemm_tc: unreachable");
   };
-  // fused column sums (bias gradient of the layer below) when not split
+  // fused column sums (bias gradient of the layer below): fp64 partials per
+  // 128-row block from the GEMM epilogue (whole tiles) and the tail stage
   void* cs_part = nullptr;
   const int cs_rows = (int)((M + BM - 1) / BM);
-  if (colsum_out && S == 1) {
+  if (colsum_out) {
     B2_TRY(b2_alloc((size_t)cs_rows * N * sizeof(double), st, &cs_part));
     p.colsum = (double*)cs_part;
   }
   int rc = run();
+  if (!rc && S > 1) {
+    const int tail = (int)T;
+    dim3 grid2(tail, cg, BN / 128);
+#define B2_SKE(E) k_tail_epilogue<E><<<grid2, dim3(128, 4), 0, st>>>(p)
+    if (!p.s_hi) B2_SKE(0);
+    else if (mode == 4) B2_SKE(4);
+    else if (mode == 5) B2_SKE(5);
+    else B2_SKE(2);
+#undef B2_SKE
+    rc = launched("b2_gemm(tcgen05 tail K-slice epilogue)");
+  }
+  if (part) b2_free(part, st);
   if (!rc && cs_part) {
     k_colsum_final<<<(unsigned)((N + 31) / 32), 256, 0, st>>>(colsum_out, (const double*)cs_part,
                                                                cs_rows, (int)N);
     rc = launched("b2_gemm(tcgen05 column sums)");
   }
   if (cs_part) b2_free(cs_part, st);
-  if (!rc && S > 1) {
-    const int64_t total = M * N;
-    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
-    __nv_bfloat16* hi = (__nv_bfloat16*)s_hi;
-    __nv_bfloat16* lo = mode == 4 ? nullptr : (__nv_bfloat16*)s_lo;
-    if (bits_out) {  // the epilogue ORs bits in: start from zero words
-      rc = cudaMemsetAsync(bits_out, 0, (size_t)M * p.bits_ld * 8, st) ? fail("gemm_tc: memset") : 0;
-      if (rc) { if (part) b2_free(part, st); return rc; }
-    }
-#define B2_SKE(E) \
-  k_splitk_epilogue<E><<<grid, 256, 0, st>>>(C, ldc, (const float*)part, (int)M, (int)N, S, bias, epi, mask, hi, lo, \
-                                          mask_bits, (unsigned long long*)bits_out, p.bits_ld)
-    if (!hi) B2_SKE(0);
-    else if (mode == 4) B2_SKE(4);
-    else if (mode == 5) B2_SKE(5);
-    else B2_SKE(2);
-#undef B2_SKE
-    rc = launched("b2_gemm(tcgen05 split-K epilogue)");
-  }
-  if (part) b2_free(part, st);
-  if (!rc && colsum_out && S > 1) {  // split-K: column sums of the finished C
-    const int64_t shape[2] = {M, N}, strides[2] = {ldc, 1};
-    rc = b2_reduce(B2_RED_SUM, colsum_out, nullptr, 2, shape, C, strides, 1u, st);
-  }
   return rc;
 }
 

@@ -421,6 +421,29 @@ def test_gemm_split_k_few_tiles_long_k(ta, tb):
         assert normwise(host(C), ref) <= tol, (algo, ta, tb)
 
 
+@pytest.mark.parametrize("shape", [(3072, 1792, 4096), (3000, 1800, 4096), (4096, 4096, 16384)])
+def test_gemm_tail_wave_k_slices(shape):
+    """More tiles than one wave: whole waves run whole tiles, the partial
+    last wave splits its tiles into K slices (k_tail_epilogue sums them in
+    slice order). Against fp64 for every layout and scheme, ragged edges
+    included, with bias + ReLU in the second stage."""
+    M, N, K = shape
+    rng = np.random.default_rng(M + N)
+    bias = dev(rng.uniform(-1, 1, N).astype(np.float32))
+    bh = host(bias).astype(np.float64)
+    for ta, tb in ((0, 1), (0, 0), (1, 0)):
+        A = rng.uniform(-1, 1, (K, M) if ta else (M, K)).astype(np.float32)
+        B = rng.uniform(-1, 1, (N, K) if tb else (K, N)).astype(np.float32)
+        ref = np.maximum(_ref_gemm(A, B, ta, tb) + bh, 0)
+        At, Bt = dev(A), dev(B)
+        for algo, tol in ((L.GEMM_3XBF16, 1e-5), (L.GEMM_TF32X, 5e-6)):
+            C = P.zeros((M, N))
+            L.call("b2_gemm", ta, tb, M, N, K, At.data_ptr, A.shape[1], Bt.data_ptr, B.shape[1],
+                   C.data_ptr, N, bias.data_ptr, L.EPI_BIAS_RELU, algo, None)
+            assert normwise(host(C), ref) <= tol, (algo, ta, tb)
+        del A, B, At, Bt
+
+
 def test_gemm_split_k_fused_epilogue_mask_and_emission():
     """Split-K second stage applies the ReLU-pullback mask and emits C's own
     3xBF16 split exactly like the single-pass epilogue."""
@@ -903,7 +926,8 @@ def test_beyond_2_31_elements_int64_indexing():
 
 
 @pytest.mark.parametrize("algo", ["3xbf16", "tf32x", "bf16"])
-@pytest.mark.parametrize("shape", [(1000, 520, 256), (65536 // 16, 4096 // 8, 512), (256, 256, 16384)])
+@pytest.mark.parametrize("shape", [(1000, 520, 256), (65536 // 16, 4096 // 8, 512), (256, 256, 16384),
+                                   (3000, 1800, 4096)])
 def test_gemm_fused_column_sums_match_the_reduction(algo, shape):
     """The epilogue's column sums (the lower layer's bias gradient) equal the
     reduction engine's sum over axis 0 of the stored, masked output -- bit
@@ -946,7 +970,8 @@ def _read_words(buf, M, W):
 
 
 @pytest.mark.parametrize("algo", ["3xbf16", "tf32x", "bf16"])
-@pytest.mark.parametrize("shape", [(1000, 520, 256), (4096, 512, 512), (256, 256, 16384), (300, 72, 64)])
+@pytest.mark.parametrize("shape", [(1000, 520, 256), (4096, 512, 512), (256, 256, 16384), (300, 72, 64),
+                                   (3000, 1800, 4096)])
 def test_gemm_relu_bits_and_bitmask_pullback(algo, shape):
     """Forward: relu_bits_out records exactly y > 0 of the stored output.
     Backward: the pullback read from those bits gives the same bits as the
