@@ -472,11 +472,23 @@ def main():
     sampler.start()
     n0 = L.launch_count()
     e0, e1 = L.Event(), L.Event()
+    marks = []
     e0.record()
     for _ in range(args.steps):
         last = step(x_dev, y_dev)
+        if os.environ.get("B2_BENCH_DEBUG"):
+            ev = L.Event()
+            ev.record()
+            marks.append(ev)
     e1.record()
     L.synchronize()
+    if marks:
+        prev, per = e0, []
+        for ev in marks:
+            per.append(round(prev.elapsed_ms(ev), 2))
+            prev = ev
+        print("per-step ms:", per, "allocator:", L.alloc_stats(),
+              file=sys.stderr)
     launches = L.launch_count() - n0
     comm.barrier()
     ms_local = e0.elapsed_ms(e1) / args.steps

@@ -407,6 +407,23 @@ __device__ __forceinline__ void split_pair(float x, __nv_bfloat16& h, __nv_bfloa
   }
 }
 
+// Two elements at once (packed F2FP conversions): the same bits as two
+// split_pair calls, packed as bf16x2 words (element a in the low half).
+template <int MODE>
+__device__ __forceinline__ void split_pair2(float a, float b, uint32_t& h, uint32_t& l) {
+  float ta = a, tb = b;
+  if (MODE != 5) {
+    ta = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+    tb = __uint_as_float(__float_as_uint(b) & 0xFFFFE000u);
+  }
+  const __nv_bfloat162 hh = __floats2bfloat162_rn(ta, tb);
+  const float ha = MODE == 5 ? __low2float(hh) : ta;
+  const float hb = MODE == 5 ? __high2float(hh) : tb;
+  const __nv_bfloat162 ll = __floats2bfloat162_rn(__fsub_rn(a, ha), __fsub_rn(b, hb));
+  h = *reinterpret_cast<const uint32_t*>(&hh);
+  l = *reinterpret_cast<const uint32_t*>(&ll);
+}
+
 template <bool A_MN, bool B_MN, int MODE, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -646,15 +663,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (m < p.M) {
         float* crow = p.C + m * p.ldc;
         const int nb = n0 + cg * 64;
+        if (p.epi == B2_EPI_BIAS || p.epi == B2_EPI_BIAS_RELU) {
+          if (nb + 64 <= p.N && (((uintptr_t)(p.bias + nb)) & 15) == 0) {
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
-          float x = acc[j];
-          if (p.epi == B2_EPI_BIAS || p.epi == B2_EPI_BIAS_RELU) {
-            const int n = nb + j;
-            x = __fadd_rn(x, n < p.N ? __ldg(p.bias + n) : 0.0f);
+            for (int j = 0; j < 64; j += 4) {  // one broadcast 16-B load per 4 columns
+              const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + nb + j));
+              acc[j] = __fadd_rn(acc[j], b.x);
+              acc[j + 1] = __fadd_rn(acc[j + 1], b.y);
+              acc[j + 2] = __fadd_rn(acc[j + 2], b.z);
+              acc[j + 3] = __fadd_rn(acc[j + 3], b.w);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 64; ++j) acc[j] = __fadd_rn(acc[j], nb + j < p.N ? __ldg(p.bias + nb + j) : 0.0f);
           }
-          if (p.epi == B2_EPI_BIAS_RELU || p.epi == B2_EPI_RELU) x = x > 0.0f ? x : 0.0f;
-          acc[j] = x;
+        }
+        if (p.epi == B2_EPI_BIAS_RELU || p.epi == B2_EPI_RELU) {
+#pragma unroll
+          for (int j = 0; j < 64; ++j) acc[j] = acc[j] > 0.0f ? acc[j] : 0.0f;
         }
         const bool full64 = vec_ok && nb + 64 <= p.N;
         if (p.bits_out) {  // ReLU forward: record y > 0 as 64 bits per (row, column group)
@@ -718,11 +744,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (full64 && (p.N % 8) == 0) {
 #pragma unroll
             for (int j = 0; j < 64; j += 8) {
-              __align__(16) __nv_bfloat16 h[8], l[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) split_pair<MODE>(acc[j + i], h[i], l[i]);
-              *reinterpret_cast<uint4*>(hrow + nb + j) = *reinterpret_cast<const uint4*>(h);
-              *reinterpret_cast<uint4*>(lrow + nb + j) = *reinterpret_cast<const uint4*>(l);
+              uint4 hv, lv;
+              split_pair2<MODE>(acc[j], acc[j + 1], hv.x, lv.x);
+              split_pair2<MODE>(acc[j + 2], acc[j + 3], hv.y, lv.y);
+              split_pair2<MODE>(acc[j + 4], acc[j + 5], hv.z, lv.z);
+              split_pair2<MODE>(acc[j + 6], acc[j + 7], hv.w, lv.w);
+              *reinterpret_cast<uint4*>(hrow + nb + j) = hv;
+              *reinterpret_cast<uint4*>(lrow + nb + j) = lv;
             }
           } else {
 #pragma unroll
@@ -742,10 +770,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
           double v[8];
+          {  // first stage on the fp32 values (one shuffle each); the pair sum in fp64
+            const bool up = (lane & 4) != 0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = valid ? (double)acc[g * 8 + j] : 0.0;
+            for (int j = 0; j < 4; ++j) {
+              const float a = valid ? acc[g * 8 + j] : 0.0f, b = valid ? acc[g * 8 + j + 4] : 0.0f;
+              const float send = up ? a : b;
+              const float keep = up ? b : a;
+              v[j] = (double)keep + (double)__shfl_xor_sync(0xffffffffu, send, 4);
+            }
+          }
 #pragma unroll
-          for (int s = 4; s >= 1; s >>= 1) {
+          for (int s = 2; s >= 1; s >>= 1) {
             const bool up = (lane & s) != 0;
 #pragma unroll
             for (int j = 0; j < s; ++j) {

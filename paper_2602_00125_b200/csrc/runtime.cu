@@ -267,6 +267,21 @@ int b2_alloc(size_t bytes, void* stream, void** out) {
     *out = b->ptr;
     return 0;
   }
+  // a fitting block still waiting for another stream (the host ran ahead of
+  // the device): wait for that stream instead of growing the pool -- bounded
+  // memory and no cudaMalloc stall in steady state
+  for (size_t i = 0; !g_capture && i < g_pending.size(); ++i) {
+    Block* b = g_pending[i].blk;
+    if (b->stream != st || b->size < sz || b->size - sz > slack) continue;
+    cudaEventSynchronize(g_pending[i].ev);
+    cudaEventDestroy(g_pending[i].ev);
+    g_pending.erase(g_pending.begin() + (std::ptrdiff_t)i);
+    g_live[b->ptr] = b;
+    g_in_use += b->size;
+    if (g_in_use > g_peak) g_peak = g_in_use;
+    *out = b->ptr;
+    return 0;
+  }
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, sz);
   if (e != cudaSuccess) {
