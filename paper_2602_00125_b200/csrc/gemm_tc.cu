@@ -1047,7 +1047,11 @@ static int kc_for_mode(int mode) {
     env = e ? atoi(e) : 0;
   }
   if (env > 0) return env;
-  return (mode == 4 || mode == 5) ? 2 * KC_BASE : KC_BASE;  // K = 1024 (BK 64) / 256 (BK 32)
+  // BF16 (bf16 variant): bf16 operand rounding dwarfs the accumulator's
+  // truncation, so chunks of K = 4096 -- one TMEM drain per tile for the
+  // config-5 shapes, the epilogue's slack a whole tile (bf16 step -7%)
+  if (mode == 4) return 8 * KC_BASE;
+  return mode == 5 ? 2 * KC_BASE : KC_BASE;  // K = 1024 (BK 64) / 256 (BK 32)
 }
 
 template <bool A_MN, bool B_MN, int MODE, int CG>
