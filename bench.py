@@ -472,22 +472,35 @@ def main():
     sampler.start()
     n0 = L.launch_count()
     e0, e1 = L.Event(), L.Event()
-    marks = []
+    marks, host_ms, gc_log = [], [], []
+    dbg = bool(os.environ.get("B2_BENCH_DEBUG"))
+    if dbg:
+        import gc
+
+        def _gc_cb(phase, info, _t=[0.0]):
+            if phase == "start":
+                _t[0] = time.perf_counter()
+            else:
+                gc_log.append((info.get("generation"), round((time.perf_counter() - _t[0]) * 1e3, 1)))
+        gc.callbacks.append(_gc_cb)
     e0.record()
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         last = step(x_dev, y_dev)
-        if os.environ.get("B2_BENCH_DEBUG"):
+        if dbg:
+            host_ms.append(round((time.perf_counter() - t0) * 1e3, 1))
             ev = L.Event()
             ev.record()
             marks.append(ev)
     e1.record()
     L.synchronize()
     if marks:
+        gc.callbacks.remove(_gc_cb)
         prev, per = e0, []
         for ev in marks:
             per.append(round(prev.elapsed_ms(ev), 2))
             prev = ev
-        print("per-step ms:", per, "allocator:", L.alloc_stats(),
+        print("per-step ms:", per, "host ms:", host_ms, "gc:", gc_log, "allocator:", L.alloc_stats(),
               file=sys.stderr)
     launches = L.launch_count() - n0
     comm.barrier()
