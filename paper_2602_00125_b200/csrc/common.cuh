@@ -15,6 +15,8 @@ int fail(const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 cudaStream_t resolve(void* stream);
 int sm_count();
+constexpr int kTickets = 4096;
+unsigned* tickets(cudaStream_t st);  // zeroed per-stream arrival counters (kTickets)
 int ensure_init();
 extern std::atomic<uint64_t> g_launches;
 

@@ -20,6 +20,7 @@
 //   contiguous x with the reduced axes one contiguous block  -> [O1, R, I]
 //   (I == 1 is a row reduction); anything else is first gathered into a
 //   [kept..., reduced...] contiguous temp and reduced as rows.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -106,6 +107,23 @@ __device__ __forceinline__ MaxAcc group_max(MaxAcc a, MaxAcc* sh) {
   return t;
 }
 
+// Single-launch second stage: thread 0 of every CTA of a group publishes the
+// CTA's partials, then arrives on the group's counter with release/acquire
+// semantics; the CTA that arrives last (it sees every other partial) folds
+// them and re-arms the counter for the next launch on this stream.
+__device__ __forceinline__ bool arrive_last(unsigned* ctr, int n, unsigned* flag) {
+  __syncthreads();  // this CTA's partial stores precede the arrival
+  if (threadIdx.x == 0) {
+    unsigned prev;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr) : "memory");
+    const bool is_last = prev == (unsigned)n - 1;
+    if (is_last) *ctr = 0;
+    *flag = is_last;
+  }
+  __syncthreads();
+  return *flag != 0;
+}
+
 // ---------------------------------------------------------------- row reduce
 // x: [O, R] contiguous rows. grid = (ceil(O / rows_per_cta), S); each group of
 // GROUP threads owns one row and the split range [s*Rs, min(R,(s+1)*Rs)).
@@ -114,9 +132,11 @@ template <int OP, int GROUP, bool VEC>
 __global__ void __launch_bounds__(256) k_rows(const float* __restrict__ x, int64_t O, int64_t R,
                                               int64_t Rs, float* __restrict__ out,
                                               int64_t* __restrict__ argr, double* __restrict__ psum,
-                                              MaxAcc* __restrict__ pmax, double count) {
+                                              MaxAcc* __restrict__ pmax, double count,
+                                              unsigned* __restrict__ ticket) {
   __shared__ double shd[8];
   __shared__ MaxAcc shm[8];
+  __shared__ unsigned last;
   constexpr int RPC = 256 / GROUP;
   const int g = threadIdx.x / GROUP, t = threadIdx.x % GROUP;
   const int64_t o = blockIdx.x * (int64_t)RPC + g;
@@ -171,12 +191,25 @@ __global__ void __launch_bounds__(256) k_rows(const float* __restrict__ x, int64
       }
     }
     const double tot = group_sum<GROUP>((a0 + a1) + (a2 + a3), shd);
-    if (live && t == 0) {
-      if (S > 1)
-        psum[(int64_t)s * O + o] = tot;
-      else
-        out[o] = OP == B2_RED_MEAN ? __double2float_rn(tot / count) : __double2float_rn(tot);
+    if (S == 1) {
+      if (live && t == 0) out[o] = OP == B2_RED_MEAN ? __double2float_rn(tot / count) : __double2float_rn(tot);
+      return;
     }
+    // thread 0 publishes the CTA's partials itself, so its release covers them
+    __shared__ double stage[RPC];
+    if (t == 0) stage[g] = tot;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < RPC; ++k)
+        if (blockIdx.x * (int64_t)RPC + k < O) psum[(int64_t)s * O + blockIdx.x * (int64_t)RPC + k] = stage[k];
+    if (!arrive_last(ticket + blockIdx.x, S, &last)) return;
+    // the last CTA of this row block folds the S partials of its rows in a
+    // fixed order: group lane t takes splits t, t+GROUP, ..., then the fixed tree
+    double f = 0;
+    if (live)
+      for (int q = t; q < S; q += GROUP) f += __ldcg(psum + (int64_t)q * O + o);
+    f = group_sum<GROUP>(f, shd);
+    if (live && t == 0) out[o] = OP == B2_RED_MEAN ? __double2float_rn(f / count) : __double2float_rn(f);
   } else {
     // each of the 4 lanes of the unroll scans its own index sequence in order
     float b0 = -INFINITY, b1 = -INFINITY, b2 = -INFINITY, b3 = -INFINITY;
@@ -223,13 +256,30 @@ __global__ void __launch_bounds__(256) k_rows(const float* __restrict__ x, int64
       }
     }
     const MaxAcc best = group_max<GROUP>(acc, shm);
-    if (live && t == 0) {
-      if (S > 1) {
-        pmax[(int64_t)s * O + o] = best;
-      } else {
+    if (S == 1) {
+      if (live && t == 0) {
         out[o] = best.v;
         if (argr) argr[o] = best.i;
       }
+      return;
+    }
+    __shared__ MaxAcc stagem[RPC];
+    if (t == 0) stagem[g] = best;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < RPC; ++k)
+        if (blockIdx.x * (int64_t)RPC + k < O) pmax[(int64_t)s * O + blockIdx.x * (int64_t)RPC + k] = stagem[k];
+    if (!arrive_last(ticket + blockIdx.x, S, &last)) return;
+    MaxAcc f{0.f, kNone};
+    if (live)
+      for (int q = t; q < S; q += GROUP) {
+        const MaxAcc* pq = pmax + (int64_t)q * O + o;
+        f = max_combine(f, MaxAcc{__ldcg(&pq->v), __ldcg(&pq->i)});
+      }
+    f = group_max<GROUP>(f, shm);
+    if (live && t == 0) {
+      out[o] = f.v;
+      if (argr) argr[o] = f.i;
     }
   }
 }
@@ -415,6 +465,164 @@ __global__ void __launch_bounds__(256) k_strip(const float* __restrict__ x, int6
   }
 }
 
+// ---------------------------------------------------------------- column reduce, cluster fold
+// x: [O1, R, I] contiguous, I % 4 == 0, 16-B aligned; reduce R. A CTA owns a
+// 32-column strip (8 column lanes x float4) and one of CS row splits; its 32
+// row lanes scan rows rl, rl+32, ... with 8 x 128-bit loads in flight (a warp
+// reads 4 rows x 128 B). The row lanes fold in a fixed order (warp butterfly,
+// then warps in index order), and the CS CTAs of a cluster -- the row splits
+// of one strip -- fold through distributed shared memory in rank order: no
+// global partials and no second launch. Measured (scripts/hbm_probe.cu): the
+// read pattern alone reaches ~82% of HBM at 512 CTAs; a separate partials
+// pass + second kernel costs ~2 us of a ~12 us op.
+template <int OP>
+__global__ void __launch_bounds__(256) k_cols(const float* __restrict__ x, int64_t R, int64_t I,
+                                              int64_t Rs, float* __restrict__ out,
+                                              int64_t* __restrict__ argr, double count,
+                                              int64_t strips) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ double shd[8][32];
+  __shared__ MaxAcc shm[OP == B2_RED_MAX ? 8 : 1][32];
+  __shared__ double cpd[32];
+  __shared__ MaxAcc cpm[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int cl = lane & 7, rl = w * 4 + (lane >> 3);  // 8 column lanes x 32 row lanes
+  constexpr int RL = 32;
+  const int64_t o1 = blockIdx.x / strips;
+  const int64_t i = ((blockIdx.x - o1 * strips) * 8 + cl) * 4;
+  const int s = blockIdx.y, S = gridDim.y;
+  const int64_t r0 = s * Rs, r1 = min(R, r0 + Rs);
+  const bool live = i < I;
+  const float* base = x + o1 * R * I + (live ? i : 0);
+  if (OP != B2_RED_MAX) {
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    if (live) {
+      int64_t r = r0 + rl;
+      for (; r + 7 * RL < r1; r += 8 * RL) {
+        float4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float4*>(base + (r + k * RL) * I));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          a0 += (double)v[k].x;
+          a1 += (double)v[k].y;
+          a2 += (double)v[k].z;
+          a3 += (double)v[k].w;
+        }
+      }
+      for (; r < r1; r += RL) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(base + r * I));
+        a0 += (double)v.x;
+        a1 += (double)v.y;
+        a2 += (double)v.z;
+        a3 += (double)v.w;
+      }
+    }
+    // fold the warp's 4 row lanes (lane bits 3, 4), then the 8 warps in order
+#pragma unroll
+    for (int off = 8; off <= 16; off <<= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, off);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, off);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, off);
+      a3 += __shfl_xor_sync(0xffffffffu, a3, off);
+    }
+    if (lane < 8) {
+      shd[w][cl * 4 + 0] = a0;
+      shd[w][cl * 4 + 1] = a1;
+      shd[w][cl * 4 + 2] = a2;
+      shd[w][cl * 4 + 3] = a3;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double t = shd[0][threadIdx.x];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) t += shd[k][threadIdx.x];
+      cpd[threadIdx.x] = t;
+    }
+    cluster.sync();
+    if (s == 0 && threadIdx.x < 32) {  // cluster rank 0 folds the row splits in rank order
+      const int64_t c = ((blockIdx.x - o1 * strips) * 8) * 4 + threadIdx.x;
+      double t = cpd[threadIdx.x];
+      for (int q = 1; q < S; ++q) t += cluster.map_shared_rank(cpd, q)[threadIdx.x];
+      if (c < I) {
+        const int64_t o = o1 * I + c;
+        out[o] = OP == B2_RED_MEAN ? __double2float_rn(t / count) : __double2float_rn(t);
+      }
+    }
+    cluster.sync();  // keep every CTA's shared memory alive until rank 0 has read it
+  } else {
+    float b[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    int bi[4] = {kNone32, kNone32, kNone32, kNone32};
+    // the first scanned slot of each column (NaN sticks, -inf ties at 0), loaded
+    // up front so the fold at the end does not wait on a global load
+    const int64_t cfirst = ((blockIdx.x - o1 * strips) * 8) * 4 + threadIdx.x;
+    const float v0 = (s == 0 && threadIdx.x < 32 && cfirst < I) ? x[o1 * R * I + cfirst] : 0.0f;
+    auto comp = [](const float4& q, int j) { return j == 0 ? q.x : j == 1 ? q.y : j == 2 ? q.z : q.w; };
+    if (live) {
+      int64_t r = r0 + rl;
+      constexpr int U = 8;
+      for (; r + (U - 1) * RL < r1; r += U * RL) {
+        float4 v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) v[k] = __ldg(reinterpret_cast<const float4*>(base + (r + k * RL) * I));
+        // per column: FMNMX tree over the U rows; only a block that beats the
+        // running best locates its first maximal row (the in-order scan's answer)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float m = comp(v[0], j);
+#pragma unroll
+          for (int k = 1; k < U; ++k) m = fmaxf(m, comp(v[k], j));
+          if (m > b[j]) {
+            int kk = U - 1;
+#pragma unroll
+            for (int k = U - 2; k >= 0; --k) kk = comp(v[k], j) == m ? k : kk;
+#pragma unroll
+            for (int k = 0; k < U; ++k) b[j] = k == kk ? comp(v[k], j) : b[j];  // keeps a zero's sign
+            bi[j] = (int)(r + kk * RL);
+          }
+        }
+      }
+      for (; r < r1; r += RL) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(base + r * I));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) max_scan(b[j], bi[j], comp(w, j), r);
+      }
+    }
+    MaxAcc acc[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = mk(b[j], bi[j]);
+#pragma unroll
+    for (int off = 8; off <= 16; off <<= 1)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] = max_combine(acc[j], shfl_max(acc[j], off));
+    if (lane < 8)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) shm[w][cl * 4 + j] = acc[j];
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      MaxAcc t = shm[0][threadIdx.x];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) t = max_combine(t, shm[k][threadIdx.x]);
+      cpm[threadIdx.x] = t;
+    }
+    cluster.sync();
+    if (s == 0 && threadIdx.x < 32) {
+      const int64_t c = ((blockIdx.x - o1 * strips) * 8) * 4 + threadIdx.x;
+      MaxAcc t = cpm[threadIdx.x];
+      for (int q = 1; q < S; ++q) t = max_combine(t, cluster.map_shared_rank(cpm, q)[threadIdx.x]);
+      if (c < I) {
+        if (isnan(v0)) t = MaxAcc{v0, 0};
+        else t = max_combine(t, MaxAcc{v0, 0});
+        const int64_t o = o1 * I + c;
+        out[o] = t.v;
+        if (argr) argr[o] = t.i;
+      }
+    }
+    cluster.sync();
+  }
+}
+
 // Second stage over partials [S][O]. A CTA owns `cpt` consecutive outputs
 // (a power of two <= 32) with 256/cpt threads per output: thread (c, k) folds
 // partials s = k, k + lpc, ... (warps read consecutive outputs: coalesced) and
@@ -551,8 +759,14 @@ int run_rows(const float* x, int64_t O, int64_t R, float* out, int64_t* argr, do
     psum = (double*)ws;
     pmax = (MaxAcc*)ws;
   }
+  unsigned* tk = nullptr;
+  if (S > 1) {
+    tk = b2::tickets(st);
+    if (!tk) return b2::fail("b2_reduce: no reduction counters for this stream");
+    if (ctas > b2::kTickets) return b2::fail("b2_reduce: too many row blocks for a split reduction");
+  }
   dim3 grid((unsigned)ctas, (unsigned)S);
-#define B2_ROWS(G, V) k_rows<OP, G, V><<<grid, 256, 0, st>>>(x, O, R, Rs, out, argr, psum, pmax, count)
+#define B2_ROWS(G, V) k_rows<OP, G, V><<<grid, 256, 0, st>>>(x, O, R, Rs, out, argr, psum, pmax, count, tk)
   if (group == 256) {
     if (vec) B2_ROWS(256, true); else B2_ROWS(256, false);
   } else {
@@ -560,10 +774,6 @@ int run_rows(const float* x, int64_t O, int64_t R, float* out, int64_t* argr, do
   }
 #undef B2_ROWS
   int rc = b2::launched("b2_reduce(rows)");
-  if (!rc && S > 1) {
-    launch_final<OP>(O, S, psum, pmax, out, argr, count, st);
-    rc = b2::launched("b2_reduce(final)");
-  }
   if (ws) b2_free(ws, st);
   return rc;
 }
@@ -573,6 +783,32 @@ int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_
             double count, cudaStream_t st) {
   const int sms = b2::sm_count();
   const int V = (I % 4 == 0 && ((uintptr_t)x & 15) == 0) ? 4 : 1;
+  if (V == 4) {
+    // cluster path: 32-column strips x CS row splits folded through DSMEM.
+    // Target ~4 resident 256-thread CTAs per SM (the probe's best); CS is a
+    // power of two <= 8 and leaves every row lane >= 8 rows.
+    const int64_t cstrips = (I + 31) / 32, base_ctas = cstrips * O1;
+    const int64_t target = 3LL * sms;  // 4 x 148 strips-splits -> cs 4 for a 4096-wide input (probe best)
+    int cs = 1;
+    while (cs < 8 && base_ctas * cs < target && R >= (int64_t)(cs * 2) * 32 * 8) cs *= 2;
+    if (base_ctas * cs >= 2LL * sms && base_ctas <= INT32_MAX) {
+      const int64_t Rs = (R + cs - 1) / cs;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)base_ctas, (unsigned)cs, 1);
+      cfg.blockDim = dim3(256, 1, 1);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 1;
+      attr[0].val.clusterDim.y = cs;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, k_cols<OP>, x, R, I, Rs, out, argr, count, cstrips);
+      if (e != cudaSuccess) return b2::cuda_fail(e, "b2_reduce(cols)");
+      return b2::launched("b2_reduce(cols)");
+    }
+  }
   // Column lanes and split policy (measured on 4096x4096, scripts/red_bench.py):
   // sums use 8 column lanes x 4 columns (128 B per row segment) and split rows
   // to fill one wave; max uses 4 x 4 (64 B segments, 4x more strips) and does

@@ -48,6 +48,23 @@ cudaStream_t resolve(void* stream) {
   return g_stream;
 }
 
+// Per-stream arrival counters for single-launch two-stage reductions (the
+// last CTA of a group folds the group's partials). Kernels on one stream run
+// in order and every kernel leaves its counters at zero, so each stream owns
+// one zeroed block, created on first use.
+unsigned* tickets(cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<cudaStream_t, unsigned*> blocks;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = blocks.find(st);
+  if (it != blocks.end()) return it->second;
+  unsigned* p = nullptr;
+  if (cudaMalloc(&p, kTickets * sizeof(unsigned)) != cudaSuccess) return nullptr;
+  if (cudaMemset(p, 0, kTickets * sizeof(unsigned)) != cudaSuccess) return nullptr;
+  blocks[st] = p;
+  return p;
+}
+
 int sm_count() {
   if (!g_sms) ensure_init();
   return g_sms ? g_sms : 148;
@@ -156,6 +173,7 @@ int b2_init(int device) {
   g_sms = prop.multiProcessorCount;
   B2_CUDA(cudaStreamCreateWithFlags(&g_stream, cudaStreamNonBlocking));
   g_device = device;
+  if (!tickets(g_stream)) return fail("b2_init: could not allocate reduction counters");
   return 0;
 }
 
