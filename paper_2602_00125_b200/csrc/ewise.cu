@@ -15,6 +15,7 @@
 //    offset of each operand is computed once per row, the innermost dim is
 //    walked with float4 when its stride is 1 and rows are 16-B aligned, a
 //    stride-0 operand is a register broadcast.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -454,6 +455,9 @@ __global__ void __launch_bounds__(kThreads) k_muladd_relu_fwd(float* __restrict_
 #ifndef B2_MULADD_CL
 #define B2_MULADD_CL 32
 #endif
+#ifndef B2_MULADD_CL_CLUSTER
+#define B2_MULADD_CL_CLUSTER 8
+#endif
 constexpr int kMuladdCL = B2_MULADD_CL;  // column lanes per CTA (x4 columns each)
 
 // backward of sum(relu(a*b + b)): ga = f32(mask*b); partial column sums of
@@ -564,6 +568,93 @@ __global__ void __launch_bounds__(256) k_muladd_relu_bwd_final(float* __restrict
   }
   // GradStore: count (add pullback) first, then f32(sum mask*a) (mul pullback)
   if (k == 0 && col < cols) gb[col] = __fadd_rn((float)sn[c], __double2float_rn(ss[c]));
+}
+
+
+// Cluster form of the fused backward (the reduce.cu k_cols scheme): a CTA
+// owns a strip of 4*CL columns and one of CS row splits; its RL = 256/CL row
+// lanes fold through shared memory in lane order, and the CS CTAs of the
+// cluster (the row splits of one strip) fold through distributed shared
+// memory in rank order -- b-bar is written by cluster rank 0, with no
+// partials pass through HBM and no second launch. Deterministic.
+template <int CL>
+__global__ void __launch_bounds__(kThreads) k_muladd_relu_bwd_cl(float* __restrict__ ga,
+                                                                 float* __restrict__ gb,
+                                                                 const float* __restrict__ a,
+                                                                 const float* __restrict__ b,
+                                                                 int64_t rows, int64_t cols,
+                                                                 int64_t rows_per_split) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int RL = kThreads / CL, W = 4 * CL;  // W columns per strip
+  __shared__ double sh_s[RL][W];
+  __shared__ int sh_n[RL][W];
+  __shared__ double cs_s[W];
+  __shared__ int cs_n[W];
+  const int cl = threadIdx.x % CL, rl = threadIdx.x / CL;
+  const int64_t col = (blockIdx.x * (int64_t)CL + cl) * 4;
+  const int64_t r0 = blockIdx.y * rows_per_split;
+  const int64_t r1 = min(rows, r0 + rows_per_split);
+  const bool live = col < cols;
+  const float4 vb = live ? *reinterpret_cast<const float4*>(b + col) : make_float4(0, 0, 0, 0);
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  int n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+  auto one = [&](const float4& va, float4* dst) {
+    const float m0 = __fadd_rn(__fmul_rn(va.x, vb.x), vb.x) > 0.f ? 1.f : 0.f;
+    const float m1 = __fadd_rn(__fmul_rn(va.y, vb.y), vb.y) > 0.f ? 1.f : 0.f;
+    const float m2 = __fadd_rn(__fmul_rn(va.z, vb.z), vb.z) > 0.f ? 1.f : 0.f;
+    const float m3 = __fadd_rn(__fmul_rn(va.w, vb.w), vb.w) > 0.f ? 1.f : 0.f;
+    *dst = make_float4(__fmul_rn(m0, vb.x), __fmul_rn(m1, vb.y), __fmul_rn(m2, vb.z),
+                       __fmul_rn(m3, vb.w));
+    s0 += (double)__fmul_rn(m0, va.x);
+    s1 += (double)__fmul_rn(m1, va.y);
+    s2 += (double)__fmul_rn(m2, va.z);
+    s3 += (double)__fmul_rn(m3, va.w);
+    n0 += m0 > 0.f;
+    n1 += m1 > 0.f;
+    n2 += m2 > 0.f;
+    n3 += m3 > 0.f;
+  };
+  if (live) {
+    int64_t r = r0 + rl;
+    for (; r + 7 * RL < r1; r += 8 * RL) {  // 8 independent 128-bit loads in flight
+      float4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float4*>(a + (r + k * RL) * cols + col));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) one(v[k], reinterpret_cast<float4*>(ga + (r + k * RL) * cols + col));
+    }
+    for (; r < r1; r += RL)
+      one(__ldg(reinterpret_cast<const float4*>(a + r * cols + col)),
+          reinterpret_cast<float4*>(ga + r * cols + col));
+  }
+  sh_s[rl][cl * 4 + 0] = s0; sh_s[rl][cl * 4 + 1] = s1; sh_s[rl][cl * 4 + 2] = s2; sh_s[rl][cl * 4 + 3] = s3;
+  sh_n[rl][cl * 4 + 0] = n0; sh_n[rl][cl * 4 + 1] = n1; sh_n[rl][cl * 4 + 2] = n2; sh_n[rl][cl * 4 + 3] = n3;
+  __syncthreads();
+  if (threadIdx.x < W) {  // row lanes in order
+    double t = sh_s[0][threadIdx.x];
+    int n = sh_n[0][threadIdx.x];
+    for (int k = 1; k < RL; ++k) {
+      t += sh_s[k][threadIdx.x];
+      n += sh_n[k][threadIdx.x];
+    }
+    cs_s[threadIdx.x] = t;
+    cs_n[threadIdx.x] = n;
+  }
+  cluster.sync();
+  if (blockIdx.y % cluster.dim_blocks().y == 0 && threadIdx.x < W) {  // rank 0: splits in rank order
+    const unsigned cs = cluster.dim_blocks().y;
+    double t = cs_s[threadIdx.x];
+    int64_t n = cs_n[threadIdx.x];
+    for (unsigned q = 1; q < cs; ++q) {
+      t += cluster.map_shared_rank(cs_s, q)[threadIdx.x];
+      n += cluster.map_shared_rank(cs_n, q)[threadIdx.x];
+    }
+    const int64_t c = blockIdx.x * (int64_t)W + threadIdx.x;
+    // GradStore: count (add pullback) first, then f32(sum mask*a) (mul pullback)
+    if (c < cols) gb[c] = __fadd_rn((float)n, __double2float_rn(t));
+  }
+  cluster.sync();  // keep each CTA's shared memory alive until rank 0 has read it
 }
 
 }  // namespace
@@ -692,6 +783,31 @@ int b2_fused_muladd_relu_bwd(float* ga, float* gb, const float* a, const float* 
   if (cols % 4 || !aligned16(a) || !aligned16(b) || !aligned16(ga))
     return b2::fail("b2_fused_muladd_relu_bwd: needs cols%4==0 and 16-B aligned rows");
   cudaStream_t st = b2::resolve(stream);
+  {
+    // cluster path: strips x CS row splits folded through DSMEM (one launch)
+    constexpr int CL = B2_MULADD_CL_CLUSTER, RL = kThreads / CL;
+    const int64_t strips = (cols + 4 * CL - 1) / (4 * CL);
+    const int64_t target = 3LL * b2::sm_count();
+    int cs = 1;
+    while (cs < 8 && strips * cs < target && rows >= (int64_t)(cs * 2) * RL * 8) cs *= 2;
+    if (strips * cs >= 2LL * b2::sm_count() && strips <= INT32_MAX) {
+      const int64_t rps = (rows + cs - 1) / cs;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)strips, (unsigned)cs, 1);
+      cfg.blockDim = dim3(kThreads, 1, 1);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 1;
+      attr[0].val.clusterDim.y = cs;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, k_muladd_relu_bwd_cl<CL>, ga, gb, a, b, rows, cols, rps);
+      if (e != cudaSuccess) return b2::cuda_fail(e, "b2_fused_muladd_relu_bwd(cluster)");
+      return b2::launched("b2_fused_muladd_relu_bwd(cluster)");
+    }
+  }
   int64_t colblocks = (cols + 4 * kMuladdCL - 1) / (4 * kMuladdCL);  // strips of 4*CL columns
   static int occ = 0;  // resident CTAs per SM: the splits fill exactly one wave
   if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_muladd_relu_bwd, kThreads, 0) !=

@@ -623,6 +623,122 @@ __global__ void __launch_bounds__(256) k_cols(const float* __restrict__ x, int64
   }
 }
 
+
+// ---------------------------------------------------------------- row splits streamed by TMA
+// Few long rows (the full sum, row sums of a handful of rows): each CTA owns a
+// run of 16-KB chunks of one row and streams them through a 4-deep
+// shared-memory ring with cp.async.bulk (one elected thread issues, an
+// mbarrier per stage carries the byte count), so the bytes in flight per SM
+// (2 CTAs x 64 KB) do not depend on registers; the threads scan shared memory
+// in row order. The row's tail past the last whole chunk goes to the last
+// split with plain loads; partials fold in the last-arriving CTA (arrive_last).
+// Measured (scripts/hbm_probe.cu): 77% of HBM for a 64 MiB full sum vs 69% for
+// register-staged loads at the best split count.
+constexpr int kBulkStages = 4, kBulkChunk = 4096;  // floats per chunk (16 KB)
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bulk_chunk(float* dst, const float* src, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)),
+               "r"(kBulkChunk * 4) : "memory");
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(su32(dst)), "l"(src), "r"(kBulkChunk * 4), "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(su32(bar)), "r"(parity) : "memory");
+}
+
+template <int OP>
+__global__ void __launch_bounds__(256) k_bulk_rows(const float* __restrict__ x, int64_t O, int64_t R,
+                                                   int64_t cps, float* __restrict__ out,
+                                                   int64_t* __restrict__ argr, double* __restrict__ psum,
+                                                   MaxAcc* __restrict__ pmax, double count,
+                                                   unsigned* __restrict__ ticket) {
+  extern __shared__ __align__(128) float sbuf[];
+  __shared__ __align__(8) uint64_t bars[kBulkStages];
+  __shared__ double shd[8];
+  __shared__ MaxAcc shm[8];
+  __shared__ unsigned last;
+  const int64_t o = blockIdx.x;
+  const int s = blockIdx.y, S = gridDim.y;
+  const float* row = x + o * R;
+  const int64_t nfull = R / kBulkChunk;
+  const int64_t c0 = min(nfull, s * cps), c1 = min(nfull, c0 + cps), nc = c1 - c0;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    for (int b = 0; b < kBulkStages; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bars[b])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int b = 0; b < kBulkStages && b < nc; ++b)
+      bulk_chunk(sbuf + b * kBulkChunk, row + (c0 + b) * kBulkChunk, &bars[b]);
+  }
+  __syncthreads();
+  double a0 = 0, a1 = 0;
+  float b0 = -INFINITY, b1 = -INFINITY, b2 = -INFINITY, b3 = -INFINITY;
+  int i0 = kNone32, i1 = kNone32, i2 = kNone32, i3 = kNone32;
+  for (int64_t c = 0; c < nc; ++c) {
+    const int st = (int)(c % kBulkStages);
+    bar_wait(&bars[st], (uint32_t)(c / kBulkStages) & 1);
+    const float4* q = reinterpret_cast<const float4*>(sbuf + st * kBulkChunk) + t;
+    const float4 v0 = q[0], v1 = q[256], v2 = q[512], v3 = q[768];
+    if (OP != B2_RED_MAX) {
+      a0 += ((double)v0.x + (double)v0.y) + ((double)v0.z + (double)v0.w);
+      a1 += ((double)v1.x + (double)v1.y) + ((double)v1.z + (double)v1.w);
+      a0 += ((double)v2.x + (double)v2.y) + ((double)v2.z + (double)v2.w);
+      a1 += ((double)v3.x + (double)v3.y) + ((double)v3.z + (double)v3.w);
+    } else {
+      const int64_t e = (c0 + c) * kBulkChunk + 4 * t;  // row-order scan per component lane
+      max_scan(b0, i0, v0.x, e);        max_scan(b1, i1, v0.y, e + 1);
+      max_scan(b2, i2, v0.z, e + 2);    max_scan(b3, i3, v0.w, e + 3);
+      max_scan(b0, i0, v1.x, e + 1024); max_scan(b1, i1, v1.y, e + 1025);
+      max_scan(b2, i2, v1.z, e + 1026); max_scan(b3, i3, v1.w, e + 1027);
+      max_scan(b0, i0, v2.x, e + 2048); max_scan(b1, i1, v2.y, e + 2049);
+      max_scan(b2, i2, v2.z, e + 2050); max_scan(b3, i3, v2.w, e + 2051);
+      max_scan(b0, i0, v3.x, e + 3072); max_scan(b1, i1, v3.y, e + 3073);
+      max_scan(b2, i2, v3.z, e + 3074); max_scan(b3, i3, v3.w, e + 3075);
+    }
+    __syncthreads();  // every thread is done with this stage before it is refilled
+    if (t == 0 && c + kBulkStages < nc)
+      bulk_chunk(sbuf + st * kBulkChunk, row + (c0 + c + kBulkStages) * kBulkChunk, &bars[st]);
+  }
+  if (s == S - 1)  // the row's tail past the last whole chunk
+    for (int64_t k = nfull * kBulkChunk + t; k < R; k += 256) {
+      if (OP != B2_RED_MAX) a0 += (double)row[k];
+      else max_scan(b0, i0, row[k], k);
+    }
+  if (OP != B2_RED_MAX) {
+    const double tot = group_sum<256>(a0 + a1, shd);
+    if (t == 0) psum[(int64_t)s * O + o] = tot;
+    if (!arrive_last(ticket + o, S, &last)) return;
+    double f = 0;
+    for (int q = t; q < S; q += 256) f += __ldcg(psum + (int64_t)q * O + o);
+    f = group_sum<256>(f, shd);
+    if (t == 0) out[o] = OP == B2_RED_MEAN ? __double2float_rn(f / count) : __double2float_rn(f);
+  } else {
+    MaxAcc acc = max_combine(max_combine(mk(b0, i0), mk(b1, i1)), max_combine(mk(b2, i2), mk(b3, i3)));
+    if (s == 0 && t == 0) {  // the first scanned slot: NaN sticks, -inf ties at index 0
+      const float v0 = row[0];
+      if (isnan(v0)) acc = MaxAcc{v0, 0};
+      else acc = max_combine(acc, MaxAcc{v0, 0});
+    }
+    const MaxAcc best = group_max<256>(acc, shm);
+    if (t == 0) pmax[(int64_t)s * O + o] = best;
+    if (!arrive_last(ticket + o, S, &last)) return;
+    MaxAcc f{0.f, kNone};
+    for (int q = t; q < S; q += 256) {
+      const MaxAcc* pq = pmax + (int64_t)q * O + o;
+      f = max_combine(f, MaxAcc{__ldcg(&pq->v), __ldcg(&pq->i)});
+    }
+    f = group_max<256>(f, shm);
+    if (t == 0) {
+      out[o] = f.v;
+      if (argr) argr[o] = f.i;
+    }
+  }
+}
+
 // Second stage over partials [S][O]. A CTA owns `cpt` consecutive outputs
 // (a power of two <= 32) with 256/cpt threads per output: thread (c, k) folds
 // partials s = k, k + lpc, ... (warps read consecutive outputs: coalesced) and
@@ -734,6 +850,29 @@ int run_rows(const float* x, int64_t O, int64_t R, float* out, int64_t* argr, do
              cudaStream_t st) {
   const bool vec = ((uintptr_t)x & 15) == 0 && R % 4 == 0;
   const int sms = b2::sm_count();
+  if (vec && O < 2 * sms && R >= 8 * kBulkChunk && O <= b2::kTickets) {
+    // few long rows: TMA-streamed splits, ~2 CTAs per SM in total
+    const int64_t nfull = R / kBulkChunk;
+    int64_t S = std::max<int64_t>(1, (2LL * sms) / O);
+    S = std::min<int64_t>(S, nfull);
+    const int64_t cps = (nfull + S - 1) / S;
+    S = (nfull + cps - 1) / cps;
+    unsigned* tk = b2::tickets(st);
+    if (!tk) return b2::fail("b2_reduce: no reduction counters for this stream");
+    void* ws = nullptr;
+    B2_TRY(b2_alloc((size_t)S * O * (OP == B2_RED_MAX ? sizeof(MaxAcc) : sizeof(double)), st, &ws));
+    const int smem = kBulkStages * kBulkChunk * 4;
+    static bool attr = false;
+    if (!attr) {
+      B2_CUDA(cudaFuncSetAttribute(k_bulk_rows<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    k_bulk_rows<OP><<<dim3((unsigned)O, (unsigned)S), 256, smem, st>>>(x, O, R, cps, out, argr, (double*)ws,
+                                                                       (MaxAcc*)ws, count, tk);
+    int rc = b2::launched("b2_reduce(bulk rows)");
+    b2_free(ws, st);
+    return rc;
+  }
   // a warp per row up to 16K elements (8 rows per CTA: no block barrier, and
   // enough bytes in flight per CTA); a whole CTA per row beyond that
   const int group = R > 16384 ? 256 : 32;
