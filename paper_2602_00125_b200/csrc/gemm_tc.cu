@@ -913,18 +913,21 @@ __global__ void k_bf16_cast(__nv_bfloat16* __restrict__ out, const float* __rest
 // ReLU, relu bits (ballot per 32 columns), the ReLU-pullback mask (bits or
 // fp32), the stores, C's operand split (EMIT = GEMM mode: 2 TF32X, 5 3xBF16,
 // 4 bf16 cast, 0 none) and the fp64 column partial sums of its 128-row block.
-// grid (tail tiles, CG row blocks of 128, BN/128 column halves), 128 x 4
-// threads: x = 128 consecutive columns, y = 32-row quarter walked in order;
-// the quarters' fp64 column sums are added in fixed order.
+// grid (tail tiles, CG row blocks of 128, BN/32 column strips), 32 x 16
+// threads: x = 32 consecutive columns (one relu-bits word per warp row),
+// y = an 8-row group walked in order; the groups' fp64 column sums are added
+// in fixed order. 8 CTAs per tile x row block keep the SMs busy (one CTA of
+// 512 threads per 128 columns left most of them idle: latency-bound).
 template <int EMIT>
 __global__ void __launch_bounds__(512) k_tail_epilogue(const TcParams p) {
-  __shared__ double csum[4][128];
+  constexpr int RG = 16, RPG = BM / RG;  // row groups x rows per group
+  __shared__ double csum[RG][32];
   const int i = blockIdx.x, cg = (int)gridDim.y;
   const int tail = p.tiles_m * p.tiles_n - p.full_tiles;
   int tm, tn;
   tile_coords(p, p.full_tiles + i, tm, tn);
-  const int r0 = blockIdx.y * BM + threadIdx.y * 32;
-  const int c = blockIdx.z * 128 + threadIdx.x;
+  const int r0 = blockIdx.y * BM + threadIdx.y * RPG;
+  const int c = blockIdx.z * 32 + threadIdx.x;
   const int64_t n = (int64_t)tn * BN + c;
   const int64_t mb = (int64_t)tm * (BM * cg) + blockIdx.y * BM;
   const bool col_ok = n < p.N;
@@ -935,12 +938,37 @@ __global__ void __launch_bounds__(512) k_tail_epilogue(const TcParams p) {
   const uint32_t* mbits32 = reinterpret_cast<const uint32_t*>(p.mask_bits);
   const bool word_ok = (n >> 5) < 2 * (int64_t)p.bits_ld;  // the words cover N rounded up to 64
   double cs = 0.0;
-#pragma unroll 4
-  for (int r = 0; r < 32; ++r) {
-    const int64_t m = (int64_t)tm * (BM * cg) + r0 + r;
-    if (m >= p.M) break;
-    float x = 0.0f;
-    for (int sl = 0; sl < p.splits; ++sl) x = __fadd_rn(x, w[sl * slice + (int64_t)r * BN]);
+  const int64_t mrow0 = (int64_t)tm * (BM * cg) + r0;
+  const int64_t left = p.M - mrow0;
+  const int nrows = left <= 0 ? 0 : (left < RPG ? (int)left : RPG);
+  // 8 rows x 4 slices of partials in flight per round (a serial walk over
+  // rows and slices would pay one L2 round trip per partial); every row still
+  // adds its slices in slice order
+  for (int rb = 0; rb < nrows; rb += 8) {
+    float acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+    for (int sl = 0; sl < p.splits; sl += 4) {
+      float v[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          v[u][q] = (sl + u < p.splits && rb + q < nrows)
+                        ? __ldcg(w + (int64_t)(sl + u) * slice + (int64_t)(rb + q) * BN)
+                        : 0.0f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (sl + u < p.splits) acc[q] = __fadd_rn(acc[q], v[u][q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+    if (rb + q >= nrows) break;
+    const int r = rb + q;
+    const int64_t m = mrow0 + r;
+    float x = acc[q];
     if (p.epi == B2_EPI_BIAS || p.epi == B2_EPI_BIAS_RELU) x = __fadd_rn(x, bias);
     if (p.epi == B2_EPI_BIAS_RELU || p.epi == B2_EPI_RELU) x = x > 0.0f ? x : 0.0f;
     if (bits32) {
@@ -956,13 +984,18 @@ __global__ void __launch_bounds__(512) k_tail_epilogue(const TcParams p) {
     if (EMIT == 4 && p.s_hi) p.s_hi[m * p.N + n] = __float2bfloat16_rn(x);
     if ((EMIT == 2 || EMIT == 5) && p.s_hi) split_pair<EMIT>(x, p.s_hi[m * p.N + n], p.s_lo[m * p.N + n]);
     cs += (double)x;
+    }
   }
   if (!p.colsum) return;
   csum[threadIdx.y][threadIdx.x] = cs;
   __syncthreads();
   if (threadIdx.y == 0 && col_ok && mb < p.M)
-    p.colsum[(mb / BM) * p.N + n] = ((csum[0][threadIdx.x] + csum[1][threadIdx.x]) + csum[2][threadIdx.x]) +
-                                    csum[3][threadIdx.x];
+  {
+    double t = csum[0][threadIdx.x];
+#pragma unroll
+    for (int g = 1; g < RG; ++g) t += csum[g][threadIdx.x];
+    p.colsum[(mb / BM) * p.N + n] = t;
+  }
 }
 
 // colsum[n] = f32(sum over the row blocks of the fp64 partials): 32 columns x
@@ -1309,8 +1342,8 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   int rc = run();
   if (!rc && S > 1) {
     const int tail = (int)T;
-    dim3 grid2(tail, cg, BN / 128);
-#define B2_SKE(E) k_tail_epilogue<E><<<grid2, dim3(128, 4), 0, st>>>(p)
+    dim3 grid2(tail, cg, BN / 32);
+#define B2_SKE(E) k_tail_epilogue<E><<<grid2, dim3(32, 16), 0, st>>>(p)
     if (!p.s_hi) B2_SKE(0);
     else if (mode == 4) B2_SKE(4);
     else if (mode == 5) B2_SKE(5);
