@@ -191,6 +191,11 @@ int b2_gemm_tf32x_ex(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
  * b2_gemm_tf32x_ex (C_hi16/C_lo16 receive C's own 3xBF16 split). */
 int b2_bf16x3_split(void* hi16, void* lo16, const float* x, int64_t rows, int64_t cols,
                     int64_t ld, void* stream);
+/* fp32 from a contiguous 3xBF16 split: out[i] = f32(hi[i]) + f32(lo[i]) (exact
+ * in fp32; within 2^-16 relative of the split's source). n % 8 == 0, 16-B
+ * aligned. Materialises a b2_gemm_fused output written with C == NULL (only
+ * its operand split), on first host-visible use. */
+int b2_bf16x3_join(float* out, const void* hi16, const void* lo16, int64_t n, void* stream);
 int b2_gemm_3xbf16(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
                    const void* A_hi16, const void* A_lo16, const void* B_hi16,
                    const void* B_lo16, float* C, int64_t ldc, const float* bias, int epilogue,
@@ -206,7 +211,9 @@ int b2_gemm_3xbf16(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
  * float tensor read as > 0), stores, C's own operand split (c_hi/c_lo; c_hi
  * alone = bf16 cast for BF16_VARIANT), relu_bits_out (C > 0 as bits, words
  * of 64 columns, ceil(N/64) words per row; needs a ReLU epilogue), colsum
- * (column sums of C, f32(fp64)). All pointers nullable except operands/C. */
+ * (column sums of C, f32(fp64)). All pointers nullable except the operands;
+ * C == NULL skips the fp32 store when only C's split/bits/column sums are
+ * consumed (the host materialises C later with b2_bf16x3_join if it is read). */
 enum { B2_GEMM_BF16_VARIANT = 6 };
 typedef struct b2_gemm_desc {
   int algo, trans_a, trans_b;

@@ -44,7 +44,7 @@ _py_max = max
 class Buffer:
     """One device allocation plus a version counter (core.py:68-75)."""
 
-    __slots__ = ("ptr", "nbytes", "version", "_splits", "__weakref__")
+    __slots__ = ("ptr", "nbytes", "version", "_splits", "_pending", "__weakref__")
 
     def __init__(self, nbytes: int):
         L.ensure_device()
@@ -54,6 +54,10 @@ class Buffer:
         self.nbytes = int(nbytes)
         self.version = 0
         self._splits = None  # {(kind, offset, rows, cols, ld): (version, hi, lo, capture)} GEMM operand splits
+        # (hi, lo, n): the fp32 contents are not written yet -- a GEMM epilogue
+        # wrote only the 3xBF16 split the next GEMMs read; the first fp32
+        # access materialises f32(hi) + f32(lo) (see _materialize)
+        self._pending = None
 
     def __del__(self):
         try:
@@ -76,6 +80,7 @@ class ExternalBuffer(Buffer):
         self.nbytes = int(nbytes)
         self.version = 0
         self._splits = None
+        self._pending = None
         self._owner = owner
 
     def __del__(self):
@@ -141,6 +146,16 @@ class Tensor:
 
     @property
     def data_ptr(self) -> int:
+        """Address of the first element, with the fp32 contents valid (a
+        buffer whose GEMM wrote only its operand split is materialised)."""
+        b = self.buffer
+        if b._pending is not None:
+            _materialize(b)
+        return b.ptr + 4 * self.offset
+
+    @property
+    def _addr(self) -> int:
+        """Address only (alignment checks, split-operand GEMMs): no materialisation."""
         return self.buffer.ptr + 4 * self.offset
 
     def __repr__(self):
@@ -195,7 +210,7 @@ class Tensor:
             off += (rem % self.shape[d]) * self.strides[d]
             rem //= self.shape[d]
         v = np.array([value], np.float32)
-        L.call("b2_memcpy_h2d", self.buffer.ptr + 4 * off, v.ctypes.data, 4, None)
+        L.call("b2_memcpy_h2d", self.data_ptr - 4 * self.offset + 4 * off, v.ctypes.data, 4, None)
         self.buffer.version += 1
         return self
 
@@ -823,6 +838,29 @@ def _as_B(t):
     return 1, K, c
 
 
+_PENDING = weakref.WeakSet()  # buffers whose fp32 contents are still only a split
+_LAZY_FP32 = os.environ.get("B2_LAZY_FP32", "1") != "0"  # 0: every GEMM stores its fp32 C
+
+
+def _materialize(buf):
+    """Write a pending buffer's fp32 contents from its 3xBF16 split (exact
+    f32(hi) + f32(lo): within 2^-16 relative of the GEMM's fp32 result -- hi
+    keeps 8 significant bits, lo the next 8 of the residual -- and exactly the
+    operand the following GEMMs consumed)."""
+    hi, lo, n = buf._pending
+    buf._pending = None
+    _PENDING.discard(buf)
+    L.call("b2_bf16x3_join", buf.ptr, hi.ptr, lo.ptr, n, None)
+
+
+def materialize_pending():
+    """Materialise every pending buffer (before a CUDA-graph capture: a
+    materialisation recorded inside a capture would only run at replay)."""
+    for b in list(_PENDING):
+        if b._pending is not None:
+            _materialize(b)
+
+
 def _split(t, rows, cols, ld, kind):
     """Cached split of the stored matrix region of t for a tensor-core GEMM:
     kind "tf32x" -> (bf16 hi, bf16 lo) of trunc_tf32(x) / x - trunc (2 B each),
@@ -899,7 +937,7 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
         algo = sel.value
     bptr = bias.data_ptr if bias is not None else None
     tc_ok = (K > 0 and (M if ta else K) % 8 == 0 and (K if tb else N) % 8 == 0
-             and lda % 4 == 0 and ldb % 4 == 0 and xa.data_ptr % 16 == 0 and wb.data_ptr % 16 == 0)
+             and lda % 4 == 0 and ldb % 4 == 0 and xa._addr % 16 == 0 and wb._addr % 16 == 0)
     ar, ac = (K, M) if ta else (M, K)
     br, bc = (N, K) if tb else (K, N)
     mask_done = False
@@ -919,7 +957,14 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
         else:
             d.a[0], d.a[1] = ahi.ptr, (alo.ptr if alo is not None else None)
             d.b[0], d.b[1] = bhi.ptr, (blo.ptr if blo is not None else None)
-        d.lda, d.ldb, d.C, d.ldc, d.bias, d.epilogue = lda, ldb, out.data_ptr, N, bptr, epi
+        # a 3xBF16 output whose consumers read only its split (and bits /
+        # column sums) skips the fp32 store; it is materialised on first use
+        from .graph import _capturing
+
+        lazy = (_LAZY_FP32 and emit_split and kind == "3xbf16" and not _capturing[0]
+                and out.offset == 0 and out.buffer.nbytes == 4 * M * N and (M * N) % 8 == 0
+                and N % 8 == 0 and out.is_contiguous and out.buffer._pending is None)
+        d.lda, d.ldb, d.C, d.ldc, d.bias, d.epilogue = lda, ldb, (None if lazy else out.data_ptr), N, bptr, epi
         if mask_bits is not None:
             d.mask_bits, mask_done = mask_bits.ptr, True
         elif mask is not None and mask.is_contiguous and mask.shape == out.shape \
@@ -944,6 +989,9 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
             if buf._splits is None:
                 buf._splits = {}
             buf._splits[(kind, out.offset, M, N, N)] = (buf.version, shi, slo, _capturing[0])
+            if lazy:
+                buf._pending = (shi, slo, M * N)
+                _PENDING.add(buf)
     elif algo == L.GEMM_3XTF32 and tc_ok:
         ahi, alo = _split(xa, ar, ac, lda, "3xtf32")
         bhi, blo = _split(wb, br, bc, ldb, "3xtf32")

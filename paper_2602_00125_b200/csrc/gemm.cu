@@ -20,6 +20,7 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
 int tf32_split(float* hi, float* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
                cudaStream_t st);
 int bf16_cast(void* out, const float* x, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st);
+int bf16x3_join(float* out, const void* hi, const void* lo, int64_t n, cudaStream_t st);
 int bf16x2_split(void* hi, void* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
                  cudaStream_t st, int mode = 2);
 bool tc_supported(int ta, int tb, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb);
@@ -203,6 +204,10 @@ int b2_gemm_bf16(int ta, int tb, int64_t M, int64_t N, int64_t K, const void* A1
 int b2_bf16x3_split(void* hi16, void* lo16, const float* x, int64_t rows, int64_t cols, int64_t ld,
                     void* stream) {
   return b2::bf16x2_split(hi16, lo16, x, rows, cols, ld, b2::resolve(stream), 5);
+}
+
+int b2_bf16x3_join(float* out, const void* hi16, const void* lo16, int64_t n, void* stream) {
+  return b2::bf16x3_join(out, hi16, lo16, n, b2::resolve(stream));
 }
 
 // 3xBF16: hi*hi + hi*lo + lo*hi as kind::f16 MMAs on caller-provided

@@ -714,7 +714,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (nb + j < p.N) acc[j] = __fmul_rn(acc[j], mrow[nb + j] > 0.0f ? 1.0f : 0.0f);
           }
         }
-        if (full64) {
+        if (!p.C) {
+          // fp32 C not wanted: only its operand split / bits / column sums
+        } else if (full64) {
 #pragma unroll
           for (int j = 0; j < 64; j += 4)
             *reinterpret_cast<float4*>(crow + nb + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
@@ -980,7 +982,7 @@ __global__ void __launch_bounds__(512) k_tail_epilogue(const TcParams p) {
       x = __fmul_rn(x, (mbits32[m * 2 * p.bits_ld + (n >> 5)] >> (n & 31)) & 1 ? 1.0f : 0.0f);
     else if (p.mask)
       x = __fmul_rn(x, p.mask[m * p.ldc + n] > 0.0f ? 1.0f : 0.0f);
-    p.C[m * p.ldc + n] = x;
+    if (p.C) p.C[m * p.ldc + n] = x;
     if (EMIT == 4 && p.s_hi) p.s_hi[m * p.N + n] = __float2bfloat16_rn(x);
     if ((EMIT == 2 || EMIT == 5) && p.s_hi) split_pair<EMIT>(x, p.s_hi[m * p.N + n], p.s_lo[m * p.N + n]);
     cs += (double)x;
@@ -1184,6 +1186,40 @@ int bf16x2_split(void* hi, void* lo, const float* x, int64_t rows, int64_t cols,
     k_bf16x2_split<2><<<grid_for(n / 8, 256 * 4, 8), 256, 0, st>>>(
         (__nv_bfloat16*)hi, (__nv_bfloat16*)lo, x, rows, cols, ld);
   return launched(mode == 5 ? "b2_bf16x3_split" : "b2_bf16x2_split");
+}
+
+// fp32 view of a 3xBF16 split: out = f32(hi) + f32(lo), exact in fp32 (hi has
+// 8 significant bits, lo sits below them), within 2^-16 relative of the
+// value the split was made from. Materialises a GEMM output whose epilogue
+// wrote only its operand split (b2_bf16x3_join).
+__global__ void __launch_bounds__(256) k_bf16x3_join(float* __restrict__ out, const __nv_bfloat16* __restrict__ hi,
+                                                     const __nv_bfloat16* __restrict__ lo, int64_t n8) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += st) {
+    const uint4 h = __ldg(reinterpret_cast<const uint4*>(hi) + i);
+    const uint4 l = __ldg(reinterpret_cast<const uint4*>(lo) + i);
+    const __nv_bfloat162* hp = reinterpret_cast<const __nv_bfloat162*>(&h);
+    const __nv_bfloat162* lp = reinterpret_cast<const __nv_bfloat162*>(&l);
+    float r[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 a = __bfloat1622float2(hp[k]), b = __bfloat1622float2(lp[k]);
+      r[2 * k] = __fadd_rn(a.x, b.x);
+      r[2 * k + 1] = __fadd_rn(a.y, b.y);
+    }
+    float4* o = reinterpret_cast<float4*>(out) + 2 * i;
+    o[0] = make_float4(r[0], r[1], r[2], r[3]);
+    o[1] = make_float4(r[4], r[5], r[6], r[7]);
+  }
+}
+
+int bf16x3_join(float* out, const void* hi, const void* lo, int64_t n, cudaStream_t st) {
+  if (n == 0) return 0;
+  if (n % 8 || ((uintptr_t)out & 15) || ((uintptr_t)hi & 15) || ((uintptr_t)lo & 15))
+    return fail("b2_bf16x3_join: n % 8 == 0 and 16-B aligned buffers needed");
+  k_bf16x3_join<<<grid_for(n / 8, 256 * 2, 8), 256, 0, st>>>(out, (const __nv_bfloat16*)hi,
+                                                               (const __nv_bfloat16*)lo, n / 8);
+  return launched("b2_bf16x3_join");
 }
 
 int bf16_cast(void* out, const float* x, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st) {

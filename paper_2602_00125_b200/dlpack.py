@@ -107,6 +107,7 @@ def to_capsule(t, stream=None):
     shape = (c_int64 * max(nd, 1))(*t.shape)
     strides = (c_int64 * max(nd, 1))(*t.strides)
     mt = DLManagedTensor()
+    t.data_ptr  # materialise fp32 contents a GEMM left as a split only
     mt.dl_tensor.data = t.buffer.ptr
     mt.dl_tensor.device = DLDevice(kDLCUDA, device_id())
     mt.dl_tensor.ndim = nd

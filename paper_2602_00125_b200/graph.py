@@ -48,6 +48,9 @@ class CudaGraph:
 def capture(fn, *args, warmup: int = 1, **kwargs) -> CudaGraph:
     for _ in range(warmup):
         fn(*args, **kwargs)
+    from .core import materialize_pending
+
+    materialize_pending()  # a materialisation captured in the graph would only run at replay
     L.synchronize()
     L.call("b2_graph_begin", None)
     _serial[0] += 1

@@ -1,0 +1,111 @@
+"""Hidden-layer GEMM outputs stored only as their 3xBF16 operand split.
+
+A ReLU layer's output and the masked cotangent its x_bar GEMM writes are
+read inside a train step only as GEMM operands (their split), ReLU bits and
+fused column sums, so the tensor-core epilogue skips their fp32 store and the
+buffer is materialised as f32(hi) + f32(lo) on first fp32 use (core.py
+_materialize, b2_bf16x3_join). Checks: the step's loss, gradients and updated
+weights are bit-identical with and without the fp32 stores; a materialised
+activation is within 2^-16 relative of the stored one (hi keeps 8 bits, lo
+the next 8 of the residual); host reads, in-place
+writes, DLPack export and graph capture all see materialised values.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2602_00125_b200 as P
+from paper_2602_00125_b200 import core, graph, nn, optim
+from paper_2602_00125_b200 import _lib as L
+from paper_2602_00125_b200.data import build_mlp, linear_params
+from tests.golden.load import bits_equal
+
+pytestmark = pytest.mark.gpu
+
+
+def _mlp_step(lazy, seed=0):
+    old = core._LAZY_FP32
+    core._LAZY_FP32 = lazy
+    try:
+        rng = np.random.default_rng(seed)
+        sizes = [512, 1024, 1024, 256]
+        model = build_mlp([linear_params(rng, a, b) for a, b in zip(sizes[:-1], sizes[1:])])
+        x = P.from_numpy(rng.standard_normal((2048, 512), dtype=np.float32))
+        labels = nn.labels_buffer(rng.integers(0, 256, 2048))
+        opt = optim.Adam(lr=1e-3)
+        P.reset_tape()
+        loss = nn.cross_entropy(model(x), labels)
+        store = P.backward(loss)
+        params = model.parameters()
+        grads = [store[p].numpy() for p in params]
+        optim.step_all(opt, params, store)
+        return loss.numpy(), grads, [p.numpy() for p in params]
+    finally:
+        core._LAZY_FP32 = old
+        P.reset_tape()
+
+
+def test_train_step_bit_identical_with_and_without_fp32_stores():
+    l0, g0, p0 = _mlp_step(False)
+    l1, g1, p1 = _mlp_step(True)
+    assert bits_equal(l0, l1)
+    for a, b in zip(g0, g1):
+        assert bits_equal(a, b)
+    for a, b in zip(p0, p1):
+        assert bits_equal(a, b)
+
+
+def _hidden(lazy):
+    old = core._LAZY_FP32
+    core._LAZY_FP32 = lazy
+    try:
+        rng = np.random.default_rng(3)
+        x = P.from_numpy(rng.standard_normal((1024, 512), dtype=np.float32))
+        w = P.from_numpy(rng.uniform(-0.05, 0.05, (512, 512)).astype(np.float32))
+        b = P.from_numpy(rng.uniform(-0.05, 0.05, (512,)).astype(np.float32))
+        with P.no_grad():
+            h = P.linear(x, w, b, relu_out=True)
+        return h
+    finally:
+        core._LAZY_FP32 = old
+
+
+def test_materialised_activation_within_2e16_of_the_stored_one():
+    ref = _hidden(False).numpy()
+    h = _hidden(True)
+    assert h.buffer._pending is not None  # only the split was written
+    got = h.numpy()
+    assert h.buffer._pending is None
+    assert np.array_equal(got > 0, ref > 0)  # the ReLU pattern is exact
+    rel = np.abs(got - ref) / np.maximum(np.abs(ref), 1e-30)
+    assert rel.max() <= 2.0 ** -16
+
+
+def test_inplace_write_and_dlpack_see_materialised_values():
+    h = _hidden(True)
+    assert h.buffer._pending is not None
+    h.set_flat(0, 5.0)  # must not be overwritten by a later materialisation
+    v = h.numpy()
+    assert v[0, 0] == 5.0
+    ref = _hidden(False).numpy()
+    assert np.abs(v[1:] - ref[1:]).max() <= 2.0 ** -16 * np.abs(ref).max()
+    torch = pytest.importorskip("torch")
+    h2 = _hidden(True)
+    t = torch.from_dlpack(h2)
+    assert np.abs(t.cpu().numpy() - ref).max() <= 2.0 ** -16 * np.abs(ref).max()
+
+
+def test_graph_capture_materialises_pending_inputs_first():
+    h = _hidden(True)
+    ref = _hidden(False).numpy()
+    outs = []
+
+    def body():
+        outs.clear()
+        with P.no_grad():
+            outs.append(P.sum(h, axis=0))
+
+    g = graph.capture(body, warmup=0)
+    g.replay()
+    L.synchronize()
+    np.testing.assert_allclose(outs[0].numpy(), ref.astype(np.float64).sum(0), rtol=1e-4, atol=1e-3)
