@@ -295,7 +295,7 @@ def op_benchmarks():
         out["config2_sum_all_gbs"] = 4 * n / ms / 1e6
     out["config2_note"] = ("device time per op from a CUDA-graph replay of 24 calls rotating "
                            "over 6 input copies (384 MiB > L2); GB/s = algorithmic bytes "
-                           "(read a [+ write out]) / time; HBM peak 6457 GB/s (measured)")
+                           "(read a [+ write out]) / time; roofline_fractions divide by MEASURED_PEAKS.json hbm_gbs")
     del copies, b
     # config 3: square matmul fwd+bwd (3 GEMMs, 6 n^3 flops)
     for size in (1024, 4096, 8192):

@@ -1,5 +1,5 @@
 """One fused-epilogue case of the config-5 dX GEMM, launched twice (for ncu:
--k regex:k_gemm_tc --launch-skip 1 -c 1).  python scripts/epi_case.py plain|full|fwd"""
+-k regex:k_gemm_tc --launch-skip 1 -c 1).  python scripts/epi_case.py plain|full|fwd|fwd_split_only"""
 import sys
 
 sys.path.insert(0, '.')
@@ -28,9 +28,11 @@ d.lda, d.ldb, d.C, d.ldc = K, N, y.data_ptr, N
 if case == "full":
     d.mask_bits, d.colsum = bits.ptr, cs.data_ptr
     d.c_hi, d.c_lo = yh.ptr, yl.ptr
-elif case == "fwd":
+elif case in ("fwd", "fwd_split_only"):
     d.epilogue, d.bias, d.relu_bits_out = L.EPI_BIAS_RELU, b.data_ptr, bits.ptr
     d.c_hi, d.c_lo = yh.ptr, yl.ptr
+    if case == "fwd_split_only":  # the product's hidden-layer forward: no fp32 C store
+        d.C = None
 for _ in range(2):
     L.call("b2_gemm_fused", L.ctypes.byref(d), None)
 L.synchronize()
