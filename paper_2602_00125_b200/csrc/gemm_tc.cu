@@ -1305,7 +1305,7 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   // scripts/tail_probe.py): few-tile long-K GEMMs (every tile split: dW
   // [1024 x 1024] over K = 32768, square n = 1024) and a short run of waves
   // whose last wave is at most half full (dW [4096 x 4096] over K = 65536:
-  // 3 waves + 34 of 74 tiles). Slices >= 8 k-blocks, S <= 16. Deterministic:
+  // 3 waves + 34 of 74 tiles). Slices >= 256 of K, S <= 16. Deterministic:
   // the partition depends only on the shape and the SM count, partials are
   // summed in slice order.
   const int bk = (mode == 4 || mode == 5) ? 64 : BK;  // Cfg::BKM
@@ -1322,7 +1322,7 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
       full = (tiles / P) * P;
       T = tiles - full;
     }
-    if (T > 0) S = (int)std::max<int64_t>(1, std::min<int64_t>({P / T, nkb / 8, 16}));
+    if (T > 0) S = (int)std::max<int64_t>(1, std::min<int64_t>({P / T, (int64_t)nkb * bk / 256, 16}));
     if (S == 1) full = tiles;
   }
   {
