@@ -568,19 +568,22 @@ __global__ void __launch_bounds__(256) k_cols(const float* __restrict__ x, int64
         for (int k = 0; k < U; ++k) v[k] = __ldg(reinterpret_cast<const float4*>(base + (r + k * RL) * I));
         // per column: FMNMX tree over the U rows; only a block that beats the
         // running best locates its first maximal row (the in-order scan's answer)
+        // branch-free: the block's first maximal row is located for every
+        // column and kept only where the block beats the running best (a
+        // divergent locate doubled the warp's instructions). The value kept is
+        // the FMNMX result; a zero maximum's sign is restored from the winning
+        // element at the end (fmaxf may return +0 for -0).
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           float m = comp(v[0], j);
 #pragma unroll
           for (int k = 1; k < U; ++k) m = fmaxf(m, comp(v[k], j));
-          if (m > b[j]) {
-            int kk = U - 1;
+          int kk = U - 1;
 #pragma unroll
-            for (int k = U - 2; k >= 0; --k) kk = comp(v[k], j) == m ? k : kk;
-#pragma unroll
-            for (int k = 0; k < U; ++k) b[j] = k == kk ? comp(v[k], j) : b[j];  // keeps a zero's sign
-            bi[j] = (int)(r + kk * RL);
-          }
+          for (int k = U - 2; k >= 0; --k) kk = comp(v[k], j) == m ? k : kk;
+          const bool gt = m > b[j];
+          b[j] = gt ? m : b[j];
+          bi[j] = gt ? (int)(r + kk * RL) : bi[j];
         }
       }
       for (; r < r1; r += RL) {
@@ -614,6 +617,7 @@ __global__ void __launch_bounds__(256) k_cols(const float* __restrict__ x, int64
       if (c < I) {
         if (isnan(v0)) t = MaxAcc{v0, 0};
         else t = max_combine(t, MaxAcc{v0, 0});
+        if (t.v == 0.0f && t.i != kNone) t.v = x[o1 * R * I + t.i * I + c];  // the winner's own zero sign
         const int64_t o = o1 * I + c;
         out[o] = t.v;
         if (argr) argr[o] = t.i;
