@@ -18,6 +18,13 @@
 #include "common.cuh"
 #include "fexp.cuh"
 
+// softmax rows: 3 resident 256-thread CTAs per SM (<= 85 registers). At the
+// unconstrained 122 registers only 2 fit and the row loop's load -> max -> exp
+// -> sum -> store chain leaves the SM idle (config-4 step 1.13 -> 0.94 ms).
+#ifndef B2_SMX_MINB
+#define B2_SMX_MINB 3
+#endif
+
 extern "C" int b2_alloc(size_t, void*, void**);
 extern "C" int b2_free(void*, void*);
 
@@ -235,7 +242,7 @@ __device__ __forceinline__ float row_max_regs(const float4 (&v)[NV], int64_t C, 
 }
 
 template <int NV>
-__global__ void __launch_bounds__(256) k_softmax_fwd_v(float* __restrict__ y, float* __restrict__ rs,
+__global__ void __launch_bounds__(256, B2_SMX_MINB) k_softmax_fwd_v(float* __restrict__ y, float* __restrict__ rs,
                                                        float* __restrict__ rm,
                                                        const float* __restrict__ z, int64_t B,
                                                        int64_t C) {
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__(256) k_softmax_fwd_v(float* __restrict__ y, fl
 }
 
 template <int NV>
-__global__ void __launch_bounds__(256) k_softmax_bwd_v(float* __restrict__ gz,
+__global__ void __launch_bounds__(256, B2_SMX_MINB) k_softmax_bwd_v(float* __restrict__ gz,
                                                        const float* __restrict__ gy,
                                                        const float* __restrict__ z,
                                                        const float* __restrict__ rs,
