@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_softmax_bwd_v(float* __res
 // stores, no per-element 64-bit index division. Same per-element arithmetic
 // as k_xent_bwd (bit-identical).
 template <int NV>
-__global__ void __launch_bounds__(256) k_xent_bwd_v(float* __restrict__ dz, const float* __restrict__ g,
+__global__ void __launch_bounds__(256, B2_SMX_MINB) k_xent_bwd_v(float* __restrict__ dz, const float* __restrict__ g,
                                                     const double* __restrict__ row_stats,
                                                     const float* __restrict__ z,
                                                     const int64_t* __restrict__ labels, int64_t B,
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(256) k_xent_bwd_v(float* __restrict__ dz, cons
 // row held in registers, one pass for the max and one for the compensated
 // sum of exp(v - m) in double (each lane a Neumaier pair, fixed butterfly).
 template <int NV>
-__global__ void __launch_bounds__(256) k_xent_rows_v(double* __restrict__ row_loss,
+__global__ void __launch_bounds__(256, B2_SMX_MINB) k_xent_rows_v(double* __restrict__ row_loss,
                                                      double* __restrict__ row_stats,
                                                      const float* __restrict__ z,
                                                      const int64_t* __restrict__ labels, int64_t B,
