@@ -929,11 +929,19 @@ int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_
   if (V == 4) {
     // cluster path: 32-column strips x CS row splits folded through DSMEM.
     // Target ~4 resident 256-thread CTAs per SM (the probe's best); CS is a
-    // power of two <= 8 and leaves every row lane >= 8 rows.
+    // power of two <= 16 and leaves every row lane >= 8 rows.
     const int64_t cstrips = (I + 31) / 32, base_ctas = cstrips * O1;
     const int64_t target = 3LL * sms;  // 4 x 148 strips-splits -> cs 4 for a 4096-wide input (probe best)
     int cs = 1;
-    while (cs < 8 && base_ctas * cs < target && R >= (int64_t)(cs * 2) * 32 * 8) cs *= 2;
+    while (cs < 16 && base_ctas * cs < target && R >= (int64_t)(cs * 2) * 32 * 8) cs *= 2;
+    if (cs == 16) {  // a non-portable cluster size (narrow, tall inputs: e.g. 1024 bias columns)
+      static bool np_ok = cudaFuncSetAttribute(k_cols<OP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                          cudaSuccess;
+      if (!np_ok) {
+        cudaGetLastError();
+        cs = 8;
+      }
+    }
     if (base_ctas * cs >= 2LL * sms && base_ctas <= INT32_MAX) {
       const int64_t Rs = (R + cs - 1) / cs;
       cudaLaunchConfig_t cfg = {};
