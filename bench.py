@@ -411,7 +411,7 @@ def main():
     import paper_2602_00125_b200 as P
     from paper_2602_00125_b200 import _lib as L, dist, nn, optim
     from paper_2602_00125_b200 import core as C
-    from paper_2602_00125_b200.data import PinnedFeeder, batch_shard, build_mlp, mlp_config5
+    from paper_2602_00125_b200.data import PinnedFeeder, ScalarReader, batch_shard, build_mlp, mlp_config5
 
     env = dist.env_from_os()
     comm = dist.Communicator(env)
@@ -423,10 +423,6 @@ def main():
     params = model.parameters()
     opt = optim.Adam(lr=1e-3, betas=(0.9, 0.999), eps=1e-8)
     x_np, y_np = batch_shard(1234, rank, rows, WIDTH, CLASSES)
-    feeder = PinnedFeeder(x_np, y_np)
-    x_dev = P.from_numpy(x_np)
-    y_dev = nn.labels_buffer(y_np)
-    del x_np
 
     gemm_log = []
     if args.gemm != "auto":
@@ -438,6 +434,12 @@ def main():
         sel = ctypes.c_int()
         L.check(L.lib().b2_gemm_select(0, 1, rows, WIDTH, WIDTH, WIDTH, WIDTH, ctypes.byref(sel)))
         g_algo = sel.value
+    # e2e data path: each batch lands (H2D) and is split into the first GEMM's
+    # 3xBF16 operand on the feeder's copy stream, overlapping the previous step
+    feeder = PinnedFeeder(x_np, y_np, presplit="3xbf16" if g_algo == L.GEMM_3XBF16 else None)
+    x_dev = P.from_numpy(x_np)
+    y_dev = nn.labels_buffer(y_np)
+    del x_np
     ALGO_INFO = {
         L.GEMM_TF32X: ("k_gemm_tc<TF32X> (tcgen05 kind::tf32 hi*hi + 2x kind::f16 bf16 cross terms)",
                        4.0, "TF32X = 1 tf32 MMA (half the bf16 rate) + 2 bf16 MMAs per fp32 MAC: "
@@ -512,17 +514,26 @@ def main():
 
     # e2e: same step through the public API, batch H2D from pinned host memory
     # every step and the loss read back to the host every step
+    # every step's loss is read back through a pinned slot; step i's value is
+    # taken after step i+1 is queued (ScalarReader), so the stream never drains
+    reader = ScalarReader()
     for _ in range(2):
         xb, yb = feeder.next()
-        step(xb, yb, read_loss=True)
+        reader.read(step(xb, yb))
+    reader.flush()
     comm.barrier()
     e2, e3 = L.Event(), L.Event()
     e2.record()
+    e2e_losses = []
     for _ in range(args.steps):
         xb, yb = feeder.next()
-        step(xb, yb, read_loss=True)
+        v = reader.read(step(xb, yb))
+        if v is not None:
+            e2e_losses.append(v)
+    e2e_losses.append(reader.flush())
     e3.record()
     L.synchronize()
+    assert len(e2e_losses) == args.steps and all(np.isfinite(e2e_losses))
     comm.barrier()
     ms_e2e = comm.max_scalar(e2.elapsed_ms(e3) / args.steps)
 

@@ -64,6 +64,10 @@ int b2_host_free(void* ptr);
 int b2_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
 int b2_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
 int b2_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
+/* stream-ordered D2H into pinned host memory (no stream drain); wait with
+ * b2_event_sync on an event recorded after it */
+int b2_memcpy_d2h_async(void* dst, const void* src, size_t bytes, void* stream);
+int b2_event_sync(void* ev);
 int b2_fill_f32(float* dst, float value, int64_t n, void* stream);
 
 /* ---------------------------------------------------------------- elementwise

@@ -51,6 +51,7 @@ _SIGS = {
     "b2_event_create": (c_int, [POINTER(c_void_p)]),
     "b2_event_destroy": (c_int, [c_void_p]),
     "b2_event_record": (c_int, [c_void_p, c_void_p]),
+    "b2_event_sync": (c_int, [c_void_p]),
     "b2_event_elapsed_ms": (c_int, [c_void_p, c_void_p, POINTER(c_float)]),
     "b2_stream_wait_event": (c_int, [c_void_p, c_void_p]),
     "b2_launch_count": (c_int, [POINTER(c_uint64)]),
@@ -67,6 +68,7 @@ _SIGS = {
     "b2_host_free": (c_int, [c_void_p]),
     "b2_memcpy_h2d": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
     "b2_memcpy_d2h": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
+    "b2_memcpy_d2h_async": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
     "b2_memcpy_d2d": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
     "b2_fill_f32": (c_int, [c_void_p, c_float, c_int64, c_void_p]),
     "b2_binary": (c_int, [c_int, c_void_p, c_int, i64p, c_void_p, i64p, c_void_p, i64p, c_void_p]),
@@ -262,6 +264,9 @@ class Event:
 
     def record(self, stream=None):
         check(lib().b2_event_record(self.h, stream))
+
+    def synchronize(self):
+        check(lib().b2_event_sync(self.h))
 
     def elapsed_ms(self, end: "Event") -> float:
         ms = c_float()

@@ -474,6 +474,18 @@ int b2_memcpy_d2h(void* dst, const void* src, size_t bytes, void* s) {
   B2_CUDA(cudaStreamSynchronize(st));
   return 0;
 }
+// stream-ordered D2H into pinned host memory; completion via an event
+// (b2_event_sync) -- lets a training loop read step i's loss after step i+1
+// is queued instead of draining the stream every step
+int b2_memcpy_d2h_async(void* dst, const void* src, size_t bytes, void* s) {
+  if (!bytes) return 0;
+  B2_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, resolve(s)));
+  return 0;
+}
+int b2_event_sync(void* ev) {
+  B2_CUDA(cudaEventSynchronize((cudaEvent_t)ev));
+  return 0;
+}
 int b2_memcpy_d2d(void* dst, const void* src, size_t bytes, void* s) {
   if (!bytes) return 0;
   B2_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, resolve(s)));

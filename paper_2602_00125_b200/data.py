@@ -94,13 +94,26 @@ class PinnedFeeder:
     stream waits until its slot's copy has landed). Every step still moves its
     full batch host -> device; the copy just overlaps the previous step."""
 
-    def __init__(self, x, labels):
+    def __init__(self, x, labels, presplit=None):
+        """presplit="3xbf16": also make each batch's 3xBF16 operand split on
+        the copy stream right after its H2D copy (the first layer's GEMM reads
+        x only through that split), so the split of step i+1's batch overlaps
+        step i instead of opening step i+1."""
+        self.presplit = presplit
         self.hx = PinnedHost(x.shape, np.float32)
         self.hx.array[...] = x
         self.hl = PinnedHost(labels.shape, np.int64)
         self.hl.array[...] = labels
         self.dx = [T._empty(x.shape) for _ in range(2)]
         self.dl = [T.Buffer(8 * max(labels.size, 1)) for _ in range(2)]
+        rows, cols = (x.shape[0], int(np.prod(x.shape[1:]))) if x.ndim > 1 else (1, x.size)
+        self._rc = (rows, cols)
+        if presplit not in (None, "3xbf16"):
+            raise ValueError("presplit must be None or '3xbf16'")
+        if presplit and cols % 8:
+            self.presplit = None  # the split kernel needs cols % 8 == 0; the GEMM splits itself
+        self.sp = [(T.Buffer(2 * rows * cols), T.Buffer(2 * rows * cols)) for _ in range(2)] \
+            if self.presplit else None
         s = ctypes.c_void_p()
         L.check(L.lib().b2_stream_create(ctypes.byref(s)))
         self.copy_stream = s.value
@@ -117,6 +130,10 @@ class PinnedFeeder:
         cs = self.copy_stream
         L.call("b2_memcpy_h2d", self.dx[slot].data_ptr, self.hx.ptr, self.hx.nbytes, cs)
         L.call("b2_memcpy_h2d", self.dl[slot].ptr, self.hl.ptr, self.hl.nbytes, cs)
+        if self.sp is not None:
+            hi, lo = self.sp[slot]
+            rows, cols = self._rc
+            L.call("b2_bf16x3_split", hi.ptr, lo.ptr, self.dx[slot].data_ptr, rows, cols, cols, cs)
         self.ready[slot].record(cs)
 
     def next(self):
@@ -128,5 +145,47 @@ class PinnedFeeder:
         L.call("b2_stream_wait_event", self.copy_stream, self.released[nxt].h)
         self._issue(nxt)
         self.i += 1
-        self.dx[cur].buffer.version += 1  # a new batch: cached operand splits are stale
+        buf = self.dx[cur].buffer
+        buf.version += 1  # a new batch: cached operand splits are stale
+        if self.sp is not None:  # ... except the one made with it on the copy stream
+            from .graph import _capturing
+
+            rows, cols = self._rc
+            if buf._splits is None:
+                buf._splits = {}
+            hi, lo = self.sp[cur]
+            buf._splits[("3xbf16", 0, rows, cols, cols)] = (buf.version, hi, lo, _capturing[0])
         return self.dx[cur], self.dl[cur]
+
+
+class ScalarReader:
+    """Reads a device scalar (a step's loss) to the host without draining the
+    stream: read(t) queues a D2H copy into a pinned slot plus an event and
+    returns the PREVIOUS read's value (waiting only for that older copy), so
+    the host queues step i+1 before it blocks on step i's loss. flush()
+    returns the last one."""
+
+    def __init__(self, slots=2):
+        self.host = PinnedHost((slots,), np.float32)
+        self.events = [L.Event() for _ in range(slots)]
+        self.i = 0
+        self.pending = None
+
+    def read(self, t):
+        slot = self.i % len(self.events)
+        self.i += 1
+        L.call("b2_memcpy_d2h_async", self.host.ptr + 4 * slot, t.data_ptr, 4, None)
+        self.events[slot].record()
+        prev, self.pending = self.pending, slot
+        return self._value(prev)
+
+    def _value(self, slot):
+        if slot is None:
+            return None
+        self.events[slot].synchronize()
+        return float(self.host.array[slot])
+
+    def flush(self):
+        prev, self.pending = self.pending, None
+        return self._value(prev)
+
