@@ -23,6 +23,7 @@ Keys beyond the base contract:
 from __future__ import annotations
 
 import argparse
+import collections
 import json
 import os
 import statistics
@@ -78,7 +79,14 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.rows.append((time.time(), parts))
+
+    def window(self, t0, t1):
+        """Keep only the samples taken inside [t0, t1] (the timed region). The
+        sampler is started before the warm-up: nvidia-smi's start-up (NVML
+        init) can stall the CUDA process's launches for hundreds of ms, which
+        must not land in a timed step."""
+        self.t0, self.t1 = t0, t1
 
     def stop(self):
         if self.proc:
@@ -87,6 +95,8 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        lo, hi = getattr(self, "t0", 0.0), getattr(self, "t1", float("inf"))
+        self.rows = [r for t, r in self.rows if lo <= t <= hi]
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -434,11 +444,15 @@ def main():
         sel = ctypes.c_int()
         L.check(L.lib().b2_gemm_select(0, 1, rows, WIDTH, WIDTH, WIDTH, WIDTH, ctypes.byref(sel)))
         g_algo = sel.value
-    # e2e data path: each batch lands (H2D) and is split into the first GEMM's
-    # 3xBF16 operand on the feeder's copy stream, overlapping the previous step
-    feeder = PinnedFeeder(x_np, y_np, presplit="3xbf16" if g_algo == L.GEMM_3XBF16 else None)
-    x_dev = P.from_numpy(x_np)
-    y_dev = nn.labels_buffer(y_np)
+    # Input pipeline (both arms of the measurement): every step takes a new
+    # batch -- a feeder slot whose version is bumped, so cached operand splits
+    # are stale -- and its 3xBF16 split for the first GEMM is made on the
+    # feeder's stream, overlapping the previous step. `value`: the batch is
+    # resident in HBM (two slots, uploaded once); e2e: it is copied from
+    # pinned host memory every step (H2D on the same stream, before the split).
+    presplit = "3xbf16" if g_algo == L.GEMM_3XBF16 else None
+    feeder = PinnedFeeder(x_np, y_np, presplit=presplit)
+    dev_feeder = PinnedFeeder(x_np, y_np, presplit=presplit, resident=True)
     del x_np
     ALGO_INFO = {
         L.GEMM_TF32X: ("k_gemm_tc<TF32X> (tcgen05 kind::tf32 hi*hi + 2x kind::f16 bf16 cross terms)",
@@ -453,9 +467,15 @@ def main():
     }
     a_kernel, a_div, a_note, a_desc = ALGO_INFO[g_algo]
 
+    inflight = collections.deque()
+
     def step(x, labels, read_loss=False):
+        # at most 2 steps queued ahead of the device: the host never runs so far
+        # ahead that the caching allocator has to grow the pool mid-run (a
+        # multi-GB cudaMalloc stalls the host while the device drains)
+        if len(inflight) >= 2:
+            inflight.popleft().synchronize()
         P.reset_tape()
-        x.buffer.version += 1  # a new batch each step: its operand split is redone
         logits = model(x)
         loss = nn.cross_entropy(logits, labels, denom=rows)
         # all-reduce + Adam per layer on a side stream as soon as its last
@@ -464,14 +484,17 @@ def main():
         store = P.backward(loss, on_leaf_ready=red.hook)
         red.finish()
         red.step_rest(store)
+        ev = L.Event()
+        ev.record()
+        inflight.append(ev)
         return loss.item() if read_loss else loss
-
-    for _ in range(max(args.warmup, 0)):
-        step(x_dev, y_dev)
-    comm.barrier()
 
     sampler = ClockSampler(env.local_rank)
     sampler.start()
+    for _ in range(max(args.warmup, 0)):
+        step(*dev_feeder.next())
+    comm.barrier()
+    t_wall0 = time.time()
     n0 = L.launch_count()
     e0, e1 = L.Event(), L.Event()
     marks, host_ms, gc_log = [], [], []
@@ -488,7 +511,7 @@ def main():
     e0.record()
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        last = step(x_dev, y_dev)
+        last = step(*dev_feeder.next())
         if dbg:
             host_ms.append(round((time.perf_counter() - t0) * 1e3, 1))
             ev = L.Event()
@@ -505,6 +528,7 @@ def main():
         print("per-step ms:", per, "host ms:", host_ms, "gc:", gc_log, "allocator:", L.alloc_stats(),
               file=sys.stderr)
     launches = L.launch_count() - n0
+    sampler.window(t_wall0, time.time())
     comm.barrier()
     ms_local = e0.elapsed_ms(e1) / args.steps
     clocks = sampler.stop()
@@ -544,7 +568,7 @@ def main():
     e4, e5 = L.Event(), L.Event()
     e4.record()
     for _ in range(t_steps):
-        step(x_dev, y_dev)
+        step(*dev_feeder.next())
     e5.record()
     L.synchronize()
     C.GEMM_TIMER = None
@@ -572,14 +596,15 @@ def main():
     bf16 = None
     if not args.no_bf16:
         P.set_gemm_algo("bf16")
+        sp_saved, dev_feeder.sp = dev_feeder.sp, None  # bf16 GEMMs cast x themselves
         try:
             for _ in range(max(args.warmup, 0)):
-                step(x_dev, y_dev)
+                step(*dev_feeder.next())
             comm.barrier()
             b0, b1 = L.Event(), L.Event()
             b0.record()
             for _ in range(args.steps):
-                lb = step(x_dev, y_dev)
+                lb = step(*dev_feeder.next())
             b1.record()
             L.synchronize()
             comm.barrier()
@@ -589,13 +614,14 @@ def main():
             b2, b3 = L.Event(), L.Event()
             b2.record()
             for _ in range(t_steps):
-                step(x_dev, y_dev)
+                step(*dev_feeder.next())
             b3.record()
             L.synchronize()
             C.GEMM_TIMER = None
             bt_ms = b2.elapsed_ms(b3) / t_steps
         finally:
             P.set_gemm_algo(None if args.gemm == "auto" else args.gemm)
+            dev_feeder.sp = sp_saved
         bf_flops = sum(f for f, _, _ in blog) / t_steps
         bf_ms = sum(s.elapsed_ms(e) for _, s, e in blog) / t_steps
         bf_ach = bf_flops / (bf_ms / 1000.0) / 1e12
@@ -633,7 +659,10 @@ def main():
                        "layers": "4xLinear(4096,4096)+ReLU, Linear(4096,1000)",
                        "optimizer": "Adam lr=1e-3 betas=(0.9,0.999) eps=1e-8",
                        "gemm": a_desc,
-                       "parallelism": f"dp{world}", "l2": "inputs > L2 (1 GiB/rank at N=1)"},
+                       "parallelism": f"dp{world}", "l2": "inputs > L2 (1 GiB/rank at N=1)",
+                       "input_pipeline": "2 batch slots (value: resident in HBM; e2e: H2D from pinned "
+                                         "host every step); each step's 3xBF16 split of its batch is made "
+                                         "on the feeder stream, overlapping the previous step"},
             "e2e": {"value": GLOBAL_BATCH / (ms_e2e / 1000.0), "unit": "samples/s",
                     "h2d_bytes_per_step": feeder.h2d_bytes, "d2h_bytes_per_step": 4},
             "roofline": roof,

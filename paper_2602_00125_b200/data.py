@@ -94,12 +94,16 @@ class PinnedFeeder:
     stream waits until its slot's copy has landed). Every step still moves its
     full batch host -> device; the copy just overlaps the previous step."""
 
-    def __init__(self, x, labels, presplit=None):
+    def __init__(self, x, labels, presplit=None, resident=False):
         """presplit="3xbf16": also make each batch's 3xBF16 operand split on
         the copy stream right after its H2D copy (the first layer's GEMM reads
         x only through that split), so the split of step i+1's batch overlaps
-        step i instead of opening step i+1."""
+        step i instead of opening step i+1.
+        resident=True: the batch is uploaded once into both device slots and
+        stays in HBM (bench.py's device-resident `value` loop); each step
+        still redoes its split (when presplit) on the copy stream."""
         self.presplit = presplit
+        self.resident = resident
         self.hx = PinnedHost(x.shape, np.float32)
         self.hx.array[...] = x
         self.hl = PinnedHost(labels.shape, np.int64)
@@ -120,16 +124,22 @@ class PinnedFeeder:
         self.ready = [L.Event(), L.Event()]
         self.released = [L.Event(), L.Event()]
         self.i = 0
+        if resident:
+            for slot in range(2):
+                L.call("b2_memcpy_h2d", self.dx[slot].data_ptr, self.hx.ptr, self.hx.nbytes, None)
+                L.call("b2_memcpy_h2d", self.dl[slot].ptr, self.hl.ptr, self.hl.nbytes, None)
+            L.synchronize()
         self._issue(0)
 
     @property
     def h2d_bytes(self):
-        return self.hx.nbytes + self.hl.nbytes
+        return 0 if self.resident else self.hx.nbytes + self.hl.nbytes
 
     def _issue(self, slot):
         cs = self.copy_stream
-        L.call("b2_memcpy_h2d", self.dx[slot].data_ptr, self.hx.ptr, self.hx.nbytes, cs)
-        L.call("b2_memcpy_h2d", self.dl[slot].ptr, self.hl.ptr, self.hl.nbytes, cs)
+        if not self.resident:
+            L.call("b2_memcpy_h2d", self.dx[slot].data_ptr, self.hx.ptr, self.hx.nbytes, cs)
+            L.call("b2_memcpy_h2d", self.dl[slot].ptr, self.hl.ptr, self.hl.nbytes, cs)
         if self.sp is not None:
             hi, lo = self.sp[slot]
             rows, cols = self._rc
