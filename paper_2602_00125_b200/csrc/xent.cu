@@ -13,11 +13,16 @@
 // GradStore-ordered pullback, so results are bit-identical to composing the
 // ops on the reference engine.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <math.h>
 
 #include "common.cuh"
 #include "fexp.cuh"
 
+#ifndef B2_SOFTMAX_TMA
+#define B2_SOFTMAX_TMA 1
+#endif
+constexpr bool kSoftmaxTma = B2_SOFTMAX_TMA;
 // softmax rows: 3 resident 256-thread CTAs per SM (<= 85 registers). At the
 // unconstrained 122 registers only 2 fit and the row loop's load -> max -> exp
 // -> sum -> store chain leaves the SM idle (config-4 step 1.13 -> 0.94 ms).
@@ -285,6 +290,87 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_softmax_fwd_v(float* __res
   }
 }
 
+// TMA-staged rows (C % 4 == 0, 16-B aligned, 4*C bytes <= 16 KB): each warp
+// owns two shared-memory row buffers; lane 0 issues the cp.async.bulk of the
+// warp's NEXT row (mbarrier-tracked) before the warp works on the current
+// one, so a row's load latency overlaps the previous row's max / exp / sum /
+// divide chain -- the register-staged kernel above waits for every row's
+// loads (config-4 forward 101 -> 81 us). Same arithmetic as k_softmax_fwd_v.
+// The backward keeps the register-staged form: staging its two rows (z, g)
+// per warp halves the warps per SM, and that measured slower.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void row_bulk(float* dst, const float* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of dst
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void row_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n.reg .pred P1;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+               "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)), "r"(parity) : "memory");
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256, B2_SMX_MINB) k_softmax_fwd_tma(float* __restrict__ y, float* __restrict__ rs,
+                                                                     float* __restrict__ rm,
+                                                                     const float* __restrict__ z, int64_t B,
+                                                                     int64_t C) {
+  extern __shared__ __align__(128) float smx[];
+  __shared__ __align__(8) uint64_t bars[8][2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float* const buf0 = smx + (wid * 2) * (NV * 128);
+  float* const buf1 = buf0 + NV * 128;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t bytes = (uint32_t)(C * 4);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[wid][0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[wid][1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (w < B) row_bulk(buf0, z + w * C, bytes, &bars[wid][0]);
+  }
+  __syncwarp();
+  int it = 0;
+  for (int64_t r = w; r < B; r += nw, ++it) {
+    const int b = it & 1;
+    if (lane == 0 && r + nw < B) row_bulk(b ? buf0 : buf1, z + (r + nw) * C, bytes, &bars[wid][b ^ 1]);
+    row_wait(&bars[wid][b], (uint32_t)(it >> 1) & 1);
+    const float4* row = reinterpret_cast<const float4*>(b ? buf1 : buf0);
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      v[i] = q * 4 < C ? row[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();  // every lane has its values: the buffer may be refilled next iteration
+    const float m = row_max_regs<NV>(v, C, lane);
+    double acc = 0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float e = b2::exp_f32(__fsub_rn(f4get(v[i], k), m));  // exp(sub(z, m))
+        f4set(v[i], k, e);
+        if ((int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)e;
+      }
+    const float s = __double2float_rn(warp_sum(acc));  // sum(e, -1, keepdims)
+    const bool ok = s >= 1.0f && s <= 0x1p100f;
+    const float rs_ = __frcp_rn(s);
+    float4* yr = reinterpret_cast<float4*>(y + r * C);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      if (q * 4 < C)
+        yr[q] = make_float4(div_by(v[i].x, s, rs_, ok), div_by(v[i].y, s, rs_, ok),
+                            div_by(v[i].z, s, rs_, ok), div_by(v[i].w, s, rs_, ok));  // div(e, s)
+    }
+    if (lane == 0) {
+      rs[r] = s;
+      rm[r] = m;
+    }
+  }
+}
+
 template <int NV>
 __global__ void __launch_bounds__(256, B2_SMX_MINB) k_softmax_bwd_v(float* __restrict__ gz,
                                                        const float* __restrict__ gy,
@@ -484,6 +570,27 @@ int b2_softmax_fwd(float* y, float* row_s, float* row_m, const float* z, int64_t
   if (rows <= 0 || cols <= 0) return 0;
   cudaStream_t st = b2::resolve(stream);
   const bool vec = cols % 4 == 0 && cols <= 2048 && ((uintptr_t)z & 15) == 0 && ((uintptr_t)y & 15) == 0;
+  if (vec && cols <= 1024 && ((uintptr_t)y & 15) == 0 && kSoftmaxTma) {
+    // TMA-staged rows, persistent: 3 CTAs of 8 warps per SM, 2 row buffers per warp
+    const int nv = (int)((cols + 127) / 128);
+    const int64_t ctas = std::min<int64_t>((rows + 7) / 8, 3LL * b2::sm_count());
+#define B2_SMT(NV)                                                                              \
+  {                                                                                             \
+    const int smem = 8 * 2 * NV * 128 * 4;                                                      \
+    static bool attr = false;                                                                   \
+    if (!attr) {                                                                                \
+      B2_CUDA(cudaFuncSetAttribute(k_softmax_fwd_tma<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+      attr = true;                                                                              \
+    }                                                                                           \
+    k_softmax_fwd_tma<NV><<<(unsigned)ctas, 256, smem, st>>>(y, row_s, row_m, z, rows, cols);   \
+  }
+    if (nv <= 1) B2_SMT(1)
+    else if (nv <= 2) B2_SMT(2)
+    else if (nv <= 4) B2_SMT(4)
+    else B2_SMT(8)
+#undef B2_SMT
+    return b2::launched("b2_softmax_fwd(tma)");
+  }
   if (vec) {
     const int nv = (int)((cols + 127) / 128);
 #define B2_SMF(NV) k_softmax_fwd_v<NV><<<rows_grid(rows), 256, 0, st>>>(y, row_s, row_m, z, rows, cols)
