@@ -404,6 +404,7 @@ def op_benchmarks():
 
 
 def main():
+    global GLOBAL_BATCH
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -412,9 +413,13 @@ def main():
     ap.add_argument("--no-ops", action="store_true", help="skip the config 2-4 op benchmarks")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-bf16", action="store_true", help="skip the bf16-variant measurement")
+    ap.add_argument("--global-batch", type=int, default=GLOBAL_BATCH,
+                    help="config-5 global batch (default: BASELINE's 65536; other values are "
+                         "for the per-GPU-size characterisation in DESIGN 6, not the headline)")
     ap.add_argument("--gemm", default="auto", choices=["auto", "tf32x", "3xbf16", "3xtf32"],
                     help="fp32-accurate GEMM algorithm for the headline run")
     args = ap.parse_args()
+    GLOBAL_BATCH = args.global_batch
     if args.impl == "reference":
         return run_reference(args)
 
@@ -654,7 +659,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
             "data": "synthetic (seeded N(0,1) inputs, uniform labels; reference Dense init)",
-            "config": {"workload": "config5_mlp_4x4096_1000_b65536_adam",
+            "config": {"workload": f"config5_mlp_4x4096_1000_b{GLOBAL_BATCH}_adam",
                        "global_batch": GLOBAL_BATCH, "per_gpu_batch": rows,
                        "layers": "4xLinear(4096,4096)+ReLU, Linear(4096,1000)",
                        "optimizer": "Adam lr=1e-3 betas=(0.9,0.999) eps=1e-8",
