@@ -502,6 +502,63 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_xent_rows_v(double* __rest
   }
 }
 
+// TMA-staged form of k_xent_rows_v (C % 4 == 0, 16-B aligned rows, C <= 1024):
+// each warp bulk-copies its next row into its second shared-memory buffer
+// while it reduces the current one, and reads the label's logit from the
+// staged row instead of a dependent global load. Same arithmetic.
+template <int NV>
+__global__ void __launch_bounds__(256, B2_SMX_MINB) k_xent_rows_tma(double* __restrict__ row_loss,
+                                                                   double* __restrict__ row_stats,
+                                                                   const float* __restrict__ z,
+                                                                   const int64_t* __restrict__ labels,
+                                                                   int64_t B, int64_t C) {
+  extern __shared__ __align__(128) float smx[];
+  __shared__ __align__(8) uint64_t bars[8][2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float* const buf0 = smx + (wid * 2) * (NV * 128);
+  float* const buf1 = buf0 + NV * 128;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t bytes = (uint32_t)(C * 4);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[wid][0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[wid][1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (w < B) row_bulk(buf0, z + w * C, bytes, &bars[wid][0]);
+  }
+  __syncwarp();
+  int it = 0;
+  for (int64_t r = w; r < B; r += nw, ++it) {
+    const int b = it & 1;
+    if (lane == 0 && r + nw < B) row_bulk(b ? buf0 : buf1, z + (r + nw) * C, bytes, &bars[wid][b ^ 1]);
+    const int64_t lab = labels[r];
+    row_wait(&bars[wid][b], (uint32_t)(it >> 1) & 1);
+    const float* rowp = b ? buf1 : buf0;
+    const float4* row = reinterpret_cast<const float4*>(rowp);
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      v[i] = q * 4 < C ? row[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float zl = rowp[lab];
+    __syncwarp();  // every lane has its values: the buffer may be refilled next iteration
+    const double m = (double)row_max_regs<NV>(v, C, lane);
+    double sum = 0, comp = 0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((int64_t)(i * 32 + lane) * 4 + k < C) neu_add(sum, comp, b2::exp_fast((double)f4get(v[i], k) - m));
+    const double tot = warp_sum(sum + comp);
+    if (lane == 0) {
+      row_stats[2 * r] = m;
+      row_stats[2 * r + 1] = tot;
+      row_loss[r] = m + log(tot) - (double)zl;
+    }
+  }
+}
+
 int rows_grid(int64_t B) {
   int64_t warps = B;
   int64_t ctas = (warps + 7) / 8;
@@ -520,7 +577,25 @@ int b2_xent_fwd(float* loss, double* row_stats, const float* logits, const int64
   void* ws = nullptr;
   B2_TRY(b2_alloc((size_t)rows * sizeof(double), st, &ws));
   const bool vec = cols % 4 == 0 && cols <= 2048 && ((uintptr_t)logits & 15) == 0;
-  if (vec) {
+  if (vec && cols <= 1024 && kSoftmaxTma) {
+    const int nv = (int)((cols + 127) / 128);
+    const int64_t ctas = std::min<int64_t>((rows + 7) / 8, 3LL * b2::sm_count());
+#define B2_XT(NV)                                                                               \
+  {                                                                                             \
+    const int smem = 8 * 2 * NV * 128 * 4;                                                      \
+    static bool attr = false;                                                                   \
+    if (!attr) {                                                                                \
+      B2_CUDA(cudaFuncSetAttribute(k_xent_rows_tma<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+      attr = true;                                                                              \
+    }                                                                                           \
+    k_xent_rows_tma<NV><<<(unsigned)ctas, 256, smem, st>>>((double*)ws, row_stats, logits, labels, rows, cols); \
+  }
+    if (nv <= 1) B2_XT(1)
+    else if (nv <= 2) B2_XT(2)
+    else if (nv <= 4) B2_XT(4)
+    else B2_XT(8)
+#undef B2_XT
+  } else if (vec) {
     const int nv = (int)((cols + 127) / 128);
 #define B2_XF(NV) \
   k_xent_rows_v<NV><<<rows_grid(rows), 256, 0, st>>>((double*)ws, row_stats, logits, labels, rows, cols)
