@@ -129,69 +129,84 @@ def ncu_traffic():
 # --------------------------------------------------------------------- reference arm
 
 
-def cpu_oracle_step_rate(sample_rows=512, width=WIDTH, seed=0, budget_s=25.0):
-    """The NumPy f64 restatement of the reference (oracle/tensorlite_np.py) on
-    this host, extrapolated per SURVEY 8d: fwd+bwd timed at two batch sizes
-    (rows/2 and rows) and fit t = fixed + slope*rows, evaluated at 65536; one
-    Adam step over all 71.2M parameters charged once per step."""
-    from oracle import tensorlite_np as O
-    from paper_2602_00125_b200.data import mlp_config5
+class CpuSampleStep:
+    """One bounded sample of the config-5 step on the host cores through the
+    NumPy f64 restatement of the reference (oracle/tensorlite_np.py): the
+    step's work cut into GLOBAL_BATCH / rows equal slices and one slice timed
+    -- forward + backward over `rows` samples (every FLOP of the step scales
+    with the batch rows) plus the Adam update of the same 1/(GLOBAL_BATCH/rows)
+    share of every parameter tensor (its rows). value = rows / seconds, the
+    same samples/s as the device arm; nothing is extrapolated from a fit."""
 
-    params = mlp_config5(seed, WIDTH, CLASSES, DEPTH)
-    rng = np.random.default_rng(1)
+    def __init__(self, rows=1024, seed=0):
+        from oracle import tensorlite_np as O
+        from paper_2602_00125_b200.data import mlp_config5
 
-    class _NoOpt:
-        def step(self, key, th, g):
-            return th
+        self.O = O
+        self.rows = rows
+        self.params = mlp_config5(seed, WIDTH, CLASSES, DEPTH)
+        rng = np.random.default_rng(1)
+        self.x = rng.standard_normal((rows, WIDTH), dtype=np.float32)
+        self.labels = rng.integers(0, CLASSES, rows)
+        self.frac = rows / GLOBAL_BATCH
+        self.adam = O.Adam(lr=1e-3)
 
-    def fwdbwd(rows):
-        x = rng.standard_normal((rows, width), dtype=np.float32)
-        labels = rng.integers(0, CLASSES, rows)
+        class _NoOpt:
+            def step(self, key, th, g):
+                return th
+
+        self._noopt = _NoOpt()
+
+    def run(self):
+        O = self.O
         t0 = time.perf_counter()
-        r = O.mlp_train_step(params, x, labels, _NoOpt())
-        return time.perf_counter() - t0, r
+        r = O.mlp_train_step(self.params, self.x, self.labels, self._noopt)
+        for i, ((w, b), (gw, gb)) in enumerate(zip(self.params, r["grads"])):
+            kw = max(1, int(round(w.shape[0] * self.frac)))
+            kb = max(1, int(round(b.shape[0] * self.frac)))
+            self.adam.step(("w", i), w[:kw], gw[:kw])
+            self.adam.step(("b", i), b[:kb], gb[:kb])
+        return time.perf_counter() - t0
 
-    half = max(sample_rows // 2, 1)
-    t_half, _ = fwdbwd(half)
-    t_fb, r = fwdbwd(sample_rows)
-    slope = max((t_fb - t_half) / (sample_rows - half), 0.0) if sample_rows > half else t_fb / sample_rows
-    fixed = max(t_half - slope * half, 0.0)
-    adam = O.Adam(lr=1e-3)
-    t0 = time.perf_counter()
-    for i, ((w, b), (gw, gb)) in enumerate(zip(params, r["grads"])):
-        adam.step(("w", i), w, gw)
-        adam.step(("b", i), b, gb)
-    t_adam = time.perf_counter() - t0
-    step_s = fixed + slope * GLOBAL_BATCH + t_adam
-    return GLOBAL_BATCH / step_s, {"t_fwdbwd_s": t_fb, "t_half_s": t_half, "fixed_s": fixed,
-                                   "t_adam_s": t_adam, "rows": sample_rows}
+    def describe(self):
+        return (f"1/{GLOBAL_BATCH // self.rows} of a config-5 step per timed step: fwd+bwd over "
+                f"{self.rows} of the 65536 rows + Adam over the same share of every parameter "
+                f"tensor (oracle/tensorlite_np.py, NumPy f64 BLAS on {os.cpu_count()} threads)")
+
+
+def cpu_oracle_step_rate(rows=1024, reps=3):
+    """The CPU baseline of the device arm: median of `reps` timed sample steps."""
+    st = CpuSampleStep(rows)
+    st.run()  # warm-up (BLAS threads, page-in)
+    ts = [st.run() for _ in range(reps)]
+    return rows / statistics.median(ts), st.describe()
 
 
 def run_reference(args):
+    """The reference arm: the reference's CPU path (its NumPy restatement;
+    the pure-Python reference cannot travel to the GPU box) on all host
+    cores, K timed steps of a bounded 1/64 sample of the config-5 workload.
+    Under torchrun rank 0 alone runs and prints."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    vals = []
-    info = None
+    st = CpuSampleStep()
     for _ in range(max(args.warmup, 0)):
-        cpu_oracle_step_rate(sample_rows=256)
-    for _ in range(args.steps):
-        v, info = cpu_oracle_step_rate()
-        vals.append(v)
-    v = statistics.median(vals)
+        st.run()
+    ts = [st.run() for _ in range(args.steps)]
+    v = st.rows * len(ts) / sum(ts)
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": GLOBAL_BATCH / v * 1000.0, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64 (fp32 stores)", "data": "synthetic",
-        "config": {"workload": "config5_mlp_4x4096_1000_b65536_adam", "global_batch": GLOBAL_BATCH,
+        "ms_per_step": sum(ts) / len(ts) * 1000.0, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64 (fp32 stores)",
+        "data": "synthetic (seeded N(0,1) inputs, uniform labels; reference Dense init)",
+        "config": {"workload": f"config5_mlp_4x4096_1000_b{GLOBAL_BATCH}_adam",
+                   "global_batch": GLOBAL_BATCH, "sample_rows_per_step": st.rows,
                    "parallelism": "cpu"},
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
-                         "sample": f"fwd+bwd at {info['rows'] // 2} and {info['rows']} rows fit as "
-                                   f"fixed + slope*rows, evaluated at 65536, + one full Adam step "
-                                   f"(oracle/tensorlite_np.py, numpy BLAS threads={cores}); "
-                                   f"extrapolated"},
+                         "sample": st.describe()},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -403,6 +418,44 @@ def op_benchmarks():
 # --------------------------------------------------------------------- main arm
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: one process per GPU, the env
+    torchrun would set (RANK, LOCAL_RANK, WORLD_SIZE, MASTER_*), NCCL's
+    communicator-init lines on stderr (NCCL_DEBUG=INFO unless set). Rank 0
+    prints the JSON line; a failing rank takes the others down and the exit
+    code is the first failure's."""
+    import signal
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        env.setdefault("NCCL_DEBUG", "INFO")
+        procs.append(subprocess.Popen([sys.executable] + sys.argv, env=env, start_new_session=True))
+    rc = 0
+    live = list(procs)
+    while live:
+        for p in list(live):
+            c = p.poll()
+            if c is None:
+                continue
+            live.remove(p)
+            if c != 0 and rc == 0:
+                rc = c
+                for q in live:  # the process groups this launcher created
+                    try:
+                        os.killpg(q.pid, signal.SIGTERM)
+                    except ProcessLookupError:
+                        pass
+        time.sleep(0.2)
+    sys.exit(rc)
+
+
 def main():
     global GLOBAL_BATCH
     ap = argparse.ArgumentParser()
@@ -422,6 +475,11 @@ def main():
     GLOBAL_BATCH = args.global_batch
     if args.impl == "reference":
         return run_reference(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus)
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env} ranks were launched")
 
     import paper_2602_00125_b200 as P
     from paper_2602_00125_b200 import _lib as L, dist, nn, optim
@@ -456,8 +514,8 @@ def main():
     # resident in HBM (two slots, uploaded once); e2e: it is copied from
     # pinned host memory every step (H2D on the same stream, before the split).
     presplit = "3xbf16" if g_algo == L.GEMM_3XBF16 else None
-    feeder = PinnedFeeder(x_np, y_np, presplit=presplit)
-    dev_feeder = PinnedFeeder(x_np, y_np, presplit=presplit, resident=True)
+    feeder = PinnedFeeder(x_np, y_np, presplit=presplit, classes=CLASSES)
+    dev_feeder = PinnedFeeder(x_np, y_np, presplit=presplit, resident=True, classes=CLASSES)
     del x_np
     ALGO_INFO = {
         L.GEMM_TF32X: ("k_gemm_tc<TF32X> (tcgen05 kind::tf32 hi*hi + 2x kind::f16 bf16 cross terms)",
@@ -647,12 +705,9 @@ def main():
         if not args.no_ops:
             ops = op_benchmarks()
         if not args.no_cpu:
-            v_cpu, info = cpu_oracle_step_rate()
+            v_cpu, desc = cpu_oracle_step_rate()
             cpu = {"value": v_cpu, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
-                   "sample": f"fwd+bwd at {info['rows'] // 2} rows ({info['t_half_s']:.2f}s) and "
-                             f"{info['rows']} rows ({info['t_fwdbwd_s']:.2f}s) fit as fixed + "
-                             f"slope*rows at 65536, + full Adam ({info['t_adam_s']:.2f}s); "
-                             f"extrapolated"}
+                   "sample": desc + "; median of 3 timed sample steps"}
             ops_cpu = cpu_ops_baseline()
 
     if rank == 0:

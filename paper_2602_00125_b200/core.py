@@ -30,7 +30,7 @@ import weakref
 import numpy as np
 
 from . import _lib as L
-from .autograd import record
+from .autograd import is_recording, record
 from .errors import BroadcastError, ShapeError
 
 _py_sum = sum
@@ -743,7 +743,11 @@ def max(x, axis=None, keepdims=False) -> Tensor:
     for a in axes:
         if x.shape[a] == 0:
             raise ShapeError("max over a zero-extent axis is undefined")
-    out, arg = _reduce(L.RED_MAX, x, axes, oshape, want_arg=True)
+    # the first-max index is only the gradient's routing (core.py:721-726):
+    # without a node to record, the value-only scan runs (no index tracking)
+    out, arg = _reduce(L.RED_MAX, x, axes, oshape, want_arg=is_recording() and x.requires_grad)
+    if arg is None:
+        return out
     in_shape = x.shape
     mask = _mask(axes)
 
@@ -897,14 +901,16 @@ GEMM_TIMER = None  # bench/profiling: a list receiving (flops, start_event, end_
 
 
 def set_gemm_algo(name):
-    """Force 'simt' | '3xtf32' | '1xtf32' | 'tf32x' | 'bf16' | None (auto) for
-    subsequent matmuls. 'bf16' is the reduced-precision variant (bf16 operands,
-    fp32 accumulation, fp32 master values everywhere else) and is only ever
-    used when asked for."""
+    """Force 'simt' | '3xtf32' | '1xtf32' | 'tf32x' | '3xbf16' | 'bf16' | 'ref' |
+    None (auto) for subsequent matmuls. 'bf16' is the reduced-precision variant
+    (bf16 operands, fp32 accumulation, fp32 master values everywhere else) and
+    is only ever used when asked for. 'ref' is the reference's own arithmetic
+    (exact fp32 products summed in fp64, one f32 rounding: core.py:802-807) on
+    the FP64 pipe -- the parity mode, not a performance path."""
     global _ALGO_OVERRIDE
     _ALGO_OVERRIDE = {None: None, "auto": None, "simt": L.GEMM_SIMT, "3xtf32": L.GEMM_3XTF32,
                       "1xtf32": L.GEMM_1XTF32, "tf32x": L.GEMM_TF32X, "3xbf16": L.GEMM_3XBF16,
-                      "bf16": L.GEMM_BF16}[name]
+                      "bf16": L.GEMM_BF16, "ref": L.GEMM_REF}[name]
 
 
 def get_gemm_algo():

@@ -34,6 +34,8 @@ extern "C" int b2_free(void*, void*);
 namespace {
 
 constexpr int64_t kNone = INT64_MAX;
+// internal op: max without the first-index routing (no gradient to route)
+constexpr int kMaxValue = 3;
 
 struct MaxAcc {
   float v;
@@ -310,7 +312,7 @@ __global__ void __launch_bounds__(256) k_strip(const float* __restrict__ x, int6
   const int64_t r0 = s * Rs, r1 = min(R, r0 + Rs);
   const bool live = i < I;
   const float* base = x + o1 * R * I + (live ? i : 0);
-  if (OP != B2_RED_MAX) {
+  if constexpr (OP == B2_RED_SUM || OP == B2_RED_MEAN) {
     double a[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) a[j] = 0.0;
@@ -495,7 +497,7 @@ __global__ void __launch_bounds__(256) k_cols(const float* __restrict__ x, int64
   const int64_t r0 = s * Rs, r1 = min(R, r0 + Rs);
   const bool live = i < I;
   const float* base = x + o1 * R * I + (live ? i : 0);
-  if (OP != B2_RED_MAX) {
+  if constexpr (OP == B2_RED_SUM || OP == B2_RED_MEAN) {
     double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
     if (live) {
       int64_t r = r0 + rl;
@@ -551,6 +553,78 @@ __global__ void __launch_bounds__(256) k_cols(const float* __restrict__ x, int64
       }
     }
     cluster.sync();  // keep every CTA's shared memory alive until rank 0 has read it
+  } else if constexpr (OP == kMaxValue) {
+    // value-only max (no gradient will be routed, so no index is tracked):
+    // fmaxf skips NaN like the strict '>' scan; the first-slot NaN rule is
+    // applied at the end, and a zero maximum takes the sign of the column's
+    // first zero (the in-order scan keeps the first of +-0 ties)
+    __shared__ float shv[8][32];
+    __shared__ float cpv[32];
+    float b[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    const int64_t cfirst = ((blockIdx.x - o1 * strips) * 8) * 4 + threadIdx.x;
+    const float v0 = (s == 0 && threadIdx.x < 32 && cfirst < I) ? x[o1 * R * I + cfirst] : 0.0f;
+    if (live) {
+      int64_t r = r0 + rl;
+      constexpr int U = 8;
+      for (; r + (U - 1) * RL < r1; r += U * RL) {
+        float4 v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) v[k] = __ldg(reinterpret_cast<const float4*>(base + (r + k * RL) * I));
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          b[0] = fmaxf(b[0], v[k].x);
+          b[1] = fmaxf(b[1], v[k].y);
+          b[2] = fmaxf(b[2], v[k].z);
+          b[3] = fmaxf(b[3], v[k].w);
+        }
+      }
+      for (; r < r1; r += RL) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(base + r * I));
+        b[0] = fmaxf(b[0], v.x);
+        b[1] = fmaxf(b[1], v.y);
+        b[2] = fmaxf(b[2], v.z);
+        b[3] = fmaxf(b[3], v.w);
+      }
+    }
+#pragma unroll
+    for (int off = 8; off <= 16; off <<= 1)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = fmaxf(b[j], __shfl_xor_sync(0xffffffffu, b[j], off));
+    if (lane < 8)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) shv[w][cl * 4 + j] = b[j];
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float t = shv[0][threadIdx.x];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) t = fmaxf(t, shv[k][threadIdx.x]);
+      cpv[threadIdx.x] = t;
+    }
+    cluster.sync();
+    if (s == 0 && threadIdx.x < 32) {
+      const int64_t c = cfirst;
+      float t = cpv[threadIdx.x];
+      for (int q = 1; q < S; ++q) t = fmaxf(t, cluster.map_shared_rank(cpv, q)[threadIdx.x]);
+      if (c < I) {
+        if (isnan(v0)) {
+          t = v0;
+        } else {
+          t = fmaxf(t, v0);
+          if (t == 0.0f) {  // every non-NaN value <= 0: the first zero in scan order wins
+            const float* col = x + o1 * R * I + c;
+            for (int64_t r = 0; r < R; ++r) {
+              const float v = col[r * I];
+              if (v == 0.0f) {
+                t = v;
+                break;
+              }
+            }
+          }
+        }
+        out[o1 * I + c] = t;
+      }
+    }
+    cluster.sync();
   } else {
     float b[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
     int bi[4] = {kNone32, kNone32, kNone32, kNone32};
@@ -935,14 +1009,16 @@ int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_
     int cs = 1;
     while (cs < 16 && base_ctas * cs < target && R >= (int64_t)(cs * 2) * 32 * 8) cs *= 2;
     if (cs == 16) {  // a non-portable cluster size (narrow, tall inputs: e.g. 1024 bias columns)
-      static bool np_ok = cudaFuncSetAttribute(k_cols<OP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                          cudaSuccess;
+      static bool np_ok =
+          cudaFuncSetAttribute(k_cols<OP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+          (OP != B2_RED_MAX ||
+           cudaFuncSetAttribute(k_cols<kMaxValue>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess);
       if (!np_ok) {
         cudaGetLastError();
         cs = 8;
       }
     }
-    if (base_ctas * cs >= 2LL * sms && base_ctas <= INT32_MAX) {
+    while (base_ctas * cs >= 2LL * sms && base_ctas <= INT32_MAX) {
       const int64_t Rs = (R + cs - 1) / cs;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)base_ctas, (unsigned)cs, 1);
@@ -955,7 +1031,16 @@ int run_mid(const float* x, int64_t O1, int64_t R, int64_t I, float* out, int64_
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      cudaError_t e = cudaLaunchKernelEx(&cfg, k_cols<OP>, x, R, I, Rs, out, argr, count, cstrips);
+      cudaError_t e = (OP == B2_RED_MAX && !argr)
+                          ? cudaLaunchKernelEx(&cfg, k_cols<kMaxValue>, x, R, I, Rs, out, argr, count, cstrips)
+                          : cudaLaunchKernelEx(&cfg, k_cols<OP>, x, R, I, Rs, out, argr, count, cstrips);
+      if (e != cudaSuccess && cs > 8) {
+        // 16-CTA clusters could not be placed (MIG/MPS partitions, busy GPCs):
+        // retry with the portable cluster size
+        cudaGetLastError();
+        cs = 8;
+        continue;
+      }
       if (e != cudaSuccess) return b2::cuda_fail(e, "b2_reduce(cols)");
       return b2::launched("b2_reduce(cols)");
     }

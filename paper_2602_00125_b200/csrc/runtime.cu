@@ -12,6 +12,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -36,16 +37,68 @@ static std::mutex g_init_mu;
 static int g_device = -1;
 static int g_sms = 0;
 static cudaStream_t g_stream = nullptr;
+static std::thread::id g_main_thread;
+
+// One engine stream per host thread (the reference keeps one tape per thread,
+// autograd.py:48-56; here each thread's ops also queue on their own CUDA
+// stream, so two threads' work is independent and each thread's launches stay
+// in program order). The thread that calls b2_init owns g_stream; any other
+// thread gets a stream on its first call (and the device selected, since
+// cudaSetDevice is per thread). A finished thread's stream goes back to a
+// pool for the next new thread: blocks cached on it stay valid (same stream).
+static std::mutex g_pool_mu;
+static std::vector<cudaStream_t> g_stream_pool;
+
+struct ThreadStream {
+  cudaStream_t st = nullptr;
+  bool owned = false;  // taken from the pool / created for this thread
+  ~ThreadStream() {
+    if (owned && st) {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      g_stream_pool.push_back(st);
+    }
+  }
+};
+static thread_local ThreadStream t_stream;
+
+static cudaStream_t thread_stream() {
+  if (t_stream.st) return t_stream.st;
+  if (!g_stream && b2_init(-1) != 0) return nullptr;
+  if (std::this_thread::get_id() == g_main_thread) {
+    t_stream.st = g_stream;
+    return g_stream;
+  }
+  cudaSetDevice(g_device);
+  cudaStream_t st = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (!g_stream_pool.empty()) {
+      st = g_stream_pool.back();
+      g_stream_pool.pop_back();
+    }
+  }
+  if (!st && cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return g_stream;
+  }
+  tickets(st);
+  t_stream.st = st;
+  t_stream.owned = true;
+  return st;
+}
 
 int ensure_init() {
-  if (g_stream) return 0;
-  return b2_init(-1);
+  if (!g_stream) B2_TRY(b2_init(-1));
+  if (!t_stream.st) thread_stream();  // selects the device on a new thread
+  return 0;
 }
 
 cudaStream_t resolve(void* stream) {
-  if (stream) return (cudaStream_t)stream;
-  if (!g_stream) ensure_init();
-  return g_stream;
+  if (stream) {
+    if (!t_stream.st) thread_stream();  // this thread's device is selected
+    return (cudaStream_t)stream;
+  }
+  return thread_stream();
 }
 
 // Per-stream arrival counters for single-launch two-stage reductions (the
@@ -173,6 +226,7 @@ int b2_init(int device) {
   g_sms = prop.multiProcessorCount;
   B2_CUDA(cudaStreamCreateWithFlags(&g_stream, cudaStreamNonBlocking));
   g_device = device;
+  g_main_thread = std::this_thread::get_id();
   if (!tickets(g_stream)) return fail("b2_init: could not allocate reduction counters");
   return 0;
 }
@@ -199,7 +253,7 @@ int b2_device_info(int* sm, int* maj, int* min, size_t* total) {
 
 int b2_default_stream(void** s) {
   B2_TRY(ensure_init());
-  *s = (void*)g_stream;
+  *s = (void*)resolve(nullptr);  // the calling thread's engine stream
   return 0;
 }
 int b2_stream_create(void** s) {
@@ -345,7 +399,10 @@ int b2_free(void* ptr, void* stream) {
     }
     b->graph = 0;
   }
-  cudaStream_t fs = stream ? (cudaStream_t)stream : b->stream;
+  // last use: the given stream, else the calling thread's engine stream (a
+  // block freed from another thread -- e.g. by the garbage collector -- waits
+  // for that thread's queued work before its owner stream may reuse it)
+  cudaStream_t fs = stream ? (cudaStream_t)stream : resolve(nullptr);
   if (fs == b->stream) {
     g_free[b->stream].emplace(b->size, b);
   } else {

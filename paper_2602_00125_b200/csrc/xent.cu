@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(256) k_xent_rows(double* __restrict__ row_loss
       double se = tot;
       row_stats[2 * r] = m;
       row_stats[2 * r + 1] = se;
-      row_loss[r] = m + log(se) - (double)row[labels[r]];
+      const int64_t lab = labels[r];  // out of range (an unchecked Buffer): NaN loss, no stray read
+      row_loss[r] = m + log(se) - (lab >= 0 && lab < C ? (double)row[lab] : (double)NAN);
     }
   }
 }
@@ -497,7 +498,8 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_xent_rows_v(double* __rest
     if (lane == 0) {
       row_stats[2 * r] = m;
       row_stats[2 * r + 1] = tot;
-      row_loss[r] = m + log(tot) - (double)z[r * C + labels[r]];
+      const int64_t lab = labels[r];
+      row_loss[r] = m + log(tot) - (lab >= 0 && lab < C ? (double)z[r * C + lab] : (double)NAN);
     }
   }
 }
@@ -541,7 +543,7 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_xent_rows_tma(double* __re
       const int64_t q = i * 32 + lane;
       v[i] = q * 4 < C ? row[q] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const float zl = rowp[lab];
+    const float zl = (lab >= 0 && lab < C) ? rowp[lab] : __int_as_float(0x7fc00000);  // guarded read
     __syncwarp();  // every lane has its values: the buffer may be refilled next iteration
     const double m = (double)row_max_regs<NV>(v, C, lane);
     double sum = 0, comp = 0;

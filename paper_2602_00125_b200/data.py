@@ -94,7 +94,7 @@ class PinnedFeeder:
     stream waits until its slot's copy has landed). Every step still moves its
     full batch host -> device; the copy just overlaps the previous step."""
 
-    def __init__(self, x, labels, presplit=None, resident=False):
+    def __init__(self, x, labels, presplit=None, resident=False, classes=None):
         """presplit="3xbf16": also make each batch's 3xBF16 operand split on
         the copy stream right after its H2D copy (the first layer's GEMM reads
         x only through that split), so the split of step i+1's batch overlaps
@@ -104,6 +104,11 @@ class PinnedFeeder:
         still redoes its split (when presplit) on the copy stream."""
         self.presplit = presplit
         self.resident = resident
+        labels = np.asarray(labels)
+        if classes is not None and labels.size and (labels.min() < 0 or labels.max() >= classes):
+            bad = int(labels[(labels < 0) | (labels >= classes)][0])
+            raise ValueError(f"label {bad} out of range for {classes} classes")
+        self.copy_stream = None
         self.hx = PinnedHost(x.shape, np.float32)
         self.hx.array[...] = x
         self.hl = PinnedHost(labels.shape, np.int64)
@@ -130,6 +135,20 @@ class PinnedFeeder:
                 L.call("b2_memcpy_h2d", self.dl[slot].ptr, self.hl.ptr, self.hl.nbytes, None)
             L.synchronize()
         self._issue(0)
+
+    def close(self):
+        """Drain the copy stream (a queued copy or split may still write the
+        slots) and destroy it; the slot buffers are then safe to free."""
+        cs, self.copy_stream = self.copy_stream, None
+        if cs is not None and L._lib is not None:
+            L._lib.b2_stream_sync(cs)
+            L._lib.b2_stream_destroy(cs)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     @property
     def h2d_bytes(self):

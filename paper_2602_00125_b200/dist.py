@@ -137,6 +137,40 @@ class Communicator:
             self.allreduce_(t, SUM)
         L.call("b2_device_sync")
 
+    # ---- the device plumbing GradReducer drives (a test double replaces these)
+
+    _side = None  # per-process side stream for single-process optimizer overlap
+
+    def side_stream(self):
+        """The stream gradient averaging / overlapped updates run on."""
+        if self.active:
+            return self.comm_stream
+        if Communicator._side is None:
+            s = ctypes.c_void_p()
+            L.check(L.lib().b2_stream_create(ctypes.byref(s)))
+            Communicator._side = s.value
+        return Communicator._side
+
+    def after_compute(self, stream):
+        """Order `stream` after everything queued so far on the engine stream;
+        returns the event (kept alive by the caller until the step ends)."""
+        ev = L.Event()
+        ev.record(None)
+        L.call("b2_stream_wait_event", stream, ev.h)
+        return ev
+
+    def join(self, stream):
+        """Order the engine stream after everything queued so far on `stream`."""
+        done = L.Event()
+        done.record(stream)
+        L.call("b2_stream_wait_event", None, done.h)
+
+    def private_copy(self, t):
+        """A fresh contiguous copy of t (engine stream)."""
+        from .core import _copy_contig
+
+        return _copy_contig(t)
+
     def max_scalar(self, v: float) -> float:
         """Max of a host float over ranks (device NCCL allreduce)."""
         if not self.active:
@@ -161,10 +195,8 @@ class GradReducer:
     its all-reduce (or right away for a single process): a layer's weights
     are no longer read once its last gradient is queued, so the HBM-bound
     update kernels overlap the remaining tensor-core GEMMs of the backward.
-    (Leaf gradients of Dense layers are fresh tensors; an aliased leaf
-    gradient would be averaged in place too.)"""
-
-    _side = None  # per-process side stream for single-process optimizer overlap
+    Leaf gradients of Dense layers are fresh tensors and are averaged in
+    place; an aliased or strided one is averaged as a private copy."""
 
     def __init__(self, comm: Communicator, params=None, timeout_s=None, optimizer=None):
         self.comm = comm
@@ -181,50 +213,49 @@ class GradReducer:
         if optimizer is not None and not params:
             raise ValueError("GradReducer(optimizer=...) needs the parameter list")
 
-    def _stream(self):
-        if self.comm.active:
-            return self.comm.comm_stream
-        if GradReducer._side is None:
-            s = ctypes.c_void_p()
-            L.check(L.lib().b2_stream_create(ctypes.byref(s)))
-            GradReducer._side = s.value
-        return GradReducer._side
-
     def _param(self, node_id):
         if self._by_node is None:
             self._by_node = {p.node.id: p for p in self.params if p.node is not None}
         return self._by_node.get(node_id)
 
     def hook(self, node_id, grad):
+        """on_leaf_ready hook: average `grad` over the ranks on the side stream
+        (and launch the parameter's update after it). A gradient that does not
+        own its whole buffer exclusively -- a view, or a first contribution the
+        store shares with another cotangent (autograd.grad_is_exclusive) -- is
+        first copied to a fresh contiguous tensor on the engine stream; that
+        copy is what gets averaged, updated from, and returned so the store
+        holds the averaged gradient."""
         if not self.comm.active and self.optimizer is None:
-            return
+            return None
+        from .autograd import grad_is_exclusive
+
+        if (self.comm.active and not grad_is_exclusive(grad)) or not grad.is_contiguous:
+            grad = self.comm.private_copy(grad)  # averaged / updated from a private copy
         handle = None
         if self.optimizer is not None:
             p = self._param(node_id)
             if p is not None:
-                # slot creation / contiguity copies go on the engine stream
-                # BEFORE the event the side stream waits on
+                # slot creation goes on the engine stream BEFORE the event the
+                # side stream waits on
                 handle = self.optimizer.prepare([(p, grad)])
                 self._updated.add(id(p))
-        s = self._stream()
-        ev = L.Event()
-        ev.record(None)  # grad produced on the compute stream
-        L.call("b2_stream_wait_event", s, ev.h)
+        s = self.comm.side_stream()
+        ev = self.comm.after_compute(s)  # grad produced on the compute stream
         if self.comm.active:
             self.comm.allreduce_(grad, AVG, s)
         if handle is not None:
             self.optimizer.launch(handle, stream=s)
         self._pending.append((ev, grad, handle))
         self._used = True
+        return grad
 
     def finish(self):
         if not self._used:
             return
         if self.comm.active and self.timeout_s is not None:
             self.comm.wait(self.timeout_s)  # failure detection: error/timeout -> abort + raise
-        done = L.Event()
-        done.record(self._stream())
-        L.call("b2_stream_wait_event", None, done.h)  # the next user of the params waits
+        self.comm.join(self.comm.side_stream())  # the next user of the params waits
         self._pending.clear()
 
     def step_rest(self, store):

@@ -96,6 +96,9 @@ def device_id() -> int:
 
 def to_capsule(t, stream=None):
     """A DLPack capsule viewing tensor t's HBM (no copy)."""
+    # materialise fp32 contents a GEMM left as a split only FIRST: the join is
+    # queued on the engine stream and must precede the event / sync below
+    t.data_ptr
     if stream is not None and stream not in (-1, 0, 1, 2):
         # the consumer will use `stream`; make the engine's queued work visible to it
         ev = L.Event()
@@ -107,7 +110,6 @@ def to_capsule(t, stream=None):
     shape = (c_int64 * max(nd, 1))(*t.shape)
     strides = (c_int64 * max(nd, 1))(*t.strides)
     mt = DLManagedTensor()
-    t.data_ptr  # materialise fp32 contents a GEMM left as a split only
     mt.dl_tensor.data = t.buffer.ptr
     mt.dl_tensor.device = DLDevice(kDLCUDA, device_id())
     mt.dl_tensor.ndim = nd

@@ -91,3 +91,183 @@ def test_shard_rows_requires_equal_shards():
     assert dist.shard_rows(65536, 3, 8) == (24576, 32768)
     with pytest.raises(ValueError):
         dist.shard_rows(10, 0, 3)
+
+
+# ------------------------------------------------------- GradReducer over gloo
+# The overlapped gradient exchange (dist.GradReducer driven by the autograd
+# engine's leaf-ready hook) with its device plumbing replaced by a gloo
+# communicator over host arrays: which gradients are averaged, in which order,
+# in place or as a private copy, and what the optimizer sees.
+
+
+class _HostBuf:
+    """Host storage standing in for a device Buffer (version-counted)."""
+
+    def __init__(self, arr):
+        self.arr = np.ascontiguousarray(arr, np.float32)
+        self.nbytes = self.arr.nbytes
+        self.version = 0
+
+
+def _ht(arr, grad=False):
+    from paper_2602_00125_b200 import core as C
+
+    a = np.ascontiguousarray(arr, np.float32)
+    return C.Tensor(_HostBuf(a), a.shape, requires_grad=grad)
+
+
+def _arr(t):
+    return t.buffer.arr.reshape(t.shape)
+
+
+class _GlooComm:
+    """dist.Communicator's interface over torch.distributed gloo."""
+
+    def __init__(self, world):
+        self.active = world > 1
+        self.world = world
+        self.log = []
+
+    def allreduce_(self, t, op=1, stream=None):
+        self.log.append(("allreduce", id(t.buffer)))
+        g = torch.from_numpy(t.buffer.arr)
+        tdist.all_reduce(g, op=tdist.ReduceOp.SUM)
+        if op == 1:
+            g /= self.world
+        return t
+
+    def side_stream(self):
+        return None
+
+    def after_compute(self, stream):
+        return None
+
+    def join(self, stream):
+        self.log.append(("join",))
+
+    def private_copy(self, t):
+        self.log.append(("copy", id(t.buffer)))
+        return _ht(_arr(t).copy())
+
+    def wait(self, timeout_s):
+        pass
+
+
+def _host_model_step(x, params, on_leaf_ready):
+    """loss = mean((relu-free) (x W1^T + B) W2^T)^2 recorded on the tape with
+    host pullbacks. B has h's shape, so the add's pullback hands the SAME
+    cotangent to B (a leaf: ready at the add) and to h (still to be consumed
+    by the first matmul) -- the aliasing case the reducer must copy."""
+    from paper_2602_00125_b200 import autograd as A
+
+    W1, B, W2 = params
+    xa = np.asarray(x, np.float32)
+
+    def mm(a, w):  # a . w^T
+        out = _ht(_arr(a) @ _arr(w).T)
+        return A.record("mm", (a, w), out,
+                        (lambda g: _ht(_arr(g) @ _arr(w)), lambda g: _ht(_arr(g).T @ _arr(a))))
+
+    def add(a, b):
+        out = _ht(_arr(a) + _arr(b))
+        return A.record("add", (a, b), out, (lambda g: g, lambda g: g))
+
+    def mean_sq(z):
+        v = _arr(z)
+        out = _ht(np.array([np.mean(v.astype(np.float64) ** 2)], np.float32))
+        return A.record("mean_sq", (z,), out,
+                        (lambda g: _ht(_arr(g)[0] * 2.0 * v / v.size),))
+
+    A.reset_tape()
+    h = mm(_ht(xa), W1)
+    h2 = add(h, B)
+    loss = mean_sq(mm(h2, W2))
+    return A.backward(loss, seed=_ht(np.ones(1, np.float32)), on_leaf_ready=on_leaf_ready)
+
+
+def _reducer_worker(rank, world, port, outq):
+    import datetime
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_2602_00125_b200 import dist
+
+    tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                             world_size=world, timeout=datetime.timedelta(seconds=120))
+    rng = np.random.default_rng(1)
+    Bt, D, H, O = 8, 6, 5, 3
+    x = rng.standard_normal((Bt, D)).astype(np.float32)
+    w1 = rng.standard_normal((H, D)).astype(np.float32) * 0.3
+    w2 = rng.standard_normal((O, H)).astype(np.float32) * 0.3
+    bfull = rng.standard_normal((Bt, H)).astype(np.float32) * 0.1
+    lo, hi = dist.shard_rows(Bt, rank, world)
+
+    class RecOpt:  # records what the overlapped update would read
+        def __init__(self):
+            self.seen = []
+
+        def prepare(self, pairs):
+            return [(p, g) for p, g in pairs]
+
+        def launch(self, handle, stream=None):
+            for p, g in handle:
+                self.seen.append((p.node.id, _arr(g).copy()))
+
+    params = [_ht(w1, True), _ht(bfull[lo:hi], True), _ht(w2, True)]
+    comm = _GlooComm(world)
+    opt = RecOpt()
+    red = dist.GradReducer(comm, params, optimizer=opt)
+    by_buf = {}
+
+    def hook(nid, g):  # the reducer's hook, noting which leaf each averaged buffer belongs to
+        out = red.hook(nid, g)
+        by_buf[id(out.buffer)] = nid
+        return out
+
+    store = _host_model_step(x[lo:hi], params, hook)
+    red.finish()
+    got = {name: _arr(store[p]).copy() for name, p in zip(("W1", "B", "W2"), params)}
+    order = [by_buf.get(e[1]) for e in comm.log if e[0] == "allreduce"]
+    ids = [p.node.id for p in params]
+    copies = sum(1 for e in comm.log if e[0] == "copy")
+    seen = {nid: g for nid, g in opt.seen}
+    # single-process full-batch reference (no reducer)
+    fparams = [_ht(w1, True), _ht(bfull, True), _ht(w2, True)]
+    fstore = _host_model_step(x, fparams, None)
+    full = {name: _arr(fstore[p]).copy() for name, p in zip(("W1", "B", "W2"), fparams)}
+    outq.put((rank, got, full, order, ids, copies, {k: v for k, v in seen.items()},
+              [e[0] for e in comm.log][-1]))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_gloo_world2_grad_reducer_hook_order_aliasing_and_averages():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_reducer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=180) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, got, full, order, ids, copies, seen, last in res:
+        w1_id, b_id, w2_id = ids
+        # leaf-ready order = reverse layer order: W2 (last matmul), B (add), W1
+        assert order == [w2_id, b_id, w1_id], order
+        assert copies == 1  # only B's gradient aliases a pending cotangent
+        assert last == "join"
+        # W's are data-parallel gradients: mean of shard means == full batch
+        # (only if B's aliased cotangent was NOT averaged in place)
+        for name in ("W1", "W2"):
+            np.testing.assert_allclose(got[name], full[name], rtol=1e-5, atol=1e-7)
+        # the optimizer read exactly the averaged gradients the store holds
+        for nid, name in ((w1_id, "W1"), (b_id, "B"), (w2_id, "W2")):
+            np.testing.assert_array_equal(seen[nid], got[name])
+    # B is per-row: its averaged gradient is the mean of the two ranks' shard
+    # gradients, each of which is world x the full-batch one on its rows
+    (_, g0, f0, *_), (_, g1, *_) = res
+    np.testing.assert_allclose(g0["B"], f0["B"][:4] + f0["B"][4:], rtol=1e-5, atol=1e-7)
+    np.testing.assert_array_equal(g0["B"], g1["B"])

@@ -1,0 +1,176 @@
+"""Host-contract tests on the device: the per-thread tape AND engine stream
+(pkg/tests/test_autograd.py:316-331; SURVEY 8b "one CUDA stream per (thread,
+device)"), label validation / the kernel's out-of-range guard, the input
+feeder's teardown, DLPack export ordering of split-only GEMM outputs, the
+value-only max and the memory released by ``keep_intermediate=False``."""
+
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2602_00125_b200 as P
+from paper_2602_00125_b200 import _lib as L
+from paper_2602_00125_b200 import autograd, nn, optim
+from tests.golden import inputs as I
+from tests.golden.load import bits_equal
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a, grad=False):
+    return P.from_numpy(np.asarray(a, np.float32), requires_grad=grad)
+
+
+def test_tapes_and_engine_streams_are_thread_local():
+    x = dev([1.0], True)
+    P.mul(x, x)
+    main_len = len(P.tape())
+    main_stream = L.default_stream()
+    seen = {}
+
+    def worker():
+        y = dev([2.0], True)
+        z = P.mul(y, y)
+        seen["len"] = len(P.tape())  # leaf + mul on a fresh tape
+        seen["stream"] = L.default_stream()
+        seen["grad"] = P.backward(P.sum(z))[y].numpy().tolist()
+
+    t = threading.Thread(target=worker)
+    t.start()
+    t.join()
+    assert seen["len"] == 2
+    assert len(P.tape()) == main_len
+    assert seen["stream"] != main_stream
+    assert seen["grad"] == [4.0]
+
+
+def _config1_steps(params, x, labels, steps, out, key):
+    layers = []
+    for i, (w, b) in enumerate(params):
+        d = nn.Dense(w.shape[1], w.shape[0], rng=0)
+        d.weight.write_flat(w.ravel())
+        d.bias.write_flat(b.ravel())
+        layers.append(d)
+        if i < len(params) - 1:
+            layers.append(nn.ReLU())
+    model = nn.Sequential(*layers)
+    opt = optim.SGD(lr=0.01)
+    xt = dev(x)
+    losses = []
+    for _ in range(steps):
+        P.reset_tape()
+        loss = nn.cross_entropy(model(xt), labels)
+        optim.step_all(opt, model.parameters(), P.backward(loss))
+        losses.append(loss.item())
+    out[key] = (losses, [p.numpy() for p in model.parameters()])
+
+
+def test_two_threads_train_concurrently_bit_identical_to_sequential():
+    """Each thread's ops queue on its own stream with its own tape: two
+    threads training their own config-1 model at the same time produce the
+    bits a sequential run produces."""
+    params, x, labels = I.config1_inputs()
+    params2, x2, labels2 = I.config1_inputs(seed=1)
+    seq = {}
+    _config1_steps(params, x, labels, 3, seq, "a")
+    _config1_steps(params2, x2, labels2, 3, seq, "b")
+    par = {}
+    ts = [threading.Thread(target=_config1_steps, args=(params, x, labels, 3, par, "a")),
+          threading.Thread(target=_config1_steps, args=(params2, x2, labels2, 3, par, "b"))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for k in ("a", "b"):
+        assert par[k][0] == seq[k][0], k
+        for g, w in zip(par[k][1], seq[k][1]):
+            assert bits_equal(g, w), k
+
+
+def test_labels_buffer_validates_and_kernel_guards_unchecked_labels():
+    z = dev(np.zeros((4, 10), np.float32))
+    with pytest.raises(ValueError, match="out of range"):
+        nn.labels_buffer([0, 1, 10, 2], classes=10)
+    bad = nn.labels_buffer([0, 1, 10, -3])  # unchecked: the kernel must not read past the row
+    assert np.isnan(nn.cross_entropy(z, bad).item())
+    ok = nn.labels_buffer([0, 1, 9, 2], classes=10)
+    assert abs(nn.cross_entropy(z, ok).item() - np.log(10.0)) < 1e-6
+
+
+def test_pinned_feeder_rejects_bad_labels_and_closes_cleanly():
+    from paper_2602_00125_b200.data import PinnedFeeder
+
+    x = np.random.default_rng(0).standard_normal((64, 128)).astype(np.float32)
+    with pytest.raises(ValueError, match="out of range"):
+        PinnedFeeder(x, np.arange(64) % 11, classes=10)
+    f = PinnedFeeder(x, np.arange(64) % 10, presplit="3xbf16", classes=10)
+    xb, _ = f.next()
+    assert bits_equal(xb.numpy(), x)
+    f.close()
+    f.close()  # idempotent
+    assert f.copy_stream is None
+
+
+def test_dlpack_export_of_a_split_only_output_orders_the_materialisation():
+    """A hidden layer's GEMM writes only its operand split; exporting it over
+    DLPack must queue the fp32 materialisation BEFORE the consumer's stream
+    is ordered after the engine (the consumer reads fp32 values)."""
+    torch = pytest.importorskip("torch")
+    from paper_2602_00125_b200 import core as C
+
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((512, 512)).astype(np.float32)
+    w = (rng.standard_normal((512, 512)) * 0.05).astype(np.float32)
+    b = np.zeros(512, np.float32)
+    P.set_gemm_algo("3xbf16")
+    try:
+        with P.no_grad():
+            h = C.linear(dev(x), dev(w), dev(b), relu_out=True)
+            h2 = C.linear(dev(x), dev(w), dev(b), relu_out=True)
+    finally:
+        P.set_gemm_algo(None)
+    assert h.buffer._pending is not None  # split-only: fp32 not written yet
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        th = torch.from_dlpack(h)
+        got = th.cpu().numpy()
+    assert bits_equal(got, h2.numpy())
+
+
+def test_keep_intermediate_false_frees_cotangents_during_backward():
+    """Same gradients, and the hidden cotangents are released as soon as their
+    pullback consumed them (only leaf gradients remain in the store)."""
+    params, x, labels = I.config5_inputs(width=256, classes=16, batch=256, depth=3)
+
+    def run(keep):
+        model = nn.Sequential(*[m for i, (w, b) in enumerate(params) for m in (
+            [nn.Dense(w.shape[1], w.shape[0], rng=0)] + ([nn.ReLU()] if i < len(params) - 1 else []))])
+        dense = [m for m in model.layers if isinstance(m, nn.Dense)]
+        for d, (w, b) in zip(dense, params):
+            d.weight.write_flat(w.ravel())
+            d.bias.write_flat(b.ravel())
+        P.reset_tape()
+        loss = nn.cross_entropy(model(dev(x)), labels)
+        store = P.backward(loss, keep_intermediate=keep)
+        return len(store), [store[p].numpy() for p in model.parameters()]
+
+    n_keep, g_keep = run(True)
+    n_drop, g_drop = run(False)
+    assert n_drop == len(g_drop) and n_keep > n_drop
+    for a, b in zip(g_keep, g_drop):
+        assert bits_equal(a, b)
+
+
+def test_backward_schedule_prunes_unreachable_nodes():
+    x = dev([1.0, 2.0], True)
+    y = dev([3.0, 4.0], True)
+    side = P.exp(y)  # recorded, but not on the loss's path
+    loss = P.sum(P.mul(x, x))
+    sch = autograd.schedule(loss)
+    assert side.node.id not in sch.order
+    calls = P.tape().pullback_calls
+    store = P.backward(loss)
+    assert P.tape().pullback_calls - calls == len(sch.order) == 2
+    assert store[x].numpy().tolist() == [2.0, 4.0]
+    assert y not in store

@@ -162,6 +162,43 @@ def test_max_dim0_ties_signed_zeros_nans_at_scale():
     assert bits_equal(host(store[xt]), O.max_pullback(np.ones(C, np.float32), pos, x.shape))
 
 
+@pytest.mark.parametrize("shape", [(4096, 4096), (8192, 1024)])
+@pytest.mark.parametrize("recording", [False, True])
+def test_max_dim0_cluster_path_value_only_and_routed(shape, recording):
+    """The DSMEM-cluster column max (k_cols; cluster of 4 at 4096^2, 16 at
+    8192x1024) in both forms: value-only when no node is recorded (no_grad or
+    an input without grad: the config-2 bench case) and with first-index
+    routing when one is. Same values either way: first-slot NaN sticks, NaNs
+    skipped, +-0 maxima take the sign of the first zero, all -inf columns."""
+    rng = np.random.default_rng(12)
+    R, C = shape
+    x = rng.standard_normal((R, C)).astype(np.float32)
+    x[rng.random((R, C)) < 0.001] = np.nan
+    x[0, 3] = np.nan                         # first-slot NaN sticks
+    x[:, 8] = -np.inf
+    x[:, 10] = -np.abs(x[:, 10])
+    x[17, 10] = -0.0
+    x[900, 10] = 0.0                         # -0 first: the max is -0
+    x[:, 12] = -np.abs(x[:, 12])
+    x[5, 12] = 0.0
+    x[6, 12] = -0.0                          # +0 first: the max is +0
+    x[:, 14] = np.nan
+    x[0, 14] = 1.0                           # NaNs after the first slot are skipped
+    x[:, 15] = -np.abs(x[:, 15])
+    x[R - 1, 15] = -0.0                      # the only zero is the last row
+    v, pos = O.axis_max(x, 0)
+    if recording:
+        xt = dev(x, grad=True)
+        r = P.max(xt, axis=0)
+        assert bits_equal(host(r), v)
+        store = P.backward(P.sum(r))
+        assert bits_equal(host(store[xt]), O.max_pullback(np.ones(C, np.float32), pos, x.shape))
+    else:
+        with P.no_grad():
+            assert bits_equal(host(P.max(dev(x, grad=True), axis=0)), v)
+        assert bits_equal(host(P.max(dev(x), axis=0)), v)
+
+
 def test_zero_extent_reductions():
     e = P.zeros((0, 3))
     assert P.sum(e).item() == 0.0
@@ -174,7 +211,7 @@ def test_zero_extent_reductions():
 # ---------------------------------------------------------------- matmul
 
 
-@pytest.mark.parametrize("algo", ["simt", "3xtf32", "tf32x", "3xbf16"])
+@pytest.mark.parametrize("algo", ["simt", "3xtf32", "tf32x", "3xbf16", "ref"])
 def test_matmul_goldens(algo):
     g = load("matmul.npz")
     P.set_gemm_algo(algo)
@@ -187,6 +224,9 @@ def test_matmul_goldens(algo):
             for got, key in ((y, "y"), (store[xt], "dx"), (store[wt], "dw")):
                 want = g[f"m{i}_{key}"]
                 assert got.shape == want.shape
+                if algo == "ref":  # the reference's compensated double dot: its exact bits
+                    assert bits_equal(host(got), want), (i, key)
+                    continue
                 tol = 1e-5 if algo == "3xbf16" else 2e-6  # 3xBF16 operands carry 16 bits
                 assert normwise(host(got), want) <= tol, (algo, i, key)
     finally:
@@ -608,6 +648,39 @@ def _run_mlp_device(params, x, labels, opt, steps):
         grads = [(host(store[d.weight]), host(store[d.bias])) for d in dense]
         optim.step_all(opt, model.parameters(), store)
     return np.array(losses, np.float32), grads, [(host(d.weight), host(d.bias)) for d in dense]
+
+
+def test_config1_train_step_reference_arithmetic_bit_exact():
+    """With the reference's GEMM arithmetic ('ref') every kernel of the
+    config-1 step reproduces the reference's bits: loss, all 4 gradients and
+    the SGD-updated parameters equal the goldens made by running it."""
+    golden = load("config1.npz")
+    params, x, labels = I.config1_inputs()
+    P.set_gemm_algo("ref")
+    try:
+        losses, grads, newp = _run_mlp_device(params, x, labels, optim.SGD(lr=0.01), 1)
+    finally:
+        P.set_gemm_algo(None)
+    assert bits_equal(losses, golden["loss"])
+    for i, ((gw, gb), (w, b)) in enumerate(zip(grads, newp)):
+        for got, key in ((gw, "gw"), (gb, "gb"), (w, "w"), (b, "b")):
+            assert bits_equal(got, golden[f"{key}{i}"]), (key, i)
+
+
+def test_config5_small_adam_reference_arithmetic_bit_exact():
+    """3 Adam steps of the config-5-shaped MLP in the 'ref' GEMM mode: losses,
+    last gradients and parameters bit-identical to the reference's goldens."""
+    golden = load("config5_small.npz")
+    params, x, labels = I.config5_inputs(width=64, classes=10, batch=32, depth=4)
+    P.set_gemm_algo("ref")
+    try:
+        losses, grads, newp = _run_mlp_device(params, x, labels, optim.Adam(lr=1e-3), 3)
+    finally:
+        P.set_gemm_algo(None)
+    assert bits_equal(losses, golden["loss"])
+    for i, ((gw, gb), (w, b)) in enumerate(zip(grads, newp)):
+        assert bits_equal(gw, golden[f"gw{i}"]), i
+        assert bits_equal(w, golden[f"w{i}"]), i
 
 
 @pytest.mark.parametrize("algo", ["simt", "3xtf32", "tf32x", "3xbf16"])
