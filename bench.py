@@ -367,6 +367,20 @@ def op_benchmarks():
         P.backward(P.mean(P.mul(Y, P.reshape(Tt, (-1, 1024)))))
 
     out["config4_fused_linear_ms_per_step"] = timed(c4_fused, 5)
+    # the step as a PyTorch user writes it with fused layers: nn.Linear (bias in
+    # the GEMM epilogue) + the fused softmax*T mean loss (one row pass each
+    # way; the backward emits the dX/dW GEMMs' operand split and the bias
+    # gradient) -- bit-identical to the composition above
+    T2 = P.reshape(Tt, (-1, 1024))
+
+    def c4_fused_loss():
+        P.reset_tape()
+        X.buffer.version += 1
+        W.buffer.version += 1
+        z = P.linear(X2, P.transpose2d(W), bias)
+        P.backward(P.softmax_mul_mean(z, T2))
+
+    out["config4_fused_loss_ms_per_step"] = timed(c4_fused_loss, 5)
     P.reset_tape()
     del X, W, bias, Tt
 

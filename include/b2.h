@@ -286,6 +286,23 @@ int b2_softmax_fwd(float* y, float* row_s, float* row_m, const float* z,
 int b2_softmax_bwd(float* gz, const float* gy, const float* z, const float* row_s,
                    const float* row_m, int64_t rows, int64_t cols, void* stream);
 
+/* Fused row softmax * t, mean -- BASELINE config 4's loss mean(softmax(z) * t),
+ * bit-identical to composing softmax (above) -> mul (core.py:469-476) -> mean
+ * (core.py:663-689), with one row pass each way (cols % 4 == 0, cols <= 1024,
+ * 16-B aligned rows).
+ * fwd: y (nullable) = softmax(z); row_s/row_m as b2_softmax_fwd; row_dot[r] =
+ *   sum64_j f32(y*t); loss = f32(sum64_r row_dot / (rows*cols)).
+ * bwd: g = the loss cotangent (device scalar); gz = the composed pullback
+ *   (mean: f32(g / count_f32); mul: f32(gp * t); softmax as b2_softmax_bwd).
+ *   Outputs, each nullable: gz (fp32), gz_hi/gz_lo (gz's 3xBF16 split, as
+ *   b2_bf16x3_split), colsum[cols] = f32(sum64 over rows of gz) (the bias
+ *   gradient of a Linear feeding z, core.py:405-423). */
+int b2_softmax_wmean_fwd(float* loss, float* y, float* row_s, float* row_m, double* row_dot,
+                         const float* z, const float* t, int64_t rows, int64_t cols, void* stream);
+int b2_softmax_wmean_bwd(float* gz, void* gz_hi, void* gz_lo, float* colsum, const float* g,
+                         float count_f32, const float* z, const float* t, const float* row_s,
+                         const float* row_m, int64_t rows, int64_t cols, void* stream);
+
 /* ---------------------------------------------------------------- optimizers
  * Optimizer.step/_update + step_all (optim.py:39-136) as ONE multi-tensor
  * launch. Slots are double, like the reference. Per-tensor bias corrections

@@ -15,7 +15,8 @@ from .autograd import (GradStore, backward, is_recording, no_grad, record, reset
 from .core import (Buffer, Tensor, abs_, absolute, add, broadcast_shapes, broadcast_to, clamp, div,
                    exp, from_buffer, from_dlpack, from_flat, from_numpy, full, fused_muladd_relu, gelu, linear,
                    log, matmul, max, mean, mm, mul, muladd_relu_sum_grads, neg, ones, ones_like,
-                   reduce_to_shape, relu, reshape, set_gemm_algo, sigmoid, softmax, sqrt, sub, sum,
+                   reduce_to_shape, relu, reshape, set_gemm_algo, sigmoid, softmax, softmax_mul_mean, sqrt,
+                   sub, sum,
                    tanh, tensor, transpose2d, uniform, zeros, zeros_like)
 from .errors import BroadcastError, DeterminismError, GradError, ShapeError
 
@@ -27,7 +28,8 @@ __all__ = [
     "full", "uniform", "zeros_like", "ones_like",
     "add", "sub", "mul", "div", "neg", "exp", "log", "sqrt", "absolute", "abs_", "relu", "clamp",
     "sigmoid", "tanh", "gelu",
-    "sum", "mean", "max", "matmul", "mm", "linear", "softmax", "reshape", "transpose2d",
+    "sum", "mean", "max", "matmul", "mm", "linear", "softmax", "softmax_mul_mean", "reshape",
+    "transpose2d",
     "broadcast_to", "reduce_to_shape", "broadcast_shapes", "fused_muladd_relu",
     "muladd_relu_sum_grads", "set_gemm_algo",
     "backward", "no_grad", "record", "reset_tape", "tape", "zero_grad", "is_recording",

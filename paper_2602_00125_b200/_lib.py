@@ -118,6 +118,9 @@ _SIGS = {
     "b2_softmax_fwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p]),
     "b2_softmax_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                                c_void_p]),
+    "b2_softmax_wmean_fwd": (c_int, [c_void_p] * 7 + [c_int64, c_int64, c_void_p]),
+    "b2_softmax_wmean_bwd": (c_int, [c_void_p] * 5 + [c_float] + [c_void_p] * 4
+                             + [c_int64, c_int64, c_void_p]),
     "b2_sgd_multi": (c_int, [POINTER(OptTensor), c_int, c_double, c_double, c_double, c_void_p]),
     "b2_adam_multi": (c_int, [POINTER(OptTensor), c_int, c_double, c_double, c_double, c_double,
                               c_double, c_void_p]),

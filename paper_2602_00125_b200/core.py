@@ -457,10 +457,15 @@ def broadcast_to(x: Tensor, shape) -> Tensor:
 
 
 def reduce_to_shape(t: Tensor, shape) -> Tensor:
-    """Sum t down to `shape` (adjoint of broadcasting; core.py:405-423)."""
+    """Sum t down to `shape` (adjoint of broadcasting; core.py:405-423). A
+    cotangent whose producing kernel already summed its columns (fp64, one f32
+    rounding: the same values) returns those sums instead of re-reading t."""
     shape = _check_shape(shape)
     if t.shape == shape:
         return t
+    cs = _COLSUM.get(t) if t.ndim == 2 else None
+    if cs is not None and shape in ((t.shape[1],), (1, t.shape[1])):
+        return reshape(cs, shape)
     pad = t.ndim - len(shape)
     if pad < 0:
         raise ShapeError(f"cannot reduce {t.shape} to larger rank {shape}")
@@ -1177,6 +1182,72 @@ def softmax(x, axis=-1) -> Tensor:
         return gz
 
     return record("softmax", (x,), y, (pull,), saved=(xc,))
+
+
+def _gemm_consumes_as_3xbf16(rows, cols) -> bool:
+    """Would a GEMM reading an [rows, cols] cotangent (x_bar = g . W, W_bar =
+    g^T . x) run the 3xBF16 tensor-core scheme? Then a producer can emit the
+    split that GEMM reads instead of the fp32 tensor."""
+    algo = _ALGO_OVERRIDE
+    if algo is None:
+        sel = ctypes.c_int()
+        L.check(L.lib().b2_gemm_select(0, 0, rows, cols, cols, cols, cols, ctypes.byref(sel)))
+        algo = sel.value
+    return algo == L.GEMM_3XBF16
+
+
+def softmax_mul_mean(z, t) -> Tensor:
+    """mean(softmax(z, -1) * t) -- BASELINE config 4's loss -- with one row pass
+    each way (b2_softmax_wmean_fwd/bwd), bit-identical to the composition
+    softmax -> mul -> mean (core.py:469-476, 663-689). The
+    backward hands its consumers what they read: the 3xBF16 split of z's
+    cotangent when a tensor-core GEMM consumes it (the fp32 values are then
+    materialised only on first fp32 use, as for split-only GEMM outputs), and
+    its column sums (the bias gradient of a Linear that produced z, picked up
+    by reduce_to_shape). Falls back to the composed ops for shapes the fused
+    kernels do not take or a t that requires a gradient."""
+    z = _as_tensor(_as_operand(z))
+    t = _as_tensor(_as_operand(t))
+    if z.shape != t.shape:
+        t = _expand_view(t, broadcast_shapes(z.shape, t.shape)) if z.ndim else t
+    C = z.shape[-1] if z.ndim else 0
+    R = z.size // C if C else 0
+    fusable = (z.ndim >= 1 and C % 4 == 0 and 0 < C <= 1024 and R > 0 and not t.requires_grad
+               and t.shape == z.shape and t.is_contiguous)
+    zc = z if z.is_contiguous else _copy_contig(z)
+    if fusable and (zc.data_ptr % 16 or t.data_ptr % 16):
+        fusable = False
+    if not fusable:
+        return mean(mul(softmax(z), t))
+    loss = _empty(())
+    rs, rm = Buffer(4 * R), Buffer(4 * R)
+    rdot = Buffer(8 * R)
+    L.call("b2_softmax_wmean_fwd", loss.data_ptr, None, rs.ptr, rm.ptr, rdot.ptr, zc.data_ptr,
+           t.data_ptr, R, C, None)
+    count_f32 = float(np.float32(float(z.size)))  # mean's divisor, promoted like a scalar
+
+    def pull(g):
+        from .graph import _capturing
+
+        gz = _empty(z.shape)
+        cs = _empty((C,)) if z.ndim == 2 else None
+        split = (_LAZY_FP32 and not _capturing[0] and z.ndim == 2 and C % 8 == 0
+                 and _gemm_consumes_as_3xbf16(R, C))
+        hi = Buffer(2 * R * C) if split else None
+        lo = Buffer(2 * R * C) if split else None
+        L.call("b2_softmax_wmean_bwd", None if split else gz.data_ptr, hi.ptr if split else None,
+               lo.ptr if split else None, cs.data_ptr if cs is not None else None, g.data_ptr,
+               count_f32, zc.data_ptr, t.data_ptr, rs.ptr, rm.ptr, R, C, None)
+        if split:
+            buf = gz.buffer
+            buf._splits = {("3xbf16", 0, R, C, C): (buf.version, hi, lo, 0)}
+            buf._pending = (hi, lo, R * C)
+            _PENDING.add(buf)
+        if cs is not None:
+            _COLSUM[gz] = cs
+        return gz
+
+    return record("softmax_mul_mean", (z,), loss, (pull,), saved=(zc, t))
 
 
 def fused_muladd_relu(a, b, c=None) -> Tensor:

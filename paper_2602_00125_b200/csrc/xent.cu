@@ -17,6 +17,8 @@
 #include <math.h>
 
 #include "common.cuh"
+#include <cuda_bf16.h>
+
 #include "fexp.cuh"
 
 #ifndef B2_SOFTMAX_TMA
@@ -561,6 +563,203 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_xent_rows_tma(double* __re
   }
 }
 
+// ---------------------------------------------------------------- softmax * t, mean (fused)
+// BASELINE config 4's loss, loss = mean(softmax(z, -1) * t), as ONE row pass
+// each way, bit-identical to composing the reference ops:
+//   forward: m, e = f32(exp(f32(z - m))), s = f32(sum64 e), y = f32(e / s)
+//     exactly as k_softmax_fwd_tma (y stored only if asked), p = f32(y * t),
+//     row_dot[r] = sum64 p, then loss = f32(sum64 row_dot / count) (mean);
+//   backward: gp = f32(g / f32(count)) (mean pullback), gy = f32(gp * t) (mul
+//     pullback), then k_softmax_bwd_v's GradStore-ordered rounding sequence.
+// The backward also emits what the next GEMMs and the bias gradient read:
+// gz's 3xBF16 split (hi = bf16(gz), lo = bf16(gz - hi), as b2_bf16x3_split)
+// and its column sums (per-warp fp64 column accumulators in shared memory,
+// folded in a fixed order: warps, then CTAs), so neither a split pass nor a
+// reduction re-reads gz -- and gz itself need not be stored in fp32.
+template <int NV>
+__global__ void __launch_bounds__(256, B2_SMX_MINB) k_smx_wmean_fwd(float* __restrict__ y,
+                                                                   float* __restrict__ rs,
+                                                                   float* __restrict__ rm,
+                                                                   double* __restrict__ row_dot,
+                                                                   const float* __restrict__ z,
+                                                                   const float* __restrict__ t,
+                                                                   int64_t B, int64_t C) {
+  extern __shared__ __align__(128) float smx[];
+  __shared__ __align__(8) uint64_t bars[8][2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float* const buf0 = smx + (wid * 2) * (NV * 128);
+  float* const buf1 = buf0 + NV * 128;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t bytes = (uint32_t)(C * 4);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[wid][0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[wid][1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (w < B) row_bulk(buf0, z + w * C, bytes, &bars[wid][0]);
+  }
+  __syncwarp();
+  int it = 0;
+  for (int64_t r = w; r < B; r += nw, ++it) {
+    const int b = it & 1;
+    if (lane == 0 && r + nw < B) row_bulk(b ? buf0 : buf1, z + (r + nw) * C, bytes, &bars[wid][b ^ 1]);
+    const float4* trow = reinterpret_cast<const float4*>(t + r * C);
+    float4 tv[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {  // t's loads in flight while the z row lands
+      const int64_t q = i * 32 + lane;
+      tv[i] = q * 4 < C ? __ldg(trow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    row_wait(&bars[wid][b], (uint32_t)(it >> 1) & 1);
+    const float4* row = reinterpret_cast<const float4*>(b ? buf1 : buf0);
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      v[i] = q * 4 < C ? row[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();
+    const float m = row_max_regs<NV>(v, C, lane);
+    double acc = 0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float e = b2::exp_f32(__fsub_rn(f4get(v[i], k), m));  // exp(sub(z, m))
+        f4set(v[i], k, e);
+        if ((int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)e;
+      }
+    const float s = __double2float_rn(warp_sum(acc));  // sum(e, -1, keepdims)
+    const bool ok = s >= 1.0f && s <= 0x1p100f;
+    const float rs_ = __frcp_rn(s);
+    double dot = 0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      if (q * 4 < C) {
+        float4 yq;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float yk = div_by(f4get(v[i], k), s, rs_, ok);  // div(e, s)
+          f4set(yq, k, yk);
+          dot += (double)__fmul_rn(yk, f4get(tv[i], k));      // mul(y, t), then the mean's sum
+        }
+        if (y) reinterpret_cast<float4*>(y + r * C)[q] = yq;
+      }
+    }
+    dot = warp_sum(dot);
+    if (lane == 0) {
+      rs[r] = s;
+      rm[r] = m;
+      row_dot[r] = dot;
+    }
+  }
+}
+
+__device__ __forceinline__ void split_store4(__nv_bfloat16* hi, __nv_bfloat16* lo, const float4& o) {
+  __nv_bfloat16 h[4], l[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float x = f4get(o, k);
+    h[k] = __float2bfloat16_rn(x);
+    l[k] = __float2bfloat16_rn(__fsub_rn(x, __bfloat162float(h[k])));
+  }
+  *reinterpret_cast<uint2*>(hi) = *reinterpret_cast<const uint2*>(h);
+  *reinterpret_cast<uint2*>(lo) = *reinterpret_cast<const uint2*>(l);
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256, B2_SMX_MINB) k_smx_wmean_bwd(float* __restrict__ gz,
+                                                                   __nv_bfloat16* __restrict__ ghi,
+                                                                   __nv_bfloat16* __restrict__ glo,
+                                                                   double* __restrict__ colpart,
+                                                                   const float* __restrict__ g,
+                                                                   float count_f32,
+                                                                   const float* __restrict__ z,
+                                                                   const float* __restrict__ t,
+                                                                   const float* __restrict__ rs,
+                                                                   const float* __restrict__ rm,
+                                                                   int64_t B, int64_t C) {
+  extern __shared__ __align__(16) double colw[];  // [8 warps][4][NV*32] column accumulators
+  constexpr int CP = NV * 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* const mycol = colw + wid * 4 * CP;
+  if (colpart) {
+    for (int i = threadIdx.x; i < 8 * 4 * CP; i += blockDim.x) colw[i] = 0.0;
+    __syncthreads();
+  }
+  const float gp = __fdiv_rn(g[0], count_f32);  // mean pullback: div(g, f32(count))
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < B; r += nw) {
+    const float4* zr = reinterpret_cast<const float4*>(z + r * C);
+    const float4* tr = reinterpret_cast<const float4*>(t + r * C);
+    float4 ev[NV], gv[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      const bool in = q * 4 < C;
+      ev[i] = in ? __ldg(zr + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      gv[i] = in ? __ldg(tr + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float s = rs[r], m = rm[r];
+    const float ss = __fmul_rn(s, s);
+    const bool ok = s >= 1.0f && ss <= 0x1p100f;
+    const float rs_ = __frcp_rn(s), rss = __frcp_rn(ss);
+    double acc = 0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float gy = __fmul_rn(gp, f4get(gv[i], k));  // mul pullback: mul(g, t)
+        f4set(gv[i], k, gy);
+        const float e = b2::exp_f32(__fsub_rn(f4get(ev[i], k), m));
+        f4set(ev[i], k, e);
+        const float tt = div_by(__fmul_rn(gy, e), ss, rss, ok);  // div(mul(g, e), mul(s, s))
+        if ((int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)(-tt);  // neg, then sum(axis=-1)
+      }
+    const float gs = __double2float_rn(warp_sum(acc));
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      if (q * 4 < C) {
+        float4 o;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float ge = div_by(f4get(gv[i], k), s, rs_, ok);  // div(g, s) -- stored first
+          f4set(o, k, __fmul_rn(__fadd_rn(ge, gs), f4get(ev[i], k)));  // GradStore add, exp pullback
+        }
+        if (gz) reinterpret_cast<float4*>(gz + r * C)[q] = o;
+        if (ghi) split_store4(ghi + r * C + q * 4, glo + r * C + q * 4, o);
+        if (colpart) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mycol[k * CP + q] += (double)f4get(o, k);
+        }
+      }
+    }
+  }
+  if (colpart) {  // fold the 8 warps in order: this CTA's column partials
+    __syncthreads();
+    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+      const int q = (int)(c >> 2), k = (int)(c & 3);
+      double v = 0;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) v += colw[ww * 4 * CP + k * CP + q];
+      colpart[blockIdx.x * C + c] = v;
+    }
+  }
+}
+
+// column sums of per-CTA fp64 partials, CTAs folded in order, one f32 rounding
+__global__ void k_colpart_fold(float* __restrict__ out, const double* __restrict__ part, int nparts,
+                               int64_t C) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double v = 0;
+  for (int p = 0; p < nparts; ++p) v += part[p * C + c];
+  out[c] = __double2float_rn(v);
+}
+
 int rows_grid(int64_t B) {
   int64_t warps = B;
   int64_t ctas = (warps + 7) / 8;
@@ -702,6 +901,71 @@ int b2_softmax_bwd(float* gz, const float* gy, const float* z, const float* row_
     k_softmax_bwd<<<rows_grid(rows), 256, 0, st>>>(gz, gy, z, row_s, row_m, rows, cols);
   }
   return b2::launched("b2_softmax_bwd");
+}
+
+int b2_softmax_wmean_fwd(float* loss, float* y, float* row_s, float* row_m, double* row_dot,
+                         const float* z, const float* t, int64_t rows, int64_t cols, void* stream) {
+  if (rows <= 0 || cols <= 0) return b2::fail("b2_softmax_wmean_fwd: empty input");
+  if (cols % 4 || cols > 1024 || ((uintptr_t)z & 15) || ((uintptr_t)t & 15) || ((uintptr_t)y & 15))
+    return b2::fail("b2_softmax_wmean_fwd: rows must be 16-B aligned with cols % 4 == 0, cols <= 1024");
+  cudaStream_t st = b2::resolve(stream);
+  const int nv = (int)((cols + 127) / 128);
+  const int64_t ctas = std::min<int64_t>((rows + 7) / 8, 3LL * b2::sm_count());
+#define B2_SWF(NV)                                                                              \
+  {                                                                                             \
+    const int smem = 8 * 2 * NV * 128 * 4;                                                      \
+    static bool attr = false;                                                                   \
+    if (!attr) {                                                                                \
+      B2_CUDA(cudaFuncSetAttribute(k_smx_wmean_fwd<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+      attr = true;                                                                              \
+    }                                                                                           \
+    k_smx_wmean_fwd<NV><<<(unsigned)ctas, 256, smem, st>>>(y, row_s, row_m, row_dot, z, t, rows, cols); \
+  }
+  if (nv <= 1) B2_SWF(1)
+  else if (nv <= 2) B2_SWF(2)
+  else if (nv <= 4) B2_SWF(4)
+  else B2_SWF(8)
+#undef B2_SWF
+  B2_TRY(b2::launched("b2_softmax_wmean_fwd(rows)"));
+  k_xent_final<<<1, 1024, 0, st>>>(loss, row_dot, rows, (double)rows * (double)cols);
+  return b2::launched("b2_softmax_wmean_fwd(final)");
+}
+
+int b2_softmax_wmean_bwd(float* gz, void* gz_hi, void* gz_lo, float* colsum, const float* g,
+                         float count_f32, const float* z, const float* t, const float* row_s,
+                         const float* row_m, int64_t rows, int64_t cols, void* stream) {
+  if (rows <= 0 || cols <= 0) return 0;
+  if (cols % 4 || cols > 1024 || ((uintptr_t)z & 15) || ((uintptr_t)t & 15) || ((uintptr_t)gz & 15) ||
+      ((uintptr_t)gz_hi & 7) || ((uintptr_t)gz_lo & 7) || (!gz_hi != !gz_lo))
+    return b2::fail("b2_softmax_wmean_bwd: rows must be 16-B aligned with cols % 4 == 0, cols <= 1024");
+  cudaStream_t st = b2::resolve(stream);
+  const int nv = (int)((cols + 127) / 128);
+  const int64_t ctas = std::min<int64_t>((rows + 7) / 8, 3LL * b2::sm_count());
+  double* part = nullptr;
+  if (colsum) B2_TRY(b2_alloc((size_t)ctas * cols * sizeof(double), st, (void**)&part));
+#define B2_SWB(NV)                                                                              \
+  {                                                                                             \
+    const int smem = colsum ? 8 * 4 * NV * 32 * 8 : 0;                                          \
+    static bool attr = false;                                                                   \
+    if (!attr) {                                                                                \
+      B2_CUDA(cudaFuncSetAttribute(k_smx_wmean_bwd<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4 * NV * 32 * 8)); \
+      attr = true;                                                                              \
+    }                                                                                           \
+    k_smx_wmean_bwd<NV><<<(unsigned)ctas, 256, smem, st>>>(gz, (__nv_bfloat16*)gz_hi,           \
+        (__nv_bfloat16*)gz_lo, part, g, count_f32, z, t, row_s, row_m, rows, cols);              \
+  }
+  if (nv <= 1) B2_SWB(1)
+  else if (nv <= 2) B2_SWB(2)
+  else if (nv <= 4) B2_SWB(4)
+  else B2_SWB(8)
+#undef B2_SWB
+  int rc = b2::launched("b2_softmax_wmean_bwd");
+  if (!rc && colsum) {
+    k_colpart_fold<<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(colsum, part, (int)ctas, cols);
+    rc = b2::launched("b2_softmax_wmean_bwd(colsum)");
+  }
+  if (part) b2_free(part, st);
+  return rc;
 }
 
 }  // extern "C"
