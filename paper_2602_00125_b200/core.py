@@ -851,6 +851,18 @@ _PENDING = weakref.WeakSet()  # buffers whose fp32 contents are still only a spl
 _LAZY_FP32 = os.environ.get("B2_LAZY_FP32", "1") != "0"  # 0: every GEMM stores its fp32 C
 
 
+def _set_pending(buf, hi, lo, n):
+    """Mark buf's fp32 contents as not yet written: only its 3xBF16 split
+    (hi, lo) is. Inside a CUDA-graph capture the capture remembers it, so
+    every replay (which rewrites hi/lo) marks the buffer pending again."""
+    from .graph import _capturing, _captured_pending
+
+    buf._pending = (hi, lo, n)
+    _PENDING.add(buf)
+    if _capturing[0]:
+        _captured_pending.append((weakref.ref(buf), hi, lo, n))
+
+
 def _materialize(buf):
     """Write a pending buffer's fp32 contents from its 3xBF16 split (exact
     f32(hi) + f32(lo): within 2^-16 relative of the GEMM's fp32 result -- hi
@@ -972,7 +984,7 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
         # column sums) skips the fp32 store; it is materialised on first use
         from .graph import _capturing
 
-        lazy = (_LAZY_FP32 and emit_split and kind == "3xbf16" and not _capturing[0]
+        lazy = (_LAZY_FP32 and emit_split and kind == "3xbf16"
                 and out.offset == 0 and out.buffer.nbytes == 4 * M * N and (M * N) % 8 == 0
                 and N % 8 == 0 and out.is_contiguous and out.buffer._pending is None)
         d.lda, d.ldb, d.C, d.ldc, d.bias, d.epilogue = lda, ldb, (None if lazy else out.data_ptr), N, bptr, epi
@@ -1001,8 +1013,7 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
                 buf._splits = {}
             buf._splits[(kind, out.offset, M, N, N)] = (buf.version, shi, slo, _capturing[0])
             if lazy:
-                buf._pending = (shi, slo, M * N)
-                _PENDING.add(buf)
+                _set_pending(buf, shi, slo, M * N)
     elif algo == L.GEMM_3XTF32 and tc_ok:
         ahi, alo = _split(xa, ar, ac, lda, "3xtf32")
         bhi, blo = _split(wb, br, bc, ldb, "3xtf32")
@@ -1231,8 +1242,7 @@ def softmax_mul_mean(z, t) -> Tensor:
 
         gz = _empty(z.shape)
         cs = _empty((C,)) if z.ndim == 2 else None
-        split = (_LAZY_FP32 and not _capturing[0] and z.ndim == 2 and C % 8 == 0
-                 and _gemm_consumes_as_3xbf16(R, C))
+        split = (_LAZY_FP32 and z.ndim == 2 and C % 8 == 0 and _gemm_consumes_as_3xbf16(R, C))
         hi = Buffer(2 * R * C) if split else None
         lo = Buffer(2 * R * C) if split else None
         L.call("b2_softmax_wmean_bwd", None if split else gz.data_ptr, hi.ptr if split else None,
@@ -1240,9 +1250,8 @@ def softmax_mul_mean(z, t) -> Tensor:
                count_f32, zc.data_ptr, t.data_ptr, rs.ptr, rm.ptr, R, C, None)
         if split:
             buf = gz.buffer
-            buf._splits = {("3xbf16", 0, R, C, C): (buf.version, hi, lo, 0)}
-            buf._pending = (hi, lo, R * C)
-            _PENDING.add(buf)
+            buf._splits = {("3xbf16", 0, R, C, C): (buf.version, hi, lo, _capturing[0])}
+            _set_pending(buf, hi, lo, R * C)
         if cs is not None:
             _COLSUM[gz] = cs
         return gz

@@ -22,6 +22,7 @@ from . import _lib as L
 
 _capturing = [0]  # id of the open capture (unique per capture), 0 when none
 _serial = [0]
+_captured_pending = []  # (weakref(buffer), hi, lo, n) split-only outputs made by the open capture
 
 
 def capturing() -> bool:
@@ -29,12 +30,24 @@ def capturing() -> bool:
 
 
 class CudaGraph:
-    def __init__(self, gid: int, outputs):
+    def __init__(self, gid: int, outputs, repend=()):
         self.id = gid
         self.outputs = outputs
+        # split-only GEMM / loss-pullback outputs still pending when the
+        # capture ended: every replay rewrites their split, so their fp32
+        # contents are pending again (materialised on first fp32 use)
+        self._repend = list(repend)
 
     def replay(self, stream=None):
         L.call("b2_graph_launch", self.id, stream)
+        if self._repend:
+            from .core import _PENDING
+
+            for ref, hi, lo, n in self._repend:
+                buf = ref()
+                if buf is not None:
+                    buf._pending = (hi, lo, n)
+                    _PENDING.add(buf)
 
     def __del__(self):
         try:
@@ -55,6 +68,7 @@ def capture(fn, *args, warmup: int = 1, **kwargs) -> CudaGraph:
     L.call("b2_graph_begin", None)
     _serial[0] += 1
     _capturing[0] = _serial[0]
+    _captured_pending.clear()
     try:
         out = fn(*args, **kwargs)
     except BaseException:
@@ -65,4 +79,6 @@ def capture(fn, *args, warmup: int = 1, **kwargs) -> CudaGraph:
         _capturing[0] = 0
     gid = ctypes.c_int(0)
     L.check(L.lib().b2_graph_end(None, ctypes.byref(gid)))
-    return CudaGraph(gid.value, out)
+    repend = [e for e in _captured_pending if e[0]() is not None and e[0]()._pending is not None]
+    _captured_pending.clear()
+    return CudaGraph(gid.value, out, repend)

@@ -229,3 +229,23 @@ def test_config5_full_width_fast_schemes(c5, algo):
     assert rec["loss"] <= TOL and rec["logits"] <= TOL, rec
     assert worst_act <= TOL and worst_cond <= TOL, rec
     assert flips <= max(1, total // 10000), rec
+
+
+def test_config4_full_size_fused_linear_and_loss():
+    """The fused form of config 4 (nn.Linear with the bias in the GEMM
+    epilogue, softmax_mul_mean) at full size against the oracle."""
+    X, W, bias, T = I.config4_inputs()
+    K = X.shape[-1]
+    P.reset_tape()
+    xt, wt, bt = dev(X.reshape(-1, K), True), dev(W, True), dev(bias, True)
+    z = P.linear(xt, P.transpose2d(wt), bt)
+    loss = P.softmax_mul_mean(z, dev(T.reshape(-1, K)))
+    store = P.backward(loss)
+    ref = O.softmax_linear_config(X.reshape(-1, K), W, bias, T.reshape(-1, K))
+    errs = {"loss": normwise(np.float32(loss.item()), ref["loss"]),
+            "dX": normwise(store[xt].numpy(), ref["dX"].reshape(-1, K)),
+            "dW": normwise(store[wt].numpy(), ref["dW"]),
+            "dbias": normwise(store[bt].numpy(), ref["dbias"])}
+    _record("config4_64x512x1024_fused", errs)
+    for k, e in errs.items():
+        assert e <= TOL, (k, e)

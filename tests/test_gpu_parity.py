@@ -1194,3 +1194,91 @@ def test_optimizer_overlapped_in_backward_matches_plain_step(force_nccl):
 
     for a, b in zip(run(True), run(False)):
         assert bits_equal(a, b)
+
+
+# ---------------------------------------------------------------- fused config-4 loss
+
+
+def _config4_step(X, W, bias, T, fused):
+    K = X.shape[-1]
+    P.reset_tape()
+    xt, wt, bt = dev(X, True), dev(W, True), dev(bias, True)
+    if fused:
+        z = P.linear(P.reshape(xt, (-1, K)), P.transpose2d(wt), bt)
+        loss = P.softmax_mul_mean(z, dev(T.reshape(-1, K)))
+    else:
+        loss = P.mean(P.mul(P.softmax(P.add(P.mm(xt, wt), bt)), dev(T)))
+    store = P.backward(loss)
+    return (host(loss), host(store[xt]).reshape(-1, K), host(store[wt]), host(store[bt]))
+
+
+def test_config4_fused_loss_reference_arithmetic_bit_exact():
+    """nn.Linear + softmax_mul_mean in the 'ref' GEMM mode reproduce the
+    reference's bits for the config-4 step (loss, dX, dW, dbias)."""
+    g = load("config4_small.npz")
+    X, W, bias, Tt = I.config4_inputs(b=2, s=16, k=64)
+    P.set_gemm_algo("ref")
+    try:
+        loss, dX, dW, db = _config4_step(X, W, bias, Tt, fused=True)
+    finally:
+        P.set_gemm_algo(None)
+    assert bits_equal(loss, g["loss"])
+    assert bits_equal(dX, g["dX"])
+    assert bits_equal(dW, g["dW"])
+    assert bits_equal(db, g["dbias"])
+
+
+@pytest.mark.parametrize("algo", ["3xbf16", "simt"])
+@pytest.mark.parametrize("shape", [(2, 16, 64), (8, 128, 1024), (4, 96, 1000)])
+def test_config4_fused_loss_bit_identical_to_the_composition(algo, shape):
+    """The fused loss (one row pass each way, split + column sums emitted by
+    the backward) gives the composed ops' bits with the same GEMM scheme."""
+    b, s, k = shape
+    X, W, bias, Tt = I.config4_inputs(b=b, s=s, k=k)
+    bias = np.random.default_rng(9).uniform(-0.1, 0.1, k).astype(np.float32)
+    P.set_gemm_algo(algo)
+    try:
+        want = _config4_step(X, W, bias, Tt, fused=False)
+        got = _config4_step(X, W, bias, Tt, fused=True)
+    finally:
+        P.set_gemm_algo(None)
+    for name, a, w in zip(("loss", "dX", "dW", "dbias"), got, want):
+        assert bits_equal(a, w), name
+
+
+def test_fused_loss_under_cuda_graph_replay_rematerialises_split_outputs():
+    """A graph whose backward emits a split-only cotangent: after every replay
+    the fp32 view of that cotangent is recomputed from the fresh split."""
+    from paper_2602_00125_b200 import graph
+
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((256, 512)).astype(np.float32)
+    W = (rng.standard_normal((512, 512)) * 0.03).astype(np.float32)
+    T = rng.uniform(0, 1, (256, 512)).astype(np.float32)
+    xt, wt, tt = dev(X, True), dev(W, True), dev(T)
+    keep = {}
+
+    def step():
+        P.reset_tape()
+        z = P.linear(xt, wt)
+        loss = P.softmax_mul_mean(z, tt)
+        store = P.backward(loss)
+        keep["gz"] = store[z]
+        return loss
+
+    P.set_gemm_algo("3xbf16")
+    try:
+        g = graph.capture(step, warmup=1)
+        gz_eager = host(keep["gz"])  # the warm-up's gz was replaced by the capture's
+        for k in range(2):
+            xt.write_flat((X * (1.0 + 0.5 * k)).ravel())
+            g.replay()
+            got = host(keep["gz"])
+            xt_ref = dev(X * (1.0 + 0.5 * k), True)
+            P.reset_tape()
+            zr = P.linear(xt_ref, wt)
+            ref = host(P.backward(P.softmax_mul_mean(zr, tt))[zr])
+            assert bits_equal(got, ref), k
+    finally:
+        P.set_gemm_algo(None)
+    assert gz_eager.shape == (256, 512)
