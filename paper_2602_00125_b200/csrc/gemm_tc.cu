@@ -249,6 +249,8 @@ struct TcParams {
   int kbps;
   float* ws;
   int l2hint;               // B operand loads with L2 evict_last (B2_GEMM_L2HINT=0 disables)
+  int stage_out;            // every CTA runs at most one unit: fp32 tile stores (C / K-slice
+                            // partials) go through shared memory as coalesced row stores
   double* colsum;           // optional [ceil(M/128)][N] fp64 column partial sums of the stored C
   const uint64_t* mask_bits;  // ReLU-pullback mask as bits ([M][bits_ld] words, bit j = column 64w+j)
   uint64_t* bits_out;         // emit C > 0 as bits (ReLU forward): the next backward's mask
@@ -424,6 +426,42 @@ __device__ __forceinline__ void split_pair2(float a, float b, uint32_t& h, uint3
   l = *reinterpret_cast<const uint32_t*>(&ll);
 }
 
+// Coalesced fp32 tile store for CTAs that run a single unit (few-tile GEMMs,
+// where the epilogue is exposed): each epilogue thread owns one row and 64
+// columns, so direct stores are 32 rows x 16 B per warp instruction (one L2
+// transaction per row). Instead the 16 epilogue warps stage the 128 x 256 tile
+// in the (now idle) pipeline buffers -- rows padded to 260 floats, so a warp's
+// 16-B writes hit the minimum 4 wavefronts -- then store whole rows, 1 KB per
+// warp instruction pair. Named barrier 5 spans the 512 epilogue threads.
+constexpr int kStageLd = BN + 4;
+__device__ __forceinline__ void stage_tile_store(uint8_t* smem, const float (&acc)[64], int row, int cg,
+                                                 int warp, int lane, float* dst, int64_t ld, int rows,
+                                                 int cols) {
+  float* t = reinterpret_cast<float*>(smem);
+  float* mine = t + row * kStageLd + cg * 64;
+#pragma unroll
+  for (int j = 0; j < 64; j += 4)
+    *reinterpret_cast<float4*>(mine + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+  asm volatile("bar.sync 5, 512;" ::: "memory");
+  const int ew = warp - 4;  // 0..15
+  const bool vec = (ld % 4) == 0 && (((uintptr_t)dst) & 15) == 0;
+  for (int r = ew; r < rows; r += 16) {
+    const float* src = t + r * kStageLd;
+    float* out = dst + (int64_t)r * ld;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = (h * 32 + lane) * 4;
+      if (vec && c + 4 <= cols) {
+        *reinterpret_cast<float4*>(out + c) = *reinterpret_cast<const float4*>(src + c);
+      } else {
+        for (int q = 0; q < 4; ++q)
+          if (c + q < cols) out[c + q] = src[c + q];
+      }
+    }
+  }
+  asm volatile("bar.sync 5, 512;" ::: "memory");  // the buffer may be reused by the next store
+}
+
 template <bool A_MN, bool B_MN, int MODE, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -482,6 +520,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: everything above (barrier init, TMEM
+  // allocation, descriptor prefetch) may overlap the previous kernel's tail;
+  // no global memory is touched before the prerequisite grids are complete.
+  // Then let the next kernel start its own prologue as SMs free up.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
@@ -653,7 +697,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (ks >= 0) {  // a K slice of a tail tile: raw partial sums, tile-local
-        float* w = p.ws + ((int64_t)ks * (BM * CG) + (int)rank * BM + row) * BN + cg * 64;
+        float* w0 = p.ws + ((int64_t)ks * (BM * CG) + (int)rank * BM) * BN;
+        if (p.stage_out) {
+          stage_tile_store(smem, acc, row, cg, warp, lane, w0, BN, BM, BN);
+          continue;
+        }
+        float* w = w0 + (int64_t)row * BN + cg * 64;
 #pragma unroll
         for (int j = 0; j < 64; j += 4)
           *reinterpret_cast<float4*>(w + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
@@ -716,6 +765,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!p.C) {
           // fp32 C not wanted: only its operand split / bits / column sums
+        } else if (p.stage_out) {
+          // stored below, coalesced through shared memory (all rows of the tile)
         } else if (full64) {
 #pragma unroll
           for (int j = 0; j < 64; j += 4)
@@ -760,6 +811,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (nb + j < p.N) split_pair<MODE>(acc[j], hrow[nb + j], lrow[nb + j]);
           }
         }
+      }
+      if (p.stage_out && p.C) {  // every epilogue warp takes part (rows past M are not stored)
+        const int rows_left = p.M - m0;
+        const int cols_left = p.N - n0;
+        stage_tile_store(smem, acc, row, cg, warp, lane, p.C + (int64_t)m0 * p.ldc + n0, p.ldc,
+                         rows_left < BM ? rows_left : BM, cols_left < BN ? cols_left : BN);
       }
       if (p.colsum) {
         // Column sums of the stored tile over this CTA's 128 rows (the bias
@@ -864,6 +921,7 @@ __global__ void k_tf32_split_vec(float* __restrict__ hi, float* __restrict__ lo,
 template <int MODE>
 __global__ void k_bf16x2_split(__nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
                                const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ld) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the consuming GEMM may start its prologue
   const int64_t c8 = cols >> 3;  // cols % 8 == 0 (checked on the host)
   const int64_t n8 = rows * c8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
@@ -1089,6 +1147,24 @@ static int kc_for_mode(int mode) {
   return mode == 5 ? 2 * KC_BASE : KC_BASE;  // K = 1024 (BK 64) / 256 (BK 32)
 }
 
+static int pdl_enabled() {
+  static int v = -1;  // B2_GEMM_PDL=0: plain stream serialisation (A/B measurements)
+  if (v < 0) {
+    const char* e = getenv("B2_GEMM_PDL");
+    v = !(e && e[0] == '0');
+  }
+  return v;
+}
+
+static int stage_out_enabled() {
+  static int v = -1;  // B2_GEMM_STAGE_OUT=0: direct per-row stores everywhere (A/B measurements)
+  if (v < 0) {
+    const char* e = getenv("B2_GEMM_STAGE_OUT");
+    v = !(e && e[0] == '0');
+  }
+  return v;
+}
+
 template <bool A_MN, bool B_MN, int MODE, int CG>
 int launch_tc(const Operands& o, TcParams& p, cudaStream_t st) {
   using CF = Cfg<MODE, CG>;
@@ -1136,18 +1212,22 @@ int launch_tc(const Operands& o, TcParams& p, cudaStream_t st) {
   }
   int sms = b2::sm_count();
   int grid = (p.num_tiles * CG < sms) ? p.num_tiles * CG : (sms / CG) * CG;
+  static_assert(CF::STAGES * CF::STAGE_BYTES >= BM * kStageLd * 4, "staged tile store needs the stage buffers");
+  p.stage_out = p.num_tiles <= grid / CG && stage_out_enabled();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = CF::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   B2_CUDA(cudaLaunchKernelEx(&cfg, kern, m[0], m[1], m[2], m[3], m[4], m[5], p));
   return b2::launched("b2_gemm(tcgen05)");
 }

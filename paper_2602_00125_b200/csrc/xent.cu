@@ -229,22 +229,22 @@ __device__ __forceinline__ float div_by(float a, float b, float rb, bool ok) {
   return (ok && aa >= 0x1p-100f && aa <= 0x1p100f) ? q1 : __fdiv_rn(a, b);
 }
 
-template <int NV>
+// Row max VALUE over the registers (padding past C excluded): fmaxf skips
+// NaNs like the strict '>' scan; the first-slot NaN rule is applied after the
+// butterfly. The sign of a zero maximum may differ from the scan's first
+// zero, which no consumer can observe: z - m and m + log(se) are the same
+// for m = +0 and m = -0.
+template <int NV, bool FULL = false>
 __device__ __forceinline__ float row_max_regs(const float4 (&v)[NV], int64_t C, int lane) {
   float m = -INFINITY;
-  bool any = false;
 #pragma unroll
   for (int i = 0; i < NV; ++i)
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int64_t idx = (int64_t)(i * 32 + lane) * 4 + k;
-      const float x = f4get(v[i], k);
-      if (idx < C && !isnan(x)) {
-        m = any ? (x > m ? x : m) : x;
-        any = true;
-      }
+      const bool in = FULL || (int64_t)(i * 32 + lane) * 4 + k < C;
+      m = fmaxf(m, in ? f4get(v[i], k) : -INFINITY);
     }
-  m = warp_max_first(any ? m : -INFINITY);
+  m = warp_max_first(m);
   const float v0 = __shfl_sync(0xffffffffu, v[0].x, 0);  // the first scanned slot
   return isnan(v0) ? v0 : m;
 }
@@ -576,8 +576,11 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_xent_rows_tma(double* __re
 // and its column sums (per-warp fp64 column accumulators in shared memory,
 // folded in a fixed order: warps, then CTAs), so neither a split pass nor a
 // reduction re-reads gz -- and gz itself need not be stored in fp32.
-template <int NV>
-__global__ void __launch_bounds__(256, B2_SMX_MINB) k_smx_wmean_fwd(float* __restrict__ y,
+#ifndef B2_WMEAN_MINB
+#define B2_WMEAN_MINB 2
+#endif
+template <int NV, bool FULL>
+__global__ void __launch_bounds__(256, B2_WMEAN_MINB) k_smx_wmean_fwd(float* __restrict__ y,
                                                                    float* __restrict__ rs,
                                                                    float* __restrict__ rm,
                                                                    double* __restrict__ row_dot,
@@ -608,7 +611,7 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_smx_wmean_fwd(float* __res
 #pragma unroll
     for (int i = 0; i < NV; ++i) {  // t's loads in flight while the z row lands
       const int64_t q = i * 32 + lane;
-      tv[i] = q * 4 < C ? __ldg(trow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      tv[i] = (FULL || q * 4 < C) ? __ldg(trow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     row_wait(&bars[wid][b], (uint32_t)(it >> 1) & 1);
     const float4* row = reinterpret_cast<const float4*>(b ? buf1 : buf0);
@@ -616,10 +619,10 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_smx_wmean_fwd(float* __res
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int64_t q = i * 32 + lane;
-      v[i] = q * 4 < C ? row[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[i] = (FULL || q * 4 < C) ? row[q] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncwarp();
-    const float m = row_max_regs<NV>(v, C, lane);
+    const float m = row_max_regs<NV, FULL>(v, C, lane);
     double acc = 0;
 #pragma unroll
     for (int i = 0; i < NV; ++i)
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_smx_wmean_fwd(float* __res
       for (int k = 0; k < 4; ++k) {
         const float e = b2::exp_f32(__fsub_rn(f4get(v[i], k), m));  // exp(sub(z, m))
         f4set(v[i], k, e);
-        if ((int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)e;
+        if (FULL || (int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)e;
       }
     const float s = __double2float_rn(warp_sum(acc));  // sum(e, -1, keepdims)
     const bool ok = s >= 1.0f && s <= 0x1p100f;
@@ -636,7 +639,7 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_smx_wmean_fwd(float* __res
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int64_t q = i * 32 + lane;
-      if (q * 4 < C) {
+      if (FULL || q * 4 < C) {
         float4 yq;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -668,8 +671,8 @@ __device__ __forceinline__ void split_store4(__nv_bfloat16* hi, __nv_bfloat16* l
   *reinterpret_cast<uint2*>(lo) = *reinterpret_cast<const uint2*>(l);
 }
 
-template <int NV>
-__global__ void __launch_bounds__(256, B2_SMX_MINB) k_smx_wmean_bwd(float* __restrict__ gz,
+template <int NV, bool FULL>
+__global__ void __launch_bounds__(256, B2_WMEAN_MINB) k_smx_wmean_bwd(float* __restrict__ gz,
                                                                    __nv_bfloat16* __restrict__ ghi,
                                                                    __nv_bfloat16* __restrict__ glo,
                                                                    double* __restrict__ colpart,
@@ -698,7 +701,7 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_smx_wmean_bwd(float* __res
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int64_t q = i * 32 + lane;
-      const bool in = q * 4 < C;
+      const bool in = FULL || q * 4 < C;
       ev[i] = in ? __ldg(zr + q) : make_float4(0.f, 0.f, 0.f, 0.f);
       gv[i] = in ? __ldg(tr + q) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -716,13 +719,13 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_smx_wmean_bwd(float* __res
         const float e = b2::exp_f32(__fsub_rn(f4get(ev[i], k), m));
         f4set(ev[i], k, e);
         const float tt = div_by(__fmul_rn(gy, e), ss, rss, ok);  // div(mul(g, e), mul(s, s))
-        if ((int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)(-tt);  // neg, then sum(axis=-1)
+        if (FULL || (int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)(-tt);  // neg, then sum(axis=-1)
       }
     const float gs = __double2float_rn(warp_sum(acc));
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int64_t q = i * 32 + lane;
-      if (q * 4 < C) {
+      if (FULL || q * 4 < C) {
         float4 o;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -750,14 +753,24 @@ __global__ void __launch_bounds__(256, B2_SMX_MINB) k_smx_wmean_bwd(float* __res
   }
 }
 
-// column sums of per-CTA fp64 partials, CTAs folded in order, one f32 rounding
-__global__ void k_colpart_fold(float* __restrict__ out, const double* __restrict__ part, int nparts,
-                               int64_t C) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  double v = 0;
-  for (int p = 0; p < nparts; ++p) v += part[p * C + c];
-  out[c] = __double2float_rn(v);
+// column sums of per-CTA fp64 partials, one f32 rounding: 32 columns x 8
+// partial lanes per CTA (lane k folds partial rows k, k+8, ... in order), then
+// a fixed shared-memory tree over the 8 lanes -- deterministic
+__global__ void __launch_bounds__(256) k_colpart_fold(float* __restrict__ out, const double* __restrict__ part,
+                                                      int nparts, int64_t C) {
+  __shared__ double sh[256];
+  const int c = threadIdx.x & 31, k = threadIdx.x >> 5;
+  const int64_t n = blockIdx.x * 32LL + c;
+  double s = 0.0;
+  if (n < C)
+    for (int r = k; r < nparts; r += 8) s += part[(int64_t)r * C + n];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = 4; h > 0; h >>= 1) {
+    if (k < h) sh[threadIdx.x] += sh[threadIdx.x + 32 * h];
+    __syncthreads();
+  }
+  if (k == 0 && n < C) out[n] = __double2float_rn(sh[c]);
 }
 
 int rows_grid(int64_t B) {
@@ -910,16 +923,20 @@ int b2_softmax_wmean_fwd(float* loss, float* y, float* row_s, float* row_m, doub
     return b2::fail("b2_softmax_wmean_fwd: rows must be 16-B aligned with cols % 4 == 0, cols <= 1024");
   cudaStream_t st = b2::resolve(stream);
   const int nv = (int)((cols + 127) / 128);
-  const int64_t ctas = std::min<int64_t>((rows + 7) / 8, 3LL * b2::sm_count());
+  const int64_t ctas = std::min<int64_t>((rows + 7) / 8, (int64_t)B2_WMEAN_MINB * b2::sm_count());
 #define B2_SWF(NV)                                                                              \
   {                                                                                             \
     const int smem = 8 * 2 * NV * 128 * 4;                                                      \
     static bool attr = false;                                                                   \
     if (!attr) {                                                                                \
-      B2_CUDA(cudaFuncSetAttribute(k_smx_wmean_fwd<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+      B2_CUDA(cudaFuncSetAttribute(k_smx_wmean_fwd<NV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+      B2_CUDA(cudaFuncSetAttribute(k_smx_wmean_fwd<NV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
       attr = true;                                                                              \
     }                                                                                           \
-    k_smx_wmean_fwd<NV><<<(unsigned)ctas, 256, smem, st>>>(y, row_s, row_m, row_dot, z, t, rows, cols); \
+    if (cols == NV * 128)                                                                       \
+      k_smx_wmean_fwd<NV, true><<<(unsigned)ctas, 256, smem, st>>>(y, row_s, row_m, row_dot, z, t, rows, cols); \
+    else                                                                                        \
+      k_smx_wmean_fwd<NV, false><<<(unsigned)ctas, 256, smem, st>>>(y, row_s, row_m, row_dot, z, t, rows, cols); \
   }
   if (nv <= 1) B2_SWF(1)
   else if (nv <= 2) B2_SWF(2)
@@ -940,7 +957,7 @@ int b2_softmax_wmean_bwd(float* gz, void* gz_hi, void* gz_lo, float* colsum, con
     return b2::fail("b2_softmax_wmean_bwd: rows must be 16-B aligned with cols % 4 == 0, cols <= 1024");
   cudaStream_t st = b2::resolve(stream);
   const int nv = (int)((cols + 127) / 128);
-  const int64_t ctas = std::min<int64_t>((rows + 7) / 8, 3LL * b2::sm_count());
+  const int64_t ctas = std::min<int64_t>((rows + 7) / 8, (int64_t)B2_WMEAN_MINB * b2::sm_count());
   double* part = nullptr;
   if (colsum) B2_TRY(b2_alloc((size_t)ctas * cols * sizeof(double), st, (void**)&part));
 #define B2_SWB(NV)                                                                              \
@@ -948,11 +965,16 @@ int b2_softmax_wmean_bwd(float* gz, void* gz_hi, void* gz_lo, float* colsum, con
     const int smem = colsum ? 8 * 4 * NV * 32 * 8 : 0;                                          \
     static bool attr = false;                                                                   \
     if (!attr) {                                                                                \
-      B2_CUDA(cudaFuncSetAttribute(k_smx_wmean_bwd<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4 * NV * 32 * 8)); \
+      B2_CUDA(cudaFuncSetAttribute(k_smx_wmean_bwd<NV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4 * NV * 32 * 8)); \
+      B2_CUDA(cudaFuncSetAttribute(k_smx_wmean_bwd<NV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4 * NV * 32 * 8)); \
       attr = true;                                                                              \
     }                                                                                           \
-    k_smx_wmean_bwd<NV><<<(unsigned)ctas, 256, smem, st>>>(gz, (__nv_bfloat16*)gz_hi,           \
-        (__nv_bfloat16*)gz_lo, part, g, count_f32, z, t, row_s, row_m, rows, cols);              \
+    if (cols == NV * 128)                                                                       \
+      k_smx_wmean_bwd<NV, true><<<(unsigned)ctas, 256, smem, st>>>(gz, (__nv_bfloat16*)gz_hi,   \
+          (__nv_bfloat16*)gz_lo, part, g, count_f32, z, t, row_s, row_m, rows, cols);            \
+    else                                                                                        \
+      k_smx_wmean_bwd<NV, false><<<(unsigned)ctas, 256, smem, st>>>(gz, (__nv_bfloat16*)gz_hi,  \
+          (__nv_bfloat16*)gz_lo, part, g, count_f32, z, t, row_s, row_m, rows, cols);            \
   }
   if (nv <= 1) B2_SWB(1)
   else if (nv <= 2) B2_SWB(2)
@@ -961,7 +983,7 @@ int b2_softmax_wmean_bwd(float* gz, void* gz_hi, void* gz_lo, float* colsum, con
 #undef B2_SWB
   int rc = b2::launched("b2_softmax_wmean_bwd");
   if (!rc && colsum) {
-    k_colpart_fold<<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(colsum, part, (int)ctas, cols);
+    k_colpart_fold<<<(unsigned)((cols + 31) / 32), 256, 0, st>>>(colsum, part, (int)ctas, cols);
     rc = b2::launched("b2_softmax_wmean_bwd(colsum)");
   }
   if (part) b2_free(part, st);
