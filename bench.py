@@ -489,7 +489,8 @@ def main():
     GLOBAL_BATCH = args.global_batch
     if args.impl == "reference":
         return run_reference(args)
-    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+    # B2_BENCH_SPAWN=1 takes the launcher path at N = 1 too (tests exercise it)
+    if "WORLD_SIZE" not in os.environ and (args.gpus > 1 or os.environ.get("B2_BENCH_SPAWN") == "1"):
         return spawn_ranks(args.gpus)
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if world_env != args.gpus:
@@ -501,7 +502,8 @@ def main():
     from paper_2602_00125_b200.data import PinnedFeeder, ScalarReader, batch_shard, build_mlp, mlp_config5
 
     env = dist.env_from_os()
-    comm = dist.Communicator(env)
+    # B2_FORCE_NCCL=1: a 1-rank NCCL communicator at N = 1 (the N > 1 code path on one GPU)
+    comm = dist.Communicator(env, force_nccl=os.environ.get("B2_FORCE_NCCL") == "1")
     world, rank = env.world, env.rank
     lo, hi = dist.shard_rows(GLOBAL_BATCH, rank, world)
     rows = hi - lo

@@ -174,3 +174,28 @@ def test_backward_schedule_prunes_unreachable_nodes():
     assert P.tape().pullback_calls - calls == len(sch.order) == 2
     assert store[x].numpy().tolist() == [2.0, 4.0]
     assert y not in store
+
+
+def test_bench_spawn_launcher_runs_an_nccl_rank_and_prints_one_line():
+    """bench.py's own N-rank launcher (used when no torchrun env is present),
+    taken at N = 1 with a 1-rank NCCL communicator: the rank process gets the
+    torchrun-style env, NCCL initialises (its INFO lines on stderr), rank 0
+    prints exactly one JSON line with n_gpus = 1."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    env.update(B2_BENCH_SPAWN="1", B2_FORCE_NCCL="1", NCCL_DEBUG="INFO")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "1", "--steps", "2", "--warmup", "3",
+                        "--no-ops", "--no-cpu", "--no-bf16", "--global-batch", "4096"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["config"]["parallelism"] == "dp1"
+    assert "NCCL INFO" in r.stderr
