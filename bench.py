@@ -318,6 +318,25 @@ def op_benchmarks():
             out[f"config2_max_dim{ax}_gbs"] = 4 * n / ms / 1e6
         ms = timed(lambda: P.sum(nxt()), 24)
         out["config2_sum_all_gbs"] = 4 * n / ms / 1e6
+    # the whole config-2 workload as one sequence (what a user runs): relu(a*b+b),
+    # exp(clamp(a)), sum/mean/max over dim 0 and dim 1, the full sum, and the
+    # gradients of sum(y) w.r.t. a and b (fused op+grad kernel) -- one CUDA graph
+    def c2_all():
+        a = nxt()
+        with P.no_grad():
+            y = P.fused_muladd_relu(a, b)
+            P.exp(P.clamp(a, -10.0, 10.0))
+            for ax in (0, 1):
+                P.sum(y, axis=ax)
+                P.mean(y, axis=ax)
+                P.max(y, axis=ax)
+            P.sum(y)
+            P.muladd_relu_sum_grads(a, b)
+
+    ms = timed(c2_all, 12)
+    out["config2_e2e_us"] = ms * 1000
+    # single-pass lower bound: read a once; write y, e, a_bar
+    out["config2_e2e_gbs_vs_single_pass_bytes"] = 4 * 4 * n / ms / 1e6
     out["config2_note"] = ("device time per op from a CUDA-graph replay of 24 calls rotating "
                            "over 6 input copies (384 MiB > L2); GB/s = algorithmic bytes "
                            "(read a [+ write out]) / time; roofline_fractions divide by MEASURED_PEAKS.json hbm_gbs")
@@ -422,9 +441,12 @@ def op_benchmarks():
     tc = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1422.1)) / 3.0
     frac = {k.replace("_gbs", "_frac_hbm"): v / hbm for k, v in out.items()
             if k.startswith("config2_") and k.endswith("_gbs")}
+    out["config4_fused_gemm_tflops_effective"] = 3 * 2 * 32768 * 1024 * 1024 / out["config4_fused_loss_ms_per_step"] / 1e9
     for k in ("config3_n1024_fwdbwd_tflops", "config3_n4096_fwdbwd_tflops",
-              "config3_n8192_fwdbwd_tflops", "config4_gemm_tflops_effective"):
+              "config3_n8192_fwdbwd_tflops", "config4_gemm_tflops_effective",
+              "config4_fused_gemm_tflops_effective"):
         frac[k.replace("_tflops", "_frac_3xbf16_ceiling")] = out[k] / tc
+    frac["config2_e2e_frac_hbm_single_pass"] = out["config2_e2e_gbs_vs_single_pass_bytes"] / hbm
     out["roofline_fractions"] = frac
     return out
 
@@ -450,6 +472,7 @@ def spawn_ranks(n):
         env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
                    LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries only rank 0's JSON line
         procs.append(subprocess.Popen([sys.executable] + sys.argv, env=env, start_new_session=True))
     rc = 0
     live = list(procs)

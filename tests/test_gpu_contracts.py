@@ -198,4 +198,4 @@ def test_bench_spawn_launcher_runs_an_nccl_rank_and_prints_one_line():
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 1 and d["value"] > 0 and d["config"]["parallelism"] == "dp1"
-    assert "NCCL INFO" in r.stderr
+    assert "NCCL INFO" in r.stderr  # the launcher routes NCCL's log to stderr
