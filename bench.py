@@ -335,6 +335,10 @@ def op_benchmarks():
 
     ms = timed(c2_all, 12)
     out["config2_e2e_us"] = ms * 1000
+    # the same workload with ONE read of a (multi-output fusion, bit-identical)
+    ms1 = timed(lambda: P.muladd_relu_stats(nxt(), b), 12)
+    out["config2_single_pass_us"] = ms1 * 1000
+    out["config2_single_pass_gbs"] = 4 * 4 * n / ms1 / 1e6
     # single-pass lower bound: read a once; write y, e, a_bar
     out["config2_e2e_gbs_vs_single_pass_bytes"] = 4 * 4 * n / ms / 1e6
     out["config2_note"] = ("device time per op from a CUDA-graph replay of 24 calls rotating "
@@ -447,6 +451,7 @@ def op_benchmarks():
               "config4_fused_gemm_tflops_effective"):
         frac[k.replace("_tflops", "_frac_3xbf16_ceiling")] = out[k] / tc
     frac["config2_e2e_frac_hbm_single_pass"] = out["config2_e2e_gbs_vs_single_pass_bytes"] / hbm
+    frac["config2_single_pass_frac_hbm"] = out["config2_single_pass_gbs"] / hbm
     out["roofline_fractions"] = frac
     return out
 

@@ -83,7 +83,7 @@ enum b2_binary_op { B2_ADD = 0, B2_SUB = 1, B2_MUL = 2, B2_DIV = 3,
                     B2_TANH_BWD = 7 /* b = y: 1 - y * y */,
                     B2_GELU_BWD = 8 /* b = x: Phi(x) + x * phi(x) */ };
 enum b2_unary_op { B2_NEG = 0, B2_EXP = 1, B2_LOG = 2, B2_SQRT = 3, B2_ABS = 4,
-                   B2_RELU = 5, B2_RELU_MASK = 6, B2_COPY = 7, B2_CLAMP = 8,
+                   B2_RELU = 5, B2_RELU_MASK = 6, B2_COPY = 7, B2_CLAMP = 8 /* min(max(x, alpha), beta); NaN passes */,
                    B2_SCALE = 9 /* x * alpha */, B2_DIV_SCALAR = 10 /* x / f32(alpha) */,
                    B2_CLAMP_MASK = 11 /* alpha <= x <= beta ? 1 : 0 */,
                    /* activations: f32(fn(double x)) (nn.py:114-144) */
@@ -115,6 +115,17 @@ int b2_fused_muladd_relu_fwd(float* y, const float* a, const float* b,
                              const float* c, int64_t rows, int64_t cols, void* stream);
 int b2_fused_muladd_relu_bwd(float* ga, float* gb, const float* a,
                              const float* b, int64_t rows, int64_t cols, void* stream);
+
+/* BASELINE config 2's whole workload in ONE pass over a [R, C] (b broadcast
+ * rows [C]): y = relu(a*b + b), e = exp(clamp(a, lo, hi)), a_bar / b_bar of
+ * sum(y) (as b2_fused_muladd_relu_bwd), sum/mean/max of y over dim 0 ([C])
+ * and dim 1 ([R]) and the full sum -- the arithmetic of the separate ops
+ * (core.py:453-483, 581-728; nn.py:108-111), bit-identical. Every output
+ * pointer is nullable; C % 4 == 0, 16-B aligned rows. */
+int b2_muladd_relu_stats(float* y, float* e, float* ga, float* gb, float* sum0, float* mean0,
+                         float* max0, float* sum1, float* mean1, float* max1, float* total,
+                         const float* a, const float* b, float clamp_lo, float clamp_hi,
+                         int64_t rows, int64_t cols, void* stream);
 
 /* ---------------------------------------------------------------- reductions
  * Replaces _sum_all / _axis_scan + sum/mean/max (core.py:581-728).

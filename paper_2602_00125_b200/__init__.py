@@ -14,7 +14,7 @@ from .autograd import (GradStore, backward, is_recording, no_grad, record, reset
                        zero_grad)
 from .core import (Buffer, Tensor, abs_, absolute, add, broadcast_shapes, broadcast_to, clamp, div,
                    exp, from_buffer, from_dlpack, from_flat, from_numpy, full, fused_muladd_relu, gelu, linear,
-                   log, matmul, max, mean, mm, mul, muladd_relu_sum_grads, neg, ones, ones_like,
+                   log, matmul, max, mean, mm, mul, muladd_relu_stats, muladd_relu_sum_grads, neg, ones, ones_like,
                    reduce_to_shape, relu, reshape, set_gemm_algo, sigmoid, softmax, softmax_mul_mean, sqrt,
                    sub, sum,
                    tanh, tensor, transpose2d, uniform, zeros, zeros_like)
@@ -31,7 +31,7 @@ __all__ = [
     "sum", "mean", "max", "matmul", "mm", "linear", "softmax", "softmax_mul_mean", "reshape",
     "transpose2d",
     "broadcast_to", "reduce_to_shape", "broadcast_shapes", "fused_muladd_relu",
-    "muladd_relu_sum_grads", "set_gemm_algo",
+    "muladd_relu_sum_grads", "muladd_relu_stats", "set_gemm_algo",
     "backward", "no_grad", "record", "reset_tape", "tape", "zero_grad", "is_recording",
     "GradStore", "ShapeError", "BroadcastError", "GradError", "DeterminismError",
     "nn", "optim",

@@ -82,6 +82,7 @@ _SIGS = {
                                          c_void_p]),
     "b2_fused_muladd_relu_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                                          c_void_p]),
+    "b2_muladd_relu_stats": (c_int, [c_void_p] * 13 + [c_float, c_float, c_int64, c_int64, c_void_p]),
     "b2_reduce": (c_int, [c_int, c_void_p, c_void_p, c_int, i64p, c_void_p, i64p, c_uint32,
                           c_void_p]),
     "b2_max_scatter": (c_int, [c_void_p, c_int, i64p, c_uint32, c_void_p, c_void_p, c_void_p]),

@@ -24,7 +24,7 @@ OUT = os.path.join(HERE, "libb2.so")
 BUILD = os.path.join(ROOT, "build", "b2")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NO_FMAD = {"ewise.cu", "reduce.cu", "xent.cu", "optim.cu"}
+NO_FMAD = {"ewise.cu", "reduce.cu", "xent.cu", "optim.cu", "fused_stats.cu"}
 
 
 def _nvcc():

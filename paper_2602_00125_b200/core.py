@@ -30,7 +30,7 @@ import weakref
 import numpy as np
 
 from . import _lib as L
-from .autograd import is_recording, record
+from .autograd import is_recording, no_grad, record
 from .errors import BroadcastError, ShapeError
 
 _py_sum = sum
@@ -1291,6 +1291,41 @@ def fused_muladd_relu(a, b, c=None) -> Tensor:
                   (lambda g: mul(pre(g), b),
                    lambda g: reduce_to_shape(mul(pre(g), a), b.shape),
                    lambda g: reduce_to_shape(pre(g), c.shape)), saved=(a, b, c))
+
+
+def muladd_relu_stats(a, b, clip=(-10.0, 10.0)) -> dict:
+    """BASELINE config 2's whole workload with ONE read of `a` (b2_muladd_relu_stats):
+    y = relu(a*b + b), e = exp(clamp(a)), the sum/mean/max of y over dim 0
+    and dim 1, its full sum, and the gradients of sum(y) w.r.t. a and b --
+    bit-identical to the separate ops (fused_muladd_relu, clamp/exp, sum, mean,
+    max, muladd_relu_sum_grads). Nothing is recorded on the tape. Returns a
+    dict with keys y, e, sum0, mean0, max0, sum1, mean1, max1, sum_all,
+    grad_a, grad_b. Falls back to those ops for layouts the kernel does not
+    take (a non-contiguous, cols % 4 != 0)."""
+    a = _as_tensor(_as_operand(a))
+    b = _as_tensor(_as_operand(b))
+    if a.ndim != 2 or b.size != a.shape[1]:
+        raise ShapeError("muladd_relu_stats expects a (R, C) and a row vector b of length C")
+    R, C = a.shape
+    lo, hi = float(clip[0]), float(clip[1])
+    if not (a.is_contiguous and b.is_contiguous and C % 4 == 0 and R > 0 and C > 0
+            and a.data_ptr % 16 == 0 and b.data_ptr % 16 == 0):
+        with no_grad():
+            y = fused_muladd_relu(a, b)
+            out = {"y": y, "e": exp(clamp(a, lo, hi)), "sum_all": sum(y)}
+            for d in (0, 1):
+                out[f"sum{d}"], out[f"mean{d}"], out[f"max{d}"] = sum(y, d), mean(y, d), max(y, d)
+        out["grad_a"], out["grad_b"] = muladd_relu_sum_grads(a, b)
+        return out
+    out = {"y": _empty((R, C)), "e": _empty((R, C)), "grad_a": _empty((R, C)),
+           "grad_b": _empty(b.shape), "sum0": _empty((C,)), "mean0": _empty((C,)),
+           "max0": _empty((C,)), "sum1": _empty((R,)), "mean1": _empty((R,)), "max1": _empty((R,)),
+           "sum_all": _empty(())}
+    ptr = {k: v.data_ptr for k, v in out.items()}
+    L.call("b2_muladd_relu_stats", ptr["y"], ptr["e"], ptr["grad_a"], ptr["grad_b"], ptr["sum0"],
+           ptr["mean0"], ptr["max0"], ptr["sum1"], ptr["mean1"], ptr["max1"], ptr["sum_all"],
+           a.data_ptr, b.data_ptr, lo, hi, R, C, None)
+    return out
 
 
 def muladd_relu_sum_grads(a, b):

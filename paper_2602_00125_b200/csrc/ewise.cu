@@ -134,7 +134,7 @@ struct Un {
     if constexpr (OP == B2_RELU) return x > 0.0f ? x : 0.0f;  // nn.py:110
     if constexpr (OP == B2_RELU_MASK) return x > 0.0f ? 1.0f : 0.0f;
     if constexpr (OP == B2_COPY) return x;
-    if constexpr (OP == B2_CLAMP) return fminf(fmaxf(x, (float)alpha), (float)beta);
+    if constexpr (OP == B2_CLAMP) return x != x ? x : fminf(fmaxf(x, (float)alpha), (float)beta);  // NaN passes (np.clip)
     if constexpr (OP == B2_SCALE) return __fmul_rn(x, (float)alpha);
     if constexpr (OP == B2_DIV_SCALAR) return __fdiv_rn(x, (float)alpha);
     if constexpr (OP == B2_CLAMP_MASK) return (x >= (float)alpha && x <= (float)beta) ? 1.0f : 0.0f;

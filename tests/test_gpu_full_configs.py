@@ -249,3 +249,15 @@ def test_config4_full_size_fused_linear_and_loss():
     _record("config4_64x512x1024_fused", errs)
     for k, e in errs.items():
         assert e <= TOL, (k, e)
+
+
+def test_config2_full_size_single_pass_bit_exact():
+    """The whole config-2 workload in ONE read of a (b2_muladd_relu_stats)
+    gives the oracle's bits for every output and both gradients."""
+    a, b = I.config2_inputs()
+    ref = O.broadcast_reduce_config(a, b)
+    out = P.muladd_relu_stats(dev(a), dev(b))
+    for k in ("y", "e", "sum0", "sum1", "mean0", "mean1", "max0", "max1", "sum_all", "grad_a",
+              "grad_b"):
+        assert bits_equal(out[k].numpy(), ref[k]), k
+    _record("config2_single_pass", {"bit_exact": True})

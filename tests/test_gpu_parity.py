@@ -1282,3 +1282,31 @@ def test_fused_loss_under_cuda_graph_replay_rematerialises_split_outputs():
     finally:
         P.set_gemm_algo(None)
     assert gz_eager.shape == (256, 512)
+
+
+@pytest.mark.parametrize("shape", [(300, 1000), (129, 4100), (1, 4), (1024, 256), (8, 512)])
+def test_single_pass_config2_matches_the_separate_ops(shape):
+    """b2_muladd_relu_stats on ragged strips / row blocks, with NaN, +-inf and
+    clamp-boundary inputs: bit-identical to the separate device ops and to
+    the oracle."""
+    R, C = shape
+    rng = np.random.default_rng(R * 7 + C)
+    a = (rng.standard_normal((R, C)) * 4).astype(np.float32)
+    b = rng.uniform(-1, 1, (1, C)).astype(np.float32)
+    flat = a.ravel()
+    flat[rng.integers(0, flat.size, max(1, flat.size // 50))] = np.nan
+    flat[rng.integers(0, flat.size, max(1, flat.size // 100))] = np.inf
+    flat[rng.integers(0, flat.size, max(1, flat.size // 100))] = -10.0
+    b[0, 0] = 0.0
+    ref = O.broadcast_reduce_config(a, b)
+    out = P.muladd_relu_stats(dev(a), dev(b))
+    at, bt = dev(a), dev(b)
+    with P.no_grad():
+        y = P.fused_muladd_relu(at, bt)
+        sep = {"y": y, "e": P.exp(P.clamp(at, -10.0, 10.0)), "sum_all": P.sum(y)}
+        for d in (0, 1):
+            sep[f"sum{d}"], sep[f"mean{d}"], sep[f"max{d}"] = P.sum(y, d), P.mean(y, d), P.max(y, d)
+    sep["grad_a"], sep["grad_b"] = P.muladd_relu_sum_grads(at, bt)
+    for k, v in sep.items():
+        assert bits_equal(host(out[k]), host(v)), k
+        assert bits_equal(host(out[k]), ref[k]), k
