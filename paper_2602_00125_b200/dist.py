@@ -51,7 +51,7 @@ def shard_rows(global_rows: int, rank: int, world: int):
     return rank * per, (rank + 1) * per
 
 
-def exchange_unique_id(store, rank: int, make_uid, key="b2_nccl_uid") -> bytes:
+def exchange_unique_id(store, rank: int, make_uid, key="b2/nccl_uid") -> bytes:
     """Rank 0 publishes `make_uid()` under `key`; everyone returns it.
     `store` is any torch.distributed Store (TCPStore / FileStore / HashStore)."""
     if rank == 0:
@@ -63,12 +63,20 @@ def exchange_unique_id(store, rank: int, make_uid, key="b2_nccl_uid") -> bytes:
 
 
 def make_store(env: Env, port_offset=1):
+    """The key-value store the NCCL unique id travels through. Under torchrun
+    (TORCHELASTIC_USE_AGENT_STORE=True) every rank joins the elastic agent's
+    own TCPStore at MASTER_PORT as a client -- no second port to collide on;
+    otherwise (bench.py's launcher, a hand-set env) rank 0 hosts a TCPStore at
+    MASTER_PORT + port_offset."""
     import datetime
 
     from torch.distributed import TCPStore
 
+    timeout = datetime.timedelta(seconds=300)
+    if os.environ.get("TORCHELASTIC_USE_AGENT_STORE", "").lower() == "true":
+        return TCPStore(env.master_addr, env.master_port, env.world, False, timeout=timeout)
     return TCPStore(env.master_addr, env.master_port + port_offset, env.world, env.rank == 0,
-                    timeout=datetime.timedelta(seconds=300))
+                    timeout=timeout)
 
 
 def nccl_unique_id() -> bytes:

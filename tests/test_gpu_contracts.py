@@ -199,3 +199,31 @@ def test_bench_spawn_launcher_runs_an_nccl_rank_and_prints_one_line():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 1 and d["value"] > 0 and d["config"]["parallelism"] == "dp1"
     assert "NCCL INFO" in r.stderr  # the launcher routes NCCL's log to stderr
+
+
+def test_bench_under_torchrun_joins_the_agent_store_for_the_nccl_id():
+    """The driver's N > 1 launch (python -m torch.distributed.run ... bench.py
+    --gpus N) at N = 1 with a 1-rank NCCL communicator: the NCCL unique id goes
+    through torchrun's own agent store (no second port), one JSON line."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    env.update(B2_FORCE_NCCL="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "1",
+                        "--steps", "2", "--warmup", "3", "--no-ops", "--no-cpu", "--no-bf16",
+                        "--global-batch", "4096"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    assert json.loads(lines[0])["n_gpus"] == 1
