@@ -1378,6 +1378,11 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
   if (cg != 1 && cg != 2) {
     int64_t pair_tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
     cg = pair_tiles >= sms / 2 ? 2 : 1;
+    // few tiles over a long K (the dW GEMMs of config 4: 1024^2 over K = 32768)
+    // run as K slices for many k-blocks per unit: there a pair's per-SM operand
+    // ingress (64 KB per k-block instead of 96 KB) is the limit, not the tile
+    // count (measured: 174 -> 158 us; short-K few-tile GEMMs stay single-CTA)
+    if (cg == 1 && K >= 8192 && M >= 2 * BM) cg = 2;
   }
   // Work units (TcParams): whole waves of whole tiles, then the tail tiles
   // split into S K slices so the last wave fills the chip. Taken where it
