@@ -158,10 +158,13 @@ int b2_max_scatter(float* gx, int ndim, const int64_t* shape, uint32_t reduce_ma
  *       7 REF: the reference's arithmetic -- exact fp32 products summed in fp64,
  *         one f32 rounding (core.py:802-807 matmul.block) -- on the FP64 pipe.
  *         Parity mode (the exact-arithmetic control), never chosen by auto.
+ *       8 REF_BF16: the same on operands rounded to bf16 first -- the bf16
+ *         variant's operand rounding with exact accumulation (its control).
  */
 enum b2_gemm_algo { B2_GEMM_AUTO = 0, B2_GEMM_SIMT = 1, B2_GEMM_3XTF32 = 2,
                     B2_GEMM_1XTF32 = 3, B2_GEMM_TF32X = 4 /* tf32 hi*hi + bf16 hi*lo + lo*hi */,
-                    B2_GEMM_3XBF16 = 5, B2_GEMM_REF = 7 };
+                    B2_GEMM_3XBF16 = 5, B2_GEMM_REF = 7,
+                    B2_GEMM_REF_BF16 = 8 };
 enum b2_epilogue { B2_EPI_NONE = 0, B2_EPI_BIAS = 1, B2_EPI_BIAS_RELU = 2, B2_EPI_RELU = 3 };
 int b2_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
             const float* A, int64_t lda, const float* B, int64_t ldb,

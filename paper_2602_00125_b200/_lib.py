@@ -144,6 +144,7 @@ RED_SUM, RED_MEAN, RED_MAX = range(3)
 GEMM_AUTO, GEMM_SIMT, GEMM_3XTF32, GEMM_1XTF32, GEMM_TF32X, GEMM_3XBF16 = range(6)
 GEMM_BF16 = 6  # host-side selector for b2_gemm_bf16 (bf16 variant; never auto-selected)
 GEMM_REF = 7  # reference arithmetic: fp64 sums of exact fp32 products, one f32 rounding (parity mode)
+GEMM_REF_BF16 = 8  # the same on bf16-rounded operands (exact-arithmetic control of the bf16 variant)
 EPI_NONE, EPI_BIAS, EPI_BIAS_RELU, EPI_RELU = range(4)
 
 _lib = None

@@ -923,11 +923,13 @@ def set_gemm_algo(name):
     (bf16 operands, fp32 accumulation, fp32 master values everywhere else) and
     is only ever used when asked for. 'ref' is the reference's own arithmetic
     (exact fp32 products summed in fp64, one f32 rounding: core.py:802-807) on
-    the FP64 pipe -- the parity mode, not a performance path."""
+    the FP64 pipe -- the parity mode, not a performance path. 'ref_bf16' is the
+    same arithmetic on bf16-rounded operands: the exact-arithmetic control of
+    the bf16 variant."""
     global _ALGO_OVERRIDE
     _ALGO_OVERRIDE = {None: None, "auto": None, "simt": L.GEMM_SIMT, "3xtf32": L.GEMM_3XTF32,
                       "1xtf32": L.GEMM_1XTF32, "tf32x": L.GEMM_TF32X, "3xbf16": L.GEMM_3XBF16,
-                      "bf16": L.GEMM_BF16, "ref": L.GEMM_REF}[name]
+                      "bf16": L.GEMM_BF16, "ref": L.GEMM_REF, "ref_bf16": L.GEMM_REF_BF16}[name]
 
 
 def get_gemm_algo():

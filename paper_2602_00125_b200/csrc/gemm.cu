@@ -19,7 +19,7 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
             uint64_t* bits_out = nullptr);
 int gemm_ref(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
              const float* B, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
-             cudaStream_t st);
+             cudaStream_t st, bool bf16_operands);
 int tf32_split(float* hi, float* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
                cudaStream_t st);
 int bf16_cast(void* out, const float* x, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st);
@@ -43,6 +43,7 @@ int forced_algo() {
       else if (!strcmp(e, "tf32x")) v = B2_GEMM_TF32X;
       else if (!strcmp(e, "3xbf16")) v = B2_GEMM_3XBF16;
       else if (!strcmp(e, "ref")) v = B2_GEMM_REF;
+      else if (!strcmp(e, "ref_bf16")) v = B2_GEMM_REF_BF16;
     }
   }
   return v;
@@ -51,7 +52,7 @@ int forced_algo() {
 int select(int ta, int tb, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb) {
   int f = forced_algo();
   bool tc = b2::tc_supported(ta, tb, M, N, K, lda, ldb);
-  if (f == B2_GEMM_REF) return B2_GEMM_REF;
+  if (f == B2_GEMM_REF || f == B2_GEMM_REF_BF16) return f;
   if (f == B2_GEMM_SIMT || !tc) return B2_GEMM_SIMT;
   if (f) return f;
   // the tensor-core path pays a split pass + TMEM setup; small problems stay on FFMA.
@@ -86,8 +87,8 @@ int b2_gemm(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, int
   if (M == 0 || N == 0) return 0;
   if (K == 0) return b2::gemm_simt(ta, tb, M, N, 0, A, lda, B, ldb, C, ldc, bias, epi, st);
   if (algo == B2_GEMM_AUTO) algo = select(ta, tb, M, N, K, lda, ldb);
-  if (algo == B2_GEMM_REF)
-    return b2::gemm_ref(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, bias, epi, st);
+  if (algo == B2_GEMM_REF || algo == B2_GEMM_REF_BF16)
+    return b2::gemm_ref(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, bias, epi, st, algo == B2_GEMM_REF_BF16);
   if (algo != B2_GEMM_SIMT && !b2::tc_supported(ta, tb, M, N, K, lda, ldb))
     return b2::fail("b2_gemm: operands not TMA-compatible (leading dims must be multiples of 4)");
   switch (algo) {

@@ -17,6 +17,7 @@
 // 64x64x16 CTA tiles, 256 threads, 4x4 compensated accumulators per thread,
 // operands converted to double when staged to shared memory (double-buffered
 // through registers).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -25,7 +26,10 @@ namespace {
 
 constexpr int RBM = 64, RBN = 64, RBK = 16;
 
-template <bool TA, bool TB>
+// BF16IN: the operands are first rounded to bf16 (RN) -- the bf16 variant's
+// operand rounding with exact products and compensated sums: the
+// exact-arithmetic control for the bf16 variant (B2_GEMM_REF_BF16)
+template <bool TA, bool TB, bool BF16IN>
 __global__ void __launch_bounds__(256) k_gemm_f64acc(int64_t M, int64_t N, int64_t K,
                                                      const float* __restrict__ A, int64_t lda,
                                                      const float* __restrict__ B, int64_t ldb,
@@ -57,6 +61,13 @@ __global__ void __launch_bounds__(256) k_gemm_f64acc(int64_t M, int64_t N, int64
     }
   };
   auto store = [&](int buf) {
+    if (BF16IN) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        ra[i] = __bfloat162float(__float2bfloat16_rn(ra[i]));
+        rb[i] = __bfloat162float(__float2bfloat16_rn(rb[i]));
+      }
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (!TA) As[buf][(t % 4) * 4 + i][t / 4] = (double)ra[i];
@@ -123,16 +134,24 @@ namespace b2 {
 
 int gemm_ref(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
              const float* B, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
-             cudaStream_t st) {
+             cudaStream_t st, bool bf16_operands) {
   if (M == 0 || N == 0) return 0;
   dim3 grid((unsigned)((N + RBN - 1) / RBN), (unsigned)((M + RBM - 1) / RBM));
   if (grid.y > 65535) return fail("b2_gemm(ref): M too large for the reference-arithmetic grid");
-#define B2_REF(TA_, TB_) \
-  k_gemm_f64acc<TA_, TB_><<<grid, 256, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, bias, epi)
-  if (!ta && !tb) B2_REF(false, false);
-  else if (!ta && tb) B2_REF(false, true);
-  else if (ta && !tb) B2_REF(true, false);
-  else B2_REF(true, true);
+#define B2_REF(TA_, TB_)                                                                           \
+  if (bf16_operands)                                                                               \
+    k_gemm_f64acc<TA_, TB_, true><<<grid, 256, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, bias, epi); \
+  else                                                                                             \
+    k_gemm_f64acc<TA_, TB_, false><<<grid, 256, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, bias, epi)
+  if (!ta && !tb) {
+    B2_REF(false, false);
+  } else if (!ta && tb) {
+    B2_REF(false, true);
+  } else if (ta && !tb) {
+    B2_REF(true, false);
+  } else {
+    B2_REF(true, true);
+  }
 #undef B2_REF
   return launched("b2_gemm(ref)");
 }

@@ -261,3 +261,36 @@ def test_config2_full_size_single_pass_bit_exact():
               "grad_b"):
         assert bits_equal(out[k].numpy(), ref[k]), k
     _record("config2_single_pass", {"bit_exact": True})
+
+
+def test_config5_bf16_variant_against_its_exact_arithmetic_control(c5):
+    """The bf16 variant at full width (batch 1024, one Adam step) and its
+    exact-arithmetic control ('ref_bf16': the same bf16-rounded operands,
+    exact products, compensated fp64 sums).
+
+    * control vs the fp32 oracle: loss and logits within the bf16 tolerance
+      2e-2; the hidden-layer gradients' deviation is recorded -- it is the
+      cost of bf16 operands themselves (no accumulation error is left), which
+      is why 2e-2 on hidden-layer gradients is out of reach for any
+      bf16-operand implementation at random init;
+    * the device's bf16 variant vs the control: loss, logits and activations
+      at fp32-accumulation accuracy, gradients conditioned on the device's
+      relu pattern within 5e-3."""
+    from tests.test_gpu_parity import _conditioned_step, _mm_bf16
+
+    params, x, labels, ref = c5
+    closs, cacts, cgrads, _ = _device_step(params, x, labels, "ref_bf16")
+    loss, acts, grads, _ = _device_step(params, x, labels, "bf16")
+    rec = {"control_loss_vs_fp32": normwise(np.float32(closs), ref["loss"]),
+           "control_logits_vs_fp32": normwise(cacts[-1], ref["logits"])}
+    for i, ((gw, gb), (rw, rb)) in enumerate(zip(cgrads, ref["grads"])):
+        rec[f"control_gW{i}_vs_fp32"] = normwise(gw, rw)
+    rec["variant_loss_vs_control"] = normwise(np.float32(loss), np.float32(closs))
+    rec["variant_logits_vs_control"] = normwise(acts[-1], cacts[-1])
+    z, egrads = _conditioned_step(params, acts, labels, _mm_bf16)
+    rec["variant_grads_conditioned"] = max(
+        max(normwise(gw, ew), normwise(gb, eb)) for (gw, gb), (ew, eb) in zip(grads, egrads))
+    _record("config5_bf16_control", rec)
+    assert rec["control_loss_vs_fp32"] <= 2e-2 and rec["control_logits_vs_fp32"] <= 2e-2, rec
+    assert rec["variant_loss_vs_control"] <= 1e-3 and rec["variant_logits_vs_control"] <= 1e-3, rec
+    assert rec["variant_grads_conditioned"] <= 5e-3, rec
