@@ -234,6 +234,20 @@ __device__ __forceinline__ float div_by(float a, float b, float rb, bool ok) {
 // butterfly. The sign of a zero maximum may differ from the scan's first
 // zero, which no consumer can observe: z - m and m + log(se) are the same
 // for m = +0 and m = -0.
+// The pieces of div_by for rows where the window check is hoisted: a row
+// whose every dividend passes `in_window` (and whose divisor is `ok`) takes
+// div_fast for all of its elements -- no IEEE division code on the path,
+// which the per-element select of div_by made the compiler evaluate anyway.
+__device__ __forceinline__ bool in_window(float a) {
+  const float aa = fabsf(a);
+  return aa == 0.0f || (aa >= 0x1p-100f && aa <= 0x1p100f);  // NaN: false
+}
+__device__ __forceinline__ float div_fast(float a, float b, float rb) {
+  const float q = __fmul_rn(a, rb);
+  const float r = __fmaf_rn(-q, b, a);
+  return __fmaf_rn(r, rb, q);
+}
+
 template <int NV, bool FULL = false>
 __device__ __forceinline__ float row_max_regs(const float4 (&v)[NV], int64_t C, int lane) {
   float m = -INFINITY;
@@ -624,29 +638,35 @@ __global__ void __launch_bounds__(256, B2_WMEAN_MINB) k_smx_wmean_fwd(float* __r
     __syncwarp();
     const float m = row_max_regs<NV, FULL>(v, C, lane);
     double acc = 0;
+    bool win = true;
 #pragma unroll
     for (int i = 0; i < NV; ++i)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float e = b2::exp_f32(__fsub_rn(f4get(v[i], k), m));  // exp(sub(z, m))
         f4set(v[i], k, e);
+        win &= in_window(e);
         if (FULL || (int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)e;
       }
     const float s = __double2float_rn(warp_sum(acc));  // sum(e, -1, keepdims)
     const bool ok = s >= 1.0f && s <= 0x1p100f;
     const float rs_ = __frcp_rn(s);
+    const bool fast = __all_sync(0xffffffffu, win) && ok;  // warp-uniform
     double dot = 0;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int64_t q = i * 32 + lane;
       if (FULL || q * 4 < C) {
         float4 yq;
+        if (fast) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float yk = div_by(f4get(v[i], k), s, rs_, ok);  // div(e, s)
-          f4set(yq, k, yk);
-          dot += (double)__fmul_rn(yk, f4get(tv[i], k));      // mul(y, t), then the mean's sum
+          for (int k = 0; k < 4; ++k) f4set(yq, k, div_fast(f4get(v[i], k), s, rs_));  // div(e, s)
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) f4set(yq, k, __fdiv_rn(f4get(v[i], k), s));
         }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dot += (double)__fmul_rn(f4get(yq, k), f4get(tv[i], k));  // mul(y, t), mean's sum
         if (y) reinterpret_cast<float4*>(y + r * C)[q] = yq;
       }
     }
@@ -709,7 +729,7 @@ __global__ void __launch_bounds__(256, B2_WMEAN_MINB) k_smx_wmean_bwd(float* __r
     const float ss = __fmul_rn(s, s);
     const bool ok = s >= 1.0f && ss <= 0x1p100f;
     const float rs_ = __frcp_rn(s), rss = __frcp_rn(ss);
-    double acc = 0;
+    bool win = true;
 #pragma unroll
     for (int i = 0; i < NV; ++i)
 #pragma unroll
@@ -718,20 +738,50 @@ __global__ void __launch_bounds__(256, B2_WMEAN_MINB) k_smx_wmean_bwd(float* __r
         f4set(gv[i], k, gy);
         const float e = b2::exp_f32(__fsub_rn(f4get(ev[i], k), m));
         f4set(ev[i], k, e);
-        const float tt = div_by(__fmul_rn(gy, e), ss, rss, ok);  // div(mul(g, e), mul(s, s))
-        if (FULL || (int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)(-tt);  // neg, then sum(axis=-1)
+        win &= in_window(gy) && in_window(__fmul_rn(gy, e));
       }
+    const bool fast = __all_sync(0xffffffffu, win) && ok;  // warp-uniform
+    // the two divisions, with the window check hoisted to the row (warp-
+    // uniform branch: the fast loops hold no IEEE-division code)
+    double acc = 0;
+    if (fast) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float tt = div_fast(__fmul_rn(f4get(gv[i], k), f4get(ev[i], k)), ss, rss);  // div(mul(g, e), mul(s, s))
+          if (FULL || (int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)(-tt);  // neg, then sum(axis=-1)
+        }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float tt = __fdiv_rn(__fmul_rn(f4get(gv[i], k), f4get(ev[i], k)), ss);
+          if (FULL || (int64_t)(i * 32 + lane) * 4 + k < C) acc += (double)(-tt);
+        }
+    }
     const float gs = __double2float_rn(warp_sum(acc));
+    // ge = div(g, s) -- stored first; kept in gv
+    if (fast) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) f4set(gv[i], k, div_fast(f4get(gv[i], k), s, rs_));
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) f4set(gv[i], k, __fdiv_rn(f4get(gv[i], k), s));
+    }
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int64_t q = i * 32 + lane;
       if (FULL || q * 4 < C) {
         float4 o;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float ge = div_by(f4get(gv[i], k), s, rs_, ok);  // div(g, s) -- stored first
-          f4set(o, k, __fmul_rn(__fadd_rn(ge, gs), f4get(ev[i], k)));  // GradStore add, exp pullback
-        }
+        for (int k = 0; k < 4; ++k)
+          f4set(o, k, __fmul_rn(__fadd_rn(f4get(gv[i], k), gs), f4get(ev[i], k)));  // GradStore add, exp pullback
         if (gz) reinterpret_cast<float4*>(gz + r * C)[q] = o;
         if (ghi) split_store4(ghi + r * C + q * 4, glo + r * C + q * 4, o);
         if (colpart) {
