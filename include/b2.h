@@ -348,6 +348,11 @@ int b2_comm_init(int rank, int nranks, const unsigned char* uid128);
 int b2_comm_destroy(void);
 /* in-place sum (op=0) / average (op=1) / max (op=2) over all ranks, fp32 */
 int b2_allreduce_f32(float* buf, int64_t n, int op, void* stream);
+/* sharded optimizer step: reduce-scatter (recv = this rank's count-element
+ * shard of the reduced send[count * nranks]) and in-place all-gather (buf
+ * [count * nranks], this rank's shard at buf + rank * count) */
+int b2_reduce_scatter_f32(const float* send, float* recv, int64_t count, int op, void* stream);
+int b2_all_gather_f32(float* buf, int64_t count, int rank, void* stream);
 /* failure detection: the communicator's asynchronous NCCL error (0 = ok),
  * abort, and a host wait for a stream with a deadline that polls the async
  * error and aborts the communicator on error or timeout */

@@ -131,6 +131,8 @@ _SIGS = {
     "b2_comm_init": (c_int, [c_int, c_int, ctypes.c_char_p]),
     "b2_comm_destroy": (c_int, []),
     "b2_allreduce_f32": (c_int, [c_void_p, c_int64, c_int, c_void_p]),
+    "b2_reduce_scatter_f32": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
+    "b2_all_gather_f32": (c_int, [c_void_p, c_int64, c_int, c_void_p]),
     "b2_comm_async_error": (c_int, [POINTER(c_int)]),
     "b2_comm_abort": (c_int, []),
     "b2_stream_wait_timeout": (c_int, [c_void_p, c_double]),

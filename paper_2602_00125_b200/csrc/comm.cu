@@ -24,6 +24,9 @@ struct Nccl {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
@@ -45,6 +48,8 @@ int load_nccl() {
   g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(g_nccl.h, "ncclCommInitRank");
   g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(g_nccl.h, "ncclCommDestroy");
   g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(g_nccl.h, "ncclAllReduce");
+  g_nccl.ReduceScatter = (decltype(g_nccl.ReduceScatter))dlsym(g_nccl.h, "ncclReduceScatter");
+  g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(g_nccl.h, "ncclAllGather");
   g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(g_nccl.h, "ncclGetErrorString");
   g_nccl.CommGetAsyncError =
       (decltype(g_nccl.CommGetAsyncError))dlsym(g_nccl.h, "ncclCommGetAsyncError");
@@ -99,6 +104,30 @@ int b2_allreduce_f32(float* buf, int64_t n, int op, void* stream) {
   ncclRedOp_t rop = op == 1 ? ncclAvg : (op == 2 ? ncclMax : ncclSum);
   ncclResult_t r = g_nccl.AllReduce(buf, buf, (size_t)n, ncclFloat32, rop, g_comm, b2::resolve(stream));
   if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+  return 0;
+}
+
+// Sharded optimizer step (ZeRO-1 style): the gradient is reduce-scattered so
+// every rank holds the average of its contiguous 1/N shard (out = recv, count
+// elements per rank), updates only that shard of the parameter, and the
+// updated shards are all-gathered back into the full parameter in place
+// (sendbuff = buf + rank * count, NCCL's in-place form). Same bytes on the
+// wire as one all-reduce; 1/N of the optimizer's HBM traffic and slot memory.
+int b2_reduce_scatter_f32(const float* send, float* recv, int64_t count, int op, void* stream) {
+  if (!g_comm) return b2::fail("b2_reduce_scatter_f32: communicator not initialised");
+  if (!g_nccl.ReduceScatter) return b2::fail("b2_reduce_scatter_f32: libnccl lacks ncclReduceScatter");
+  ncclRedOp_t rop = op == 1 ? ncclAvg : (op == 2 ? ncclMax : ncclSum);
+  ncclResult_t r = g_nccl.ReduceScatter(send, recv, (size_t)count, ncclFloat32, rop, g_comm, b2::resolve(stream));
+  if (r != ncclSuccess) return nccl_fail(r, "ncclReduceScatter");
+  return 0;
+}
+
+int b2_all_gather_f32(float* buf, int64_t count, int rank, void* stream) {
+  if (!g_comm) return b2::fail("b2_all_gather_f32: communicator not initialised");
+  if (!g_nccl.AllGather) return b2::fail("b2_all_gather_f32: libnccl lacks ncclAllGather");
+  ncclResult_t r = g_nccl.AllGather(buf + (int64_t)rank * count, buf, (size_t)count, ncclFloat32, g_comm,
+                                    b2::resolve(stream));
+  if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
   return 0;
 }
 

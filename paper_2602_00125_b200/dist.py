@@ -179,6 +179,36 @@ class Communicator:
 
         return _copy_contig(t)
 
+    # ---- sharded optimizer step (ZeRO-1 style)
+
+    def shard_view(self, p):
+        """This rank's contiguous 1/world slice of parameter p as a persistent
+        1-D view (the optimizer keys its slots by it, so they hold 1/world of
+        the parameter)."""
+        if not hasattr(self, "_shards"):
+            self._shards = {}
+        v = self._shards.get(id(p))
+        if v is None or v.buffer is not p.buffer:
+            from .core import Tensor
+
+            cnt = p.size // self.world
+            v = Tensor(p.buffer, (cnt,), offset=p.offset + self.env.rank * cnt)
+            self._shards[id(p)] = v
+        return v
+
+    def new_shard(self, cnt):
+        from .core import _empty
+
+        return _empty((cnt,))
+
+    def reduce_scatter_(self, send, recv, op=AVG, stream=None):
+        L.call("b2_reduce_scatter_f32", send.data_ptr, recv.data_ptr, recv.size, op, stream)
+        return recv
+
+    def all_gather_(self, t, cnt, stream=None):
+        L.call("b2_all_gather_f32", t.data_ptr, cnt, self.env.rank, stream)
+        return t
+
     def max_scalar(self, v: float) -> float:
         """Max of a host float over ranks (device NCCL allreduce)."""
         if not self.active:
@@ -206,8 +236,13 @@ class GradReducer:
     Leaf gradients of Dense layers are fresh tensors and are averaged in
     place; an aliased or strided one is averaged as a private copy."""
 
-    def __init__(self, comm: Communicator, params=None, timeout_s=None, optimizer=None):
+    def __init__(self, comm: Communicator, params=None, timeout_s=None, optimizer=None, shard=None):
         self.comm = comm
+        # sharded update (default when several ranks exchange gradients):
+        # reduce-scatter -> the optimizer on this rank's 1/N shard -> all-gather
+        # of the updated parameter; same wire bytes as the all-reduce, 1/N of
+        # the optimizer's HBM traffic and fp64 slot memory
+        self.shard = (comm.active and comm.world > 1) if shard is None else bool(shard)
         self._pending = []
         if timeout_s is None:
             env = os.environ.get("B2_COMM_TIMEOUT_S")
@@ -236,6 +271,10 @@ class GradReducer:
         holds the averaged gradient."""
         if not self.comm.active and self.optimizer is None:
             return None
+        if self.optimizer is not None and self.shard and self.comm.active:
+            p = self._param(node_id)
+            if p is not None and p.is_contiguous and p.size and p.size % self.comm.world == 0:
+                return self._sharded_step(p, grad)
         from .autograd import grad_is_exclusive
 
         if (self.comm.active and not grad_is_exclusive(grad)) or not grad.is_contiguous:
@@ -257,6 +296,26 @@ class GradReducer:
         self._pending.append((ev, grad, handle))
         self._used = True
         return grad
+
+    def _sharded_step(self, p, grad):
+        """reduce-scatter(grad) -> update of this rank's shard -> all-gather(p),
+        in that order on the side stream after the gradient is produced. The
+        gradient itself is only read (never averaged in place), so aliasing
+        cannot bite; the store keeps this rank's local gradient."""
+        g = grad if grad.is_contiguous else self.comm.private_copy(grad)
+        cnt = p.size // self.comm.world
+        view = self.comm.shard_view(p)
+        gs = self.comm.new_shard(cnt)
+        handle = self.optimizer.prepare([(view, gs)])  # slot creation on the engine stream first
+        self._updated.add(id(p))
+        s = self.comm.side_stream()
+        ev = self.comm.after_compute(s)
+        self.comm.reduce_scatter_(g, gs, AVG, s)
+        self.optimizer.launch(handle, stream=s)
+        self.comm.all_gather_(p, cnt, s)
+        self._pending.append((ev, g, (gs, handle)))
+        self._used = True
+        return None
 
     def finish(self):
         if not self._used:

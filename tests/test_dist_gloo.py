@@ -217,7 +217,7 @@ def _reducer_worker(rank, world, port, outq):
     params = [_ht(w1, True), _ht(bfull[lo:hi], True), _ht(w2, True)]
     comm = _GlooComm(world)
     opt = RecOpt()
-    red = dist.GradReducer(comm, params, optimizer=opt)
+    red = dist.GradReducer(comm, params, optimizer=opt, shard=False)
     by_buf = {}
 
     def hook(nid, g):  # the reducer's hook, noting which leaf each averaged buffer belongs to
@@ -271,3 +271,129 @@ def test_gloo_world2_grad_reducer_hook_order_aliasing_and_averages():
     (_, g0, f0, *_), (_, g1, *_) = res
     np.testing.assert_allclose(g0["B"], f0["B"][:4] + f0["B"][4:], rtol=1e-5, atol=1e-7)
     np.testing.assert_array_equal(g0["B"], g1["B"])
+
+
+# ------------------------------------------------- sharded update over gloo
+
+
+class _ShardComm(_GlooComm):
+    """_GlooComm plus the sharded-update plumbing (reduce-scatter emulated by
+    an all-reduce + slice: gloo has no reduce-scatter)."""
+
+    def __init__(self, world, rank):
+        super().__init__(world)
+
+        class _E:
+            pass
+
+        self.env = _E()
+        self.env.rank = rank
+        self._views = {}
+
+    def shard_view(self, p):
+        from paper_2602_00125_b200 import core as C
+
+        cnt = p.size // self.world
+        return self._views.setdefault(id(p), C.Tensor(p.buffer, (cnt,), offset=p.offset + self.env.rank * cnt))
+
+    def new_shard(self, cnt):
+        return _ht(np.zeros(cnt, np.float32))
+
+    def reduce_scatter_(self, send, recv, op=1, stream=None):
+        self.log.append(("reduce_scatter", recv.size))
+        full = torch.from_numpy(np.array(_flat(send)))
+        tdist.all_reduce(full, op=tdist.ReduceOp.SUM)
+        if op == 1:
+            full /= self.world
+        r, n = self.env.rank, recv.size
+        recv.buffer.arr.reshape(-1)[recv.offset:recv.offset + n] = full.numpy()[r * n:(r + 1) * n]
+        return recv
+
+    def all_gather_(self, t, cnt, stream=None):
+        self.log.append(("all_gather", cnt))
+        mine = torch.from_numpy(np.array(_flat(t)[self.env.rank * cnt:(self.env.rank + 1) * cnt]))
+        parts = [torch.zeros_like(mine) for _ in range(self.world)]
+        tdist.all_gather(parts, mine)
+        t.buffer.arr.reshape(-1)[t.offset:t.offset + t.size] = torch.cat(parts).numpy()
+        return t
+
+
+def _flat(t):
+    return t.buffer.arr.reshape(-1)[t.offset:t.offset + t.size]
+
+
+class _HostSGD:
+    """The optimizer interface GradReducer drives, over host views."""
+
+    def __init__(self, lr):
+        self.lr = lr
+        self.seen = []
+
+    def prepare(self, pairs):
+        return list(pairs)
+
+    def launch(self, handle, stream=None):
+        for p, g in handle:
+            self.seen.append(p.size)
+            _flat(p)[:] = _flat(p) - np.float32(self.lr) * _flat(g)
+
+
+def _shard_worker(rank, world, port, outq):
+    import datetime
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_2602_00125_b200 import dist
+
+    tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                             world_size=world, timeout=datetime.timedelta(seconds=120))
+    rng = np.random.default_rng(5)
+    Bt, D, H, O = 8, 6, 4, 2                      # W1: 24 elements, W2: 8 (both split in 2)
+    x = rng.standard_normal((Bt, D)).astype(np.float32)
+    w1 = rng.standard_normal((H, D)).astype(np.float32) * 0.3
+    w2 = rng.standard_normal((O, H)).astype(np.float32) * 0.3
+    bfull = rng.standard_normal((Bt, H)).astype(np.float32) * 0.1
+    lo, hi = dist.shard_rows(Bt, rank, world)
+    # data parallel: every parameter is replicated (B too: the same rows on both ranks)
+    init = {"W1": w1.copy(), "W2": w2.copy(), "B": bfull[:hi - lo].copy()}
+    params = [_ht(w1.copy(), True), _ht(bfull[:hi - lo].copy(), True), _ht(w2.copy(), True)]
+    comm = _ShardComm(world, rank)
+    opt = _HostSGD(0.5)
+    red = dist.GradReducer(comm, params, optimizer=opt, shard=True)
+    assert red.shard
+    store = _host_model_step(x[lo:hi], params, red.hook)
+    red.finish()
+    local = {n: _arr(store[p]).copy() for n, p in zip(("W1", "B", "W2"), params)}
+    avg = {}
+    for n, g in local.items():
+        t = torch.from_numpy(g.copy())
+        tdist.all_reduce(t)
+        avg[n] = (t / world).numpy()
+    outq.put((rank, {n: _arr(p).copy() for n, p in zip(("W1", "B", "W2"), params)}, avg,
+              sorted(opt.seen), [e[0] for e in comm.log], init))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_update_equals_the_full_update_on_every_rank():
+    """reduce-scatter -> update of the rank's half -> all-gather: every rank
+    ends with the parameters a full update with the averaged gradient gives,
+    while its optimizer only ever touched half of each parameter."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=180) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, params, avg, seen, log, init in res:
+        assert seen == [4, 8, 12]  # half of W2 (8 elements), of this rank's B rows (16), of W1 (24)
+        assert log.count("reduce_scatter") == 3 and log.count("all_gather") == 3
+        for n in ("W1", "W2", "B"):
+            want = init[n] - np.float32(0.5) * avg[n]
+            np.testing.assert_allclose(params[n], want, rtol=1e-6, atol=1e-7)
+    np.testing.assert_array_equal(res[0][1]["W1"], res[1][1]["W1"])

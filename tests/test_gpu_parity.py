@@ -1163,11 +1163,13 @@ def test_softmax_row_constant_division_exact_at_scale():
     assert bits_equal(host(store[zt]), O.softmax_backward_composed(gy, e, s))
 
 
-@pytest.mark.parametrize("force_nccl", [False, True])
-def test_optimizer_overlapped_in_backward_matches_plain_step(force_nccl):
+@pytest.mark.parametrize("force_nccl,shard", [(False, False), (True, False), (True, True)])
+def test_optimizer_overlapped_in_backward_matches_plain_step(force_nccl, shard):
     """GradReducer(optimizer=...) launches each layer's Adam update on a side
     stream as soon as its gradient is final (after its all-reduce with NCCL):
-    three steps give bit-identical parameters to backward-then-step_all."""
+    three steps give bit-identical parameters to backward-then-step_all. With
+    shard=True the update runs as reduce-scatter -> Adam on the rank's shard
+    -> all-gather (NCCL, here one rank: the whole tensor is the shard)."""
     from paper_2602_00125_b200 import dist
     from paper_2602_00125_b200.data import build_mlp, mlp_config5
 
@@ -1183,7 +1185,8 @@ def test_optimizer_overlapped_in_backward_matches_plain_step(force_nccl):
         for _ in range(3):
             P.reset_tape()
             loss = nn.cross_entropy(model(x), lab, denom=512)
-            red = dist.GradReducer(comm, ps, optimizer=opt if overlap else None)
+            red = dist.GradReducer(comm, ps, optimizer=opt if overlap else None,
+                                   shard=shard if overlap else False)
             store = P.backward(loss, on_leaf_ready=red.hook)
             red.finish()
             if overlap:
