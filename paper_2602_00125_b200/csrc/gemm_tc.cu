@@ -51,6 +51,21 @@ extern "C" int b2_reduce(int, float*, int64_t*, int, const int64_t*, const float
 
 namespace {
 
+// B2_GEMM_TRACE builds (scripts/gemm_trace.py, a separate library) stamp the
+// global timer at the phases of every CTA's first unit -- where a few-tile
+// GEMM's fixed cost goes. Not in the product library.
+#ifdef B2_GEMM_TRACE
+__device__ unsigned long long g_trace[1024][8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define B2_TRACE(slot) g_trace[blockIdx.x & 1023][slot] = gtime()
+#else
+#define B2_TRACE(slot) ((void)0)
+#endif
+
 constexpr int BM = 128, BN = 256, BK = 32;  // BK fp32 = 128 bytes = one swizzle row
 constexpr int kThreads = 640;  // 4 control warps + 16 epilogue warps
 constexpr int KC_BASE = 8;     // k-blocks per accumulation chunk for the tf32 modes (K = 256)
@@ -483,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   double* colsum_smem = (double*)(smem + STAGES * CF::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) B2_TRACE(0);  // entry
   const int nkb = (p.K + CF::BKM - 1) / CF::BKM;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const bool leader = rank == 0;
@@ -524,8 +540,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // allocation, descriptor prefetch) may overlap the previous kernel's tail;
   // no global memory is touched before the prerequisite grids are complete.
   // Then let the next kernel start its own prologue as SMs free up.
+  if (threadIdx.x == 0) B2_TRACE(1);  // prologue done (barriers, TMEM)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
+  if (threadIdx.x == 0) B2_TRACE(2);  // prerequisite grids complete
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
@@ -598,6 +616,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+#ifdef B2_GEMM_TRACE
+          if (lane == 0 && kb == kb0 && tile == cl_id) B2_TRACE(3);  // first operands landed
+#endif
           if (lane == 0) {
             const uint32_t s0 = smem_u32(smem + stage * CF::STAGE_BYTES);
             if (MODE == 4) {
@@ -678,6 +699,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cb = chunk & 1;
         mbar_wait(&tfull[cb], (chunk >> 1) & 1);
         tc_fence_after();
+#ifdef B2_GEMM_TRACE
+        if (warp == 4 && lane == 0 && c == nch - 1 && tile == cl_id) B2_TRACE(4);  // last chunk's MMAs done
+#endif
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * BN + cg * 64);
 #pragma unroll
         for (int j = 0; j < 64; j += 16) {
@@ -868,10 +892,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if (threadIdx.x == 4 * 32) B2_TRACE(5);  // this epilogue warp's stores issued
   __syncthreads();
+  if (threadIdx.x == 0) B2_TRACE(6);  // every warp done
   if (CG == 2) cluster_sync();  // the peer may still be reading our smem / arriving on us
   if (warp == 2) {
     tc_fence_after();
+#ifdef B2_GEMM_TRACE
+    if (lane == 0) B2_TRACE(7);  // teardown
+#endif
     if (CG == 1)
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                    "r"(kTmemCols));
@@ -1233,6 +1262,12 @@ int launch_tc(const Operands& o, TcParams& p, cudaStream_t st) {
 }
 
 }  // namespace
+
+#ifdef B2_GEMM_TRACE
+extern "C" int b2_gemm_trace_read(unsigned long long* out /* [1024][8] */) {
+  return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 namespace b2 {
 
