@@ -282,15 +282,22 @@ int b2_col2im(float* dx, const float* dpatches, int64_t B, int64_t C, int64_t H,
 /* ---------------------------------------------------------------- losses
  * cross_entropy (nn.py:453-503): fwd writes the mean loss (f32 scalar) and
  * per-row stats (max, sum exp) in double; bwd writes
- * dlogits = (exp(z-m)/se - onehot) * (g[0] * inv_b).
+ * dlogits = (exp(z-m)/se - onehot) * (g[0] / denom) (denom: the mean's divisor, b).
  * labels are int64, validated on the host (nn.py:465-472).
  */
 int b2_xent_fwd(float* loss, double* row_stats, const float* logits,
-                const int64_t* labels, int64_t rows, int64_t cols, double inv_b,
+                const int64_t* labels, int64_t rows, int64_t cols, double denom,
                 void* stream);
 int b2_xent_bwd(float* dlogits, const float* g, const double* row_stats,
                 const float* logits, const int64_t* labels, int64_t rows,
-                int64_t cols, double inv_b, void* stream);
+                int64_t cols, double denom, void* stream);
+/* b2_xent_bwd with the outputs the last Linear's pullbacks read: dlogits'
+ * 3xBF16 split (dl_hi/dl_lo, as b2_bf16x3_split) and its column sums
+ * (f32(sum64 over rows), the bias gradient); every output nullable (dlogits
+ * too: the split alone when only GEMMs consume it). cols % 8 == 0, <= 1024. */
+int b2_xent_bwd_split(float* dlogits, void* dl_hi, void* dl_lo, float* colsum, const float* g,
+                      const double* row_stats, const float* logits, const int64_t* labels, int64_t rows,
+                      int64_t cols, double denom, void* stream);
 /* row softmax over the last axis, composed-semantics:
  * m = rowmax (detached), e = f32(exp(f32(z-m))), s = f32(sum64 e), y = f32(e/s).
  * bwd mirrors the GradStore order of the composition:

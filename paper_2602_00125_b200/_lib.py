@@ -116,6 +116,7 @@ _SIGS = {
                             c_void_p]),
     "b2_xent_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                             c_double, c_void_p]),
+    "b2_xent_bwd_split": (c_int, [c_void_p] * 8 + [c_int64, c_int64, c_double, c_void_p]),
     "b2_softmax_fwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p]),
     "b2_softmax_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                                c_void_p]),

@@ -803,6 +803,75 @@ __global__ void __launch_bounds__(256, B2_WMEAN_MINB) k_smx_wmean_bwd(float* __r
   }
 }
 
+// Cross-entropy pullback that hands its consumers what they read (the last
+// Linear's dX / dW GEMMs and its bias gradient): dlogits' 3xBF16 split and
+// its column sums (per-warp fp64 column accumulators in shared memory,
+// warps then CTAs folded in order), instead of the fp32 tensor that a split
+// pass and a column reduction would re-read. Same per-element arithmetic as
+// k_xent_bwd_v (bit-identical values); C % 8 == 0, 16-B aligned rows.
+template <int NV>
+__global__ void __launch_bounds__(256, 2) k_xent_bwd_split(float* __restrict__ dz,
+                                                          __nv_bfloat16* __restrict__ ghi,
+                                                          __nv_bfloat16* __restrict__ glo,
+                                                          double* __restrict__ colpart,
+                                                          const float* __restrict__ g,
+                                                          const double* __restrict__ row_stats,
+                                                          const float* __restrict__ z,
+                                                          const int64_t* __restrict__ labels, int64_t B,
+                                                          int64_t C, double denom) {
+  extern __shared__ __align__(16) double xcol[];  // [8 warps][4][NV*32]
+  constexpr int CP = NV * 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* const mycol = xcol + wid * 4 * CP;
+  if (colpart) {
+    for (int i = threadIdx.x; i < 8 * 4 * CP; i += blockDim.x) xcol[i] = 0.0;
+    __syncthreads();
+  }
+  const double gv = (double)g[0] / denom;  // nn.py:489
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < B; r += nw) {
+    const double m = row_stats[2 * r], se = row_stats[2 * r + 1];
+    const int64_t lab = labels[r];
+    const float4* zr = reinterpret_cast<const float4*>(z + r * C);
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      v[i] = q * 4 < C ? __ldg(zr + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t q = i * 32 + lane;
+      if (q * 4 < C) {
+        float4 o;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t j = q * 4 + k;
+          const double pr = b2::exp_fast((double)f4get(v[i], k) - m) / se - (j == lab ? 1.0 : 0.0);
+          f4set(o, k, __double2float_rn(pr * gv));  // nn.py:500
+        }
+        if (dz) reinterpret_cast<float4*>(dz + r * C)[q] = o;
+        if (ghi) split_store4(ghi + r * C + q * 4, glo + r * C + q * 4, o);
+        if (colpart) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mycol[k * CP + q] += (double)f4get(o, k);
+        }
+      }
+    }
+  }
+  if (colpart) {
+    __syncthreads();
+    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+      const int q = (int)(c >> 2), k = (int)(c & 3);
+      double t = 0;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) t += xcol[ww * 4 * CP + k * CP + q];
+      colpart[blockIdx.x * C + c] = t;
+    }
+  }
+}
+
 // column sums of per-CTA fp64 partials, one f32 rounding: 32 columns x 8
 // partial lanes per CTA (lane k folds partial rows k, k+8, ... in order), then
 // a fixed shared-memory tree over the 8 lanes -- deterministic
@@ -1035,6 +1104,43 @@ int b2_softmax_wmean_bwd(float* gz, void* gz_hi, void* gz_lo, float* colsum, con
   if (!rc && colsum) {
     k_colpart_fold<<<(unsigned)((cols + 31) / 32), 256, 0, st>>>(colsum, part, (int)ctas, cols);
     rc = b2::launched("b2_softmax_wmean_bwd(colsum)");
+  }
+  if (part) b2_free(part, st);
+  return rc;
+}
+
+int b2_xent_bwd_split(float* dlogits, void* dl_hi, void* dl_lo, float* colsum, const float* g,
+                      const double* row_stats, const float* logits, const int64_t* labels, int64_t rows,
+                      int64_t cols, double denom, void* stream) {
+  if (rows <= 0 || cols <= 0) return 0;
+  if (cols % 8 || cols > 1024 || ((uintptr_t)logits & 15) || ((uintptr_t)dlogits & 15) ||
+      ((uintptr_t)dl_hi & 15) || ((uintptr_t)dl_lo & 15) || (!dl_hi != !dl_lo))
+    return b2::fail("b2_xent_bwd_split: needs cols % 8 == 0, cols <= 1024 and 16-B aligned rows");
+  cudaStream_t st = b2::resolve(stream);
+  const int nv = (int)((cols + 127) / 128);
+  const int64_t ctas = std::min<int64_t>((rows + 7) / 8, 2LL * b2::sm_count());
+  double* part = nullptr;
+  if (colsum) B2_TRY(b2_alloc((size_t)ctas * cols * sizeof(double), st, (void**)&part));
+#define B2_XBS(NV)                                                                              \
+  {                                                                                             \
+    const int smem = colsum ? 8 * 4 * NV * 32 * 8 : 0;                                          \
+    static bool attr = false;                                                                   \
+    if (!attr) {                                                                                \
+      B2_CUDA(cudaFuncSetAttribute(k_xent_bwd_split<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4 * NV * 32 * 8)); \
+      attr = true;                                                                              \
+    }                                                                                           \
+    k_xent_bwd_split<NV><<<(unsigned)ctas, 256, smem, st>>>(dlogits, (__nv_bfloat16*)dl_hi,     \
+        (__nv_bfloat16*)dl_lo, part, g, row_stats, logits, labels, rows, cols, denom);           \
+  }
+  if (nv <= 1) B2_XBS(1)
+  else if (nv <= 2) B2_XBS(2)
+  else if (nv <= 4) B2_XBS(4)
+  else B2_XBS(8)
+#undef B2_XBS
+  int rc = b2::launched("b2_xent_bwd_split");
+  if (!rc && colsum) {
+    k_colpart_fold<<<(unsigned)((cols + 31) / 32), 256, 0, st>>>(colsum, part, (int)ctas, cols);
+    rc = b2::launched("b2_xent_bwd_split(colsum)");
   }
   if (part) b2_free(part, st);
   return rc;
