@@ -255,6 +255,18 @@ typedef struct b2_gemm_desc {
   float* colsum;
 } b2_gemm_desc;
 int b2_gemm_fused(const b2_gemm_desc* desc, void* stream);
+/* Up to 3 independent b2_gemm_fused problems of one algo in ONE persistent
+ * launch -- the x_bar and w_bar GEMMs of a matmul pullback (core.py:815-817),
+ * which read the same cotangent: units of all problems are drawn from one
+ * queue, the most expensive first, so short-K and long-K GEMMs fill each
+ * other's idle SMs. Outputs are bit-identical to separate b2_gemm_fused
+ * calls; no output may alias another descriptor's input. Replaces the two
+ * matmul calls of the pullback pair (core.py:815-817). */
+int b2_gemm_fused_group(const b2_gemm_desc* descs, int n, void* stream);
+/* SMs the persistent GEMM grids leave free (default 0): under data
+ * parallelism the collectives' kernels run beside the backward GEMMs. */
+int b2_gemm_set_sm_reserve(int n);
+int b2_gemm_get_sm_reserve(int* n);
 
 /* BF16 variant (explicitly requested precision only; bf16 tolerance 2e-2):
  * contiguous round-to-nearest bf16 cast of a [rows, cols] (ld) matrix, and a

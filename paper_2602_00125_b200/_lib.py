@@ -107,6 +107,9 @@ _SIGS = {
                                c_void_p, c_void_p, c_int64, c_void_p, c_int, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_void_p]),
     "b2_gemm_fused": (c_int, [c_void_p, c_void_p]),
+    "b2_gemm_fused_group": (c_int, [c_void_p, c_int, c_void_p]),
+    "b2_gemm_set_sm_reserve": (c_int, [c_int]),
+    "b2_gemm_get_sm_reserve": (c_int, [c_void_p]),
     "b2_bf16_cast": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     "b2_gemm_bf16": (c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                              c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -21,15 +21,18 @@ dot products.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import math
 import os
 import random
+import threading
 import weakref
 
 import numpy as np
 
 from . import _lib as L
+from . import autograd as _autograd
 from .autograd import is_recording, no_grad, record
 from .errors import BroadcastError, ShapeError
 
@@ -1005,17 +1008,30 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
         cs_done = cs_ptr is not None and (mask is None or mask_done)
         if cs_done:
             d.colsum = cs_ptr
+
+        def after():
+            if shi is not None:
+                from .graph import _capturing
+
+                buf = out.buffer
+                if buf._splits is None:
+                    buf._splits = {}
+                buf._splits[(kind, out.offset, M, N, N)] = (buf.version, shi, slo, _capturing[0])
+                if lazy:
+                    _set_pending(buf, shi, slo, M * N)
+            _gemm_fallbacks(out, mask, mask_done, cs_ptr, cs_done)
+
+        grp = _GROUP.pending
+        if grp is not None:  # launched with the other GEMMs of this pullback (gemm_group)
+            # the descriptor holds raw pointers: keep their owners alive until the launch
+            keep = (xa, wb, ahi, alo, bhi, blo, out, bias, mask, mask_bits, bits_out, colsum)
+            grp.append((d, after, 2.0 * M * N * K, keep, (M, N, K, ta, tb)))
+            return bits_out is not None
         ev = _timer_start()
         L.call("b2_gemm_fused", ctypes.byref(d), None)
-        if shi is not None:
-            from .graph import _capturing
-
-            buf = out.buffer
-            if buf._splits is None:
-                buf._splits = {}
-            buf._splits[(kind, out.offset, M, N, N)] = (buf.version, shi, slo, _capturing[0])
-            if lazy:
-                _set_pending(buf, shi, slo, M * N)
+        _timer_end(ev, 2.0 * M * N * K, ((M, N, K, ta, tb),))
+        after()
+        return bits_out is not None
     elif algo == L.GEMM_3XTF32 and tc_ok:
         ahi, alo = _split(xa, ar, ac, lda, "3xtf32")
         bhi, blo = _split(wb, br, bc, ldb, "3xtf32")
@@ -1028,17 +1044,61 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
         ev = _timer_start()
         L.call("b2_gemm", ta, tb, M, N, K, xa.data_ptr, lda, wb.data_ptr, ldb, out.data_ptr, N,
                bptr, epi, algo, None)
-    if ev is not None:
-        end = L.Event()
-        end.record()
-        GEMM_TIMER.append((2.0 * M * N * K, ev, end))
+    _timer_end(ev, 2.0 * M * N * K, ((M, N, K, ta, tb),))
+    _gemm_fallbacks(out, mask, mask_done, cs_ptr, cs_done)
+    return False
+
+
+def _gemm_fallbacks(out, mask, mask_done, cs_ptr, cs_done):
+    """The epilogue stages a GEMM could not fuse, as separate kernels."""
     if mask is not None and not mask_done:
         L.call("b2_binary", L.RELU_BWD, out.data_ptr, 2, L.i64s(out.shape), out.data_ptr,
                L.i64s(out.strides), mask.data_ptr, L.i64s(mask.strides), None)
     if cs_ptr is not None and not cs_done:
         L.call("b2_reduce", L.RED_SUM, cs_ptr, None, 2, L.i64s(out.shape), out.data_ptr,
                L.i64s(out.strides), 1, None)
-    return fused is not None and bits_out is not None
+
+
+class _GroupState(threading.local):
+    pending = None
+
+
+_GROUP = _GroupState()
+_GROUP_ON = os.environ.get("B2_GEMM_GROUP", "1") != "0"  # 0: one launch per GEMM (A/B)
+
+
+@contextlib.contextmanager
+def gemm_group():
+    """Defer the fused tensor-core GEMMs issued inside the block and launch
+    them together (b2_gemm_fused_group, up to 3 per launch) when it exits --
+    for the pullbacks of one node (x_bar and w_bar of a matmul/linear read the
+    same cotangent and write independent outputs). Nothing inside the block
+    may read a deferred GEMM's output. Values are bit-identical to separate
+    launches. Nested blocks join the outermost one."""
+    if _GROUP.pending is not None or not _GROUP_ON:
+        yield
+        return
+    _GROUP.pending = items = []
+    try:
+        yield
+    except BaseException:
+        _GROUP.pending = None
+        raise
+    _GROUP.pending = None
+    for i in range(0, len(items), 3):
+        part = items[i:i + 3]
+        ev = _timer_start()
+        if len(part) == 1:
+            L.call("b2_gemm_fused", ctypes.byref(part[0][0]), None)
+        else:
+            arr = (L.GemmDesc * len(part))(*[it[0] for it in part])
+            L.call("b2_gemm_fused_group", arr, len(part), None)
+        _timer_end(ev, _py_sum(it[2] for it in part), tuple(it[4] for it in part))
+        for it in part:
+            it[1]()
+
+
+_autograd.PULL_GROUP = gemm_group
 
 
 def _timer_start():
@@ -1047,6 +1107,18 @@ def _timer_start():
     ev = L.Event()
     ev.record()
     return ev
+
+
+GEMM_TIMER_LABELS = None  # profiling: receives the (M, N, K, ta, tb) problems of each timed launch
+
+
+def _timer_end(ev, flops, probs=()):
+    if ev is not None:
+        end = L.Event()
+        end.record()
+        GEMM_TIMER.append((flops, ev, end))
+        if GEMM_TIMER_LABELS is not None:
+            GEMM_TIMER_LABELS.append(probs)
 
 
 def matmul(x, w) -> Tensor:
@@ -1065,7 +1137,7 @@ def matmul(x, w) -> Tensor:
     return record("matmul", (x, w), out,
                   (lambda g: matmul(g, transpose2d(w)),               # x_bar = g w
                    lambda g: matmul(transpose2d(g), transpose2d(x))),  # w_bar = g^T x
-                  saved=(x, w))
+                  saved=(x, w), group=True)
 
 
 def mm(a, b) -> Tensor:
@@ -1162,7 +1234,7 @@ def linear(x, weight, bias=None, relu_out=False) -> Tensor:
 
         pulls.append(b_bar)
     return record("linear_relu" if relu_out else "linear", tuple(inputs), out, tuple(pulls),
-                  saved=(x, weight, y) if relu_out else (x, weight))
+                  saved=(x, weight, y) if relu_out else (x, weight), group=True)
 
 
 # ---------------------------------------------------------------------------

@@ -16,8 +16,35 @@ int cuda_fail(cudaError_t e, const char* what);
 cudaStream_t resolve(void* stream);
 int sm_count();
 constexpr int kTickets = 4096;
-unsigned* tickets(cudaStream_t st);  // zeroed per-stream arrival counters (kTickets)
+constexpr int kGemmTicket = kTickets;           // GEMM unit scheduler: [draw counter, done counter]
+constexpr int kTicketsAlloc = kTickets + 64;
+unsigned* tickets(cudaStream_t st);  // zeroed per-stream arrival counters (kTicketsAlloc)
 int ensure_init();
+// SMs the persistent GEMM grids use: all of them, minus the ones reserved
+// (b2_gemm_set_sm_reserve) for kernels that must run beside the GEMMs --
+// NCCL's collectives during a data-parallel backward.
+int gemm_sms();
+
+// One tensor-core GEMM problem (gemm_tc.cu); up to 3 run in one launch.
+struct TcDesc {
+  int ta, tb;
+  int64_t M, N, K;
+  const void *a0, *a1, *a2;
+  int64_t lda;
+  const void *b0, *b1, *b2;
+  int64_t ldb;
+  float* C;
+  int64_t ldc;
+  const float* bias;
+  int epi;
+  const float* mask;
+  void* s_hi;
+  void* s_lo;
+  float* colsum;
+  const uint64_t* mask_bits;
+  uint64_t* bits_out;
+};
+int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st);
 extern std::atomic<uint64_t> g_launches;
 
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }

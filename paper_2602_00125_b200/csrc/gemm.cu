@@ -252,9 +252,7 @@ int b2_gemm_tf32x_ex(int ta, int tb, int64_t M, int64_t N, int64_t K, const floa
 
 // The fused tensor-core GEMM behind one descriptor (include/b2.h
 // b2_gemm_desc): every epilogue stage of the MLP chain in one launch.
-int b2_gemm_fused(const b2_gemm_desc* d, void* stream) {
-  if (!d) return b2::fail("b2_gemm_fused: null descriptor");
-  if (d->M == 0 || d->N == 0) return 0;
+static int desc_to_tc(const b2_gemm_desc* d, b2::TcDesc* t, int* mode_out) {
   const int ta = d->trans_a, tb = d->trans_b;
   const int64_t M = d->M, N = d->N, K = d->K;
   const int64_t ac = ta ? M : K, bc = tb ? K : N;
@@ -266,17 +264,49 @@ int b2_gemm_fused(const b2_gemm_desc* d, void* stream) {
     case B2_GEMM_BF16_VARIANT: mode = 4; lda = ac; ldb = bc; break;
     default: return b2::fail("b2_gemm_fused: algo must be 3XBF16, TF32X or BF16_VARIANT");
   }
+  if (M < 0 || N < 0 || K < 0) return b2::fail("b2_gemm_fused: negative extent");
   if (!b2::tc_supported(ta, tb, M, N, K, lda, ldb))
     return b2::fail("b2_gemm_fused: operands not TMA-compatible");
   if (d->mask && (((uintptr_t)d->mask & 15) || d->ldc % 4))
     return b2::fail("b2_gemm_fused: mask alignment");
   if (d->relu_bits_out && !(d->epilogue == B2_EPI_RELU || d->epilogue == B2_EPI_BIAS_RELU))
     return b2::fail("b2_gemm_fused: relu_bits_out needs a ReLU epilogue");
-  const void* a2 = mode == 2 ? d->a[2] : nullptr;
-  const void* b2p = mode == 2 ? d->b[2] : nullptr;
-  return b2::gemm_tc(ta, tb, mode, M, N, K, d->a[0], d->a[1], a2, lda, d->b[0], d->b[1], b2p, ldb,
-                     d->C, d->ldc, d->bias, d->epilogue, b2::resolve(stream), d->mask, d->c_hi,
-                     mode == 4 ? nullptr : d->c_lo, d->colsum, d->mask_bits, d->relu_bits_out);
+  if ((d->epilogue == B2_EPI_BIAS || d->epilogue == B2_EPI_BIAS_RELU) && !d->bias)
+    return b2::fail("b2_gemm_fused: bias epilogue without a bias pointer");
+  *t = b2::TcDesc{ta, tb, M, N, K, d->a[0], d->a[1], mode == 2 ? d->a[2] : nullptr, lda,
+                  d->b[0], d->b[1], mode == 2 ? d->b[2] : nullptr, ldb, d->C, d->ldc, d->bias,
+                  d->epilogue, d->mask, d->c_hi, mode == 4 ? nullptr : d->c_lo, d->colsum,
+                  d->mask_bits, d->relu_bits_out};
+  *mode_out = mode;
+  return 0;
+}
+
+int b2_gemm_fused(const b2_gemm_desc* d, void* stream) {
+  if (!d) return b2::fail("b2_gemm_fused: null descriptor");
+  if (d->M == 0 || d->N == 0) return 0;
+  b2::TcDesc t;
+  int mode;
+  B2_TRY(desc_to_tc(d, &t, &mode));
+  return b2::gemm_tc_group(mode, &t, 1, b2::resolve(stream));
+}
+
+// Up to 3 independent fused GEMMs of one algo in ONE persistent launch (the
+// dX and dW GEMMs of a matmul/linear pullback: they read the same cotangent
+// and write different outputs). Units are drawn dynamically, the most
+// expensive first; every output is bit-identical to b2_gemm_fused of the
+// same descriptor. No output may alias another problem's input.
+int b2_gemm_fused_group(const b2_gemm_desc* d, int n, void* stream) {
+  if (!d || n < 1 || n > 3) return b2::fail("b2_gemm_fused_group: 1 to 3 descriptors");
+  b2::TcDesc t[3];
+  int modes[3], m = 0;
+  for (int i = 0; i < n; ++i) {
+    if (d[i].M == 0 || d[i].N == 0) continue;  // empty output: nothing to launch
+    B2_TRY(desc_to_tc(&d[i], &t[m], &modes[m]));
+    if (m && modes[m] != modes[0]) return b2::fail("b2_gemm_fused_group: descriptors differ in algo");
+    ++m;
+  }
+  if (!m) return 0;
+  return b2::gemm_tc_group(modes[0], t, m, b2::resolve(stream));
 }
 
 }  // extern "C"

@@ -252,7 +252,6 @@ struct TcParams {
   const float* mask;        // C = C * (mask > 0 ? 1 : 0), mask [M, N] with ld = ldc (ReLU pullback)
   __nv_bfloat16* s_hi;      // emit the TF32X split of C: bf16(trunc_tf32(C)) ...
   __nv_bfloat16* s_lo;      // ... and bf16(C - trunc_tf32(C)), both [M, N] contiguous
-  int kc;                   // k-blocks per fp32 promotion chunk
   int group_n;              // raster group width in tile-columns
   // work units: units [0, full_tiles) are whole tiles (all of K); the rest
   // split the remaining tail tiles into `splits` K slices of kbps k-blocks
@@ -263,20 +262,55 @@ struct TcParams {
   int splits;
   int kbps;
   float* ws;
-  int l2hint;               // B operand loads with L2 evict_last (B2_GEMM_L2HINT=0 disables)
-  int stage_out;            // every CTA runs at most one unit: fp32 tile stores (C / K-slice
-                            // partials) go through shared memory as coalesced row stores
+  int nkb;                  // k-blocks of K
   double* colsum;           // optional [ceil(M/128)][N] fp64 column partial sums of the stored C
   const uint64_t* mask_bits;  // ReLU-pullback mask as bits ([M][bits_ld] words, bit j = column 64w+j)
   uint64_t* bits_out;         // emit C > 0 as bits (ReLU forward): the next backward's mask
   int bits_ld;                // words per row of both bit arrays = ceil(N / 64)
+  int a_mn, b_mn;             // operand layouts: A stored [K,M] (MN-major) / B stored [K,N]
+};
+
+// One launch runs up to kMaxProb independent problems of one mode (the dX and
+// dW GEMMs of a pullback): their work units are numbered back to back
+// (problem g owns units [ustart[g], ustart[g+1])). Every CTA (pair) takes
+// units from a ring in shared memory that its producer thread fills: with
+// sched == nullptr unit i of cluster c is c + i * clusters (the static
+// persistent raster of a single problem); otherwise the producer draws units
+// from an atomic counter (sched[0]; sched[1] counts finished clusters, the
+// last one re-zeroes both), so problems whose units differ in cost (long-K dW
+// slices first, then dX tiles) balance dynamically. Which CTA computes a unit
+// never changes its result (K-slice partials have fixed slots, folded in
+// slice order): deterministic either way.
+constexpr int kMaxProb = 3;
+// Unit ids published ahead of the consumers. The ring needs no "slot free"
+// barrier: every consumer is within 2 + STAGES + 1 units of the producer
+// (the producer publishes unit k+1 only after issuing unit k-1's loads, which
+// needs all but STAGES k-blocks consumed by the MMAs; the MMAs of unit m
+// need the epilogue warps of both CTAs to have drained up to unit m-2; the
+// peer's loads gate the leader's MMAs), so with STAGES <= 8 a ring of 16
+// never overwrites an id a consumer has yet to read -- and a consumer's
+// release would cost a memory barrier behind its own global stores.
+constexpr int kUnitRing = 16;
+struct TcGroup {
+  TcParams p[kMaxProb];
+  int nprob;
+  int ustart[kMaxProb + 1];
+  int num_units;
+  unsigned* sched;
+  int kc;         // k-blocks per fp32 promotion chunk
+  int l2hint;     // B operand loads with L2 evict_last (B2_GEMM_L2HINT=0 disables)
+  int stage_out;  // every CTA runs at most one unit: fp32 tile stores go through shared memory
+};
+struct TcMaps {
+  CUtensorMap m[kMaxProb][6];  // per problem: MODE 1 {A, B}; 3/5 {A, B, Alo, Blo}; 2 {A, B, Ah, Bh, Al, Bl}; 4 {A, B}
 };
 
 // unit u -> (output tile, k-block range, partial slot); slot -1 = a whole
 // tile finished in the fused epilogue, else the unit's index into ws
 __device__ __forceinline__ void tile_coords(const TcParams& p, int t, int& tm, int& tn);
-__device__ __forceinline__ void tile_info(const TcParams& p, int u, int nkb, int& tm, int& tn,
-                                          int& kb0, int& kb1, int& slot) {
+__device__ __forceinline__ void tile_info(const TcParams& p, int u, int& tm, int& tn, int& kb0,
+                                          int& kb1, int& slot) {
+  const int nkb = p.nkb;
   if (u < p.full_tiles) {
     tile_coords(p, u, tm, tn);
     kb0 = 0;
@@ -342,7 +376,7 @@ struct Cfg {
                   : A32 + B32 + 2 * (A16 + B16);
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
   // + the column-sum exchange (4 column groups x 4 warps x 64 doubles)
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 8192;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers, unit ring*/ + 8192;
   // byte offsets inside a stage
   static constexpr int OFF_A = 0;
   static constexpr int OFF_ALO = A32;                                 // MODE 3
@@ -367,10 +401,10 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t
 }
 
 // fp32 tile (tf32 consumption): K-major = one box {32 K, rows}; MN-major = 32x32 boxes
-template <bool MN, int ROWS, int CG>
-__device__ __forceinline__ void load32(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
+template <int ROWS, int CG>
+__device__ __forceinline__ void load32(bool mn, uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
                                        uint32_t bar_cl, int mn0, int k0, uint64_t pol) {
-  if (MN) {
+  if (mn) {
 #pragma unroll
     for (int j = 0; j < ROWS / 32; ++j) tma2d<CG>(dst + j * 4096, tm, bar, bar_cl, mn0 + 32 * j, k0, pol);
   } else {
@@ -380,10 +414,10 @@ __device__ __forceinline__ void load32(uint8_t* dst, const CUtensorMap* tm, uint
 
 // bf16 tile: K-major = one box {KB K, rows}; MN-major = boxes {64 MN (128 B), KB K}
 // (KB = 32 with 64-B rows in MODE 2, 64 with 128-B rows in the pure-bf16 modes)
-template <bool MN, int ROWS, int CG, int KB = 32>
-__device__ __forceinline__ void load16(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
+template <int ROWS, int CG, int KB = 32>
+__device__ __forceinline__ void load16(bool mn, uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
                                        uint32_t bar_cl, int mn0, int k0, uint64_t pol) {
-  if (MN) {
+  if (mn) {
 #pragma unroll
     for (int j = 0; j < ROWS / 64; ++j)
       tma2d<CG>(dst + j * (KB * 128), tm, bar, bar_cl, mn0 + 64 * j, k0, pol);
@@ -477,16 +511,83 @@ __device__ __forceinline__ void stage_tile_store(uint8_t* smem, const float (&ac
   asm volatile("bar.sync 5, 512;" ::: "memory");  // the buffer may be reused by the next store
 }
 
-template <bool A_MN, bool B_MN, int MODE, int CG>
+// ---- unit ring (see TcGroup): shared::cluster store + cluster-scope waits
+__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, int v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// The MMAs of one k-block (stage at shared address s0) for one operand
+// layout; acc_flag = 0 starts a new accumulation chunk.
+template <int MODE, int CG, bool A_MN, bool B_MN>
+__device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t s0, uint32_t acc_flag) {
+  using CF = Cfg<MODE, CG>;
+  constexpr uint32_t id32 = make_idesc(false, A_MN, B_MN, BM * CG);
+  constexpr uint32_t id16 = make_idesc(true, A_MN, B_MN, BM * CG);
+  if (MODE == 4) {
+#pragma unroll
+    for (int ks = 0; ks < CF::BKM / 16; ++ks)
+      tc_mma<CG>(d_tmem, desc16<CF::BKM>(s0 + CF::OFF_AH16, A_MN, ks),
+                 desc16<CF::BKM>(s0 + CF::OFF_BH16, B_MN, ks), id16, (acc_flag | ks) ? 1u : 0u, true);
+  }
+  if (MODE == 5) {
+#pragma unroll
+    for (int ks = 0; ks < CF::BKM / 16; ++ks) {
+      const uint64_t ah = desc16<CF::BKM>(s0 + CF::OFF_AH16, A_MN, ks);
+      const uint64_t bh = desc16<CF::BKM>(s0 + CF::OFF_BH16, B_MN, ks);
+      tc_mma<CG>(d_tmem, ah, bh, id16, (acc_flag | ks) ? 1u : 0u, true);
+      tc_mma<CG>(d_tmem, ah, desc16<CF::BKM>(s0 + CF::OFF_BL16, B_MN, ks), id16, 1u, true);
+      tc_mma<CG>(d_tmem, desc16<CF::BKM>(s0 + CF::OFF_AL16, A_MN, ks), bh, id16, 1u, true);
+    }
+  }
+#pragma unroll
+  for (int ks = 0; ks < ((MODE == 4 || MODE == 5) ? 0 : BK / 8); ++ks) {
+    const uint64_t a = desc32(s0 + CF::OFF_A, A_MN, ks);
+    const uint64_t b = desc32(s0 + CF::OFF_B, B_MN, ks);
+    tc_mma<CG>(d_tmem, a, b, id32, (acc_flag | ks) ? 1u : 0u, false);
+    if (MODE == 3) {
+      tc_mma<CG>(d_tmem, a, desc32(s0 + CF::OFF_BLO, B_MN, ks), id32, 1u, false);
+      tc_mma<CG>(d_tmem, desc32(s0 + CF::OFF_ALO, A_MN, ks), b, id32, 1u, false);
+    }
+  }
+  if (MODE == 2) {
+#pragma unroll
+    for (int ks = 0; ks < BK / 16; ++ks) {
+      tc_mma<CG>(d_tmem, desc16(s0 + CF::OFF_AH16, A_MN, ks), desc16(s0 + CF::OFF_BL16, B_MN, ks), id16,
+                 1u, true);
+      tc_mma<CG>(d_tmem, desc16(s0 + CF::OFF_AL16, A_MN, ks), desc16(s0 + CF::OFF_BH16, B_MN, ks), id16,
+                 1u, true);
+    }
+  }
+}
+
+// problem of unit u (MULTI = false: a single-problem launch, problem 0 with
+// every parameter at a static offset)
+template <bool MULTI>
+__device__ __forceinline__ int prob_of(const TcGroup& G, int u) {
+  if (!MULTI) return 0;
+  int g = 0;
+  while (g + 1 < G.nprob && u >= G.ustart[g + 1]) ++g;
+  return g;
+}
+
+template <int MODE, int CG, bool MULTI>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
-              const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB3,
-              const TcParams p) {
+    k_gemm_tc(const __grid_constant__ TcMaps tmaps, const __grid_constant__ TcGroup G) {
   using CF = Cfg<MODE, CG>;
   constexpr int STAGES = CF::STAGES;
   // bf16 operands carry 2^-9 relative error: promote every K = 1024 instead
-  const int KC = p.kc;  // k-blocks per accumulation chunk (host: kc_for_mode)
+  const int KC = G.kc;  // k-blocks per accumulation chunk (host: kc_for_mode)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + STAGES * CF::STAGE_BYTES);
@@ -495,15 +596,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
-  double* colsum_smem = (double*)(smem + STAGES * CF::STAGE_BYTES + 256);
+  uint64_t* ufull = bars + 2 * STAGES + 5;
+  int* uring = (int*)(ufull + kUnitRing);
+  double* colsum_smem = (double*)(smem + STAGES * CF::STAGE_BYTES + 512);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) B2_TRACE(0);  // entry
-  const int nkb = (p.K + CF::BKM - 1) / CF::BKM;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const bool leader = rank == 0;
   const int cl_id = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int cl_num = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int num_units = G.num_units;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -514,9 +617,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 16 * CG);  // every epilogue warp of the pair drains before reuse
     }
+    for (int s = 0; s < kUnitRing; ++s) mbar_init(&ufull[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+    for (int g = 0; g < (MULTI ? G.nprob : 1); ++g) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmaps.m[g][0]) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmaps.m[g][1]) : "memory");
+    }
   }
   if (warp == 2) {
     if (CG == 1) {
@@ -545,16 +651,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0) B2_TRACE(2);  // prerequisite grids complete
 
+  // consumer side of the unit ring: unit i of this cluster (see kUnitRing)
+  auto take = [&](int i) -> int {
+    const int slot = i & (kUnitRing - 1);
+    const uint32_t ph = (uint32_t)(i / kUnitRing) & 1u;
+    if (CG == 2 && !leader)
+      mbar_wait_cl(&ufull[slot], ph);
+    else
+      mbar_wait(&ufull[slot], ph);
+    return *(volatile int*)&uring[slot];
+  };
+
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       const uint64_t pa = l2_policy_normal();
-      const uint64_t pb = p.l2hint ? l2_policy_last() : pa;
-      for (int tile = cl_id; tile < p.num_tiles; tile += cl_num) {
+      const uint64_t pb = G.l2hint ? l2_policy_last() : pa;
+      auto produce = [&](int u) {
+        const int gi = prob_of<MULTI>(G, u);
+        const TcParams& p = G.p[gi];
+        const CUtensorMap* mp = &tmaps.m[gi][0];
+        const bool amn = p.a_mn != 0, bmn = p.b_mn != 0;
         int tm, tn, kb0, kb1, ks;
-        tile_info(p, tile, nkb, tm, tn, kb0, kb1, ks);
+        tile_info(p, u - G.ustart[gi], tm, tn, kb0, kb1, ks);
         const int m0 = tm * (BM * CG) + (int)rank * BM;
         const int n0 = tn * BN + (int)rank * CF::BNL;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -565,29 +686,68 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (leader) mbar_expect_tx(fb, CF::STAGE_BYTES * CG);
           const int k0 = kb * CF::BKM;
           if (MODE == 4 || MODE == 5) {  // bf16 operands only
-            load16<A_MN, BM, CG, CF::BKM>(st + CF::OFF_AH16, &tmA, fb, fb_cl, m0, k0, pa);
-            load16<B_MN, CF::BNL, CG, CF::BKM>(st + CF::OFF_BH16, &tmB, fb, fb_cl, n0, k0, pb);
+            load16<BM, CG, CF::BKM>(amn, st + CF::OFF_AH16, mp + 0, fb, fb_cl, m0, k0, pa);
+            load16<CF::BNL, CG, CF::BKM>(bmn, st + CF::OFF_BH16, mp + 1, fb, fb_cl, n0, k0, pb);
             if (MODE == 5) {
-              load16<A_MN, BM, CG, CF::BKM>(st + CF::OFF_AL16, &tmA2, fb, fb_cl, m0, k0, pa);
-              load16<B_MN, CF::BNL, CG, CF::BKM>(st + CF::OFF_BL16, &tmB2, fb, fb_cl, n0, k0, pb);
+              load16<BM, CG, CF::BKM>(amn, st + CF::OFF_AL16, mp + 2, fb, fb_cl, m0, k0, pa);
+              load16<CF::BNL, CG, CF::BKM>(bmn, st + CF::OFF_BL16, mp + 3, fb, fb_cl, n0, k0, pb);
             }
           } else {
-            load32<A_MN, BM, CG>(st + CF::OFF_A, &tmA, fb, fb_cl, m0, k0, pa);
-            load32<B_MN, CF::BNL, CG>(st + CF::OFF_B, &tmB, fb, fb_cl, n0, k0, pb);
+            load32<BM, CG>(amn, st + CF::OFF_A, mp + 0, fb, fb_cl, m0, k0, pa);
+            load32<CF::BNL, CG>(bmn, st + CF::OFF_B, mp + 1, fb, fb_cl, n0, k0, pb);
           }
           if (MODE == 3) {
-            load32<A_MN, BM, CG>(st + CF::OFF_ALO, &tmA2, fb, fb_cl, m0, k0, pa);
-            load32<B_MN, CF::BNL, CG>(st + CF::OFF_BLO, &tmB2, fb, fb_cl, n0, k0, pb);
+            load32<BM, CG>(amn, st + CF::OFF_ALO, mp + 2, fb, fb_cl, m0, k0, pa);
+            load32<CF::BNL, CG>(bmn, st + CF::OFF_BLO, mp + 3, fb, fb_cl, n0, k0, pb);
           } else if (MODE == 2) {
-            load16<A_MN, BM, CG>(st + CF::OFF_AH16, &tmA2, fb, fb_cl, m0, k0, pa);
-            load16<A_MN, BM, CG>(st + CF::OFF_AL16, &tmA3, fb, fb_cl, m0, k0, pa);
-            load16<B_MN, CF::BNL, CG>(st + CF::OFF_BH16, &tmB2, fb, fb_cl, n0, k0, pb);
-            load16<B_MN, CF::BNL, CG>(st + CF::OFF_BL16, &tmB3, fb, fb_cl, n0, k0, pb);
+            load16<BM, CG>(amn, st + CF::OFF_AH16, mp + 2, fb, fb_cl, m0, k0, pa);
+            load16<BM, CG>(amn, st + CF::OFF_AL16, mp + 4, fb, fb_cl, m0, k0, pa);
+            load16<CF::BNL, CG>(bmn, st + CF::OFF_BH16, mp + 3, fb, fb_cl, n0, k0, pb);
+            load16<CF::BNL, CG>(bmn, st + CF::OFF_BL16, mp + 5, fb, fb_cl, n0, k0, pb);
           }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
+        }
+      };
+      if (leader) {
+        // draw units (static raster or the atomic counter) and publish them
+        // one ahead of the loads, to this CTA's ring and the peer's
+        auto next_unit = [&](int i) -> int {
+          return G.sched ? (int)atomicAdd(G.sched, 1u) : cl_id + i * cl_num;
+        };
+        auto publish = [&](int i, int u) {
+          const int slot = i & (kUnitRing - 1);
+          uring[slot] = u;
+          if (CG == 2) {
+            st_cluster_u32(mapa(smem_u32(&uring[slot]), 1), u);
+            mbar_arrive_remote(mapa(smem_u32(&ufull[slot]), 1));
+          }
+          mbar_arrive(&ufull[slot]);
+        };
+        int i = 0;
+        int u = next_unit(0);
+        publish(0, u);
+        while (u < num_units) {
+          const int un = next_unit(i + 1);
+          publish(i + 1, un);
+          produce(u);
+          u = un;
+          ++i;
+        }
+        if (G.sched) {  // the last cluster to finish drawing re-zeroes the counters
+          __threadfence();
+          if (atomicAdd(G.sched + 1, 1u) == (unsigned)cl_num - 1) {
+            atomicExch(G.sched, 0u);
+            atomicExch(G.sched + 1, 0u);
+          }
+        }
+      } else {
+        for (int i = 0;; ++i) {
+          const int u = take(i);
+          if (u >= num_units) break;
+          produce(u);
         }
       }
     }
@@ -597,15 +757,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     // fp32 accumulation loses ~1 ulp per MMA step (2e-5 normwise at K=8192 with
     // exact inputs), so the epilogue promotes each chunk into RN fp32 sums.
     if (leader) {
-      constexpr uint32_t id32 = make_idesc(false, A_MN, B_MN, BM * CG);
-      constexpr uint32_t id16 = make_idesc(true, A_MN, B_MN, BM * CG);
       int stage = 0;
       uint32_t phase = 0;
       int chunk = 0;
       uint32_t d_tmem = tmem_base;
-      for (int tile = cl_id; tile < p.num_tiles; tile += cl_num) {
+      for (int i = 0;; ++i) {
+        const int u = take(i);
+        if (u >= num_units) break;
+        const int gi = prob_of<MULTI>(G, u);
+        const TcParams& p = G.p[gi];
+        const bool amn = p.a_mn != 0, bmn = p.b_mn != 0;
         int tm, tn, kb0, kb1, ks_;
-        tile_info(p, tile, nkb, tm, tn, kb0, kb1, ks_);
+        tile_info(p, u - G.ustart[gi], tm, tn, kb0, kb1, ks_);
         for (int kb = kb0; kb < kb1; ++kb) {
           const int kc = (kb - kb0) % KC;
           if (kc == 0) {  // claim the next chunk accumulator (ping-pong)
@@ -617,45 +780,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
 #ifdef B2_GEMM_TRACE
-          if (lane == 0 && kb == kb0 && tile == cl_id) B2_TRACE(3);  // first operands landed
+          if (lane == 0 && kb == kb0 && i == 0) B2_TRACE(3);  // first operands landed
 #endif
           if (lane == 0) {
             const uint32_t s0 = smem_u32(smem + stage * CF::STAGE_BYTES);
-            if (MODE == 4) {
-#pragma unroll
-              for (int ks = 0; ks < CF::BKM / 16; ++ks)
-                tc_mma<CG>(d_tmem, desc16<CF::BKM>(s0 + CF::OFF_AH16, A_MN, ks),
-                           desc16<CF::BKM>(s0 + CF::OFF_BH16, B_MN, ks), id16, (kc | ks) ? 1u : 0u,
-                           true);
-            }
-            if (MODE == 5) {
-#pragma unroll
-              for (int ks = 0; ks < CF::BKM / 16; ++ks) {
-                const uint64_t ah = desc16<CF::BKM>(s0 + CF::OFF_AH16, A_MN, ks);
-                const uint64_t bh = desc16<CF::BKM>(s0 + CF::OFF_BH16, B_MN, ks);
-                tc_mma<CG>(d_tmem, ah, bh, id16, (kc | ks) ? 1u : 0u, true);
-                tc_mma<CG>(d_tmem, ah, desc16<CF::BKM>(s0 + CF::OFF_BL16, B_MN, ks), id16, 1u, true);
-                tc_mma<CG>(d_tmem, desc16<CF::BKM>(s0 + CF::OFF_AL16, A_MN, ks), bh, id16, 1u, true);
-              }
-            }
-#pragma unroll
-            for (int ks = 0; ks < ((MODE == 4 || MODE == 5) ? 0 : BK / 8); ++ks) {
-              const uint64_t a = desc32(s0 + CF::OFF_A, A_MN, ks);
-              const uint64_t b = desc32(s0 + CF::OFF_B, B_MN, ks);
-              tc_mma<CG>(d_tmem, a, b, id32, (kc | ks) ? 1u : 0u, false);
-              if (MODE == 3) {
-                tc_mma<CG>(d_tmem, a, desc32(s0 + CF::OFF_BLO, B_MN, ks), id32, 1u, false);
-                tc_mma<CG>(d_tmem, desc32(s0 + CF::OFF_ALO, A_MN, ks), b, id32, 1u, false);
-              }
-            }
-            if (MODE == 2) {
-#pragma unroll
-              for (int ks = 0; ks < BK / 16; ++ks) {
-                tc_mma<CG>(d_tmem, desc16(s0 + CF::OFF_AH16, A_MN, ks),
-                           desc16(s0 + CF::OFF_BL16, B_MN, ks), id16, 1u, true);
-                tc_mma<CG>(d_tmem, desc16(s0 + CF::OFF_AL16, A_MN, ks),
-                           desc16(s0 + CF::OFF_BH16, B_MN, ks), id16, 1u, true);
-              }
+            const uint32_t acc_flag = kc ? 1u : 0u;
+            // one branch per k-block into layout-specialised issue code (the
+            // descriptors fold to constants: no address math between MMAs)
+            if (amn) {
+              if (bmn) mma_kblock<MODE, CG, true, true>(d_tmem, s0, acc_flag);
+              else mma_kblock<MODE, CG, true, false>(d_tmem, s0, acc_flag);
+            } else {
+              if (bmn) mma_kblock<MODE, CG, false, true>(d_tmem, s0, acc_flag);
+              else mma_kblock<MODE, CG, false, false>(d_tmem, s0, acc_flag);
             }
             // smem slot free (in both CTAs) once these MMAs retire; chunk ready
             const bool last = kc == KC - 1 || kb == kb1 - 1;
@@ -684,11 +821,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int cg = (warp - 4) >> 2;
     const int row = q * 32 + lane;
-    const bool vec_ok = (p.ldc % 4) == 0 && (((uintptr_t)p.C) & 15) == 0;
     int chunk = 0;
-    for (int tile = cl_id; tile < p.num_tiles; tile += cl_num) {
+    for (int i = 0;; ++i) {
+      const int u = take(i);
+      if (u >= num_units) break;
+      const int gi = prob_of<MULTI>(G, u);
+      const TcParams& p = G.p[gi];
+      const bool vec_ok = (p.ldc % 4) == 0 && (((uintptr_t)p.C) & 15) == 0;
       int tm, tn, kb0, kb1, ks;
-      tile_info(p, tile, nkb, tm, tn, kb0, kb1, ks);
+      tile_info(p, u - G.ustart[gi], tm, tn, kb0, kb1, ks);
       const int nch = (kb1 - kb0 + KC - 1) / KC;
       const int m0 = tm * (BM * CG) + (int)rank * BM;
       const int n0 = tn * BN;
@@ -700,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tfull[cb], (chunk >> 1) & 1);
         tc_fence_after();
 #ifdef B2_GEMM_TRACE
-        if (warp == 4 && lane == 0 && c == nch - 1 && tile == cl_id) B2_TRACE(4);  // last chunk's MMAs done
+        if (warp == 4 && lane == 0 && c == nch - 1 && i == 0) B2_TRACE(4);  // last chunk's MMAs done
 #endif
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * BN + cg * 64);
 #pragma unroll
@@ -709,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           TMEM_LD16(tbase + j, v);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int i = 0; i < 16; ++i) acc[j + i] = __fadd_rn(acc[j + i], __uint_as_float(v[i]));
+          for (int t = 0; t < 16; ++t) acc[j + t] = __fadd_rn(acc[j + t], __uint_as_float(v[t]));
         }
         tc_fence_before();
         __syncwarp();
@@ -722,7 +863,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (ks >= 0) {  // a K slice of a tail tile: raw partial sums, tile-local
         float* w0 = p.ws + ((int64_t)ks * (BM * CG) + (int)rank * BM) * BN;
-        if (p.stage_out) {
+        if (G.stage_out) {
           stage_tile_store(smem, acc, row, cg, warp, lane, w0, BN, BM, BN);
           continue;
         }
@@ -789,7 +930,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!p.C) {
           // fp32 C not wanted: only its operand split / bits / column sums
-        } else if (p.stage_out) {
+        } else if (G.stage_out) {
           // stored below, coalesced through shared memory (all rows of the tile)
         } else if (full64) {
 #pragma unroll
@@ -836,7 +977,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (p.stage_out && p.C) {  // every epilogue warp takes part (rows past M are not stored)
+      if (G.stage_out && p.C) {  // every epilogue warp takes part (rows past M are not stored)
         const int rows_left = p.M - m0;
         const int cols_left = p.N - n0;
         stage_tile_store(smem, acc, row, cg, warp, lane, p.C + (int64_t)m0 * p.ldc + n0, p.ldc,
@@ -1194,55 +1335,84 @@ static int stage_out_enabled() {
   return v;
 }
 
-template <bool A_MN, bool B_MN, int MODE, int CG>
-int launch_tc(const Operands& o, TcParams& p, cudaStream_t st) {
+// One problem of a launch as the host prepares it (gemm_tc_group).
+struct Prob {
+  TcParams p;
+  Operands o;
+  int64_t tiles;      // output tiles at the launch's CTA grouping
+  int S;              // K slices of the split tiles (1: whole tiles only)
+  int64_t T;          // tiles split into S slices
+  void* part;         // K-slice partials
+  void* cs_part;      // fp64 column partials
+  float* colsum_out;
+  int cs_rows;
+};
+
+static int group_n_env() {
+  static int gn = -1;
+  if (gn < 0) {
+    const char* e = getenv("B2_GEMM_GROUPN");
+    gn = e ? atoi(e) : 0;
+    if (gn <= 0) gn = kGroupN;
+  }
+  return gn;
+}
+
+// Tensor maps of every problem (box shapes from the mode's Cfg), the
+// TcGroup, one launch. A is [M,K] (K-major) or stored [K,M] (MN-major); B is
+// [N,K] or stored [K,N].
+template <int MODE, int CG>
+int launch_tc(Prob* pr, int n, TcGroup& G, cudaStream_t st) {
   using CF = Cfg<MODE, CG>;
-  CUtensorMap m[6];
-  // A is [M,K] (K-major) or stored [K,M] (MN-major); B is [N,K] or stored [K,N]
-  const int64_t ar = A_MN ? p.K : p.M, ac = A_MN ? p.M : p.K;
-  const int64_t br = B_MN ? p.K : p.N, bc = B_MN ? p.N : p.K;
-  const int abox = A_MN ? CF::BKM : BM, bbox = B_MN ? CF::BKM : CF::BNL;
-  // MODE 4 / 5 read bf16 operand arrays (contiguous casts / splits) through bf16 maps
+  static TcMaps maps;  // host staging (copied into the launch's parameters)
   constexpr bool kB16 = MODE == 4 || MODE == 5;
-  B2_TRY(make_map(&m[0], o.a[0], ar, ac, o.lda, abox, A_MN, kB16, CF::W64));
-  B2_TRY(make_map(&m[1], o.b[0], br, bc, o.ldb, bbox, B_MN, kB16, CF::W64));
-  m[2] = m[0]; m[3] = m[1]; m[4] = m[0]; m[5] = m[1];
-  if (MODE == 5) {
-    B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, true, CF::W64));
-    B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, true, CF::W64));
-  } else if (MODE == 3) {
-    B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, false));
-    B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, false));
-  } else if (MODE == 2) {
-    B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, true));
-    B2_TRY(make_map(&m[4], o.a[2], ar, ac, ac, abox, A_MN, true));
-    B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, true));
-    B2_TRY(make_map(&m[5], o.b[2], br, bc, bc, bbox, B_MN, true));
-  }
-  p.kc = kc_for_mode(MODE);
-  {
-    static int gn = -1;
-    if (gn < 0) {
-      const char* e = getenv("B2_GEMM_GROUPN");
-      gn = e ? atoi(e) : 0;
-      if (gn <= 0) gn = kGroupN;
+  for (int g = 0; g < n; ++g) {
+    const TcParams& p = pr[g].p;
+    const Operands& o = pr[g].o;
+    CUtensorMap* m = maps.m[g];
+    const bool A_MN = p.a_mn != 0, B_MN = p.b_mn != 0;
+    const int64_t ar = A_MN ? p.K : p.M, ac = A_MN ? p.M : p.K;
+    const int64_t br = B_MN ? p.K : p.N, bc = B_MN ? p.N : p.K;
+    const int abox = A_MN ? CF::BKM : BM, bbox = B_MN ? CF::BKM : CF::BNL;
+    B2_TRY(make_map(&m[0], o.a[0], ar, ac, o.lda, abox, A_MN, kB16, CF::W64));
+    B2_TRY(make_map(&m[1], o.b[0], br, bc, o.ldb, bbox, B_MN, kB16, CF::W64));
+    m[2] = m[0]; m[3] = m[1]; m[4] = m[0]; m[5] = m[1];
+    if (MODE == 5) {
+      B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, true, CF::W64));
+      B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, true, CF::W64));
+    } else if (MODE == 3) {
+      B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, false));
+      B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, false));
+    } else if (MODE == 2) {
+      B2_TRY(make_map(&m[2], o.a[1], ar, ac, ac, abox, A_MN, true));
+      B2_TRY(make_map(&m[4], o.a[2], ar, ac, ac, abox, A_MN, true));
+      B2_TRY(make_map(&m[3], o.b[1], br, bc, bc, bbox, B_MN, true));
+      B2_TRY(make_map(&m[5], o.b[2], br, bc, bc, bbox, B_MN, true));
     }
-    p.group_n = gn;
+    G.p[g] = p;
   }
-  p.tiles_n = (p.N + BN - 1) / BN;
-  p.tiles_m = (p.M + BM * CG - 1) / (BM * CG);
-  p.num_tiles = p.full_tiles + (p.tiles_m * p.tiles_n - p.full_tiles) * p.splits;  // units
-  auto kern = k_gemm_tc<A_MN, B_MN, MODE, CG>;
+  G.kc = kc_for_mode(MODE);
+  auto kern = n > 1 ? k_gemm_tc<MODE, CG, true> : k_gemm_tc<MODE, CG, false>;
   static bool attr_set = false;
   if (!attr_set) {
-    B2_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
-    if (CG == 2) B2_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    for (auto k : {k_gemm_tc<MODE, CG, true>, k_gemm_tc<MODE, CG, false>}) {
+      B2_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+      if (CG == 2) B2_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    }
     attr_set = true;
   }
-  int sms = b2::sm_count();
-  int grid = (p.num_tiles * CG < sms) ? p.num_tiles * CG : (sms / CG) * CG;
+  const int sms = b2::gemm_sms();
+  const int grid = (G.num_units * CG < sms) ? G.num_units * CG : (sms / CG) * CG;
   static_assert(CF::STAGES * CF::STAGE_BYTES >= BM * kStageLd * 4, "staged tile store needs the stage buffers");
-  p.stage_out = p.num_tiles <= grid / CG && stage_out_enabled();
+  G.stage_out = G.num_units <= grid / CG && stage_out_enabled();
+  // several problems with more units than CTA (pairs): units are drawn from
+  // the stream's zeroed scheduler counters (dynamic balance); else the raster
+  G.sched = nullptr;
+  if (n > 1 && G.num_units > grid / CG) {
+    unsigned* tk = b2::tickets(st);
+    if (!tk) return b2::fail("gemm_tc: no scheduler counters for this stream");
+    G.sched = tk + b2::kGemmTicket;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -1257,8 +1427,8 @@ int launch_tc(const Operands& o, TcParams& p, cudaStream_t st) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  B2_CUDA(cudaLaunchKernelEx(&cfg, kern, m[0], m[1], m[2], m[3], m[4], m[5], p));
-  return b2::launched("b2_gemm(tcgen05)");
+  B2_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, G));
+  return b2::launched(n > 1 ? "b2_gemm(tcgen05, grouped)" : "b2_gemm(tcgen05)");
 }
 
 }  // namespace
@@ -1373,6 +1543,210 @@ static int cg_mode() {
   return v;
 }
 
+int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st) {
+  B2_TRY(get_encode());
+  if (n < 1 || n > kMaxProb) return fail("gemm_tc: 1 to 3 problems per launch");
+  Prob pr[kMaxProb];
+  for (int g = 0; g < n; ++g) {
+    const TcDesc& x = d[g];
+    TcParams& p = pr[g].p;
+    memset(&p, 0, sizeof(p));
+    p.C = x.C;
+    p.bias = x.bias;
+    p.ldc = x.ldc;
+    p.M = (int)x.M;
+    p.N = (int)x.N;
+    p.K = (int)x.K;
+    p.epi = x.epi;
+    p.mask = x.mask;
+    p.mask_bits = x.mask_bits;
+    p.bits_out = x.bits_out;
+    p.bits_ld = (int)((x.N + 63) / 64);
+    if (((uintptr_t)x.mask_bits & 7) || ((uintptr_t)x.bits_out & 7))
+      return fail("gemm_tc: bit masks need 8-B aligned word arrays");
+    p.s_hi = (__nv_bfloat16*)x.s_hi;
+    p.s_lo = (__nv_bfloat16*)x.s_lo;
+    if ((x.s_hi == nullptr) != (x.s_lo == nullptr) && mode != 4)
+      return fail("gemm_tc: split outputs come in pairs");
+    if (((uintptr_t)x.s_hi & 15) || ((uintptr_t)x.s_lo & 15) || ((uintptr_t)x.C & 3))
+      return fail("gemm_tc: C must be 4-B and the emitted split arrays 16-B aligned");
+    if (mode == 4) p.s_lo = nullptr;  // BF16 mode emits a single bf16 cast
+    p.a_mn = x.ta != 0;
+    p.b_mn = x.tb == 0;
+    p.group_n = group_n_env();
+    pr[g].o = Operands{{x.a0, x.a1, x.a2}, {x.b0, x.b1, x.b2}, x.lda, x.ldb};
+    pr[g].part = pr[g].cs_part = nullptr;
+    pr[g].colsum_out = x.colsum;
+    pr[g].S = 1;
+    pr[g].T = 0;
+  }
+  const int sms = gemm_sms();
+  const int bk = (mode == 4 || mode == 5) ? 64 : BK;  // Cfg::BKM
+  // CTA pairs once there are enough 256-row tiles to fill the chip
+  auto cg_alone = [&](const TcDesc& x) -> int {
+    const int f = cg_mode();
+    if (f == 1 || f == 2) return f;
+    const int64_t pair_tiles = ((x.M + 2 * BM - 1) / (2 * BM)) * ((x.N + BN - 1) / BN);
+    if (pair_tiles >= sms / 2) return 2;
+    // few tiles over a long K (the dW GEMMs of config 4: 1024^2 over K = 32768)
+    // run as K slices for many k-blocks per unit: there a pair's per-SM operand
+    // ingress (64 KB per k-block instead of 96 KB) is the limit, not the tile
+    // count (measured: 174 -> 158 us; short-K few-tile GEMMs stay single-CTA)
+    return (x.K >= 8192 && x.M >= 2 * BM) ? 2 : 1;
+  };
+  int cg = 1;
+  for (int g = 0; g < n; ++g) cg = std::max(cg, cg_alone(d[g]));
+  // a group of few tiles in all (config 3's dA + dB at n = 1024) fills the
+  // chip once with K slices of every tile: one unit per CTA (pair)
+  int64_t group_tiles = 0;
+  for (int g = 0; g < n; ++g)
+    group_tiles += ((d[g].M + (int64_t)BM * cg - 1) / ((int64_t)BM * cg)) * ((d[g].N + BN - 1) / BN);
+  const bool few_group = n > 1 && group_tiles * cg <= sms / 2;
+  // Work units (TcParams): whole tiles, and tiles split into S K slices
+  // whose fp32 partials a fixed-order second stage folds. Taken where it pays
+  // for the partials' round trip and the second stage (measured,
+  // scripts/tail_probe.py): few-tile long-K GEMMs split every tile (dW
+  // [1024 x 1024] over K = 32768, square n = 1024); a short run of waves
+  // whose last wave is at most half full splits its tail tiles (dW
+  // [4096 x 4096] over K = 65536: 3 waves + 34 of 74 tiles). Slices >= 256
+  // of K, S <= 16. The K partition of a problem is the one it gets when
+  // launched alone -- it fixes the rounding of every output, so a grouped
+  // launch is bit-identical to separate ones -- except in a group of few
+  // tiles (below); either way it depends only on the shapes and the SM count
+  // (deterministic).
+  for (int g = 0; g < n; ++g) {
+    TcParams& p = pr[g].p;
+    p.nkb = (int)((d[g].K + bk - 1) / bk);
+    p.tiles_n = (int)((d[g].N + BN - 1) / BN);
+    p.tiles_m = (int)((d[g].M + (int64_t)BM * cg - 1) / ((int64_t)BM * cg));
+    pr[g].tiles = (int64_t)p.tiles_m * p.tiles_n;
+    const int ca = cg_alone(d[g]);
+    const int64_t Pa = sms / ca;
+    const int64_t tiles_a = ((d[g].M + (int64_t)BM * ca - 1) / ((int64_t)BM * ca)) * p.tiles_n;
+    const int nkb = p.nkb;
+    int64_t full = pr[g].tiles, T = 0;
+    int S = 1;
+    if (few_group && nkb >= 16 && splitk_enabled()) {
+      // the group's own partition (outputs differ from separate launches in
+      // rounding only; still a function of the shapes and the SM count)
+      S = (int)std::max<int64_t>(
+          1, std::min<int64_t>({(sms / cg) / group_tiles, (int64_t)nkb * bk / 256, 16}));
+      if (S > 1) {
+        full = 0;
+        T = pr[g].tiles;
+      }
+    } else if (nkb >= 16 && splitk_enabled()) {
+      int64_t fa = tiles_a, Ta = 0;
+      if (tiles_a * ca <= sms / 2) {
+        fa = 0;
+        Ta = tiles_a;
+      } else if (tiles_a >= Pa && tiles_a < 8 * Pa && 2 * (tiles_a % Pa) <= Pa) {
+        fa = (tiles_a / Pa) * Pa;
+        Ta = tiles_a - fa;
+      }
+      if (Ta > 0)
+        S = (int)std::max<int64_t>(1, std::min<int64_t>({Pa / Ta, (int64_t)nkb * bk / 256, 16}));
+      if (S > 1) {
+        if (fa == 0) {  // every tile split: any tile shape gives the same K partition
+          full = 0;
+          T = pr[g].tiles;
+        } else if (ca == cg) {  // the same tiles as alone
+          full = fa;
+          T = Ta;
+        } else {
+          S = 1;
+        }
+      }
+    }
+    p.full_tiles = (int)full;
+    p.kbps = nkb;
+    p.splits = 1;
+    p.ws = nullptr;
+    if (S > 1) {
+      p.kbps = (nkb + S - 1) / S;
+      S = (nkb + p.kbps - 1) / p.kbps;
+      p.splits = S;
+    } else {
+      p.full_tiles = (int)pr[g].tiles;
+      T = 0;
+    }
+    pr[g].S = S;
+    pr[g].T = T;
+  }
+  // most expensive units first (longest-processing-time order for the
+  // dynamic draw); a stable order otherwise
+  if (n > 1)
+    std::stable_sort(pr, pr + n, [](const Prob& a, const Prob& b) {
+      return (a.S > 1 ? a.p.kbps : a.p.nkb) > (b.S > 1 ? b.p.kbps : b.p.nkb);
+    });
+  TcGroup G;
+  memset(&G, 0, sizeof(G));
+  G.nprob = n;
+  int units = 0;
+  for (int g = 0; g < n; ++g) {
+    TcParams& p = pr[g].p;
+    p.num_tiles = (int)(p.full_tiles + (pr[g].tiles - p.full_tiles) * p.splits);  // units
+    G.ustart[g] = units;
+    units += p.num_tiles;
+  }
+  G.ustart[n] = units;
+  G.num_units = units;
+  {
+    static int h = -1;
+    if (h < 0) {
+      const char* e = getenv("B2_GEMM_L2HINT");
+      h = !(e && e[0] == '0');
+    }
+    G.l2hint = h;
+  }
+  int rc = 0;
+  for (int g = 0; g < n && !rc; ++g) {
+    TcParams& p = pr[g].p;
+    if (pr[g].S > 1) {
+      rc = b2_alloc((size_t)pr[g].S * pr[g].T * (BM * cg) * BN * sizeof(float), st, &pr[g].part);
+      p.ws = (float*)pr[g].part;
+    }
+    // fused column sums (bias gradient of the layer below): fp64 partials per
+    // 128-row block from the GEMM epilogue (whole tiles) and the tail stage
+    pr[g].cs_rows = (p.M + BM - 1) / BM;
+    if (!rc && pr[g].colsum_out) {
+      rc = b2_alloc((size_t)pr[g].cs_rows * p.N * sizeof(double), st, &pr[g].cs_part);
+      p.colsum = (double*)pr[g].cs_part;
+    }
+  }
+  if (!rc) {
+    auto run = [&]() -> int {
+#define B2_TC(MD)                                                        \
+  if (mode == MD) return cg == 2 ? launch_tc<MD, 2>(pr, n, G, st) : launch_tc<MD, 1>(pr, n, G, st);
+      B2_TC(1) B2_TC(2) B2_TC(3) B2_TC(4) B2_TC(5)
+#undef B2_TC
+      return fail("gemm_tc: unknown mode");
+    };
+    rc = run();
+  }
+  for (int g = 0; g < n; ++g) {
+    const TcParams& p = pr[g].p;
+    if (!rc && pr[g].S > 1) {
+      dim3 grid2((unsigned)pr[g].T, cg, BN / 32);
+#define B2_SKE(E) k_tail_epilogue<E><<<grid2, dim3(32, 16), 0, st>>>(p)
+      if (!p.s_hi) B2_SKE(0);
+      else if (mode == 4) B2_SKE(4);
+      else if (mode == 5) B2_SKE(5);
+      else B2_SKE(2);
+#undef B2_SKE
+      rc = launched("b2_gemm(tcgen05 tail K-slice epilogue)");
+    }
+    if (pr[g].part) b2_free(pr[g].part, st);
+    if (!rc && pr[g].cs_part) {
+      k_colsum_final<<<(unsigned)((p.N + 31) / 32), 256, 0, st>>>(
+          pr[g].colsum_out, (const double*)pr[g].cs_part, pr[g].cs_rows, p.N);
+      rc = launched("b2_gemm(tcgen05 column sums)");
+    }
+    if (pr[g].cs_part) b2_free(pr[g].cs_part, st);
+  }
+  return rc;
+}
+
 // mode 1: a0/b0 raw; mode 3: a0/b0 = hi arrays, a1/b1 = lo arrays (contiguous);
 // mode 2: a0/b0 raw fp32 (lda/ldb), a1/b1 = bf16 hi, a2/b2 = bf16 lo (contiguous);
 // mode 4: a0/b0 = bf16 casts; mode 5: a0/b0 = bf16 hi, a1/b1 = bf16 lo (contiguous)
@@ -1381,140 +1755,9 @@ int gemm_tc(int ta, int tb, int mode, int64_t M, int64_t N, int64_t K, const voi
             const void* b2_, int64_t ldb, float* C, int64_t ldc, const float* bias, int epi,
             cudaStream_t st, const float* mask, void* s_hi, void* s_lo, float* colsum_out,
             const uint64_t* mask_bits, uint64_t* bits_out) {
-  B2_TRY(get_encode());
-  TcParams p;
-  p.C = C;
-  p.bias = bias;
-  p.ldc = ldc;
-  p.M = (int)M;
-  p.N = (int)N;
-  p.K = (int)K;
-  p.epi = epi;
-  p.tiles_n = p.num_tiles = p.tiles_m = 0;
-  p.mask = mask;
-  p.colsum = nullptr;
-  p.mask_bits = mask_bits;
-  p.bits_out = bits_out;
-  p.bits_ld = (int)((N + 63) / 64);
-  if (((uintptr_t)mask_bits & 7) || ((uintptr_t)bits_out & 7))
-    return fail("gemm_tc: bit masks need 8-B aligned word arrays");
-  p.s_hi = (__nv_bfloat16*)s_hi;
-  p.s_lo = (__nv_bfloat16*)s_lo;
-  if ((s_hi == nullptr) != (s_lo == nullptr) && mode != 4)
-    return fail("gemm_tc: split outputs come in pairs");
-  if (((uintptr_t)s_hi & 15) || ((uintptr_t)s_lo & 15) || ((uintptr_t)C & 3))
-    return fail("gemm_tc: C must be 4-B and the emitted split arrays 16-B aligned");
-  if (mode == 4) p.s_lo = nullptr;  // BF16 mode emits a single bf16 cast
-  Operands o{{a0, a1, a2}, {b0, b1, b2_}, lda, ldb};
-  const bool a_mn = ta != 0, b_mn = tb == 0;
-  const int sms = sm_count();
-  // CTA pairs once there are enough 256-row tiles to fill the chip
-  int cg = cg_mode();
-  if (cg != 1 && cg != 2) {
-    int64_t pair_tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
-    cg = pair_tiles >= sms / 2 ? 2 : 1;
-    // few tiles over a long K (the dW GEMMs of config 4: 1024^2 over K = 32768)
-    // run as K slices for many k-blocks per unit: there a pair's per-SM operand
-    // ingress (64 KB per k-block instead of 96 KB) is the limit, not the tile
-    // count (measured: 174 -> 158 us; short-K few-tile GEMMs stay single-CTA)
-    if (cg == 1 && K >= 8192 && M >= 2 * BM) cg = 2;
-  }
-  // Work units (TcParams): whole waves of whole tiles, then the tail tiles
-  // split into S K slices so the last wave fills the chip. Taken where it
-  // pays for the partials' round trip and the second stage (measured,
-  // scripts/tail_probe.py): few-tile long-K GEMMs (every tile split: dW
-  // [1024 x 1024] over K = 32768, square n = 1024) and a short run of waves
-  // whose last wave is at most half full (dW [4096 x 4096] over K = 65536:
-  // 3 waves + 34 of 74 tiles). Slices >= 256 of K, S <= 16. Deterministic:
-  // the partition depends only on the shape and the SM count, partials are
-  // summed in slice order.
-  const int bk = (mode == 4 || mode == 5) ? 64 : BK;  // Cfg::BKM
-  const int nkb = (int)((K + bk - 1) / bk);
-  const int64_t tiles = ((M + (int64_t)BM * cg - 1) / ((int64_t)BM * cg)) * ((N + BN - 1) / BN);
-  const int64_t P = sms / cg;
-  int64_t full = tiles, T = 0;
-  int S = 1;
-  if (nkb >= 16 && splitk_enabled()) {
-    if (tiles * cg <= sms / 2) {
-      full = 0;
-      T = tiles;
-    } else if (tiles >= P && tiles < 8 * P && 2 * (tiles % P) <= P) {
-      full = (tiles / P) * P;
-      T = tiles - full;
-    }
-    if (T > 0) S = (int)std::max<int64_t>(1, std::min<int64_t>({P / T, (int64_t)nkb * bk / 256, 16}));
-    if (S == 1) full = tiles;
-  }
-  {
-    static int h = -1;
-    if (h < 0) {
-      const char* e = getenv("B2_GEMM_L2HINT");
-      h = !(e && e[0] == '0');
-    }
-    p.l2hint = h;
-  }
-  p.full_tiles = (int)full;
-  p.splits = S;
-  p.kbps = nkb;
-  p.ws = nullptr;
-  void* part = nullptr;
-  if (S > 1) {
-    p.kbps = (nkb + S - 1) / S;
-    S = p.splits = (nkb + p.kbps - 1) / p.kbps;
-    B2_TRY(b2_alloc((size_t)S * T * (BM * cg) * BN * sizeof(float), st, &part));
-    p.ws = (float*)part;
-  }
-  auto run = [&]() -> int {
-#define B2_TC(AMN, BMN)                                                             \
-  if (a_mn == AMN && b_mn == BMN) {                                                 \
-    if (cg == 2) {                                                                  \
-      if (mode == 3) return launch_tc<AMN, BMN, 3, 2>(o, p, st);                    \
-      if (mode == 4) return launch_tc<AMN, BMN, 4, 2>(o, p, st);                    \
-      if (mode == 5) return launch_tc<AMN, BMN, 5, 2>(o, p, st);                    \
-      if (mode == 2) return launch_tc<AMN, BMN, 2, 2>(o, p, st);                    \
-      return launch_tc<AMN, BMN, 1, 2>(o, p, st);                                   \
-    }                                                                               \
-    if (mode == 3) return launch_tc<AMN, BMN, 3, 1>(o, p, st);                      \
-    if (mode == 4) return launch_tc<AMN, BMN, 4, 1>(o, p, st);                      \
-    if (mode == 5) return launch_tc<AMN, BMN, 5, 1>(o, p, st);                      \
-    if (mode == 2) return launch_tc<AMN, BMN, 2, 1>(o, p, st);                      \
-    return launch_tc<AMN, BMN, 1, 1>(o, p, st);                                     \
-  }
-    B2_TC(false, false)
-    B2_TC(false, true)
-    B2_TC(true, false)
-    B2_TC(true, true)
-#undef B2_TC
-    return fail("gemm_tc: unreachable");
-  };
-  // fused column sums (bias gradient of the layer below): fp64 partials per
-  // 128-row block from the GEMM epilogue (whole tiles) and the tail stage
-  void* cs_part = nullptr;
-  const int cs_rows = (int)((M + BM - 1) / BM);
-  if (colsum_out) {
-    B2_TRY(b2_alloc((size_t)cs_rows * N * sizeof(double), st, &cs_part));
-    p.colsum = (double*)cs_part;
-  }
-  int rc = run();
-  if (!rc && S > 1) {
-    const int tail = (int)T;
-    dim3 grid2(tail, cg, BN / 32);
-#define B2_SKE(E) k_tail_epilogue<E><<<grid2, dim3(32, 16), 0, st>>>(p)
-    if (!p.s_hi) B2_SKE(0);
-    else if (mode == 4) B2_SKE(4);
-    else if (mode == 5) B2_SKE(5);
-    else B2_SKE(2);
-#undef B2_SKE
-    rc = launched("b2_gemm(tcgen05 tail K-slice epilogue)");
-  }
-  if (part) b2_free(part, st);
-  if (!rc && cs_part) {
-    k_colsum_final<<<(unsigned)((N + 31) / 32), 256, 0, st>>>(colsum_out, (const double*)cs_part,
-                                                               cs_rows, (int)N);
-    rc = launched("b2_gemm(tcgen05 column sums)");
-  }
-  if (cs_part) b2_free(cs_part, st);
-  return rc;
+  TcDesc d{ta, tb, M, N, K, a0, a1, a2, lda, b0, b1, b2_, ldb, C, ldc, bias, epi,
+           mask, s_hi, s_lo, colsum_out, mask_bits, bits_out};
+  return gemm_tc_group(mode, &d, 1, st);
 }
 
 }  // namespace b2

@@ -112,8 +112,8 @@ unsigned* tickets(cudaStream_t st) {
   auto it = blocks.find(st);
   if (it != blocks.end()) return it->second;
   unsigned* p = nullptr;
-  if (cudaMalloc(&p, kTickets * sizeof(unsigned)) != cudaSuccess) return nullptr;
-  if (cudaMemset(p, 0, kTickets * sizeof(unsigned)) != cudaSuccess) return nullptr;
+  if (cudaMalloc(&p, kTicketsAlloc * sizeof(unsigned)) != cudaSuccess) return nullptr;
+  if (cudaMemset(p, 0, kTicketsAlloc * sizeof(unsigned)) != cudaSuccess) return nullptr;
   blocks[st] = p;
   return p;
 }
@@ -121,6 +121,14 @@ unsigned* tickets(cudaStream_t st) {
 int sm_count() {
   if (!g_sms) ensure_init();
   return g_sms ? g_sms : 148;
+}
+
+static std::atomic<int> g_gemm_reserve{0};
+
+int gemm_sms() {
+  const int n = sm_count();
+  const int r = g_gemm_reserve.load(std::memory_order_relaxed);
+  return n - r >= 2 ? n - r : 2;
 }
 
 // ------------------------------------------------------------ allocator
@@ -228,6 +236,21 @@ int b2_init(int device) {
   g_device = device;
   g_main_thread = std::this_thread::get_id();
   if (!tickets(g_stream)) return fail("b2_init: could not allocate reduction counters");
+  return 0;
+}
+
+// Persistent GEMM grids leave `n` SMs free (0..sm_count-2): under data
+// parallelism NCCL's collective kernels then run beside the backward GEMMs
+// instead of waiting for a GEMM boundary (dist.Communicator sets it).
+int b2_gemm_set_sm_reserve(int n) {
+  B2_TRY(b2::ensure_init());
+  if (n < 0 || n > b2::sm_count() - 2) return b2::fail("b2_gemm_set_sm_reserve: 0 <= n <= SMs - 2");
+  b2::g_gemm_reserve.store(n, std::memory_order_relaxed);
+  return 0;
+}
+
+int b2_gemm_get_sm_reserve(int* n) {
+  *n = b2::g_gemm_reserve.load(std::memory_order_relaxed);
   return 0;
 }
 

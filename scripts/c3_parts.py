@@ -44,4 +44,12 @@ with P.no_grad():
     t("gemm NN (presplit)", lambda: C._gemm_into(out, A, P.transpose2d(B)), flops=2 * n ** 3)
     t("gemm NT (presplit)", lambda: C._gemm_into(out, dC, B), flops=2 * n ** 3)
     t("gemm TN (presplit)", lambda: C._gemm_into(out, P.transpose2d(A), P.transpose2d(dC)), flops=2 * n ** 3)
+    out2 = P.zeros((n, n))
+
+    def grouped():
+        with C.gemm_group():
+            C._gemm_into(out, dC, B)
+            C._gemm_into(out2, P.transpose2d(A), P.transpose2d(dC))
+
+    t("gemm NT + TN grouped (presplit)", grouped, flops=4 * n ** 3)
 print("ok")

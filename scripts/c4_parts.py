@@ -60,4 +60,28 @@ with P.no_grad():
     t("gemm NN dX = gz.W (presplit)", lambda: C._gemm_into(out, Z, P.transpose2d(W)), flops=2 * R * K * K)
     t("gemm TN dW = X^T.gz", lambda: C._gemm_into(P.zeros((K, K)), P.transpose2d(X), P.transpose2d(Z)),
       flops=2 * R * K * K)
+    dWo = P.zeros((K, K))
+
+    def grp():
+        with C.gemm_group():
+            C._gemm_into(out, Z, P.transpose2d(W))
+            C._gemm_into(dWo, P.transpose2d(X), P.transpose2d(Z))
+
+    t("gemm dX + dW grouped", grp, flops=4 * R * K * K)
+P.set_gemm_algo(None)
+# the whole fused config-4 step as bench.py times it (nn.Linear + fused loss)
+Xg = P.from_numpy(rng.standard_normal((R, K), dtype=np.float32), requires_grad=True)
+Wg = P.from_numpy(rng.normal(0, 0.03, (K, K)).astype(np.float32), requires_grad=True)
+bg = P.zeros((K,), requires_grad=True)
+
+
+def step():
+    P.reset_tape()
+    Xg.buffer.version += 1
+    Wg.buffer.version += 1
+    z = P.linear(Xg, P.transpose2d(Wg), bg)
+    P.backward(P.softmax_mul_mean(z, T))
+
+
+t("config-4 fused step", step, n=5, flops=6 * R * K * K)
 print("ok")
