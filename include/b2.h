@@ -33,6 +33,8 @@ int b2_device_count(int* n);
 int b2_device_info(int* sm_count, int* cc_major, int* cc_minor, size_t* total_mem);
 int b2_default_stream(void** stream);
 int b2_stream_create(void** stream);
+/* the same at the device's greatest stream priority (collectives beside the GEMMs) */
+int b2_stream_create_priority(void** stream);
 int b2_stream_destroy(void* stream);
 int b2_stream_sync(void* stream);
 int b2_device_sync(void);

@@ -45,6 +45,7 @@ _SIGS = {
     "b2_device_info": (c_int, [POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_size_t)]),
     "b2_default_stream": (c_int, [POINTER(c_void_p)]),
     "b2_stream_create": (c_int, [POINTER(c_void_p)]),
+    "b2_stream_create_priority": (c_int, [c_void_p]),
     "b2_stream_destroy": (c_int, [c_void_p]),
     "b2_stream_sync": (c_int, [c_void_p]),
     "b2_device_sync": (c_int, []),

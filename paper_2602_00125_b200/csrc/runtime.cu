@@ -286,6 +286,18 @@ int b2_stream_create(void** s) {
   *s = (void*)st;
   return 0;
 }
+// A non-blocking stream at the device's greatest priority: the block
+// scheduler hands freed SMs to its kernels first (the data-parallel
+// collectives and optimizer updates that overlap the backward GEMMs).
+int b2_stream_create_priority(void** s) {
+  B2_TRY(ensure_init());
+  int least = 0, greatest = 0;
+  B2_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  cudaStream_t st;
+  B2_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, greatest));
+  *s = (void*)st;
+  return 0;
+}
 int b2_stream_destroy(void* s) {
   B2_CUDA(cudaStreamDestroy((cudaStream_t)s));
   return 0;

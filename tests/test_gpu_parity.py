@@ -1199,6 +1199,57 @@ def test_optimizer_overlapped_in_backward_matches_plain_step(force_nccl, shard):
         assert bits_equal(a, b)
 
 
+def test_comm_sm_reserve_only_while_collectives_overlap(monkeypatch):
+    """With B2_COMM_SMS (default 8 for world > 1) the backward GEMMs queued
+    after the first leaf-ready hook leave that many SMs to the collectives and
+    the optimizer; finish() gives them back. Parameters stay within 1e-5 of
+    the plain step (a smaller persistent grid may split K differently)."""
+    import ctypes
+
+    from paper_2602_00125_b200 import dist
+    from paper_2602_00125_b200.data import build_mlp, mlp_config5
+
+    monkeypatch.setenv("B2_COMM_SMS", "8")
+    comm = dist.Communicator(dist.Env(), force_nccl=True)
+    assert comm.sm_reserve == 8
+
+    def reserve():
+        v = ctypes.c_int(-1)
+        L.check(L.lib().b2_gemm_get_sm_reserve(ctypes.byref(v)))
+        return v.value
+
+    params0 = mlp_config5(0, width=512, classes=10, depth=3)
+    x = dev(np.random.default_rng(5).standard_normal((2048, 512)))
+    lab = nn.labels_buffer(np.arange(2048) % 10)
+    seen = []
+
+    def run(overlap):
+        model = build_mlp([(w.copy(), b.copy()) for w, b in params0])
+        ps = model.parameters()
+        opt = optim.SGD(lr=0.1)  # (Adam's first step is lr * sign(g): rounding-sensitive near g = 0)
+        P.reset_tape()
+        loss = nn.cross_entropy(model(x), lab, denom=2048)
+        if overlap:
+            red = dist.GradReducer(comm, ps, optimizer=opt)
+
+            def hook(nid, g):
+                r = red.hook(nid, g)
+                seen.append(reserve())
+                return r
+
+            store = P.backward(loss, on_leaf_ready=hook)
+            red.finish()
+            red.step_rest(store)
+        else:
+            optim.step_all(opt, ps, P.backward(loss))
+        return [host(p) for p in ps]
+
+    got, want = run(True), run(False)
+    assert seen and all(v == 8 for v in seen) and reserve() == 0
+    for a, b in zip(got, want):
+        assert normwise(a, b) <= 1e-5
+
+
 # ---------------------------------------------------------------- fused config-4 loss
 
 
