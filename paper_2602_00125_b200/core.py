@@ -21,7 +21,6 @@ dot products.
 
 from __future__ import annotations
 
-import contextlib
 import ctypes
 import math
 import os
@@ -1067,35 +1066,42 @@ _GROUP = _GroupState()
 _GROUP_ON = os.environ.get("B2_GEMM_GROUP", "1") != "0"  # 0: one launch per GEMM (A/B)
 
 
-@contextlib.contextmanager
-def gemm_group():
+class gemm_group:
     """Defer the fused tensor-core GEMMs issued inside the block and launch
     them together (b2_gemm_fused_group, up to 3 per launch) when it exits --
     for the pullbacks of one node (x_bar and w_bar of a matmul/linear read the
     same cotangent and write independent outputs). Nothing inside the block
     may read a deferred GEMM's output. Values are bit-identical to separate
     launches. Nested blocks join the outermost one."""
-    if _GROUP.pending is not None or not _GROUP_ON:
-        yield
-        return
-    _GROUP.pending = items = []
-    try:
-        yield
-    except BaseException:
-        _GROUP.pending = None
-        raise
-    _GROUP.pending = None
-    for i in range(0, len(items), 3):
-        part = items[i:i + 3]
-        ev = _timer_start()
-        if len(part) == 1:
-            L.call("b2_gemm_fused", ctypes.byref(part[0][0]), None)
+
+    __slots__ = ("items",)
+
+    def __enter__(self):
+        if _GROUP.pending is not None or not _GROUP_ON:
+            self.items = None
         else:
-            arr = (L.GemmDesc * len(part))(*[it[0] for it in part])
-            L.call("b2_gemm_fused_group", arr, len(part), None)
-        _timer_end(ev, _py_sum(it[2] for it in part), tuple(it[4] for it in part))
-        for it in part:
-            it[1]()
+            self.items = _GROUP.pending = []
+        return self
+
+    def __exit__(self, et, ev_, tb):
+        items = self.items
+        if items is None:
+            return False
+        _GROUP.pending = None
+        if et is not None:
+            return False
+        for i in range(0, len(items), 3):
+            part = items[i:i + 3]
+            ev = _timer_start()
+            if len(part) == 1:
+                L.call("b2_gemm_fused", ctypes.byref(part[0][0]), None)
+            else:
+                arr = (L.GemmDesc * len(part))(*[it[0] for it in part])
+                L.call("b2_gemm_fused_group", arr, len(part), None)
+            _timer_end(ev, _py_sum(it[2] for it in part), tuple(it[4] for it in part))
+            for it in part:
+                it[1]()
+        return False
 
 
 _autograd.PULL_GROUP = gemm_group
