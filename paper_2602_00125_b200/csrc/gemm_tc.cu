@@ -300,6 +300,9 @@ struct TcGroup {
   int kc;         // k-blocks per fp32 promotion chunk
   int l2hint;     // B operand loads with L2 evict_last (B2_GEMM_L2HINT=0 disables)
   int stage_out;  // every CTA runs at most one unit: fp32 tile stores go through shared memory
+  int csplit;     // > 1: cluster split-K -- the S CTAs of a cluster compute the S K slices of one
+                  // tile and fold them through distributed shared memory (no partials, no second
+                  // kernel); every CTA runs exactly one unit
 };
 struct TcMaps {
   CUtensorMap m[kMaxProb][6];  // per problem: MODE 1 {A, B}; 3/5 {A, B, Alo, Blo}; 2 {A, B, Ah, Bh, Al, Bl}; 4 {A, B}
@@ -571,6 +574,149 @@ __device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t s0, uint32_
   }
 }
 
+__device__ __forceinline__ float ld_dsmem_f32(uint32_t cluster_addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_dsmem_f64(uint32_t cluster_addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(cluster_addr) : "memory");
+  return v;
+}
+
+// Cluster split-K (TcGroup::csplit = S): every CTA of the cluster staged its
+// K slice's fp32 partial tile (rows padded to kStageLd) at the start of its
+// shared memory; CTA `krank` finishes rows [krank*128/S, +128/S) of the tile:
+// the S partials added in slice order (as k_tail_epilogue adds them), then
+// k_tail_epilogue's epilogue stages, with its 8-row groups and fixed-order
+// fp64 column sums -- the fold of the 16 group sums per column is done by
+// krank 0 (csplit_colsum) -- so outputs are bit-identical to the partials +
+// second-stage path. Epilogue warps only (512 threads; ew = warp - 4).
+template <int EMIT, int S>
+__device__ __forceinline__ void csplit_reduce(const TcParams& p, uint8_t* smem, int tm, int tn,
+                                              int krank, int ew, int lane) {
+  constexpr int RPG = 8;  // rows per group (k_tail_epilogue: BM / 16)
+  const int R = BM / S, ngroups = R / RPG;
+  const int r0 = krank * R;
+  const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN;
+  uint32_t base[S];
+#pragma unroll
+  for (int s2 = 0; s2 < S; ++s2) base[s2] = mapa(smem_u32(smem), (uint32_t)s2);
+  double* gsum = reinterpret_cast<double*>(smem + BM * kStageLd * 4);  // [16 groups][BN]
+  uint32_t* bits32 = reinterpret_cast<uint32_t*>(p.bits_out);
+  const uint32_t* mbits32 = reinterpret_cast<const uint32_t*>(p.mask_bits);
+  // a lane owns 4 consecutive columns (16-B distributed shared memory loads:
+  // the cluster network is request-bound, 4-B loads ran at ~14 GB/s per SM);
+  // a warp covers a 128-column strip of one 8-row group
+  constexpr int STRIPS = BN / 128;
+  for (int it = ew; it < ngroups * STRIPS; it += 16) {
+    const int grp = it / STRIPS, strip = it % STRIPS;
+    const int c = strip * 128 + lane * 4;
+    const int64_t n = n0 + c;
+    bool cok[4];
+    float bias[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      cok[k] = n + k < p.N;
+      bias[k] = (cok[k] && (p.epi == B2_EPI_BIAS || p.epi == B2_EPI_BIAS_RELU)) ? p.bias[n + k] : 0.0f;
+    }
+    const bool vec = cok[3] && (p.ldc % 4) == 0 && ((((uintptr_t)p.C) + 4 * (n + m0 * p.ldc)) & 15) == 0;
+    double cs[4] = {0.0, 0.0, 0.0, 0.0};
+    const int rbase = r0 + grp * RPG;
+#pragma unroll 2
+    for (int q = 0; q < RPG; ++q) {
+      const int64_t m = m0 + rbase + q;
+      if (m >= p.M) break;
+      float4 v[S];  // the row's S partials in flight, added in slice order
+#pragma unroll
+      for (int s2 = 0; s2 < S; ++s2) {
+        const uint32_t a = base[s2] + (uint32_t)((rbase + q) * kStageLd + c) * 4u;
+        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v[s2].x), "=f"(v[s2].y), "=f"(v[s2].z), "=f"(v[s2].w)
+                     : "r"(a)
+                     : "memory");
+      }
+      float x[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int s2 = 0; s2 < S; ++s2) {
+        x[0] = __fadd_rn(x[0], v[s2].x);
+        x[1] = __fadd_rn(x[1], v[s2].y);
+        x[2] = __fadd_rn(x[2], v[s2].z);
+        x[3] = __fadd_rn(x[3], v[s2].w);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (p.epi == B2_EPI_BIAS || p.epi == B2_EPI_BIAS_RELU) x[k] = __fadd_rn(x[k], bias[k]);
+        if (p.epi == B2_EPI_BIAS_RELU || p.epi == B2_EPI_RELU) x[k] = x[k] > 0.0f ? x[k] : 0.0f;
+      }
+      if (bits32) {  // 8 lanes x 4 columns = one 32-bit word of y > 0
+        uint32_t nib = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nib |= (cok[k] && x[k] > 0.0f ? 1u : 0u) << k;
+        uint32_t word = nib << (4 * (lane & 7));
+        word |= __shfl_xor_sync(0xffffffffu, word, 1);
+        word |= __shfl_xor_sync(0xffffffffu, word, 2);
+        word |= __shfl_xor_sync(0xffffffffu, word, 4);
+        const int64_t wn = (n0 + strip * 128 + (lane & ~7) * 4) >> 5;
+        if ((lane & 7) == 0 && wn < 2 * (int64_t)p.bits_ld) bits32[m * 2 * p.bits_ld + wn] = word;
+      }
+      if (mbits32) {
+        const uint32_t w = mbits32[m * 2 * p.bits_ld + (n >> 5)];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = __fmul_rn(x[k], (w >> ((n + k) & 31)) & 1 ? 1.0f : 0.0f);
+      } else if (p.mask) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (cok[k]) x[k] = __fmul_rn(x[k], p.mask[m * p.ldc + n + k] > 0.0f ? 1.0f : 0.0f);
+      }
+      if (p.C) {
+        if (vec) {
+          *reinterpret_cast<float4*>(p.C + m * p.ldc + n) = make_float4(x[0], x[1], x[2], x[3]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (cok[k]) p.C[m * p.ldc + n + k] = x[k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (!cok[k]) continue;
+        if (EMIT == 4 && p.s_hi) p.s_hi[m * p.N + n + k] = __float2bfloat16_rn(x[k]);
+        if ((EMIT == 2 || EMIT == 5) && p.s_hi)
+          split_pair<EMIT>(x[k], p.s_hi[m * p.N + n + k], p.s_lo[m * p.N + n + k]);
+        cs[k] += (double)x[k];
+      }
+    }
+    if (p.colsum) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) gsum[(krank * ngroups + grp) * BN + c + k] = cs[k];
+    }
+  }
+}
+
+// krank 0 of a cluster split-K tile: the tile's 128-row block column sums,
+// the 16 group sums folded in group order across the cluster's CTAs.
+__device__ __forceinline__ void csplit_colsum(const TcParams& p, uint8_t* smem, int tm, int tn, int S,
+                                              int tid) {
+  const int ngroups = BM / S / 8;
+  const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN;
+  if (m0 >= p.M) return;
+  const uint32_t goff = (uint32_t)(BM * kStageLd * 4);
+  for (int c = tid; c < BN; c += 512) {
+    const int64_t n = n0 + c;
+    if (n >= p.N) continue;
+    double v[16];  // all 16 group sums in flight, folded in group order
+#pragma unroll
+    for (int g = 0; g < 16; ++g)
+      v[g] = ld_dsmem_f64(mapa(smem_u32(smem) + goff, (uint32_t)(g / ngroups)) + (uint32_t)((g * BN + c) * 8));
+    double t = v[0];
+#pragma unroll
+    for (int g = 1; g < 16; ++g) t += v[g];
+    p.colsum[(m0 / BM) * p.N + n] = t;
+  }
+}
+
 // problem of unit u (MULTI = false: a single-problem launch, problem 0 with
 // every parameter at a static offset)
 template <bool MULTI>
@@ -579,6 +725,21 @@ __device__ __forceinline__ int prob_of(const TcGroup& G, int u) {
   int g = 0;
   while (g + 1 < G.nprob && u >= G.ustart[g + 1]) ++g;
   return g;
+}
+
+// cluster split-K: the unit of CTA b -- cluster b / S takes the cluster-th
+// tile of the launch (problems back to back), its CTA of rank r the r-th K
+// slice (units of a split problem are numbered slice-major)
+__device__ __forceinline__ int csplit_unit(const TcGroup& G, int b) {
+  const int S = G.csplit;
+  int c = b / S;
+  const int r = b - c * S;
+  for (int g = 0; g < G.nprob; ++g) {
+    const int tiles = G.p[g].tiles_m * G.p[g].tiles_n;
+    if (c < tiles) return G.ustart[g] + r * tiles + c;
+    c -= tiles;
+  }
+  return G.num_units;
 }
 
 template <int MODE, int CG, bool MULTI>
@@ -662,6 +823,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     return *(volatile int*)&uring[slot];
   };
 
+  int cs_unit = -1;  // cluster split-K: this CTA's unit (epilogue warps)
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
@@ -715,6 +877,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // draw units (static raster or the atomic counter) and publish them
         // one ahead of the loads, to this CTA's ring and the peer's
         auto next_unit = [&](int i) -> int {
+          if (G.csplit > 1) return i == 0 ? csplit_unit(G, (int)blockIdx.x) : num_units;
           return G.sched ? (int)atomicAdd(G.sched, 1u) : cl_id + i * cl_num;
         };
         auto publish = [&](int i, int u) {
@@ -860,6 +1023,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           else
             mbar_arrive_remote(mapa(smem_u32(&tempty[cb]), 0));  // the leader's barrier
         }
+      }
+      if (ks >= 0 && G.csplit > 1) {  // cluster split-K: the partial stays in shared memory
+        float* mine = reinterpret_cast<float*>(smem) + row * kStageLd + cg * 64;
+#pragma unroll
+        for (int j = 0; j < 64; j += 4)
+          *reinterpret_cast<float4*>(mine + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        cs_unit = u;
+        continue;
       }
       if (ks >= 0) {  // a K slice of a tail tile: raw partial sums, tile-local
         float* w0 = p.ws + ((int64_t)ks * (BM * CG) + (int)rank * BM) * BN;
@@ -1036,6 +1207,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 4 * 32) B2_TRACE(5);  // this epilogue warp's stores issued
   __syncthreads();
   if (threadIdx.x == 0) B2_TRACE(6);  // every warp done
+  if (CG == 1 && G.csplit > 1) {
+    // every CTA of the cluster has staged its K slice: fold, finish, store
+    const int S = G.csplit;
+    const int krank = (int)cluster_rank();
+    cluster_sync();
+    if (threadIdx.x == 4 * 32) B2_TRACE(5);  // (trace builds: cluster split-K -- all partials staged)
+    int gi = 0, tm = 0, tn = 0;
+    if (warp >= 4 && cs_unit >= 0) {
+      gi = prob_of<MULTI>(G, cs_unit);
+      int kb0, kb1, ks;
+      tile_info(G.p[gi], cs_unit - G.ustart[gi], tm, tn, kb0, kb1, ks);
+      const TcParams& p = G.p[gi];
+      constexpr int EM = MODE == 4 ? 4 : (MODE == 5 ? 5 : 2);
+#define B2_CSR(SS)                                                                        \
+  if (S == SS) {                                                                          \
+    if (!p.s_hi) csplit_reduce<0, SS>(p, smem, tm, tn, krank, warp - 4, lane);           \
+    else csplit_reduce<EM, SS>(p, smem, tm, tn, krank, warp - 4, lane);                  \
+  }
+      B2_CSR(2) B2_CSR(4) B2_CSR(8)
+#undef B2_CSR
+    }
+    if (threadIdx.x == 4 * 32) B2_TRACE(6);  // (trace builds: this CTA's rows folded and stored)
+    cluster_sync();  // the group column sums are visible
+    if (warp >= 4 && cs_unit >= 0 && krank == 0 && G.p[gi].colsum)
+      csplit_colsum(G.p[gi], smem, tm, tn, S, threadIdx.x - 128);
+    cluster_sync();  // no CTA leaves while a peer reads its shared memory
+  }
   if (CG == 2) cluster_sync();  // the peer may still be reading our smem / arriving on us
   if (warp == 2) {
     tc_fence_after();
@@ -1408,7 +1606,10 @@ int launch_tc(Prob* pr, int n, TcGroup& G, cudaStream_t st) {
   // several problems with more units than CTA (pairs): units are drawn from
   // the stream's zeroed scheduler counters (dynamic balance); else the raster
   G.sched = nullptr;
-  if (n > 1 && G.num_units > grid / CG) {
+  if (G.csplit > 1) {
+    if (CG != 1 || grid != G.num_units || grid % G.csplit) return b2::fail("gemm_tc: bad cluster split-K launch");
+    G.stage_out = 0;
+  } else if (n > 1 && G.num_units > grid / CG) {
     unsigned* tk = b2::tickets(st);
     if (!tk) return b2::fail("gemm_tc: no scheduler counters for this stream");
     G.sched = tk + b2::kGemmTicket;
@@ -1419,8 +1620,10 @@ int launch_tc(Prob* pr, int n, TcGroup& G, cudaStream_t st) {
   cfg.dynamicSmemBytes = CF::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
+  static_assert(CG == 2 || CF::STAGES * CF::STAGE_BYTES >= BM * kStageLd * 4 + 16 * BN * 8,
+                "cluster split-K stages the partial tile and the group column sums in the stage buffers");
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = (CG == 1 && G.csplit > 1) ? G.csplit : CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1529,6 +1732,15 @@ static int splitk_enabled() {
   static int v = -1;  // B2_GEMM_SPLITK=0 disables split-K (A/B measurements)
   if (v < 0) {
     const char* e = getenv("B2_GEMM_SPLITK");
+    v = !(e && e[0] == '0');
+  }
+  return v;
+}
+
+static int csplit_enabled() {
+  static int v = -1;  // B2_GEMM_CSPLIT=0: K slices through L2 partials + k_tail_epilogue (A/B)
+  if (v < 0) {
+    const char* e = getenv("B2_GEMM_CSPLIT");
     v = !(e && e[0] == '0');
   }
   return v;
@@ -1691,6 +1903,17 @@ int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st) {
   }
   G.ustart[n] = units;
   G.num_units = units;
+  // Cluster split-K: a launch whose every tile is split into the same S slices
+  // with one unit per CTA (the few-tile regime at cg 1: config 3 at n = 1024)
+  // folds the slices through distributed shared memory inside each cluster of
+  // S CTAs -- no fp32 partials through L2, no second-stage kernel.
+  G.csplit = 1;
+  if (cg == 1 && csplit_enabled() && units <= sms) {
+    const int S0 = pr[0].S;
+    bool ok = S0 == 2 || S0 == 4 || S0 == 8;
+    for (int g = 0; g < n && ok; ++g) ok = pr[g].S == S0 && pr[g].p.full_tiles == 0;
+    if (ok) G.csplit = S0;
+  }
   {
     static int h = -1;
     if (h < 0) {
@@ -1702,7 +1925,7 @@ int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st) {
   int rc = 0;
   for (int g = 0; g < n && !rc; ++g) {
     TcParams& p = pr[g].p;
-    if (pr[g].S > 1) {
+    if (pr[g].S > 1 && G.csplit == 1) {
       rc = b2_alloc((size_t)pr[g].S * pr[g].T * (BM * cg) * BN * sizeof(float), st, &pr[g].part);
       p.ws = (float*)pr[g].part;
     }
@@ -1726,7 +1949,7 @@ int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st) {
   }
   for (int g = 0; g < n; ++g) {
     const TcParams& p = pr[g].p;
-    if (!rc && pr[g].S > 1) {
+    if (!rc && pr[g].S > 1 && G.csplit == 1) {
       dim3 grid2((unsigned)pr[g].T, cg, BN / 32);
 #define B2_SKE(E) k_tail_epilogue<E><<<grid2, dim3(32, 16), 0, st>>>(p)
       if (!p.s_hi) B2_SKE(0);

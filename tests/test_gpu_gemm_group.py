@@ -221,3 +221,28 @@ def test_autograd_backward_grouped_equals_ungrouped(monkeypatch, shape):
             assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
         else:
             assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
+
+
+def test_cluster_split_k_bit_identical_to_l2_partials(tmp_path):
+    """Few-tile GEMMs whose K slices fold through distributed shared memory
+    inside a cluster (B2_GEMM_CSPLIT, default on) give the same bits -- C,
+    emitted split, relu bits, column sums -- as the K-slice partials through
+    L2 + k_tail_epilogue, for 2 / 4 / 8 slices, ragged edges and every
+    epilogue stage."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        f = tmp_path / f"cs{flag}.npz"
+        env = dict(os.environ, B2_GEMM_CSPLIT=flag, PYTHONPATH=root)
+        r = subprocess.run([sys.executable, os.path.join(root, "tests", "csplit_cases.py"), str(f)],
+                           env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    a, b = outs
+    assert set(a.files) == set(b.files)
+    for k in a.files:
+        assert np.array_equal(a[k], b[k]), k
