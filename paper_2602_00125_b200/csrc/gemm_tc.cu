@@ -1546,6 +1546,8 @@ struct Prob {
   int cs_rows;
 };
 
+constexpr int kCsplitNoFit = -77;  // launch_tc: the split-K clusters cannot all be resident
+
 static int group_n_env() {
   static int gn = -1;
   if (gn < 0) {
@@ -1609,10 +1611,6 @@ int launch_tc(Prob* pr, int n, TcGroup& G, cudaStream_t st) {
   if (G.csplit > 1) {
     if (CG != 1 || grid != G.num_units || grid % G.csplit) return b2::fail("gemm_tc: bad cluster split-K launch");
     G.stage_out = 0;
-  } else if (n > 1 && G.num_units > grid / CG) {
-    unsigned* tk = b2::tickets(st);
-    if (!tk) return b2::fail("gemm_tc: no scheduler counters for this stream");
-    G.sched = tk + b2::kGemmTicket;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1630,6 +1628,23 @@ int launch_tc(Prob* pr, int n, TcGroup& G, cudaStream_t st) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  if (G.csplit > 1) {
+    // every cluster must be resident at once (S CTAs of ~200 KB in one GPC):
+    // otherwise the K slices go through L2 partials instead (host fallback)
+    int fit = 0;
+    cudaLaunchConfig_t q = cfg;
+    q.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&fit, (void*)kern, &q) != cudaSuccess) {
+      cudaGetLastError();
+      fit = 0;
+    }
+    if (fit * G.csplit < G.num_units) return kCsplitNoFit;
+  }
+  if (n > 1 && G.num_units > grid / CG && G.csplit == 1) {
+    unsigned* tk = b2::tickets(st);
+    if (!tk) return b2::fail("gemm_tc: no scheduler counters for this stream");
+    G.sched = tk + b2::kGemmTicket;
+  }
   B2_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, G));
   return b2::launched(n > 1 ? "b2_gemm(tcgen05, grouped)" : "b2_gemm(tcgen05)");
 }
@@ -1937,6 +1952,16 @@ int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st) {
       p.colsum = (double*)pr[g].cs_part;
     }
   }
+  auto alloc_parts = [&]() -> int {  // K-slice partials (the L2 path)
+    for (int g = 0; g < n; ++g) {
+      TcParams& p = pr[g].p;
+      if (pr[g].S > 1 && G.csplit == 1 && !pr[g].part) {
+        B2_TRY(b2_alloc((size_t)pr[g].S * pr[g].T * (BM * cg) * BN * sizeof(float), st, &pr[g].part));
+        p.ws = (float*)pr[g].part;
+      }
+    }
+    return 0;
+  };
   if (!rc) {
     auto run = [&]() -> int {
 #define B2_TC(MD)                                                        \
@@ -1946,6 +1971,11 @@ int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st) {
       return fail("gemm_tc: unknown mode");
     };
     rc = run();
+    if (rc == kCsplitNoFit) {  // not every cluster fits at once: partials through L2
+      G.csplit = 1;
+      rc = alloc_parts();
+      if (!rc) rc = run();
+    }
   }
   for (int g = 0; g < n; ++g) {
     const TcParams& p = pr[g].p;
