@@ -146,6 +146,11 @@ __device__ __forceinline__ uint64_t l2_policy_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t l2_policy_normal() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
@@ -829,7 +834,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t pa = l2_policy_normal();
+      const uint64_t pa = G.l2hint == 2 ? l2_policy_first() : l2_policy_normal();
       const uint64_t pb = G.l2hint ? l2_policy_last() : pa;
       auto produce = [&](int u) {
         const int gi = prob_of<MULTI>(G, u);
@@ -1640,7 +1645,18 @@ int launch_tc(Prob* pr, int n, TcGroup& G, cudaStream_t st) {
     }
     if (fit * G.csplit < G.num_units) return kCsplitNoFit;
   }
-  if (n > 1 && G.num_units > grid / CG && G.csplit == 1) {
+  // Units are drawn dynamically whenever there are more than CTA (pairs):
+  // also for one problem, where the next clusters to finish take the next
+  // tiles of the raster, so the 8 consumers of an A panel stay in step and
+  // find it in L2 -- config-5 forward GEMM: DRAM reads 3.92 -> 3.35 GB and
+  // 4.22 -> 4.11 ms per launch (ncu) against the static raster, which lets
+  // the clusters drift apart over ~56 waves. B2_GEMM_DYNAMIC=0: static (A/B).
+  static int dyn = -1;
+  if (dyn < 0) {
+    const char* e = getenv("B2_GEMM_DYNAMIC");
+    dyn = !(e && e[0] == '0');
+  }
+  if ((n > 1 || dyn) && G.num_units > grid / CG && G.csplit == 1) {
     unsigned* tk = b2::tickets(st);
     if (!tk) return b2::fail("gemm_tc: no scheduler counters for this stream");
     G.sched = tk + b2::kGemmTicket;
@@ -1932,8 +1948,8 @@ int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st) {
   {
     static int h = -1;
     if (h < 0) {
-      const char* e = getenv("B2_GEMM_L2HINT");
-      h = !(e && e[0] == '0');
+      const char* e = getenv("B2_GEMM_L2HINT");  // 0: no hints; 2: also A evict_first (A/B)
+      h = !e ? 1 : atoi(e);
     }
     G.l2hint = h;
   }
