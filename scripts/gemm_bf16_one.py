@@ -6,6 +6,8 @@ import paper_2602_00125_b200 as P
 from paper_2602_00125_b200 import _lib as L, graph
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 M, N, K = n, n, n
+if len(sys.argv) > 2 and sys.argv[2].isdigit():
+    M = int(sys.argv[2])
 rng = np.random.default_rng(0)
 a = P.from_numpy(rng.uniform(-1, 1, (M, K)).astype(np.float32))
 b = P.from_numpy(rng.uniform(-1, 1, (N, K)).astype(np.float32))
@@ -28,7 +30,7 @@ if "--time" in sys.argv:
     g.replay()
     e1.record()
     us = e0.elapsed_ms(e1) / 20 * 1000
-    print(f"bf16 GEMM n={n}: {us:.1f} us  {2 * M * N * K / us * 1e-6:.0f} TF/s")
+    print(f"bf16 GEMM {M}x{N}x{K}: {us:.1f} us  {2 * M * N * K / us * 1e-6:.0f} TF/s")
 else:
     for _ in range(3):
         one()
