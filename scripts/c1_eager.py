@@ -36,3 +36,17 @@ for rep in range(3):
     L.synchronize()
     print(f"eager: {e0.elapsed_ms(e1) / 50 * 1000:.1f} us/step device span, "
           f"{(time.perf_counter() - t0) / 50 * 1e6:.1f} us/step host")
+
+from paper_2602_00125_b200 import graph  # noqa: E402
+
+g1 = graph.capture(step, warmup=1)
+g1.replay()
+L.synchronize()
+for rep in range(3):
+    e0, e1 = L.Event(), L.Event()
+    e0.record()
+    for _ in range(50):
+        g1.replay()
+    e1.record()
+    L.synchronize()
+    print(f"graph: {e0.elapsed_ms(e1) / 50 * 1000:.1f} us/step")

@@ -1,6 +1,6 @@
 # The round's measurement set at HEAD (run on the GPU box via gpurun). Outputs go to
 # gpurun_out/$TAG_*; summarise with scripts/summarize_launches.py / summarize_ncu.py into profiles/.
-TAG=${TAG:-r02b}
+TAG=${TAG:-r02c}
 O=gpurun_out
 NCU="ncu --clock-control none"
 # 1) the bench step's launch list (config 5, N=1)
