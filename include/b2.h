@@ -214,6 +214,10 @@ int b2_gemm_tf32x_ex(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
  * b2_gemm_tf32x_ex (C_hi16/C_lo16 receive C's own 3xBF16 split). */
 int b2_bf16x3_split(void* hi16, void* lo16, const float* x, int64_t rows, int64_t cols,
                     int64_t ld, void* stream);
+/* b2_bf16x3_split of two matrices in one launch (a GEMM's two fresh operands) */
+int b2_bf16x3_split2(void* hi_a, void* lo_a, const float* a, int64_t rows_a, int64_t cols_a,
+                     int64_t ld_a, void* hi_b, void* lo_b, const float* b, int64_t rows_b,
+                     int64_t cols_b, int64_t ld_b, void* stream);
 /* fp32 from a contiguous 3xBF16 split: out[i] = f32(hi[i]) + f32(lo[i]) (exact
  * in fp32; within 2^-16 relative of the split's source). n % 8 == 0, 16-B
  * aligned. Materialises a b2_gemm_fused output written with C == NULL (only

@@ -103,6 +103,8 @@ _SIGS = {
                                  c_void_p, c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
                                  c_void_p, c_void_p]),
     "b2_bf16x3_split": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
+    "b2_bf16x3_split2": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64,
+                                 c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     "b2_bf16x3_join": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "b2_gemm_3xbf16": (c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_int64, c_void_p, c_int, c_void_p, c_void_p,

@@ -884,6 +884,36 @@ def materialize_pending():
             _materialize(b)
 
 
+def _split_pair(xa, ashape, wb, bshape, kind):
+    """_split of a GEMM's two operands; when both are fresh 3xBF16 splits of
+    different regions, one launch makes both (b2_bf16x3_split2)."""
+    if kind == "3xbf16":
+        from .graph import _capturing
+
+        cap = _capturing[0]
+        ka = ("3xbf16", xa.offset) + tuple(ashape)
+        kb = ("3xbf16", wb.offset) + tuple(bshape)
+
+        def fresh(t, key):
+            ent = (t.buffer._splits or {}).get(key)
+            return not (ent is not None and ent[0] == t.buffer.version and (not cap or ent[3] == cap))
+
+        if fresh(xa, ka) and fresh(wb, kb) and not (xa.buffer is wb.buffer and ka == kb):
+            (ra, ca, lda), (rb, cb, ldb) = ashape, bshape
+            ahi, alo = Buffer(2 * ra * ca), Buffer(2 * ra * ca)
+            bhi, blo = Buffer(2 * rb * cb), Buffer(2 * rb * cb)
+            L.call("b2_bf16x3_split2", ahi.ptr, alo.ptr, xa.data_ptr, ra, ca, lda, bhi.ptr, blo.ptr,
+                   wb.data_ptr, rb, cb, ldb, None)
+            for t, key, hi, lo in ((xa, ka, ahi, alo), (wb, kb, bhi, blo)):
+                if t.buffer._splits is None:
+                    t.buffer._splits = {}
+                t.buffer._splits[key] = (t.buffer.version, hi, lo, cap)
+            return ahi, alo, bhi, blo
+    ahi, alo = _split(xa, *ashape, kind)
+    bhi, blo = _split(wb, *bshape, kind)
+    return ahi, alo, bhi, blo
+
+
 def _split(t, rows, cols, ld, kind):
     """Cached split of the stored matrix region of t for a tensor-core GEMM:
     kind "tf32x" -> (bf16 hi, bf16 lo) of trunc_tf32(x) / x - trunc (2 B each),
@@ -974,8 +1004,7 @@ def _gemm_into(out, x, w, bias=None, epi=L.EPI_NONE, mask=None, emit_split=False
              L.GEMM_BF16: ("bf16", L.GEMM_BF16)}.get(algo) if tc_ok else None
     if fused is not None:
         kind, dalgo = fused
-        ahi, alo = _split(xa, ar, ac, lda, kind)
-        bhi, blo = _split(wb, br, bc, ldb, kind)
+        ahi, alo, bhi, blo = _split_pair(xa, (ar, ac, lda), wb, (br, bc, ldb), kind)
         d = L.GemmDesc()
         d.algo, d.trans_a, d.trans_b, d.M, d.N, d.K = dalgo, ta, tb, M, N, K
         if kind == "tf32x":

@@ -24,6 +24,8 @@ int tf32_split(float* hi, float* lo, const float* x, int64_t rows, int64_t cols,
                cudaStream_t st);
 int bf16_cast(void* out, const float* x, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st);
 int bf16x3_join(float* out, const void* hi, const void* lo, int64_t n, cudaStream_t st);
+int bf16x3_split2(void* hia, void* loa, const float* xa, int64_t ra, int64_t ca, int64_t lda, void* hib,
+                  void* lob, const float* xb, int64_t rb, int64_t cb, int64_t ldb, cudaStream_t st);
 int bf16x2_split(void* hi, void* lo, const float* x, int64_t rows, int64_t cols, int64_t ld,
                  cudaStream_t st, int mode = 2);
 bool tc_supported(int ta, int tb, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb);
@@ -212,6 +214,13 @@ int b2_gemm_bf16(int ta, int tb, int64_t M, int64_t N, int64_t K, const void* A1
 int b2_bf16x3_split(void* hi16, void* lo16, const float* x, int64_t rows, int64_t cols, int64_t ld,
                     void* stream) {
   return b2::bf16x2_split(hi16, lo16, x, rows, cols, ld, b2::resolve(stream), 5);
+}
+
+int b2_bf16x3_split2(void* hi_a, void* lo_a, const float* a, int64_t rows_a, int64_t cols_a,
+                     int64_t ld_a, void* hi_b, void* lo_b, const float* b, int64_t rows_b,
+                     int64_t cols_b, int64_t ld_b, void* stream) {
+  return b2::bf16x3_split2(hi_a, lo_a, a, rows_a, cols_a, ld_a, hi_b, lo_b, b, rows_b, cols_b, ld_b,
+                           b2::resolve(stream));
 }
 
 int b2_bf16x3_join(float* out, const void* hi16, const void* lo16, int64_t n, void* stream) {

@@ -1317,6 +1317,42 @@ __global__ void k_bf16x2_split(__nv_bfloat16* __restrict__ hi, __nv_bfloat16* __
   }
 }
 
+// Two matrices' 3xBF16 splits in one launch (a GEMM's two fresh operands):
+// threads [0, n8a) take the first matrix's 8-element groups, the rest the
+// second's -- the same per-element arithmetic as k_bf16x2_split<5>.
+struct SplitJob {
+  __nv_bfloat16* hi;
+  __nv_bfloat16* lo;
+  const float* x;
+  int64_t rows, cols, ld;
+};
+__global__ void k_bf16x3_split2(const SplitJob ja, const SplitJob jb) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int64_t n8a = ja.rows * (ja.cols >> 3), n8 = n8a + jb.rows * (jb.cols >> 3);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool first = i < n8a;
+    const SplitJob& j = first ? ja : jb;
+    const int64_t k = first ? i : i - n8a;
+    const int64_t c8 = j.cols >> 3;
+    const int64_t r = k / c8, c = (k - r * c8) * 8;
+    const float* src = j.x + r * j.ld + c;
+    float v[8];
+    if (((uintptr_t)src & 15) == 0) {
+      float4 a = reinterpret_cast<const float4*>(src)[0], b = reinterpret_cast<const float4*>(src)[1];
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = src[q];
+    }
+    __align__(16) __nv_bfloat16 h[8], l[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) split_pair<5>(v[q], h[q], l[q]);
+    *reinterpret_cast<uint4*>(j.hi + r * j.cols + c) = *reinterpret_cast<const uint4*>(h);
+    *reinterpret_cast<uint4*>(j.lo + r * j.cols + c) = *reinterpret_cast<const uint4*>(l);
+  }
+}
+
 // BF16 mode operand: contiguous bf16 round-to-nearest copy of a [rows, cols] (ld) matrix
 __global__ void k_bf16_cast(__nv_bfloat16* __restrict__ out, const float* __restrict__ x,
                             int64_t rows, int64_t cols, int64_t ld) {
@@ -1730,6 +1766,19 @@ __global__ void __launch_bounds__(256) k_bf16x3_join(float* __restrict__ out, co
     o[0] = make_float4(r[0], r[1], r[2], r[3]);
     o[1] = make_float4(r[4], r[5], r[6], r[7]);
   }
+}
+
+int bf16x3_split2(void* hia, void* loa, const float* xa, int64_t ra, int64_t ca, int64_t lda, void* hib,
+                  void* lob, const float* xb, int64_t rb, int64_t cb, int64_t ldb, cudaStream_t st) {
+  if (ca % 8 || cb % 8 || ((uintptr_t)hia & 15) || ((uintptr_t)loa & 15) || ((uintptr_t)hib & 15) ||
+      ((uintptr_t)lob & 15))
+    return fail("b2_bf16x3_split2: cols must be multiples of 8 and outputs 16-B aligned");
+  const int64_t n8 = ra * (ca / 8) + rb * (cb / 8);
+  if (n8 == 0) return 0;
+  const SplitJob ja{(__nv_bfloat16*)hia, (__nv_bfloat16*)loa, xa, ra, ca, lda};
+  const SplitJob jb{(__nv_bfloat16*)hib, (__nv_bfloat16*)lob, xb, rb, cb, ldb};
+  k_bf16x3_split2<<<grid_for(n8, 256 * 4, 8), 256, 0, st>>>(ja, jb);
+  return launched("b2_bf16x3_split2");
 }
 
 int bf16x3_join(float* out, const void* hi, const void* lo, int64_t n, cudaStream_t st) {
