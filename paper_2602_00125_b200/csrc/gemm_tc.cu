@@ -370,8 +370,14 @@ struct Cfg {
   // k-block depth: 32 for every mode that stages fp32 tiles (128-B rows), 64
   // for the pure-bf16 modes (128-B rows of bf16, SW128): twice the MMAs per
   // barrier round trip
-  static constexpr bool W64 = MODE == 4 || MODE == 5;
+  static constexpr bool W64 = MODE == 4 || MODE == 5 || MODE == 6;
   static constexpr int BKM = W64 ? 64 : BK;
+  // MODE 6 (bf16 variant, 512-row pair tiles): each CTA holds two 128-row
+  // blocks of A and the pair issues two M=256 MMAs per k-step into TMEM
+  // columns [0, 256) and [256, 512) -- a quarter fewer operand bytes per MAC
+  // (the bf16 mode is bound by the ~43 B/clk of shared-memory ingress per SM);
+  // the single 512-column accumulator is not double-buffered
+  static constexpr int RM = MODE == 6 ? 2 : 1;
   static constexpr int A32 = BM * BK * 4;  // 16 KB
   static constexpr int B32 = BNL * BK * 4;
   static constexpr int A16 = BM * BKM * 2;
@@ -380,6 +386,7 @@ struct Cfg {
       MODE == 1 ? A32 + B32
       : MODE == 3 ? 2 * (A32 + B32)
       : MODE == 4 ? A16 + B16
+      : MODE == 6 ? 2 * A16 + B16
       : MODE == 5 ? 2 * (A16 + B16)
                   : A32 + B32 + 2 * (A16 + B16);
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
@@ -390,9 +397,9 @@ struct Cfg {
   static constexpr int OFF_ALO = A32;                                 // MODE 3
   static constexpr int OFF_B = MODE == 3 ? 2 * A32 : A32;
   static constexpr int OFF_BLO = 2 * A32 + B32;                       // MODE 3
-  static constexpr int F32 = (MODE == 4 || MODE == 5) ? 0 : A32 + B32;  // fp32 part (MODE 2)
-  static constexpr int OFF_AH16 = F32;                                // MODE 2 / 4 / 5
-  static constexpr int OFF_AL16 = F32 + A16;                          // MODE 2 / 5
+  static constexpr int F32 = (MODE == 4 || MODE == 5 || MODE == 6) ? 0 : A32 + B32;  // fp32 part (MODE 2)
+  static constexpr int OFF_AH16 = F32;                                // MODE 2 / 4 / 5 / 6 (block 0)
+  static constexpr int OFF_AL16 = F32 + A16;                          // MODE 2 / 5; MODE 6: block 1
   static constexpr int OFF_BH16 = MODE == 4 ? A16 : F32 + 2 * A16;
   static constexpr int OFF_BL16 = F32 + 2 * A16 + B16;
 };
@@ -542,11 +549,13 @@ __device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t s0, uint32_
   using CF = Cfg<MODE, CG>;
   constexpr uint32_t id32 = make_idesc(false, A_MN, B_MN, BM * CG);
   constexpr uint32_t id16 = make_idesc(true, A_MN, B_MN, BM * CG);
-  if (MODE == 4) {
+  if (MODE == 4 || MODE == 6) {
 #pragma unroll
-    for (int ks = 0; ks < CF::BKM / 16; ++ks)
-      tc_mma<CG>(d_tmem, desc16<CF::BKM>(s0 + CF::OFF_AH16, A_MN, ks),
-                 desc16<CF::BKM>(s0 + CF::OFF_BH16, B_MN, ks), id16, (acc_flag | ks) ? 1u : 0u, true);
+    for (int b = 0; b < CF::RM; ++b)
+#pragma unroll
+      for (int ks = 0; ks < CF::BKM / 16; ++ks)
+        tc_mma<CG>(d_tmem + b * BN, desc16<CF::BKM>(s0 + CF::OFF_AH16 + b * CF::A16, A_MN, ks),
+                   desc16<CF::BKM>(s0 + CF::OFF_BH16, B_MN, ks), id16, (acc_flag | ks) ? 1u : 0u, true);
   }
   if (MODE == 5) {
 #pragma unroll
@@ -559,7 +568,7 @@ __device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t s0, uint32_
     }
   }
 #pragma unroll
-  for (int ks = 0; ks < ((MODE == 4 || MODE == 5) ? 0 : BK / 8); ++ks) {
+  for (int ks = 0; ks < ((MODE == 4 || MODE == 5 || MODE == 6) ? 0 : BK / 8); ++ks) {
     const uint64_t a = desc32(s0 + CF::OFF_A, A_MN, ks);
     const uint64_t b = desc32(s0 + CF::OFF_B, B_MN, ks);
     tc_mma<CG>(d_tmem, a, b, id32, (acc_flag | ks) ? 1u : 0u, false);
@@ -843,7 +852,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool amn = p.a_mn != 0, bmn = p.b_mn != 0;
         int tm, tn, kb0, kb1, ks;
         tile_info(p, u - G.ustart[gi], tm, tn, kb0, kb1, ks);
-        const int m0 = tm * (BM * CG) + (int)rank * BM;
+        const int m0 = tm * (BM * CG * CF::RM) + (int)rank * BM;
         const int n0 = tn * BN + (int)rank * CF::BNL;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -852,8 +861,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t fb_cl = CG == 2 ? mapa(smem_u32(fb), 0) : 0;
           if (leader) mbar_expect_tx(fb, CF::STAGE_BYTES * CG);
           const int k0 = kb * CF::BKM;
-          if (MODE == 4 || MODE == 5) {  // bf16 operands only
+          if (MODE == 4 || MODE == 5 || MODE == 6) {  // bf16 operands only
             load16<BM, CG, CF::BKM>(amn, st + CF::OFF_AH16, mp + 0, fb, fb_cl, m0, k0, pa);
+            if (MODE == 6)  // the second 256-row block of the pair tile
+              load16<BM, CG, CF::BKM>(amn, st + CF::OFF_AL16, mp + 0, fb, fb_cl, m0 + BM * CG, k0, pa);
             load16<CF::BNL, CG, CF::BKM>(bmn, st + CF::OFF_BH16, mp + 1, fb, fb_cl, n0, k0, pb);
             if (MODE == 5) {
               load16<BM, CG, CF::BKM>(amn, st + CF::OFF_AL16, mp + 2, fb, fb_cl, m0, k0, pa);
@@ -939,11 +950,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tile_info(p, u - G.ustart[gi], tm, tn, kb0, kb1, ks_);
         for (int kb = kb0; kb < kb1; ++kb) {
           const int kc = (kb - kb0) % KC;
-          if (kc == 0) {  // claim the next chunk accumulator (ping-pong)
-            const int cb = chunk & 1;
-            mbar_wait(&tempty[cb], ((chunk >> 1) & 1) ^ 1);
+          if (kc == 0) {  // claim the next chunk accumulator (ping-pong; MODE 6: the whole TMEM)
+            if (CF::RM == 1) {
+              const int cb = chunk & 1;
+              mbar_wait(&tempty[cb], ((chunk >> 1) & 1) ^ 1);
+              d_tmem = tmem_base + cb * BN;
+            } else {
+              mbar_wait(&tempty[0], (chunk & 1) ^ 1);
+              d_tmem = tmem_base;
+            }
             tc_fence_after();
-            d_tmem = tmem_base + cb * BN;
           }
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -964,12 +980,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             // smem slot free (in both CTAs) once these MMAs retire; chunk ready
             const bool last = kc == KC - 1 || kb == kb1 - 1;
+            const int fb2 = CF::RM == 1 ? (chunk & 1) : 0;
             if (CG == 1) {
               tc_commit(&empty[stage]);
-              if (last) tc_commit(&tfull[chunk & 1]);
+              if (last) tc_commit(&tfull[fb2]);
             } else {
               tc_commit_pair(&empty[stage]);
-              if (last) tc_commit_pair(&tfull[chunk & 1]);
+              if (last) tc_commit_pair(&tfull[fb2]);
             }
           }
           __syncwarp();
@@ -999,12 +1016,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       int tm, tn, kb0, kb1, ks;
       tile_info(p, u - G.ustart[gi], tm, tn, kb0, kb1, ks);
       const int nch = (kb1 - kb0 + KC - 1) / KC;
-      const int m0 = tm * (BM * CG) + (int)rank * BM;
       const int n0 = tn * BN;
+#pragma unroll 1
+      for (int blk = 0; blk < CF::RM; ++blk) {  // 128-row blocks of this CTA (MODE 6: two)
+      const int m0 = tm * (BM * CG * CF::RM) + blk * (BM * CG) + (int)rank * BM;
       float acc[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j) acc[j] = 0.0f;
-      for (int c = 0; c < nch; ++c, ++chunk) {
+      if (CF::RM > 1) {  // MODE 6: one chunk per unit, block blk in TMEM columns [blk*256, +256)
+        if (blk == 0) {
+          mbar_wait(&tfull[0], chunk & 1);
+          tc_fence_after();
+        }
+        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(blk * BN + cg * 64);
+#pragma unroll
+        for (int j = 0; j < 64; j += 16) {
+          uint32_t v[16];
+          TMEM_LD16(tbase + j, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int t = 0; t < 16; ++t) acc[j + t] = __fadd_rn(acc[j + t], __uint_as_float(v[t]));
+        }
+        if (blk == CF::RM - 1) {  // the accumulator is free once both blocks are in registers
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(mapa(smem_u32(&tempty[0]), 0));
+          ++chunk;
+        }
+      }
+      for (int c = 0; c < (CF::RM > 1 ? 0 : nch); ++c, ++chunk) {
         const int cb = chunk & 1;
         mbar_wait(&tfull[cb], (chunk >> 1) & 1);
         tc_fence_after();
@@ -1117,7 +1157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 64; ++j)
             if (nb + j < p.N) crow[nb + j] = acc[j];
         }
-        if (MODE == 4 && p.s_hi) {  // BF16 mode: the next GEMM's bf16 operand (RN cast)
+        if ((MODE == 4 || MODE == 6) && p.s_hi) {  // BF16 mode: the next GEMM's bf16 operand (RN cast)
           __nv_bfloat16* hrow = p.s_hi + m * (int64_t)p.N;
           if (full64 && (p.N % 8) == 0) {
 #pragma unroll
@@ -1207,6 +1247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         asm volatile("bar.sync %0, 128;" ::"r"(1 + cg) : "memory");
       }
+      }  // blk
     }
   }
   if (threadIdx.x == 4 * 32) B2_TRACE(5);  // this epilogue warp's stores issued
@@ -1224,7 +1265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int kb0, kb1, ks;
       tile_info(G.p[gi], cs_unit - G.ustart[gi], tm, tn, kb0, kb1, ks);
       const TcParams& p = G.p[gi];
-      constexpr int EM = MODE == 4 ? 4 : (MODE == 5 ? 5 : 2);
+      constexpr int EM = (MODE == 4 || MODE == 6) ? 4 : (MODE == 5 ? 5 : 2);
 #define B2_CSR(SS)                                                                        \
   if (S == SS) {                                                                          \
     if (!p.s_hi) csplit_reduce<0, SS>(p, smem, tm, tn, krank, warp - 4, lane);           \
@@ -1553,6 +1594,7 @@ static int kc_for_mode(int mode) {
   // truncation, so chunks of K = 4096 -- one TMEM drain per tile for the
   // config-5 shapes, the epilogue's slack a whole tile (bf16 step -7%)
   if (mode == 4) return 8 * KC_BASE;
+  if (mode == 6) return 1 << 30;  // one chunk per unit: the single 512-column accumulator
   return mode == 5 ? 2 * KC_BASE : KC_BASE;  // K = 1024 (BK 64) / 256 (BK 32)
 }
 
@@ -1606,7 +1648,7 @@ template <int MODE, int CG>
 int launch_tc(Prob* pr, int n, TcGroup& G, cudaStream_t st) {
   using CF = Cfg<MODE, CG>;
   static TcMaps maps;  // host staging (copied into the launch's parameters)
-  constexpr bool kB16 = MODE == 4 || MODE == 5;
+  constexpr bool kB16 = MODE == 4 || MODE == 5 || MODE == 6;
   for (int g = 0; g < n; ++g) {
     const TcParams& p = pr[g].p;
     const Operands& o = pr[g].o;
@@ -1817,6 +1859,15 @@ static int splitk_enabled() {
   return v;
 }
 
+static int m2_enabled() {
+  static int v = -1;  // B2_GEMM_M2=0: the bf16 variant keeps 256-row pair tiles (A/B)
+  if (v < 0) {
+    const char* e = getenv("B2_GEMM_M2");
+    v = !(e && e[0] == '0');
+  }
+  return v;
+}
+
 static int csplit_enabled() {
   static int v = -1;  // B2_GEMM_CSPLIT=0: K slices through L2 partials + k_tail_epilogue (A/B)
   if (v < 0) {
@@ -1894,6 +1945,15 @@ int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st) {
   for (int g = 0; g < n; ++g)
     group_tiles += ((d[g].M + (int64_t)BM * cg - 1) / ((int64_t)BM * cg)) * ((d[g].N + BN - 1) / BN);
   const bool few_group = n > 1 && group_tiles * cg <= sms / 2;
+  // bf16 variant with CTA pairs and at least two waves of 512-row pair tiles:
+  // MODE 6 (Cfg::RM), whole tiles only (no K slices; one chunk per unit)
+  bool m2 = false;
+  if (mode == 4 && cg == 2 && m2_enabled()) {
+    int64_t t2 = 0;
+    for (int g = 0; g < n; ++g) t2 += ((d[g].M + 4 * BM - 1) / (4 * BM)) * ((d[g].N + BN - 1) / BN);
+    m2 = t2 >= 2 * (int64_t)(sms / 2);
+  }
+  const int rows_per_tile = BM * cg * (m2 ? 2 : 1);
   // Work units (TcParams): whole tiles, and tiles split into S K slices
   // whose fp32 partials a fixed-order second stage folds. Taken where it pays
   // for the partials' round trip and the second stage (measured,
@@ -1910,7 +1970,7 @@ int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st) {
     TcParams& p = pr[g].p;
     p.nkb = (int)((d[g].K + bk - 1) / bk);
     p.tiles_n = (int)((d[g].N + BN - 1) / BN);
-    p.tiles_m = (int)((d[g].M + (int64_t)BM * cg - 1) / ((int64_t)BM * cg));
+    p.tiles_m = (int)((d[g].M + (int64_t)rows_per_tile - 1) / rows_per_tile);
     pr[g].tiles = (int64_t)p.tiles_m * p.tiles_n;
     const int ca = cg_alone(d[g]);
     const int64_t Pa = sms / ca;
@@ -1918,7 +1978,9 @@ int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st) {
     const int nkb = p.nkb;
     int64_t full = pr[g].tiles, T = 0;
     int S = 1;
-    if (few_group && nkb >= 16 && splitk_enabled()) {
+    if (m2) {
+      // whole 512-row tiles (the unit queue balances them dynamically)
+    } else if (few_group && nkb >= 16 && splitk_enabled()) {
       // the group's own partition (outputs differ from separate launches in
       // rounding only; still a function of the shapes and the SM count)
       S = (int)std::max<int64_t>(
@@ -2031,6 +2093,7 @@ int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st) {
     auto run = [&]() -> int {
 #define B2_TC(MD)                                                        \
   if (mode == MD) return cg == 2 ? launch_tc<MD, 2>(pr, n, G, st) : launch_tc<MD, 1>(pr, n, G, st);
+      if (m2) return launch_tc<6, 2>(pr, n, G, st);
       B2_TC(1) B2_TC(2) B2_TC(3) B2_TC(4) B2_TC(5)
 #undef B2_TC
       return fail("gemm_tc: unknown mode");

@@ -246,3 +246,31 @@ def test_cluster_split_k_bit_identical_to_l2_partials(tmp_path):
     assert set(a.files) == set(b.files)
     for k in a.files:
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_bf16_512_row_pair_tiles_match_256_row_tiles(tmp_path):
+    """The bf16 variant's 512-row pair tiles (MODE 6, default for big launches)
+    give the 256-row path's bits -- C, its bf16 cast, relu bits, column sums --
+    for K <= 4096 (one accumulation chunk either way), ragged M/N included;
+    beyond (one chunk instead of K = 4096 promotion) within bf16 noise."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        f = tmp_path / f"m2_{flag}.npz"
+        env = dict(os.environ, B2_GEMM_M2=flag, PYTHONPATH=root)
+        r = subprocess.run([sys.executable, os.path.join(root, "tests", "m2_cases.py"), str(f)],
+                           env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    a, b = outs
+    for k in a.files:
+        if k.startswith("2_"):  # K = 16384: 4 promotion chunks vs one
+            if k == "2_C":
+                x, y = a[k].view(np.float32), b[k].view(np.float32)
+                assert np.abs(x - y).max() <= 1e-4 * np.abs(y).max()
+            continue
+        assert np.array_equal(a[k], b[k]), k
