@@ -545,17 +545,19 @@ __device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
 // The MMAs of one k-block (stage at shared address s0) for one operand
 // layout; acc_flag = 0 starts a new accumulation chunk.
 template <int MODE, int CG, bool A_MN, bool B_MN>
-__device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t s0, uint32_t acc_flag) {
+__device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t s0, uint32_t acc_flag,
+                                           int blocks = 3 /* MODE 6: bit b = row block b */) {
   using CF = Cfg<MODE, CG>;
   constexpr uint32_t id32 = make_idesc(false, A_MN, B_MN, BM * CG);
   constexpr uint32_t id16 = make_idesc(true, A_MN, B_MN, BM * CG);
   if (MODE == 4 || MODE == 6) {
 #pragma unroll
     for (int b = 0; b < CF::RM; ++b)
+      if (CF::RM == 1 || ((blocks >> b) & 1))
 #pragma unroll
-      for (int ks = 0; ks < CF::BKM / 16; ++ks)
-        tc_mma<CG>(d_tmem + b * BN, desc16<CF::BKM>(s0 + CF::OFF_AH16 + b * CF::A16, A_MN, ks),
-                   desc16<CF::BKM>(s0 + CF::OFF_BH16, B_MN, ks), id16, (acc_flag | ks) ? 1u : 0u, true);
+        for (int ks = 0; ks < CF::BKM / 16; ++ks)
+          tc_mma<CG>(d_tmem + b * BN, desc16<CF::BKM>(s0 + CF::OFF_AH16 + b * CF::A16, A_MN, ks),
+                     desc16<CF::BKM>(s0 + CF::OFF_BH16, B_MN, ks), id16, (acc_flag | ks) ? 1u : 0u, true);
   }
   if (MODE == 5) {
 #pragma unroll
@@ -948,6 +950,66 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool amn = p.a_mn != 0, bmn = p.b_mn != 0;
         int tm, tn, kb0, kb1, ks_;
         tile_info(p, u - G.ustart[gi], tm, tn, kb0, kb1, ks_);
+        auto issue = [&](uint32_t s0, uint32_t acc_flag, int blocks) {
+          if (amn) {
+            if (bmn) mma_kblock<MODE, CG, true, true>(d_tmem, s0, acc_flag, blocks);
+            else mma_kblock<MODE, CG, true, false>(d_tmem, s0, acc_flag, blocks);
+          } else {
+            if (bmn) mma_kblock<MODE, CG, false, true>(d_tmem, s0, acc_flag, blocks);
+            else mma_kblock<MODE, CG, false, false>(d_tmem, s0, acc_flag, blocks);
+          }
+        };
+        if (CF::RM > 1) {
+          // MODE 6: the epilogue frees row block 0 of the accumulator (tempty[0])
+          // before it has even drained block 1 (tempty[1]); the next unit's
+          // block-0 MMAs run ahead over every k-block already staged, and its
+          // block-1 MMAs (and the stage releases) follow once block 1 is free
+          const int L = min(STAGES, kb1 - kb0);
+          mbar_wait(&tempty[0], (chunk & 1) ^ 1);
+          tc_fence_after();
+          d_tmem = tmem_base;
+          int st0 = stage;
+          uint32_t ph0 = phase;
+          for (int j = 0; j < L; ++j) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            if (lane == 0) issue(smem_u32(smem + stage * CF::STAGE_BYTES), j ? 1u : 0u, 1);
+            __syncwarp();
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          mbar_wait(&tempty[1], (chunk & 1) ^ 1);
+          tc_fence_after();
+          stage = st0;
+          phase = ph0;
+          for (int kb = kb0; kb < kb1; ++kb) {
+            const int j = kb - kb0;
+            if (j >= L) {
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+            }
+            if (lane == 0) {
+              const uint32_t s0 = smem_u32(smem + stage * CF::STAGE_BYTES);
+              issue(s0, j ? 1u : 0u, j < L ? 2 : 3);
+              if (CG == 1) {
+                tc_commit(&empty[stage]);
+                if (kb == kb1 - 1) tc_commit(&tfull[0]);
+              } else {
+                tc_commit_pair(&empty[stage]);
+                if (kb == kb1 - 1) tc_commit_pair(&tfull[0]);
+              }
+            }
+            __syncwarp();
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          ++chunk;
+          continue;
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
           const int kc = (kb - kb0) % KC;
           if (kc == 0) {  // claim the next chunk accumulator (ping-pong; MODE 6: the whole TMEM)
@@ -968,16 +1030,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
           if (lane == 0) {
             const uint32_t s0 = smem_u32(smem + stage * CF::STAGE_BYTES);
-            const uint32_t acc_flag = kc ? 1u : 0u;
             // one branch per k-block into layout-specialised issue code (the
             // descriptors fold to constants: no address math between MMAs)
-            if (amn) {
-              if (bmn) mma_kblock<MODE, CG, true, true>(d_tmem, s0, acc_flag);
-              else mma_kblock<MODE, CG, true, false>(d_tmem, s0, acc_flag);
-            } else {
-              if (bmn) mma_kblock<MODE, CG, false, true>(d_tmem, s0, acc_flag);
-              else mma_kblock<MODE, CG, false, false>(d_tmem, s0, acc_flag);
-            }
+            issue(s0, kc ? 1u : 0u, 3);
             // smem slot free (in both CTAs) once these MMAs retire; chunk ready
             const bool last = kc == KC - 1 || kb == kb1 - 1;
             const int fb2 = CF::RM == 1 ? (chunk & 1) : 0;
@@ -1037,12 +1092,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int t = 0; t < 16; ++t) acc[j + t] = __fadd_rn(acc[j + t], __uint_as_float(v[t]));
         }
-        if (blk == CF::RM - 1) {  // the accumulator is free once both blocks are in registers
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_remote(mapa(smem_u32(&tempty[0]), 0));
-          ++chunk;
-        }
+        // this row block of the accumulator is free (the next unit's MMAs for
+        // block 0 may start while block 0's outputs are still being stored)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(mapa(smem_u32(&tempty[blk]), 0));
+        if (blk == CF::RM - 1) ++chunk;
       }
       for (int c = 0; c < (CF::RM > 1 ? 0 : nch); ++c, ++chunk) {
         const int cb = chunk & 1;
