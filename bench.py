@@ -750,7 +750,7 @@ def main():
     if not args.no_bf16:
         try:
             bf16 = variant("bf16", "bf16 GEMM operands, fp32 accumulate/master weights/Adam",
-                           "k_gemm_tc<BF16> (tcgen05 kind::f16, cta_group::2)", 1.0)
+                           "k_gemm_tc<BF16> (tcgen05 kind::f16, cta_group::2, 512-row pair tiles)", 1.0)
         except Exception as e:  # noqa: BLE001
             bf16 = {"error": f"{type(e).__name__}: {e}"[:300]}
     # the north star's sanctioned fp32 scheme (3xTF32 on tcgen05) for the record
