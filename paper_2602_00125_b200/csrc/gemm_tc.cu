@@ -275,6 +275,18 @@ struct TcParams {
   int a_mn, b_mn;             // operand layouts: A stored [K,M] (MN-major) / B stored [K,N]
 };
 
+// Epilogue stores of outputs that are read next as another launch's operand
+// (too large to stay in L2): with G.l2hint & 4 they go out as cache-streaming
+// stores (L2 evict-first), so they do not push the raster's A / B panels out.
+__device__ __forceinline__ void st_out16(void* p, uint4 v, bool cs) {
+  if (cs)
+    asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+  else
+    *reinterpret_cast<uint4*>(p) = v;
+}
+
+
 // One launch runs up to kMaxProb independent problems of one mode (the dX and
 // dW GEMMs of a pullback): their work units are numbered back to back
 // (problem g owns units [ustart[g], ustart[g+1])). Every CTA (pair) takes
@@ -845,8 +857,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t pa = G.l2hint == 2 ? l2_policy_first() : l2_policy_normal();
-      const uint64_t pb = G.l2hint ? l2_policy_last() : pa;
+      const uint64_t pa = (G.l2hint & 3) == 2 ? l2_policy_first() : l2_policy_normal();
+      const uint64_t pb = (G.l2hint & 3) ? l2_policy_last() : pa;
       auto produce = [&](int u) {
         const int gi = prob_of<MULTI>(G, u);
         const TcParams& p = G.p[gi];
@@ -1168,6 +1180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 64; ++j) acc[j] = acc[j] > 0.0f ? acc[j] : 0.0f;
         }
         const bool full64 = vec_ok && nb + 64 <= p.N;
+        const bool stcs = (G.l2hint & 4) != 0;
         if (p.bits_out) {  // ReLU forward: record y > 0 as 64 bits per (row, column group)
           uint32_t lo = 0, hi = 0;
 #pragma unroll
@@ -1206,7 +1219,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else if (full64) {
 #pragma unroll
           for (int j = 0; j < 64; j += 4)
-            *reinterpret_cast<float4*>(crow + nb + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            st_out16(crow + nb + j,
+                     make_uint4(__float_as_uint(acc[j]), __float_as_uint(acc[j + 1]), __float_as_uint(acc[j + 2]),
+                                __float_as_uint(acc[j + 3])),
+                     stcs);
         } else {
 #pragma unroll
           for (int j = 0; j < 64; ++j)
@@ -1220,7 +1236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               __align__(16) __nv_bfloat16 h[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) h[i] = __float2bfloat16_rn(acc[j + i]);
-              *reinterpret_cast<uint4*>(hrow + nb + j) = *reinterpret_cast<const uint4*>(h);
+              st_out16(hrow + nb + j, *reinterpret_cast<const uint4*>(h), stcs);
             }
           } else {
 #pragma unroll
@@ -1238,8 +1254,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               split_pair2<MODE>(acc[j + 2], acc[j + 3], hv.y, lv.y);
               split_pair2<MODE>(acc[j + 4], acc[j + 5], hv.z, lv.z);
               split_pair2<MODE>(acc[j + 6], acc[j + 7], hv.w, lv.w);
-              *reinterpret_cast<uint4*>(hrow + nb + j) = hv;
-              *reinterpret_cast<uint4*>(lrow + nb + j) = lv;
+              st_out16(hrow + nb + j, hv, stcs);
+              st_out16(lrow + nb + j, lv, stcs);
             }
           } else {
 #pragma unroll
@@ -2114,7 +2130,7 @@ int gemm_tc_group(int mode, const TcDesc* d, int n, cudaStream_t st) {
   {
     static int h = -1;
     if (h < 0) {
-      const char* e = getenv("B2_GEMM_L2HINT");  // 0: no hints; 2: also A evict_first (A/B)
+      const char* e = getenv("B2_GEMM_L2HINT");  // 0: no hints; 2: also A evict_first (A/B); +4: streaming output stores
       h = !e ? 1 : atoi(e);
     }
     G.l2hint = h;
