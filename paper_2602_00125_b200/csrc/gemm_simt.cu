@@ -5,8 +5,9 @@
 // Replaces matmul.block (tensorlite/core.py:802-807) and its pullbacks
 // (core.py:815-817); the three operand layouts of those pullbacks are
 // template parameters, so transposed views are read in place, never copied.
-// 128x128x8 CTA tile, 256 threads, 8x8 outputs per thread (two 4x4 quads per
-// axis to keep shared-memory reads conflict-free), register double buffering.
+// 128x128x16 CTA tile, 256 threads, 8x8 outputs per thread (two 4x4 quads per
+// axis to keep shared-memory reads conflict-free), 128-bit global loads staged
+// through registers across the k-tile (double-buffered shared memory).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -18,93 +19,162 @@ extern "C" int b2_free(void*, void*);
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 8;
+constexpr int BM = 128, BN = 128, BK = 16;
+// shared-memory row stride: the +4 keeps rows 16-byte aligned for the 128-bit
+// fragment reads and spreads the transposing stores of a k-contiguous operand
+// (4 k-quads of a warp land 16 banks apart: 2-way instead of 4-way conflicts)
+constexpr int LDS = BM + 4;
 
-template <bool TA, bool TB>
-__device__ __forceinline__ void load_tiles(const float* __restrict__ A, int64_t lda,
-                                           const float* __restrict__ B, int64_t ldb, int64_t M,
-                                           int64_t N, int64_t K, int64_t m0, int64_t n0,
-                                           int64_t k0, float ra[4], float rb[4]) {
-  int tid = threadIdx.x;
+// One operand tile (128 rows/columns r x 16 k) from global memory into registers.
+// KC: element (r, k) at X[r * ld + k] (k contiguous), else X[k * ld + r].
+// VEC: base pointer 16-byte aligned and ld % 4 == 0, so a quad that lies inside
+// the matrix is one 128-bit load; edge quads (and VEC = false) take guarded
+// scalar loads with zero fill.
+template <bool KC, bool VEC>
+__device__ __forceinline__ void gload(const float* __restrict__ X, int64_t ld, int64_t R, int64_t K,
+                                      int64_t r0, int64_t k0, float4 q[2]) {
+  const int tid = threadIdx.x;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int64_t m, k;
-    if (!TA) { m = m0 + tid / 2; k = k0 + (tid % 2) * 4 + i; }
-    else     { k = k0 + tid / 32; m = m0 + (tid % 32) * 4 + i; }
-    ra[i] = (m < M && k < K) ? (TA ? A[k * lda + m] : A[m * lda + k]) : 0.0f;
-    int64_t n, kb;
-    if (TB) { n = n0 + tid / 2; kb = k0 + (tid % 2) * 4 + i; }
-    else    { kb = k0 + tid / 32; n = n0 + (tid % 32) * 4 + i; }
-    rb[i] = (n < N && kb < K) ? (TB ? B[n * ldb + kb] : B[kb * ldb + n]) : 0.0f;
+  for (int i = 0; i < 2; ++i) {
+    int64_t r, k;
+    if (KC) { r = r0 + (tid >> 2) + 64 * i; k = k0 + (tid & 3) * 4; }
+    else    { k = k0 + (tid >> 5) + 8 * i;  r = r0 + (tid & 31) * 4; }
+    const bool whole = KC ? (r < R && k + 3 < K) : (k < K && r + 3 < R);
+    if (VEC && whole) {
+      q[i] = __ldg(reinterpret_cast<const float4*>(KC ? X + r * ld + k : X + k * ld + r));
+    } else {
+      float v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t rr = KC ? r : r + j, kk = KC ? k + j : k;
+        v[j] = (rr < R && kk < K) ? (KC ? X[rr * ld + kk] : X[kk * ld + rr]) : 0.0f;
+      }
+      q[i] = make_float4(v[0], v[1], v[2], v[3]);
+    }
   }
 }
 
-template <bool TA, bool TB>
-__device__ __forceinline__ void store_tiles(float (*As)[BM], float (*Bs)[BN], const float ra[4],
-                                            const float rb[4]) {
-  int tid = threadIdx.x;
+// registers -> the [k][r] shared-memory tile (transposing when k-contiguous)
+template <bool KC>
+__device__ __forceinline__ void sstore(float (*S)[LDS], const float4 q[2]) {
+  const int tid = threadIdx.x;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (!TA) As[(tid % 2) * 4 + i][tid / 2] = ra[i];
-    else     As[tid / 32][(tid % 32) * 4 + i] = ra[i];
-    if (TB)  Bs[(tid % 2) * 4 + i][tid / 2] = rb[i];
-    else     Bs[tid / 32][(tid % 32) * 4 + i] = rb[i];
+  for (int i = 0; i < 2; ++i) {
+    if (KC) {
+      const int r = (tid >> 2) + 64 * i, k = (tid & 3) * 4;
+      S[k + 0][r] = q[i].x;
+      S[k + 1][r] = q[i].y;
+      S[k + 2][r] = q[i].z;
+      S[k + 3][r] = q[i].w;
+    } else {
+      *reinterpret_cast<float4*>(&S[(tid >> 5) + 8 * i][(tid & 31) * 4]) = q[i];
+    }
   }
 }
 
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(256) k_gemm_simt(int64_t M, int64_t N, int64_t K,
-                                                   const float* __restrict__ A, int64_t lda,
-                                                   const float* __restrict__ B, int64_t ldb,
-                                                   float* __restrict__ C, int64_t ldc,
-                                                   const float* __restrict__ bias, int epi) {
-  __shared__ __align__(16) float As[2][BK][BM];
-  __shared__ __align__(16) float Bs[2][BK][BN];
-  int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  int64_t m0 = blockIdx.y * (int64_t)BM, n0 = blockIdx.x * (int64_t)BN;
+// 128x128x16 CTA tile, 256 threads (2 CTAs per SM), 8x8 outputs per thread as
+// four 4x4 quads 64 apart on each axis. A warp is 4 threads along m x 8 along n,
+// so a k-step's fragment reads are 2 x 64 B of A and 2 x 128 B of B (one
+// wavefront each) for 64 FFMAs per thread; the next k-tile's global loads are in
+// flight in registers across the 16 k-steps, one __syncthreads per k-tile.
+// Every output is a sequential fp32 fmaf chain over k = 0..K-1 (fixed order).
+template <bool TA, bool TB, bool VEC>
+__global__ void __launch_bounds__(256, 2) k_gemm_simt(int64_t M, int64_t N, int64_t K,
+                                                      const float* __restrict__ A, int64_t lda,
+                                                      const float* __restrict__ B, int64_t ldb,
+                                                      float* __restrict__ C, int64_t ldc,
+                                                      const float* __restrict__ bias, int epi) {
+  __shared__ __align__(16) float As[2][BK][LDS];
+  __shared__ __align__(16) float Bs[2][BK][LDS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // warp w: m-quads 4 * (w / 2) .. +3, n-quads 8 * (w % 2) .. +7
+  // (2 x 16, 8 x 4 and the transposed 4 x 8 arrangements measured the same: every
+  // 128-bit fragment read costs 3 shared-memory wavefronts whatever the lanes share)
+  const int ty = (warp >> 1) * 4 + (lane >> 3), tx = (warp & 1) * 8 + (lane & 7);
+  const int64_t m0 = blockIdx.y * (int64_t)BM, n0 = blockIdx.x * (int64_t)BN;
   float acc[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
-  float ra[4], rb[4];
-  load_tiles<TA, TB>(A, lda, B, ldb, M, N, K, m0, n0, 0, ra, rb);
-  store_tiles<TA, TB>(As[0], Bs[0], ra, rb);
+  float4 qa[2], qb[2];
+  gload<!TA, VEC>(A, lda, M, K, m0, 0, qa);
+  gload<TB, VEC>(B, ldb, N, K, n0, 0, qb);
+  sstore<!TA>(As[0], qa);
+  sstore<TB>(Bs[0], qb);
   __syncthreads();
-  int nk = (int)((K + BK - 1) / BK);
+  const int nk = (int)((K + BK - 1) / BK);
+  // interior CTAs (whole 128x128 tile inside the matrix) load whole k-tiles with
+  // four unguarded 128-bit loads from pointers that advance by one k-tile
+  const bool interior = VEC && m0 + BM <= M && n0 + BN <= N;
+  const int nk_whole = (int)(K / BK);
+  const float* pa[2];
+  const float* pb[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    pa[i] = !TA ? A + (m0 + (tid >> 2) + 64 * i) * lda + (tid & 3) * 4
+                : A + (int64_t)((tid >> 5) + 8 * i) * lda + m0 + (tid & 31) * 4;
+    pb[i] = TB ? B + (n0 + (tid >> 2) + 64 * i) * ldb + (tid & 3) * 4
+               : B + (int64_t)((tid >> 5) + 8 * i) * ldb + n0 + (tid & 31) * 4;
+  }
+  const int64_t sa = !TA ? BK : BK * lda, sb = TB ? BK : BK * ldb;
   for (int kt = 0; kt < nk; ++kt) {
-    int cur = kt & 1;
-    if (kt + 1 < nk) load_tiles<TA, TB>(A, lda, B, ldb, M, N, K, m0, n0, (int64_t)(kt + 1) * BK, ra, rb);
+    const int cur = kt & 1;
+    if (interior && kt + 1 < nk_whole) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        pa[i] += sa;
+        pb[i] += sb;
+        qa[i] = __ldg(reinterpret_cast<const float4*>(pa[i]));
+        qb[i] = __ldg(reinterpret_cast<const float4*>(pb[i]));
+      }
+    } else if (kt + 1 < nk) {
+      gload<!TA, VEC>(A, lda, M, K, m0, (int64_t)(kt + 1) * BK, qa);
+      gload<TB, VEC>(B, ldb, N, K, n0, (int64_t)(kt + 1) * BK, qb);
+    }
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
-      float4 a0 = *reinterpret_cast<const float4*>(&As[cur][k][ty * 4]);
-      float4 a1 = *reinterpret_cast<const float4*>(&As[cur][k][64 + ty * 4]);
-      float4 b0 = *reinterpret_cast<const float4*>(&Bs[cur][k][tx * 4]);
-      float4 b1 = *reinterpret_cast<const float4*>(&Bs[cur][k][64 + tx * 4]);
-      float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[cur][k][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[cur][k][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[cur][k][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[cur][k][64 + tx * 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
     if (kt + 1 < nk) {
-      store_tiles<TA, TB>(As[cur ^ 1], Bs[cur ^ 1], ra, rb);
+      sstore<!TA>(As[cur ^ 1], qa);
+      sstore<TB>(Bs[cur ^ 1], qb);
       __syncthreads();
     }
   }
+  const bool vec_out = VEC && (ldc & 3) == 0 && ((uintptr_t)C & 15) == 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    const int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
     if (m >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-      if (n >= N) continue;
-      float v = acc[i][j];
-      if (epi == B2_EPI_BIAS || epi == B2_EPI_BIAS_RELU) v = __fadd_rn(v, bias[n]);
-      if (epi == B2_EPI_BIAS_RELU || epi == B2_EPI_RELU) v = v > 0.0f ? v : 0.0f;
-      C[m * ldc + n] = v;
+    for (int h = 0; h < 2; ++h) {
+      const int64_t n = n0 + 64 * h + tx * 4;
+      float v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[j] = acc[i][4 * h + j];
+        if (n + j < N) {
+          if (epi == B2_EPI_BIAS || epi == B2_EPI_BIAS_RELU) v[j] = __fadd_rn(v[j], bias[n + j]);
+          if (epi == B2_EPI_BIAS_RELU || epi == B2_EPI_RELU) v[j] = v[j] > 0.0f ? v[j] : 0.0f;
+        }
+      }
+      if (vec_out && n + 3 < N) {
+        *reinterpret_cast<float4*>(&C[m * ldc + n]) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (n + j < N) C[m * ldc + n + j] = v[j];
+      }
     }
   }
 }
@@ -262,8 +332,12 @@ int gemm_simt(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, i
   }
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
   if (grid.y > 65535) return fail("b2_gemm(simt): M too large for the SIMT grid");
-#define B2_SIMT(TA_, TB_) \
-  k_gemm_simt<TA_, TB_><<<grid, 256, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, bias, epi)
+  const bool vec = (lda & 3) == 0 && (ldb & 3) == 0 && (((uintptr_t)A | (uintptr_t)B) & 15) == 0;
+#define B2_SIMT(TA_, TB_)                                                                      \
+  do {                                                                                         \
+    if (vec) k_gemm_simt<TA_, TB_, true><<<grid, 256, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, bias, epi);  \
+    else k_gemm_simt<TA_, TB_, false><<<grid, 256, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc, bias, epi); \
+  } while (0)
   if (!ta && !tb) B2_SIMT(false, false);
   else if (!ta && tb) B2_SIMT(false, true);
   else if (ta && !tb) B2_SIMT(true, false);
