@@ -19,11 +19,13 @@ extern "C" int b2_free(void*, void*);
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16;
-// shared-memory row stride: the +4 keeps rows 16-byte aligned for the 128-bit
-// fragment reads and spreads the transposing stores of a k-contiguous operand
-// (4 k-quads of a warp land 16 banks apart: 2-way instead of 4-way conflicts)
-constexpr int LDS = BM + 4;
+constexpr int BM = 128, BN = 128, BK = 16, GW = 16;
+// Shared-memory tiles are [k][r] rows of 128 floats with the column XOR-swizzled by
+// the k-quad, c = r ^ (8 * ((k >> 2) & 3)): the transposing stores of a
+// k-contiguous operand (a warp holds 8 rows x 4 k-quads) then hit 32 distinct banks,
+// and 16-byte groups stay whole for the 128-bit fragment reads.
+constexpr int LDS = BM;
+__device__ __forceinline__ int swz(int k) { return 8 * ((k >> 2) & 3); }
 
 // One operand tile (128 rows/columns r x 16 k) from global memory into registers.
 // KC: element (r, k) at X[r * ld + k] (k contiguous), else X[k * ld + r].
@@ -61,15 +63,30 @@ __device__ __forceinline__ void sstore(float (*S)[LDS], const float4 q[2]) {
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     if (KC) {
-      const int r = (tid >> 2) + 64 * i, k = (tid & 3) * 4;
-      S[k + 0][r] = q[i].x;
-      S[k + 1][r] = q[i].y;
-      S[k + 2][r] = q[i].z;
-      S[k + 3][r] = q[i].w;
+      const int k = (tid & 3) * 4, c = ((tid >> 2) + 64 * i) ^ swz(k);
+      S[k + 0][c] = q[i].x;
+      S[k + 1][c] = q[i].y;
+      S[k + 2][c] = q[i].z;
+      S[k + 3][c] = q[i].w;
     } else {
-      *reinterpret_cast<float4*>(&S[(tid >> 5) + 8 * i][(tid & 31) * 4]) = q[i];
+      const int k = (tid >> 5) + 8 * i;
+      *reinterpret_cast<float4*>(&S[k][((tid & 31) * 4) ^ swz(k)]) = q[i];
     }
   }
+}
+
+// Two fp32 FMAs in one instruction (Blackwell FFMA2, PTX fma.rn.f32x2): each half
+// is an IEEE round-to-nearest fmaf, so results are bit-identical to scalar FFMAs,
+// at half the issue slots -- an 8x8 FFMA micro-tile otherwise needs every issue
+// slot of the SM sub-partition for the FMAs alone. ptxas folds the {a, a} pack
+// into a broadcast operand (FFMA2 Rc, Ra.F32, Rb.F32x2, Rc.F32x2): no extra moves.
+__device__ __forceinline__ void fma2(float2& c, float a, float2 b) {
+  unsigned long long aa, bb, cc;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "f"(c.x), "f"(c.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(cc) : "l"(aa), "l"(bb));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(c.x), "=f"(c.y) : "l"(cc));
 }
 
 // 128x128x16 CTA tile, 256 threads (2 CTAs per SM), 8x8 outputs per thread as
@@ -91,12 +108,18 @@ __global__ void __launch_bounds__(256, 2) k_gemm_simt(int64_t M, int64_t N, int6
   // (2 x 16, 8 x 4 and the transposed 4 x 8 arrangements measured the same: every
   // 128-bit fragment read costs 3 shared-memory wavefronts whatever the lanes share)
   const int ty = (warp >> 1) * 4 + (lane >> 3), tx = (warp & 1) * 8 + (lane & 7);
-  const int64_t m0 = blockIdx.y * (int64_t)BM, n0 = blockIdx.x * (int64_t)BN;
-  float acc[8][8];
+  // grouped raster over a 1-D grid: tiles run down M inside groups of GW tile
+  // columns, so the CTAs resident together (2 per SM) cover a ~16 x 18 block of
+  // tiles -- each operand tile they fetch is shared by 16-18 of them in L2
+  const int tiles_m = (int)((M + BM - 1) / BM), tiles_n = (int)((N + BN - 1) / BN);
+  const int per_group = GW * tiles_m, g = blockIdx.x / per_group, t = blockIdx.x - g * per_group;
+  const int gw = min(GW, tiles_n - g * GW);
+  const int64_t m0 = (int64_t)(t / gw) * BM, n0 = (int64_t)(g * GW + t % gw) * BN;
+  float2 acc[8][4];  // acc[i][j] = outputs (i, 2j) and (i, 2j + 1) of the micro-tile
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.0f, 0.0f);
   float4 qa[2], qb[2];
   gload<!TA, VEC>(A, lda, M, K, m0, 0, qa);
   gload<TB, VEC>(B, ldb, N, K, n0, 0, qb);
@@ -108,42 +131,38 @@ __global__ void __launch_bounds__(256, 2) k_gemm_simt(int64_t M, int64_t N, int6
   // four unguarded 128-bit loads from pointers that advance by one k-tile
   const bool interior = VEC && m0 + BM <= M && n0 + BN <= N;
   const int nk_whole = (int)(K / BK);
-  const float* pa[2];
-  const float* pb[2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    pa[i] = !TA ? A + (m0 + (tid >> 2) + 64 * i) * lda + (tid & 3) * 4
-                : A + (int64_t)((tid >> 5) + 8 * i) * lda + m0 + (tid & 31) * 4;
-    pb[i] = TB ? B + (n0 + (tid >> 2) + 64 * i) * ldb + (tid & 3) * 4
-               : B + (int64_t)((tid >> 5) + 8 * i) * ldb + n0 + (tid & 31) * 4;
-  }
-  const int64_t sa = !TA ? BK : BK * lda, sb = TB ? BK : BK * ldb;
+  const float* pa = !TA ? A + (m0 + (tid >> 2)) * lda + (tid & 3) * 4
+                        : A + (int64_t)(tid >> 5) * lda + m0 + (tid & 31) * 4;
+  const float* pb = TB ? B + (n0 + (tid >> 2)) * ldb + (tid & 3) * 4
+                       : B + (int64_t)(tid >> 5) * ldb + n0 + (tid & 31) * 4;
+  const int64_t ha = (!TA ? 64 : 8) * lda, hb = (TB ? 64 : 8) * ldb;  // the thread's second quad
+  const int64_t sa = !TA ? BK : BK * lda, sb = TB ? BK : BK * ldb;    // one k-tile ahead
   for (int kt = 0; kt < nk; ++kt) {
     const int cur = kt & 1;
     if (interior && kt + 1 < nk_whole) {
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        pa[i] += sa;
-        pb[i] += sb;
-        qa[i] = __ldg(reinterpret_cast<const float4*>(pa[i]));
-        qb[i] = __ldg(reinterpret_cast<const float4*>(pb[i]));
-      }
+      pa += sa;
+      pb += sb;
+      qa[0] = __ldg(reinterpret_cast<const float4*>(pa));
+      qa[1] = __ldg(reinterpret_cast<const float4*>(pa + ha));
+      qb[0] = __ldg(reinterpret_cast<const float4*>(pb));
+      qb[1] = __ldg(reinterpret_cast<const float4*>(pb + hb));
     } else if (kt + 1 < nk) {
       gload<!TA, VEC>(A, lda, M, K, m0, (int64_t)(kt + 1) * BK, qa);
       gload<TB, VEC>(B, ldb, N, K, n0, (int64_t)(kt + 1) * BK, qb);
     }
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[cur][k][ty * 4]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[cur][k][64 + ty * 4]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[cur][k][tx * 4]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[cur][k][64 + tx * 4]);
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[cur][k][(ty * 4) ^ swz(k)]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[cur][k][64 + ((ty * 4) ^ swz(k))]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[cur][k][(tx * 4) ^ swz(k)]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[cur][k][64 + ((tx * 4) ^ swz(k))]);
       const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                            make_float2(b1.z, b1.w)};
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) fma2(acc[i][j], av[i], bv[j]);
     }
     if (kt + 1 < nk) {
       sstore<!TA>(As[cur ^ 1], qa);
@@ -162,7 +181,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_simt(int64_t M, int64_t N, int6
       float v[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        v[j] = acc[i][4 * h + j];
+        v[j] = (j & 1) ? acc[i][2 * h + j / 2].y : acc[i][2 * h + j / 2].x;
         if (n + j < N) {
           if (epi == B2_EPI_BIAS || epi == B2_EPI_BIAS_RELU) v[j] = __fadd_rn(v[j], bias[n + j]);
           if (epi == B2_EPI_BIAS_RELU || epi == B2_EPI_RELU) v[j] = v[j] > 0.0f ? v[j] : 0.0f;
@@ -330,8 +349,8 @@ int gemm_simt(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, i
     if (ws) b2_free(ws, st);
     return rc;
   }
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
-  if (grid.y > 65535) return fail("b2_gemm(simt): M too large for the SIMT grid");
+  if (big_tiles > INT32_MAX) return fail("b2_gemm(simt): too many tiles for the SIMT grid");
+  dim3 grid((unsigned)big_tiles);
   const bool vec = (lda & 3) == 0 && (ldb & 3) == 0 && (((uintptr_t)A | (uintptr_t)B) & 15) == 0;
 #define B2_SIMT(TA_, TB_)                                                                      \
   do {                                                                                         \
