@@ -420,10 +420,14 @@ def test_config5_small_bf16_variant_adam_losses():
 
 @pytest.mark.parametrize("ta,tb", [(0, 1), (0, 0), (1, 0), (1, 1)])
 @pytest.mark.parametrize("shape", [(2048, 1056, 72), (256, 256, 784), (256, 10, 256), (10, 784, 256),
-                                   (3, 5, 1000), (70, 130, 17)])
+                                   (3, 5, 1000), (70, 130, 17), (1100, 1302, 70), (1024, 2200, 64),
+                                   (1500, 1500, 16), (1281, 1153, 9)])
 def test_gemm_simt_paths(ta, tb, shape):
-    """FP32 FFMA paths: the 128x128 tile kernel (many tiles) and the
-    64x64 split-K latency kernel (config-1 shapes, ragged, K split 1..32)."""
+    """FP32 FFMA paths: the 128x128 tile kernel (many tiles: FFMA2, interior
+    128-bit loads and guarded edge tiles, leading dimensions that are not a
+    multiple of 4 -> scalar loads, a ragged last raster group, K below and
+    across one k-tile) and the 64x64 split-K latency kernel (config-1 shapes,
+    ragged, K split 1..32)."""
     from paper_2602_00125_b200 import _lib as L
 
     M, N, K = shape
@@ -1364,3 +1368,28 @@ def test_single_pass_config2_matches_the_separate_ops(shape):
     for k, v in sep.items():
         assert bits_equal(host(out[k]), host(v)), k
         assert bits_equal(host(out[k]), ref[k]), k
+
+
+def test_gemm_simt_is_a_sequential_fp32_fma_chain():
+    """The FP32 SIMT GEMM's FFMA2 halves are IEEE fmaf: every output equals the
+    sequential chain acc = fmaf(a[k], b[k], acc), k = 0..K-1. The host chain
+    forms a*b + acc in 80-bit long double (the 48-bit product is exact; the sum
+    is exact unless the exponents are far apart) and rounds once to f32 per
+    step, so only rare double-rounding cases may differ from a true fmaf."""
+    from paper_2602_00125_b200 import _lib as L
+
+    M, N, K = 1280, 1280, 40
+    rng = np.random.default_rng(5)
+    A = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    B = rng.uniform(-1, 1, (N, K)).astype(np.float32)
+    At, Bt = dev(A), dev(B)
+    C = P.zeros((M, N))
+    L.call("b2_gemm", 0, 1, M, N, K, At.data_ptr, K, Bt.data_ptr, K, C.data_ptr, N, None, 0,
+           L.GEMM_SIMT, None)
+    got = host(C)
+    acc = np.zeros((M, N), dtype=np.float32)
+    a80, b80 = A.astype(np.longdouble), B.astype(np.longdouble)
+    for k in range(K):
+        acc = (a80[:, k:k + 1] * b80[None, :, k] + acc.astype(np.longdouble)).astype(np.float32)
+    mism = int((got.view(np.uint32) != acc.view(np.uint32)).sum())
+    assert mism <= M * N * 1e-5, mism
