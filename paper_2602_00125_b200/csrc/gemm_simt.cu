@@ -200,103 +200,176 @@ __global__ void __launch_bounds__(256, 2) k_gemm_simt(int64_t M, int64_t N, int6
 
 // ---------------------------------------------------------------- small / skinny GEMMs
 // Latency path for problems whose 128x128 tiling leaves most SMs idle (BASELINE
-// config 1: 256x256x784, 256x10x256, ...): 64x64x16 tiles, 4x4 outputs per
-// thread, and the K loop split over S CTAs (grid.z). S > 1 writes fp32 partials
-// [S][M][N] that k_splitk_reduce sums in fixed order s = 0..S-1 (deterministic)
-// before the bias/ReLU epilogue.
-constexpr int SBM = 64, SBN = 64, SBK = 16;
+// config 1: 256x256x784, 256x10x256, ...): 64x64 tiles, 4x4 outputs per thread
+// (FFMA2), and the K loop split over the S <= 6 CTAs of a thread-block cluster
+// (grid.z). A CTA stages its whole K slice (up to 112 k at a time) in shared
+// memory with every global load issued before the first is consumed -- one
+// memory latency per slice instead of one per k-tile -- and keeps its 64x64 fp32
+// partial in shared memory; after a cluster barrier CTA r finishes its 1/S of the
+// tile by reading the S partials through distributed shared memory, summed in
+// slice order s = 0..S-1 (deterministic), then bias / ReLU and the store. No
+// partials through L2, no second launch.
+constexpr int SBM = 64, SBN = 64, SBK = 16, SKT = 7;  // SKT k-tiles (112 k) staged per pass
 
-template <bool TA, bool TB>
+// one 64 x 16 operand sub-tile: a quad per thread (layouts as gload)
+template <bool KC, bool VEC>
+__device__ __forceinline__ float4 gload_small(const float* __restrict__ X, int64_t ld, int64_t R,
+                                              int64_t kend, int64_t r0, int64_t k0) {
+  const int tid = threadIdx.x;
+  int64_t r, k;
+  if (KC) { r = r0 + (tid >> 2); k = k0 + (tid & 3) * 4; }
+  else    { k = k0 + (tid >> 4); r = r0 + (tid & 15) * 4; }
+  const bool whole = KC ? (r < R && k + 3 < kend) : (k < kend && r + 3 < R);
+  if (VEC && whole) return __ldg(reinterpret_cast<const float4*>(KC ? X + r * ld + k : X + k * ld + r));
+  float v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t rr = KC ? r : r + j, kk = KC ? k + j : k;
+    v[j] = (rr < R && kk < kend) ? (KC ? X[rr * ld + kk] : X[kk * ld + rr]) : 0.0f;
+  }
+  return make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// into the [k][64] tile (swizzled like the big kernel's: conflict-free transposing stores)
+template <bool KC>
+__device__ __forceinline__ void sstore_small(float* S, int kt, const float4& q) {
+  const int tid = threadIdx.x;
+  if (KC) {
+    const int k = (tid & 3) * 4, c = (tid >> 2) ^ swz(k);
+    float* row = S + (kt * SBK + k) * SBM + c;
+    row[0] = q.x;
+    row[SBM] = q.y;
+    row[2 * SBM] = q.z;
+    row[3 * SBM] = q.w;
+  } else {
+    const int k = tid >> 4;
+    *reinterpret_cast<float4*>(S + (kt * SBK + k) * SBM + (((tid & 15) * 4) ^ swz(k))) = q;
+  }
+}
+
+__device__ __forceinline__ float4 ld_cluster_f4(const float* p, unsigned rank) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(ra)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <bool TA, bool TB, bool VEC>
 __global__ void __launch_bounds__(256) k_gemm_small(int64_t M, int64_t N, int64_t K, int64_t kslice,
                                                     const float* __restrict__ A, int64_t lda,
                                                     const float* __restrict__ B, int64_t ldb,
                                                     float* __restrict__ C, int64_t ldc,
-                                                    const float* __restrict__ bias, int epi,
-                                                    float* __restrict__ part) {
-  __shared__ __align__(16) float As[2][SBK][SBM];
-  __shared__ __align__(16) float Bs[2][SBK][SBN];
-  const int t = threadIdx.x, tx = t % 16, ty = t / 16;
+                                                    const float* __restrict__ bias, int epi) {
+  extern __shared__ __align__(16) float sm_small[];
+  float* const As = sm_small;                     // [SKT * 16][64]
+  float* const Bs = sm_small + SKT * SBK * SBM;   // [SKT * 16][64]
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int S = (int)gridDim.z, rank = (int)blockIdx.z;  // the cluster spans grid.z
   const int64_t m0 = blockIdx.y * (int64_t)SBM, n0 = blockIdx.x * (int64_t)SBN;
-  const int64_t kb = blockIdx.z * kslice, ke = min(K, kb + kslice);
-  float acc[4][4] = {};
-  float ra[4], rb[4];
-  auto load = [&](int64_t k0) {
+  const int64_t kb = rank * kslice, ke = min(K, kb + kslice);
+  float2 acc[4][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      int64_t m, k;
-      if (!TA) { m = m0 + t / 4; k = k0 + (t % 4) * 4 + i; }
-      else     { k = k0 + t / 16; m = m0 + (t % 16) * 4 + i; }
-      ra[i] = (m < M && k < ke) ? (TA ? A[k * lda + m] : A[m * lda + k]) : 0.0f;
-      int64_t n, kk;
-      if (TB) { n = n0 + t / 4; kk = k0 + (t % 4) * 4 + i; }
-      else    { kk = k0 + t / 16; n = n0 + (t % 16) * 4 + i; }
-      rb[i] = (n < N && kk < ke) ? (TB ? B[n * ldb + kk] : B[kk * ldb + n]) : 0.0f;
-    }
-  };
-  auto store = [&](int buf) {
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = make_float2(0.0f, 0.0f);
+  for (int64_t kc = kb; kc < ke; kc += SKT * SBK) {
+    const int64_t left = (ke - kc + SBK - 1) / SBK;
+    const int nkt = left < SKT ? (int)left : SKT;
+    // (prefetching the next pass over this pass's FMAs measured slower: the 14 staged
+    // quads then live across the FMA loop)
+    float4 qa[SKT], qb[SKT];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (!TA) As[buf][(t % 4) * 4 + i][t / 4] = ra[i];
-      else     As[buf][t / 16][(t % 16) * 4 + i] = ra[i];
-      if (TB)  Bs[buf][(t % 4) * 4 + i][t / 4] = rb[i];
-      else     Bs[buf][t / 16][(t % 16) * 4 + i] = rb[i];
-    }
-  };
-  const int nk = (int)((ke - kb + SBK - 1) / SBK);
-  if (nk > 0) {
-    load(kb);
-    store(0);
-  }
-  __syncthreads();
-  for (int kt = 0; kt < nk; ++kt) {
-    const int cur = kt & 1;
-    if (kt + 1 < nk) load(kb + (int64_t)(kt + 1) * SBK);
-#pragma unroll
-    for (int k = 0; k < SBK; ++k) {
-      const float4 a = *reinterpret_cast<const float4*>(&As[cur][k][ty * 4]);
-      const float4 b = *reinterpret_cast<const float4*>(&Bs[cur][k][tx * 4]);
-      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-    }
-    if (kt + 1 < nk) {
-      store(cur ^ 1);
-      __syncthreads();
-    }
-  }
-  const bool split = gridDim.z > 1;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t m = m0 + ty * 4 + i;
-    if (m >= M) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t n = n0 + tx * 4 + j;
-      if (n >= N) continue;
-      float v = acc[i][j];
-      if (split) {
-        part[(blockIdx.z * M + m) * N + n] = v;
-        continue;
+    for (int i = 0; i < SKT; ++i)
+      if (i < nkt) {
+        qa[i] = gload_small<!TA, VEC>(A, lda, M, ke, m0, kc + i * SBK);
+        qb[i] = gload_small<TB, VEC>(B, ldb, N, ke, n0, kc + i * SBK);
       }
-      if (epi == B2_EPI_BIAS || epi == B2_EPI_BIAS_RELU) v = __fadd_rn(v, bias[n]);
-      if (epi == B2_EPI_BIAS_RELU || epi == B2_EPI_RELU) v = v > 0.0f ? v : 0.0f;
-      C[m * ldc + n] = v;
+    if (kc != kb) __syncthreads();  // the previous pass's tiles have been consumed
+#pragma unroll
+    for (int i = 0; i < SKT; ++i)
+      if (i < nkt) {
+        sstore_small<!TA>(As, i, qa[i]);
+        sstore_small<TB>(Bs, i, qb[i]);
+      }
+    __syncthreads();
+    for (int i = 0; i < nkt; ++i) {
+      const float* ar = As + i * SBK * SBM;
+      const float* br = Bs + i * SBK * SBM;
+#pragma unroll
+      for (int k = 0; k < SBK; ++k) {
+        const float4 a = *reinterpret_cast<const float4*>(ar + k * SBM + ((ty * 4) ^ swz(k)));
+        const float4 b = *reinterpret_cast<const float4*>(br + k * SBM + ((tx * 4) ^ swz(k)));
+        const float av[4] = {a.x, a.y, a.z, a.w};
+        const float2 b01 = make_float2(b.x, b.y), b23 = make_float2(b.z, b.w);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          fma2(acc[r][0], av[r], b01);
+          fma2(acc[r][1], av[r], b23);
+        }
+      }
     }
   }
-}
-
-__global__ void k_splitk_reduce(float* __restrict__ C, int64_t ldc, const float* __restrict__ part,
-                                int64_t M, int64_t N, int S, const float* __restrict__ bias, int epi) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= M * N) return;
-  const int64_t m = i / N, n = i - m * N;
-  float v = 0.0f;
-  for (int s = 0; s < S; ++s) v = __fadd_rn(v, part[s * M * N + i]);  // fixed order
-  if (epi == B2_EPI_BIAS || epi == B2_EPI_BIAS_RELU) v = __fadd_rn(v, bias[n]);
-  if (epi == B2_EPI_BIAS_RELU || epi == B2_EPI_RELU) v = v > 0.0f ? v : 0.0f;
-  C[m * ldc + n] = v;
+  const bool vec_out = VEC && (ldc & 3) == 0 && ((uintptr_t)C & 15) == 0;
+  auto finish = [&](int r, int c4, float4 v) {  // bias / ReLU epilogue + store of one quad
+    const int64_t m = m0 + r, n = n0 + c4;
+    if (m >= M) return;
+    float o[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (n + j < N) {
+        if (epi == B2_EPI_BIAS || epi == B2_EPI_BIAS_RELU) o[j] = __fadd_rn(o[j], bias[n + j]);
+        if (epi == B2_EPI_BIAS_RELU || epi == B2_EPI_RELU) o[j] = o[j] > 0.0f ? o[j] : 0.0f;
+      }
+    if (vec_out && n + 3 < N) {
+      *reinterpret_cast<float4*>(&C[m * ldc + n]) = make_float4(o[0], o[1], o[2], o[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (n + j < N) C[m * ldc + n + j] = o[j];
+    }
+  };
+  if (S == 1) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      finish(ty * 4 + r, tx * 4, make_float4(acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y));
+    return;
+  }
+  // this CTA's partial tile, [64][64] row-major over the (consumed) A tiles
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    *reinterpret_cast<float4*>(As + (ty * 4 + r) * SBN + tx * 4) =
+        make_float4(acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y);
+  cluster_barrier();  // every slice's partial is staged and visible cluster-wide
+  // CTA r finishes quads [r * Q, (r + 1) * Q) of the tile's 1024: the S remote
+  // reads of a quad are issued together, then added in slice order
+  const int Q = (SBM * (SBN / 4) + S - 1) / S;
+  const int q_end = min((rank + 1) * Q, SBM * (SBN / 4));
+  for (int qi = rank * Q + t; qi < q_end; qi += 256) {
+    const int r = qi >> 4, c4 = (qi & 15) * 4;
+    float4 p[8];
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2)
+      if (s2 < S) p[s2] = ld_cluster_f4(As + r * SBN + c4, (unsigned)s2);
+    float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2)
+      if (s2 < S) {  // fixed slice order
+        v.x = __fadd_rn(v.x, p[s2].x);
+        v.y = __fadd_rn(v.y, p[s2].y);
+        v.z = __fadd_rn(v.z, p[s2].z);
+        v.w = __fadd_rn(v.w, p[s2].w);
+      }
+    finish(r, c4, v);
+  }
+  cluster_barrier();  // no CTA leaves while a peer still reads its partial
 }
 
 __global__ void k_fill_bias(float* C, int64_t M, int64_t N, int64_t ldc, const float* bias, int epi) {
@@ -323,31 +396,52 @@ int gemm_simt(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, i
   }
   const int64_t big_tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
   if (big_tiles < sm_count() / 2) {
-    // latency path: 64x64 tiles, K split so the grid covers ~2 CTAs per SM
+    // latency path: 64x64 tiles, K split over a cluster of S <= 6 CTAs so the grid
+    // covers ~2 CTAs per SM (at least 64 k per slice)
     const int64_t tiles = ((N + SBN - 1) / SBN) * ((M + SBM - 1) / SBM);
     int64_t S = std::max<int64_t>(1, std::min<int64_t>((2 * sm_count()) / tiles, K / (4 * SBK)));
-    S = std::min<int64_t>(S, 32);
+    // clusters of up to 6: 7 and 8 CTAs measured slower (256x256x784: 8.6 us at S = 6
+    // with two staging passes per CTA, 9.9-10.3 us at S = 7 / 8 with one)
+    S = std::min<int64_t>(S, 6);
     int64_t kslice = (K + S - 1) / S;
-    kslice = (kslice + SBK - 1) / SBK * SBK;
+    kslice = (kslice + 3) / 4 * 4;  // slices start on 16-byte boundaries of k-contiguous rows
     S = (K + kslice - 1) / kslice;
     dim3 g((unsigned)((N + SBN - 1) / SBN), (unsigned)((M + SBM - 1) / SBM), (unsigned)S);
-    void* ws = nullptr;
-    if (S > 1) B2_TRY(b2_alloc((size_t)S * M * N * sizeof(float), st, &ws));
-    float* part = (float*)ws;
-#define B2_SMALL(TA_, TB_) \
-  k_gemm_small<TA_, TB_><<<g, 256, 0, st>>>(M, N, K, kslice, A, lda, B, ldb, C, ldc, bias, epi, part)
-    if (!ta && !tb) B2_SMALL(false, false);
-    else if (!ta && tb) B2_SMALL(false, true);
-    else if (ta && !tb) B2_SMALL(true, false);
-    else B2_SMALL(true, true);
+    if (g.y > 65535) return fail("b2_gemm(simt-small): M too large");
+    const bool vec = (lda & 3) == 0 && (ldb & 3) == 0 && (((uintptr_t)A | (uintptr_t)B) & 15) == 0;
+    constexpr int kSmem = 2 * SKT * SBK * SBM * (int)sizeof(float);  // 56 KB
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = (unsigned)S;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaSuccess;
+#define B2_SMALL(TA_, TB_, V_)                                                                       \
+  do {                                                                                               \
+    static bool attr_set = false;                                                                    \
+    if (!attr_set) {                                                                                 \
+      B2_CUDA(cudaFuncSetAttribute(k_gemm_small<TA_, TB_, V_>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem)); \
+      attr_set = true;                                                                               \
+    }                                                                                                \
+    e = cudaLaunchKernelEx(&cfg, k_gemm_small<TA_, TB_, V_>, M, N, K, kslice, A, lda, B, ldb, C, ldc, bias, epi); \
+  } while (0)
+#define B2_SMALL_V(TA_, TB_) \
+  do { if (vec) B2_SMALL(TA_, TB_, true); else B2_SMALL(TA_, TB_, false); } while (0)
+    if (!ta && !tb) B2_SMALL_V(false, false);
+    else if (!ta && tb) B2_SMALL_V(false, true);
+    else if (ta && !tb) B2_SMALL_V(true, false);
+    else B2_SMALL_V(true, true);
+#undef B2_SMALL_V
 #undef B2_SMALL
-    int rc = launched("b2_gemm(simt-small)");
-    if (!rc && S > 1) {
-      k_splitk_reduce<<<(unsigned)((M * N + 255) / 256), 256, 0, st>>>(C, ldc, part, M, N, (int)S, bias, epi);
-      rc = launched("b2_gemm(splitk-reduce)");
-    }
-    if (ws) b2_free(ws, st);
-    return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "b2_gemm(simt-small)");
+    return launched("b2_gemm(simt-small)");
   }
   if (big_tiles > INT32_MAX) return fail("b2_gemm(simt): too many tiles for the SIMT grid");
   dim3 grid((unsigned)big_tiles);

@@ -968,7 +968,9 @@ int b2_xent_bwd(float* dlogits, const float* g, const double* row_stats, const f
 #undef B2_XB
     return b2::launched("b2_xent_bwd");
   }
-  int grid = b2::grid_for(rows * cols, 256 * 8, 8);
+  // one element per thread while that fills the chip (config 1's [256, 10]: 10 CTAs
+  // of latency-bound fp64 exp + div chains instead of 2 CTAs x 5 elements deep)
+  int grid = b2::grid_for(rows * cols, rows * cols <= 256LL * 8 * b2::sm_count() ? 256 : 256 * 8, 8);
   k_xent_bwd<<<grid, 256, 0, st>>>(dlogits, g, row_stats, logits, labels, rows, cols, denom);
   return b2::launched("b2_xent_bwd");
 }
