@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def fresh_state():
     tlnp.reset_tape()
-    tlnp._last_store = None
+    tlnp.clear_grads()
     yield
     tlnp.reset_tape()
 
@@ -173,3 +173,31 @@ def test_mlp_training_through_bindings_descends():
         loss.backward()
         opt.step()
     assert losses[-1] < 0.5 * losses[0]
+
+
+def test_grad_store_is_per_thread():
+    """backward() keeps its gradient store per host thread (next to the
+    engine's per-thread tape and stream): a thread's .grad never reads another
+    thread's backward, and clear_grads() only forgets the caller's."""
+    import threading
+
+    seen = {}
+
+    def worker(tag, scale):
+        tlnp.reset_tape()
+        w = tlnp.tensor([1.0, 2.0, 3.0], requires_grad=True)
+        (w * scale).sum().backward()
+        seen[tag] = w.grad.numpy().tolist()
+        tlnp.reset_tape()
+
+    w0 = tlnp.tensor([4.0, 5.0], requires_grad=True)
+    (w0 * 7.0).sum().backward()
+    ts = [threading.Thread(target=worker, args=(i, float(i + 2))) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert seen == {0: [2.0, 2.0, 2.0], 1: [3.0, 3.0, 3.0]}
+    assert w0.grad.numpy().tolist() == [7.0, 7.0]  # untouched by the workers' backward()
+    tlnp.clear_grads()
+    assert w0.grad is None
