@@ -68,7 +68,9 @@ def test_no_cpu_fallback_without_a_device():
 
 
 def test_kernels_are_sm100a():
-    """The shipped library carries sm_100a SASS with tcgen05/TMA instructions."""
+    """The shipped library carries sm_100a SASS with tcgen05/TMA instructions
+    (the tensor-core GEMM), bulk copies, and FFMA2 (the FP32 SIMT GEMM's
+    two-FMAs-per-instruction inner loop)."""
     import shutil
     import subprocess
 
@@ -79,5 +81,5 @@ def test_kernels_are_sm100a():
         pytest.skip("cuobjdump not available")
     out = subprocess.run([cuobjdump, "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
-    for mnem in ("UTCHMMA", "UTMALDG", "LDTM"):
+    for mnem in ("UTCHMMA", "UTMALDG", "LDTM", "UBLKCP", "FFMA2"):
         assert mnem in out, mnem
