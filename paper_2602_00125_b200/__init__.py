@@ -9,7 +9,7 @@ libb2.so (hand-written CUDA for sm_100a behind the C ABI in include/b2.h);
 importing works anywhere, the first op needs a B200.
 """
 
-from . import nn, optim
+from . import gradcheck, nn, optim, parallel
 from .autograd import (GradStore, backward, is_recording, no_grad, record, reset_tape, tape,
                        zero_grad)
 from .core import (Buffer, Tensor, abs_, absolute, add, broadcast_shapes, broadcast_to, clamp, div,
@@ -19,6 +19,7 @@ from .core import (Buffer, Tensor, abs_, absolute, add, broadcast_shapes, broadc
                    sub, sum,
                    tanh, tensor, transpose2d, uniform, zeros, zeros_like)
 from .errors import BroadcastError, DeterminismError, GradError, ShapeError
+from .parallel import max_workers, thread_limit
 
 __version__ = "0.1.0"
 
@@ -34,5 +35,5 @@ __all__ = [
     "muladd_relu_sum_grads", "muladd_relu_stats", "set_gemm_algo",
     "backward", "no_grad", "record", "reset_tape", "tape", "zero_grad", "is_recording",
     "GradStore", "ShapeError", "BroadcastError", "GradError", "DeterminismError",
-    "nn", "optim",
+    "nn", "optim", "gradcheck", "parallel", "thread_limit", "max_workers",
 ]

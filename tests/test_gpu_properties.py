@@ -130,3 +130,21 @@ def test_deterministic_across_processes():
         subprocess.run([sys.executable, "-c", code, path], check=True, cwd=ROOT, timeout=600)
         child = np.load(path)
     assert bits_equal(child, _workload_checksum())
+
+
+def test_results_do_not_depend_on_the_worker_setting():
+    """The reference's determinism contract (parallel.py:1-8): the
+    worker count never changes a number. On the device the partitions are fixed
+    by shape, so thread_limit() is a recorded setting only."""
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((700, 433)).astype(np.float32)
+    outs = []
+    for workers in (1, 8):
+        with P.thread_limit(workers):
+            t = P.from_numpy(a, requires_grad=True)
+            P.reset_tape()
+            s = P.sum(P.mul(P.exp(t), t))
+            g = P.backward(s).get(t)
+            outs.append((s.numpy().copy(), P.sum(t, axis=0).numpy().copy(), g.numpy().copy()))
+    for x, y in zip(*outs):
+        assert x.tobytes() == y.tobytes()

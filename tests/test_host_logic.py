@@ -119,3 +119,74 @@ def test_backward_walk_order_and_leaf_ready_hook():
     assert ready == [x.node.id]
     assert store.get(x) is seed              # first contribution stored as is (aliasing)
     assert A.tape().pullback_calls == 2
+
+
+# The reference's public names (tensorlite/__init__.py:8-66, bindings/src/tlnp.py:36-45 and the
+# handle / module / optimizer methods its tests call): a program written against the reference
+# must find every one of them here.
+_ENGINE_NAMES = """BroadcastError DeterminismError GradError GradStore ShapeError Tensor abs_ absolute add
+autograd backward broadcast_shapes broadcast_to core div errors exp from_buffer from_flat full gradcheck
+is_recording log matmul max max_workers mean mul neg nn no_grad ones ones_like optim parallel record
+reduce_to_shape reset_tape reshape sqrt sub sum tape tensor thread_limit transpose2d uniform zero_grad zeros
+zeros_like""".split()
+_TLNP_NAMES = """Adam BatchNorm BroadcastError Conv2D Dense DeterminismError Dropout GELU GradError Module
+RMSprop ReLU SGD Sequential ShapeError Sigmoid Tanh Tensor cross_entropy full matmul mse no_grad ones
+reset_tape tensor to_host_array uniform wrap_host_array zeros""".split()
+_HANDLE_NAMES = """T __abs__ __add__ __bool__ __eq__ __float__ __ge__ __getitem__ __gt__ __le__ __len__ __lt__
+__matmul__ __mul__ __ne__ __neg__ __radd__ __rmul__ __rsub__ __rtruediv__ __setitem__ __sub__ __truediv__
+backward detach exp grad log max mean numpy requires_grad requires_grad_ reshape sqrt sum
+transpose""".split()
+
+
+def test_reference_public_names_are_all_present():
+    import importlib
+
+    import paper_2602_00125_b200 as P
+    from paper_2602_00125_b200 import tlnp
+
+    missing = [n for n in _ENGINE_NAMES if not hasattr(P, n)]
+    for sub in ("autograd", "core", "errors"):
+        importlib.import_module(f"paper_2602_00125_b200.{sub}")
+    missing = [n for n in missing if not hasattr(P, n)]
+    assert not missing, missing
+    assert not [n for n in _TLNP_NAMES if not hasattr(tlnp, n)]
+    assert not [n for n in _HANDLE_NAMES if not hasattr(tlnp.Tensor, n)]
+    # forwarded introspection and flags of a handle are instance attributes
+    assert set(("shape", "ndim", "size", "item", "tolist")) <= set(tlnp.Tensor._FORWARDED)
+    assert set(("origin", "copied")) <= set(tlnp.Tensor.__slots__)
+    for cls in (tlnp.Dense, tlnp.Sequential):
+        assert not [n for n in ("eval", "train", "parameters", "named_parameters") if not hasattr(cls, n)]
+    for cls in (tlnp.SGD, tlnp.Adam, tlnp.RMSprop):
+        assert hasattr(cls, "step") and hasattr(cls, "zero_grad")
+
+
+def test_worker_setting_contract(monkeypatch):
+    """max_workers / thread_limit / TENSORLITE_THREADS keep the reference's
+    semantics (parallel.py:25-46); spans are worker-independent CHUNK cuts."""
+    import threading
+
+    from paper_2602_00125_b200 import parallel
+
+    monkeypatch.delenv("TENSORLITE_THREADS", raising=False)
+    base = parallel.max_workers()
+    assert 1 <= base <= 8
+    monkeypatch.setenv("TENSORLITE_THREADS", "3")
+    assert parallel.max_workers() == 3
+    monkeypatch.setenv("TENSORLITE_THREADS", "zero")
+    assert parallel.max_workers() == base
+    with parallel.thread_limit(5):
+        assert parallel.max_workers() == 5
+        with parallel.thread_limit(0):
+            assert parallel.max_workers() == 1
+        seen = []
+        t = threading.Thread(target=lambda: seen.append(parallel.max_workers()))
+        t.start()
+        t.join()
+        assert seen == [base]  # a limit belongs to the thread that set it
+        assert parallel.max_workers() == 5
+    assert parallel.max_workers() == base
+    assert parallel.spans(0) == [] and parallel.spans(-3) == []
+    assert parallel.spans(5) == [(0, 5)]
+    cuts = parallel.spans(3 * parallel.CHUNK + 7)
+    assert cuts[0] == (0, parallel.CHUNK) and cuts[-1] == (3 * parallel.CHUNK, 3 * parallel.CHUNK + 7)
+    assert all(a[1] == b[0] for a, b in zip(cuts, cuts[1:]))
