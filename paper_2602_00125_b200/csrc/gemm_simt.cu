@@ -1,21 +1,21 @@
-// FP32 SIMT GEMM (FFMA, fp32 accumulate): the exact-fp32 fallback of the
-// matmul engine for shapes the tcgen05 path does not take (tiny problems,
-// operands whose leading dimension breaks TMA's 16-byte stride rule).
+// FP32 SIMT GEMM (FFMA2, exact fp32 FMA chains): the FP32-pipe path of the matmul
+// engine -- the north star's "FP32 SIMT" scheme, and the fallback for shapes the
+// tcgen05 path does not take (tiny problems, operands whose leading dimension
+// breaks TMA's 16-byte stride rule).
 //
 // Replaces matmul.block (tensorlite/core.py:802-807) and its pullbacks
-// (core.py:815-817); the three operand layouts of those pullbacks are
-// template parameters, so transposed views are read in place, never copied.
-// 128x128x16 CTA tile, 256 threads, 8x8 outputs per thread (two 4x4 quads per
-// axis to keep shared-memory reads conflict-free), 128-bit global loads staged
-// through registers across the k-tile (double-buffered shared memory).
+// (core.py:815-817); the operand layouts of those pullbacks are template
+// parameters, so transposed views are read in place, never copied.
+// Many tiles: 128x128x16 CTA tiles, 256 threads x 8x8 outputs, 128-bit global
+// loads staged through registers across the k-tile, double-buffered swizzled
+// shared memory, grouped raster (k_gemm_simt). Few tiles: 64x64 tiles with K
+// split over a thread-block cluster and folded through distributed shared
+// memory (k_gemm_small).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 
 #include "common.cuh"
-
-extern "C" int b2_alloc(size_t, void*, void**);
-extern "C" int b2_free(void*, void*);
 
 namespace {
 
