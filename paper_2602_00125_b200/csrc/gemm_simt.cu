@@ -438,6 +438,19 @@ int gemm_simt(int ta, int tb, int64_t M, int64_t N, int64_t K, const float* A, i
     else if (!ta && tb) B2_SMALL_V(false, true);
     else if (ta && !tb) B2_SMALL_V(true, false);
     else B2_SMALL_V(true, true);
+    if (e != cudaSuccess && S > 1) {
+      // the clusters could not be placed (MIG / MPS partitions): one CTA per tile
+      // walks the whole K in staging passes, no cluster
+      cudaGetLastError();
+      S = 1;
+      kslice = K;
+      cfg.gridDim = dim3(g.x, g.y, 1);
+      attr[0].val.clusterDim.z = 1;
+      if (!ta && !tb) B2_SMALL_V(false, false);
+      else if (!ta && tb) B2_SMALL_V(false, true);
+      else if (ta && !tb) B2_SMALL_V(true, false);
+      else B2_SMALL_V(true, true);
+    }
 #undef B2_SMALL_V
 #undef B2_SMALL
     if (e != cudaSuccess) return cuda_fail(e, "b2_gemm(simt-small)");
