@@ -421,13 +421,14 @@ def test_config5_small_bf16_variant_adam_losses():
 @pytest.mark.parametrize("ta,tb", [(0, 1), (0, 0), (1, 0), (1, 1)])
 @pytest.mark.parametrize("shape", [(2048, 1056, 72), (256, 256, 784), (256, 10, 256), (10, 784, 256),
                                    (3, 5, 1000), (70, 130, 17), (1100, 1302, 70), (1024, 2200, 64),
-                                   (1500, 1500, 16), (1281, 1153, 9)])
+                                   (1500, 1500, 16), (1281, 1153, 9), (832, 832, 300)])
 def test_gemm_simt_paths(ta, tb, shape):
     """FP32 FFMA paths: the 128x128 tile kernel (many tiles: FFMA2, interior
     128-bit loads and guarded edge tiles, leading dimensions that are not a
     multiple of 4 -> scalar loads, a ragged last raster group, K below and
-    across one k-tile) and the 64x64 split-K latency kernel (config-1 shapes,
-    ragged, K split 1..32)."""
+    across one k-tile) and the 64x64 cluster split-K latency kernel (config-1
+    shapes, ragged, clusters of 1..6 K slices, and 832x832x300: one CTA per
+    tile walking K in three staging passes)."""
     from paper_2602_00125_b200 import _lib as L
 
     M, N, K = shape
