@@ -366,9 +366,11 @@ def op_benchmarks():
             P.set_gemm_algo("simt")
             try:
                 ms = timed(fb, 3)
+                out["config3_n4096_fwdbwd_fp32_simt_tflops"] = 6 * size ** 3 / ms / 1e9
+            except Exception as e:  # noqa: BLE001 -- a secondary figure never costs the others
+                out["config3_n4096_fwdbwd_fp32_simt_error"] = f"{type(e).__name__}: {e}"[:200]
             finally:
                 P.set_gemm_algo(None)
-            out["config3_n4096_fwdbwd_fp32_simt_tflops"] = 6 * size ** 3 / ms / 1e9
         del A, B, dC
     P.reset_tape()
     # config 4: softmax(X@W + b), loss = mean(Y*T), full backward
@@ -460,8 +462,9 @@ def op_benchmarks():
               "config4_fused_gemm_tflops_effective"):
         frac[k.replace("_tflops", "_frac_3xbf16_ceiling")] = out[k] / tc
     # FP32 FFMA peak: 148 SMs x 128 lanes x 2 flops x the maximum SM clock (1965 MHz)
-    frac["config3_n4096_fwdbwd_fp32_simt_frac_fp32_peak"] = (
-        out["config3_n4096_fwdbwd_fp32_simt_tflops"] / (148 * 128 * 2 * 1.965e-3))
+    if "config3_n4096_fwdbwd_fp32_simt_tflops" in out:
+        frac["config3_n4096_fwdbwd_fp32_simt_frac_fp32_peak"] = (
+            out["config3_n4096_fwdbwd_fp32_simt_tflops"] / (148 * 128 * 2 * 1.965e-3))
     frac["config2_e2e_frac_hbm_single_pass"] = out["config2_e2e_gbs_vs_single_pass_bytes"] / hbm
     frac["config2_single_pass_frac_hbm"] = out["config2_single_pass_gbs"] / hbm
     out["roofline_fractions"] = frac
